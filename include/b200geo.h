@@ -1,0 +1,204 @@
+/*
+ * b200geo — C ABI of the B200-native direct-geolocation engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference `digeo`
+ * library (paths relative to /root/reference/proj/include/digeo): the
+ * position-domain correlation (Eq. 11) over every (candidate grid point,
+ * time step), with the geometry that feeds it and the accumulation / peak
+ * search after it. Every entry point below names the reference interface it
+ * replaces. Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Errors: every int-returning function returns DG_OK (0) or a DG_E* code and
+ * leaves a thread-local message in dg_last_error(). Code 1 corresponds to the
+ * reference's std::invalid_argument, 2 to std::runtime_error (CUDA, NCCL,
+ * I/O), 3 to out-of-memory. The C++ shim (include/b200geo/digeo_plugin.hpp)
+ * rethrows them as those exception types.
+ *
+ * Threading: one dg_engine per GPU (one process per GPU). A dg_engine may be
+ * used from several host threads; every session / call owns its own stream
+ * and device buffers (backend.hpp:196-209 "sessions are independent").
+ */
+#ifndef B200GEO_H
+#define B200GEO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_ABI_VERSION 1
+
+enum {
+    DG_OK = 0,
+    DG_EINVAL = 1,   /* std::invalid_argument */
+    DG_ERUNTIME = 2, /* std::runtime_error / CUDA failure */
+    DG_ENOMEM = 3
+};
+
+/* == digeo::PairOffsets (geometry.hpp:68-71): {int64 tdoa_samples; double fdoa_hz} */
+typedef struct {
+    int64_t tdoa_samples;
+    double fdoa_hz;
+} dg_pair_offsets;
+
+/* == digeo::EcefVector (geodesy.hpp:43-50) */
+typedef struct {
+    double x, y, z;
+} dg_ecef;
+
+/* == digeo::EcefStateVector (state.hpp:27-39) */
+typedef struct {
+    dg_ecef position, velocity;
+} dg_state;
+
+/* == digeo::LatLonBounds (geodesy.hpp:126-138) */
+typedef struct {
+    double lat_min_deg, lat_max_deg, lon_min_deg, lon_max_deg;
+} dg_latlon_bounds;
+
+/* == digeo::EmitterEstimate (correlate.hpp:117-122), location flattened */
+typedef struct {
+    double lat_deg, lon_deg, alt_m;
+    int64_t grid_index;
+    double score;
+    double score_zsigma;
+} dg_emitter_estimate;
+
+typedef struct dg_engine dg_engine;
+typedef struct dg_session dg_session;
+typedef struct dg_grid dg_grid;
+typedef struct dg_staged dg_staged;
+
+const char* dg_last_error(void);
+int dg_abi_version(void);
+
+/* ---- engine == digeo::CorrelationBackend (backend.hpp:211-217) ----------
+ * Bound to one CUDA device. Descriptor is {"b200", "parallel-batched",
+ * workers = 1 GPU} — never "gpu", which the reference's tests require to be
+ * rejected by its own registry (test_backend.cpp:181). */
+int dg_engine_create(int device, dg_engine** out);
+void dg_engine_destroy(dg_engine* engine);
+int dg_engine_descriptor(const dg_engine* engine, char* name, size_t name_len, char* kind,
+                         size_t kind_len, unsigned* workers);
+
+/* ---- session == CorrelationBackend::stage + CorrelationSession ---------
+ * dg_stage replaces backend.hpp:214-215 (+ check_pair :221-228): copies both
+ * captures (interleaved complex double, std::complex<double> layout) to the
+ * device. n1/n2 and fs1/fs2 are validated like the reference (mismatch ->
+ * DG_EINVAL). dg_stage_f32 takes float I/Q (the DGIQ on-disk format,
+ * io.hpp:123-167). */
+int dg_stage(dg_engine* engine, const double* y1_iq, int64_t n1, double fs1, const double* y2_iq,
+             int64_t n2, double fs2, dg_session** out);
+int dg_stage_f32(dg_engine* engine, const float* y1_iq, int64_t n1, double fs1,
+                 const float* y2_iq, int64_t n2, double fs2, dg_session** out);
+void dg_session_destroy(dg_session* session);
+
+/* CorrelationSession::correlate_batch (backend.hpp:204-205): out[i] = S for
+ * batch[i]; host spans, out fully written on return. Empty batch or
+ * n_out != n -> DG_EINVAL (backend.hpp:236-238). */
+int dg_correlate_batch(dg_session* session, const dg_pair_offsets* batch, int64_t n, double* out,
+                       int64_t n_out);
+
+/* ---- candidate grid == digeo::CandidateGrid / build_candidate_grid -----
+ * geodesy.hpp:182-207: validation and axis counts exactly as the reference;
+ * the lat-major ECEF lattice is formed on the GPU (bit-identical doubles to
+ * lla_to_ecef). point_cap 0 means the reference default (20,000,000). */
+int dg_build_candidate_grid(dg_engine* engine, const dg_latlon_bounds* bounds, double spacing_deg,
+                            double altitude_m, uint64_t point_cap, dg_grid** out);
+/* Sub-grid of lattice rows [row_begin, row_end): the slab one rank owns when
+ * the grid is sharded across GPUs. Flat indices stay global via row offset. */
+int dg_grid_slab(const dg_grid* grid, int64_t row_begin, int64_t row_end, dg_grid** out);
+/* Arbitrary host ECEF points (e.g. CandidateGrid::points of a reference grid),
+ * lattice shape n_lat x n_lon for detection (n_lat*n_lon == n_points). */
+int dg_grid_from_points(dg_engine* engine, const dg_ecef* points, int64_t n_points, double lat_start,
+                        double lat_step, int64_t n_lat, double lon_start, double lon_step,
+                        int64_t n_lon, double altitude_m, dg_grid** out);
+/* GridAxis fields + row offset of this slab in the full lattice */
+int dg_grid_info(const dg_grid* grid, double* lat_start, double* lat_step, int64_t* n_lat,
+                 double* lon_start, double* lon_step, int64_t* n_lon, double* altitude_m,
+                 int64_t* row_offset);
+int dg_grid_points(const dg_grid* grid, dg_ecef* out_host); /* D2H of the eager lattice */
+void dg_grid_destroy(dg_grid* grid);
+
+/* predict_pair_offsets (geometry.hpp:73-83) for every grid point, on the GPU,
+ * bit-identical to the reference. */
+int dg_predict_offsets(dg_engine* engine, const dg_grid* grid, const dg_state* rx_i,
+                       const dg_state* rx_j, double sample_rate_hz, double wavelength_m,
+                       dg_pair_offsets* out_host);
+
+/* correlate_snapshot (geolocate.hpp:41-75): one snapshot, one pair, the whole
+ * grid, offsets computed on the GPU; out_host has grid-size doubles. */
+int dg_correlate_snapshot(dg_session* session, const dg_grid* grid, const dg_state* rx_i,
+                          const dg_state* rx_j, double center_freq_hz, double* out_host);
+
+/* ---- whole-run driver == geolocate_snapshots (geolocate.hpp:96-146) ---- */
+typedef struct {
+    int64_t n_snapshots;
+    int64_t n_receivers;
+    int64_t n_samples;
+    double sample_rate_hz;
+    double center_freq_hz;
+    const dg_state* states;            /* [n_snapshots][n_receivers] */
+    const double* const* captures_iq;  /* n_snapshots*n_receivers pointers, complex double */
+    const float* const* captures_f32;  /* alternative (DGIQ float I/Q); used if captures_iq NULL */
+} dg_snapshots;
+
+typedef struct {
+    double k_sigma;             /* GeolocateOptions::k_sigma (default 5) */
+    int exclusion_radius_cells; /* default 5 */
+    int normalize_per_snapshot; /* median normalisation (geolocate.hpp:115-122) */
+    int detect;                 /* run detect_emitters on the accumulated surface */
+    void* stream;               /* cudaStream_t to launch on; NULL = private stream */
+    int profile;                /* record per-kernel CUDA events into dg_result stats */
+} dg_options;
+
+typedef struct {
+    /* outputs (all nullable) */
+    double* accumulated;        /* host [P] */
+    double* accumulated_device; /* device [P] (caller-owned, e.g. a torch tensor) */
+    double* per_snapshot;       /* host [n_snapshots][P] */
+    dg_emitter_estimate* detections;
+    int64_t detections_capacity;
+    /* filled by the call */
+    int64_t n_detections;
+    int64_t argmax_index;       /* flat index in the FULL lattice (slab row offset applied) */
+    double argmax_value;        /* exact FP64 accumulated value at argmax */
+    int64_t n_refined;          /* elements re-evaluated in FP64 (small |S|) */
+    int64_t n_reranked;         /* near-peak cells re-evaluated in FP64 for the argmax */
+    double sum_overlap_samples; /* sum over (point, step, pair) of N_ov (algorithmic work) */
+    double correlate_ms;        /* profile: summed CUDA-event time of the correlate kernel */
+    int64_t correlate_launches;
+    double total_ms;            /* profile: event time of the whole device pipeline */
+    int64_t kernel_launches;    /* all kernels this call launched */
+} dg_result;
+
+void dg_options_default(dg_options* opt);
+
+/* Host snapshots in, host results out (H2D/D2H inside). */
+int dg_geolocate_snapshots(dg_engine* engine, const dg_grid* grid, const dg_snapshots* snaps,
+                           const dg_options* opt, dg_result* result);
+
+/* Stage a run's captures/states on the device once (H2D + FP32 conversion) … */
+int dg_stage_snapshots(dg_engine* engine, const dg_snapshots* snaps, dg_staged** out);
+/* … and solve with inputs already resident in HBM. */
+int dg_geolocate_staged(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
+                        const dg_options* opt, dg_result* result);
+void dg_staged_destroy(dg_staged* staged);
+
+/* detect_emitters (correlate.hpp:127-201) on a caller-provided surface over a
+ * grid lattice (host or device pointer; is_device selects). */
+int dg_detect_emitters(dg_engine* engine, const dg_grid* grid, const double* values, int is_device,
+                       double k_sigma, int exclusion_radius_cells, dg_emitter_estimate* out,
+                       int64_t capacity, int64_t* n_out);
+
+/* plan_batches (backend.hpp:77-93): same validation/messages; 0 budget means
+ * the reference default (512 MiB). */
+int dg_plan_batches(uint64_t n_points, uint64_t batch_size, uint64_t memory_budget_bytes,
+                    uint64_t capture_bytes_total, uint64_t* batch_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200GEO_H */

@@ -1,0 +1,974 @@
+// C ABI of the B200 direct-geolocation engine (include/b200geo.h).
+//
+// Host orchestration only: validation mirrors the reference's exceptions
+// (messages kept verbatim where the reference has them), every numeric step
+// runs in the kernels of dg_kernels.cu. Reference paths are relative to
+// /root/reference/proj/include/digeo.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <numbers>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "b200geo.h"
+#include "dg_internal.cuh"
+
+using namespace dg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DgError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw DgError{code, msg}; }
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            raise(e_ == cudaErrorMemoryAllocation ? DG_ENOMEM : DG_ERUNTIME,               \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                        \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return DG_OK;
+    } catch (const DgError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return DG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DG_ERUNTIME;
+    }
+}
+
+// owning device allocation (synchronous free; objects that outlive a call)
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    explicit DevMem(size_t n) : bytes(n) {
+        if (n) CK(cudaMalloc(&p, n));
+    }
+    ~DevMem() {
+        if (p) cudaFree(p);
+    }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+};
+
+// stream-ordered scratch for one call
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        CK(cudaMallocAsync(&p, n * sizeof(T), st));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+struct StreamGuard {
+    cudaStream_t st = nullptr;
+    bool own = false;
+    explicit StreamGuard(void* user) {
+        if (user) {
+            st = static_cast<cudaStream_t>(user);
+        } else {
+            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            own = true;
+        }
+    }
+    ~StreamGuard() {
+        if (own) cudaStreamDestroy(st);
+    }
+};
+
+int64_t stride_for(int64_t n) { return (n + 31) & ~int64_t(31); }
+
+// geodesy.hpp:31-38
+constexpr double kA = 6378137.0;
+constexpr double kF = 1.0 / 298.257223563;
+constexpr double kE2 = kF * (2.0 - kF);
+constexpr double kC = 299792458.0;
+inline double deg2rad(double d) { return d * std::numbers::pi / 180.0; }
+
+std::string fmt_double(double v) { return std::to_string(v); }
+
+// GeodeticCoord::validate (geodesy.hpp:69-78)
+void validate_geodetic(double lat, double lon, double alt) {
+    if (!(lat >= -90.0 && lat <= 90.0))
+        raise(DG_EINVAL, "GeodeticCoord: lat_deg out of [-90, 90]: " + fmt_double(lat));
+    if (!(lon >= -180.0 && lon < 180.0))
+        raise(DG_EINVAL, "GeodeticCoord: lon_deg out of [-180, 180): " + fmt_double(lon));
+    if (!std::isfinite(alt)) raise(DG_EINVAL, "GeodeticCoord: alt_m not finite");
+}
+
+}  // namespace
+
+// ===========================================================================
+struct dg_engine {
+    int device = 0;
+    int sm_count = 148;
+};
+
+struct dg_grid {
+    dg_engine* eng = nullptr;
+    double lat_start = 0, lat_step = 0, lon_start = 0, lon_step = 0, alt = 0;
+    int64_t n_lat = 0, n_lon = 0, row_offset = 0;
+    std::shared_ptr<DevMem> mem;  // x | y | z of the full lattice
+    const double *x = nullptr, *y = nullptr, *z = nullptr;
+    int64_t size() const { return n_lat * n_lon; }
+};
+
+struct dg_session {
+    dg_engine* eng = nullptr;
+    int64_t N = 0, stride = 0;
+    double fs = 0;
+    std::unique_ptr<DevMem> y32;  // float2 [2][stride]
+    std::unique_ptr<DevMem> y64;  // double2 [2][stride]
+    cudaStream_t st = nullptr;
+    ~dg_session() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+struct dg_staged {
+    dg_engine* eng = nullptr;
+    int64_t S = 0, R = 0, N = 0, stride = 0;
+    double fs = 0, fc = 0;
+    std::unique_ptr<DevMem> y32, y64;
+    std::vector<dg_state> states;
+};
+
+namespace {
+
+void set_device(const dg_engine* e) { CK(cudaSetDevice(e->device)); }
+
+// ---------------------------------------------------------------------------
+// The per-(snapshot, pair) pipeline shared by correlate_batch, correlate_snapshot
+// and the full driver: offsets -> d-buckets -> warp tasks -> correlator.
+struct Pipeline {
+    int64_t P = 0;
+    int N = 0, nbins = 0, max_tasks = 0;
+    int *d = nullptr, *sorted = nullptr, *hist = nullptr, *off = nullptr, *toff = nullptr,
+        *cursor = nullptr, *n_tasks = nullptr, *err = nullptr;
+    double* fdoa = nullptr;
+    Task* tasks = nullptr;
+    unsigned long long* overlap = nullptr;
+    int64_t launches = 0;
+
+    void init(Scratch& sc, int64_t P_, int64_t N_) {
+        if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
+        if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
+        P = P_;
+        N = (int)N_;
+        nbins = 2 * N - 1;
+        const int64_t mt = P / 32 + std::min<int64_t>(P, nbins) + 1;
+        max_tasks = (int)std::min<int64_t>(mt, INT32_MAX);
+        d = sc.alloc<int>(P);
+        sorted = sc.alloc<int>(P);
+        fdoa = sc.alloc<double>(P);
+        tasks = sc.alloc<Task>(max_tasks);
+        hist = sc.alloc<int>(nbins);
+        off = sc.alloc<int>(nbins);
+        toff = sc.alloc<int>(nbins);
+        cursor = sc.alloc<int>(nbins);
+        n_tasks = sc.alloc<int>(1);
+        err = sc.alloc<int>(1);
+        overlap = sc.alloc<unsigned long long>(1);
+        CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins, sc.st));
+        CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
+        CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
+    }
+
+    void bucket_and_correlate(const float2* y1, const float2* y2, double fs, double* s_out,
+                              uint32_t* bits, int64_t flag_base, cudaStream_t st,
+                              cudaEvent_t ev0, cudaEvent_t ev1) {
+        launch_bucket(hist, nbins, N, off, toff, cursor, n_tasks, d, P, sorted, tasks, st);
+        if (ev0) CK(cudaEventRecord(ev0, st));
+        launch_correlate(tasks, n_tasks, max_tasks, sorted, fdoa, y1, y2, N, fs, s_out, bits,
+                         flag_base, st);
+        if (ev1) CK(cudaEventRecord(ev1, st));
+        launches += 4;
+    }
+};
+
+// compact the refine bitmap and re-evaluate flagged elements exactly
+int64_t run_refine(Scratch& sc, const uint32_t* bits, int64_t n_elems, const RefineCtx& ctx,
+                   int64_t* launches) {
+    const int64_t n_words = (n_elems + 31) / 32;
+    auto* cnt = sc.alloc<unsigned long long>(2);
+    CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), sc.st));
+    launch_count_flags(bits, n_words, cnt, sc.st);
+    unsigned long long n = 0;
+    CK(cudaMemcpyAsync(&n, cnt, sizeof n, cudaMemcpyDeviceToHost, sc.st));
+    CK(cudaStreamSynchronize(sc.st));
+    *launches += 1;
+    if (n == 0) return 0;
+    auto* list = sc.alloc<int64_t>(n);
+    launch_compact_flags(bits, n_words, list, cnt + 1, sc.st);
+    launch_refine(list, (int64_t)n, ctx, sc.st);
+    *launches += 2;
+    return (int64_t)n;
+}
+
+void check_err_flag(Scratch& sc, const int* err) {
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, err, sizeof h, cudaMemcpyDeviceToHost, sc.st));
+    CK(cudaStreamSynchronize(sc.st));
+    if (h) raise(DG_EINVAL, "predict_geometry: candidate coincides with receiver");
+}
+
+std::unique_ptr<dg_session> make_session(dg_engine* eng, int64_t n1, double fs1, int64_t n2,
+                                         double fs2) {
+    // check_pair (backend.hpp:221-228) via BasebandCapture::validate (capture.hpp:42-46)
+    if (n1 <= 0 || n2 <= 0) raise(DG_EINVAL, "BasebandCapture: no samples");
+    if (!(fs1 > 0.0) || !(fs2 > 0.0)) raise(DG_EINVAL, "BasebandCapture: sample_rate_hz <= 0");
+    if (fs1 != fs2) raise(DG_EINVAL, "backend stage: sample rates differ");
+    if (n1 != n2) raise(DG_EINVAL, "backend stage: sample counts differ");
+    set_device(eng);
+    auto s = std::make_unique<dg_session>();
+    s->eng = eng;
+    s->N = n1;
+    s->stride = stride_for(n1);
+    s->fs = fs1;
+    s->y32 = std::make_unique<DevMem>(2 * s->stride * sizeof(float2));
+    s->y64 = std::make_unique<DevMem>(2 * s->stride * sizeof(double2));
+    CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    return s;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+int dg_abi_version(void) { return DG_ABI_VERSION; }
+
+void dg_options_default(dg_options* o) {
+    std::memset(o, 0, sizeof *o);
+    o->k_sigma = 5.0;
+    o->exclusion_radius_cells = 5;
+    o->detect = 1;
+}
+
+int dg_engine_create(int device, dg_engine** out) {
+    return guard([&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n)
+            raise(DG_EINVAL, "dg_engine_create: device " + std::to_string(device) +
+                                 " out of range (" + std::to_string(n) + " visible)");
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            raise(DG_ERUNTIME, std::string("b200: sm_100a build cannot run on ") + prop.name);
+        auto e = std::make_unique<dg_engine>();
+        e->device = device;
+        e->sm_count = prop.multiProcessorCount;
+        *out = e.release();
+    });
+}
+
+void dg_engine_destroy(dg_engine* e) { delete e; }
+
+int dg_engine_descriptor(const dg_engine* e, char* name, size_t nl, char* kind, size_t kl,
+                         unsigned* workers) {
+    return guard([&] {
+        if (!e) raise(DG_EINVAL, "null engine");
+        if (name && nl) std::snprintf(name, nl, "%s", "b200");
+        if (kind && kl) std::snprintf(kind, kl, "%s", "parallel-batched");
+        if (workers) *workers = 1;
+    });
+}
+
+// ---- sessions --------------------------------------------------------------
+int dg_stage(dg_engine* eng, const double* y1, int64_t n1, double fs1, const double* y2, int64_t n2,
+             double fs2, dg_session** out) {
+    return guard([&] {
+        auto s = make_session(eng, n1, fs1, n2, fs2);
+        auto* y64 = static_cast<double2*>(s->y64->p);
+        auto* y32 = static_cast<float2*>(s->y32->p);
+        CK(cudaMemcpyAsync(y64, y1, n1 * sizeof(double2), cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemcpyAsync(y64 + s->stride, y2, n1 * sizeof(double2), cudaMemcpyHostToDevice, s->st));
+        launch_f64_to_f32(y64, y32, n1, s->st);
+        launch_f64_to_f32(y64 + s->stride, y32 + s->stride, n1, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        *out = s.release();
+    });
+}
+
+int dg_stage_f32(dg_engine* eng, const float* y1, int64_t n1, double fs1, const float* y2,
+                 int64_t n2, double fs2, dg_session** out) {
+    return guard([&] {
+        auto s = make_session(eng, n1, fs1, n2, fs2);
+        auto* y64 = static_cast<double2*>(s->y64->p);
+        auto* y32 = static_cast<float2*>(s->y32->p);
+        CK(cudaMemcpyAsync(y32, y1, n1 * sizeof(float2), cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemcpyAsync(y32 + s->stride, y2, n1 * sizeof(float2), cudaMemcpyHostToDevice, s->st));
+        launch_f32_to_f64(y32, y64, n1, s->st);
+        launch_f32_to_f64(y32 + s->stride, y64 + s->stride, n1, s->st);
+        CK(cudaStreamSynchronize(s->st));
+        *out = s.release();
+    });
+}
+
+void dg_session_destroy(dg_session* s) { delete s; }
+
+int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, double* out,
+                       int64_t n_out) {
+    return guard([&] {
+        if (!s) raise(DG_EINVAL, "null session");
+        // SerialSession::correlate_batch (backend.hpp:235-242)
+        if (n <= 0 || !batch) raise(DG_EINVAL, "correlate_batch: empty batch");
+        if (n_out != n) raise(DG_EINVAL, "correlate_batch: output size mismatch");
+        set_device(s->eng);
+        Scratch sc(s->st);
+        Pipeline pl;
+        pl.init(sc, n, s->N);
+        auto* off = sc.alloc<dg_pair_offsets>(n);
+        auto* vals = sc.alloc<double>(n);
+        const int64_t n_words = (n + 31) / 32;
+        auto* bits = sc.alloc<uint32_t>(n_words);
+        CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
+        CK(cudaMemcpyAsync(off, batch, n * sizeof(dg_pair_offsets), cudaMemcpyHostToDevice, s->st));
+        launch_offsets_hist(off, n, pl.N, pl.d, pl.fdoa, pl.hist, vals, pl.overlap, s->st);
+        const auto* y32 = static_cast<const float2*>(s->y32->p);
+        pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr, nullptr);
+        RefineCtx ctx{};
+        ctx.P = n;
+        ctx.offsets = off;
+        ctx.y64 = static_cast<const double2*>(s->y64->p);
+        ctx.stride = s->stride;
+        ctx.N = (int)s->N;
+        ctx.fs = s->fs;
+        ctx.raw = vals;
+        int64_t launches = 0;
+        run_refine(sc, bits, n, ctx, &launches);
+        CK(cudaMemcpyAsync(out, vals, n * sizeof(double), cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+    });
+}
+
+// ---- grids -----------------------------------------------------------------
+int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double spacing, double alt,
+                            uint64_t cap, dg_grid** out) {
+    return guard([&] {
+        if (!eng || !b) raise(DG_EINVAL, "null argument");
+        if (cap == 0) cap = 20'000'000;  // default_grid_point_cap (geodesy.hpp:170)
+        // LatLonBounds::validate (geodesy.hpp:132-137) — lon_max is not range-checked there
+        validate_geodetic(b->lat_min_deg, b->lon_min_deg, 0.0);
+        validate_geodetic(b->lat_max_deg, b->lon_min_deg, 0.0);
+        if (b->lat_max_deg < b->lat_min_deg || b->lon_max_deg < b->lon_min_deg)
+            raise(DG_EINVAL, "LatLonBounds: max < min");
+        if (!(spacing > 0.0)) raise(DG_EINVAL, "build_candidate_grid: spacing_deg <= 0");
+        if (!std::isfinite(alt)) raise(DG_EINVAL, "build_candidate_grid: altitude_m not finite");
+        auto axis_count = [](double span, double step) {  // geodesy.hpp:175-177
+            return static_cast<int64_t>(std::floor(span / step + 1e-6)) + 1;
+        };
+        const int64_t n_lat = axis_count(b->lat_max_deg - b->lat_min_deg, spacing);
+        const int64_t n_lon = axis_count(b->lon_max_deg - b->lon_min_deg, spacing);
+        const int64_t n = n_lat * n_lon;
+        if ((uint64_t)n > cap)
+            raise(DG_EINVAL, "build_candidate_grid: " + std::to_string(n) +
+                                 " points exceed cap of " + std::to_string(cap));
+        // per-row / per-column libm trig, validated in the reference's loop order
+        std::vector<double> ra(n_lat), rz(n_lat), cc(n_lon), cs(n_lon);
+        for (int64_t i = 0; i < n_lat; ++i) {
+            const double lat_deg = b->lat_min_deg + static_cast<double>(i) * spacing;
+            if (!(lat_deg >= -90.0 && lat_deg <= 90.0))
+                raise(DG_EINVAL, "GeodeticCoord: lat_deg out of [-90, 90]: " + fmt_double(lat_deg));
+            if (i == 0)
+                for (int64_t j = 0; j < n_lon; ++j) {
+                    const double lon_deg = b->lon_min_deg + static_cast<double>(j) * spacing;
+                    validate_geodetic(lat_deg, lon_deg, alt);
+                }
+            // lla_to_ecef (geodesy.hpp:82-92), the lat-dependent factors
+            const double lat = deg2rad(lat_deg);
+            const double slat = std::sin(lat), clat = std::cos(lat);
+            const double nn = kA / std::sqrt(1.0 - kE2 * slat * slat);
+            ra[i] = (nn + alt) * clat;
+            rz[i] = (nn * (1.0 - kE2) + alt) * slat;
+        }
+        for (int64_t j = 0; j < n_lon; ++j) {
+            const double lon = deg2rad(b->lon_min_deg + static_cast<double>(j) * spacing);
+            cc[j] = std::cos(lon);
+            cs[j] = std::sin(lon);
+        }
+        set_device(eng);
+        auto g = std::make_unique<dg_grid>();
+        g->eng = eng;
+        g->lat_start = b->lat_min_deg;
+        g->lon_start = b->lon_min_deg;
+        g->lat_step = g->lon_step = spacing;
+        g->alt = alt;
+        g->n_lat = n_lat;
+        g->n_lon = n_lon;
+        g->mem = std::make_shared<DevMem>(3 * n * sizeof(double));
+        double* base = static_cast<double*>(g->mem->p);
+        g->x = base;
+        g->y = base + n;
+        g->z = base + 2 * n;
+        StreamGuard sg(nullptr);
+        Scratch sc(sg.st);
+        double* t = sc.alloc<double>(2 * n_lat + 2 * n_lon);
+        CK(cudaMemcpyAsync(t, ra.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
+        CK(cudaMemcpyAsync(t + n_lat, rz.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
+        CK(cudaMemcpyAsync(t + 2 * n_lat, cc.data(), n_lon * 8, cudaMemcpyHostToDevice, sg.st));
+        CK(cudaMemcpyAsync(t + 2 * n_lat + n_lon, cs.data(), n_lon * 8, cudaMemcpyHostToDevice,
+                           sg.st));
+        launch_grid_ecef(t, t + n_lat, t + 2 * n_lat, t + 2 * n_lat + n_lon, n_lat, n_lon, base,
+                         base + n, base + 2 * n, sg.st);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(sg.st));
+        *out = g.release();
+    });
+}
+
+int dg_grid_slab(const dg_grid* g, int64_t r0, int64_t r1, dg_grid** out) {
+    return guard([&] {
+        if (!g) raise(DG_EINVAL, "null grid");
+        if (r0 < 0 || r1 > g->n_lat || r0 > r1) raise(DG_EINVAL, "dg_grid_slab: bad row range");
+        auto s = std::make_unique<dg_grid>(*g);
+        s->n_lat = r1 - r0;
+        s->row_offset = g->row_offset + r0;
+        s->x = g->x + r0 * g->n_lon;
+        s->y = g->y + r0 * g->n_lon;
+        s->z = g->z + r0 * g->n_lon;
+        *out = s.release();
+    });
+}
+
+int dg_grid_from_points(dg_engine* eng, const dg_ecef* pts, int64_t n, double lat_start,
+                        double lat_step, int64_t n_lat, double lon_start, double lon_step,
+                        int64_t n_lon, double alt, dg_grid** out) {
+    return guard([&] {
+        if (!eng || !pts || n <= 0) raise(DG_EINVAL, "correlate_snapshot: empty grid");
+        if (n_lat * n_lon != n) raise(DG_EINVAL, "dg_grid_from_points: n_lat*n_lon != n_points");
+        set_device(eng);
+        auto g = std::make_unique<dg_grid>();
+        g->eng = eng;
+        g->lat_start = lat_start;
+        g->lat_step = lat_step;
+        g->lon_start = lon_start;
+        g->lon_step = lon_step;
+        g->n_lat = n_lat;
+        g->n_lon = n_lon;
+        g->alt = alt;
+        std::vector<double> soa(3 * n);
+        for (int64_t i = 0; i < n; ++i) {
+            soa[i] = pts[i].x;
+            soa[n + i] = pts[i].y;
+            soa[2 * n + i] = pts[i].z;
+        }
+        g->mem = std::make_shared<DevMem>(3 * n * sizeof(double));
+        double* base = static_cast<double*>(g->mem->p);
+        CK(cudaMemcpy(base, soa.data(), 3 * n * sizeof(double), cudaMemcpyHostToDevice));
+        g->x = base;
+        g->y = base + n;
+        g->z = base + 2 * n;
+        *out = g.release();
+    });
+}
+
+int dg_grid_info(const dg_grid* g, double* lat_start, double* lat_step, int64_t* n_lat,
+                 double* lon_start, double* lon_step, int64_t* n_lon, double* alt,
+                 int64_t* row_offset) {
+    return guard([&] {
+        if (!g) raise(DG_EINVAL, "null grid");
+        if (lat_start) *lat_start = g->lat_start;
+        if (lat_step) *lat_step = g->lat_step;
+        if (n_lat) *n_lat = g->n_lat;
+        if (lon_start) *lon_start = g->lon_start;
+        if (lon_step) *lon_step = g->lon_step;
+        if (n_lon) *n_lon = g->n_lon;
+        if (alt) *alt = g->alt;
+        if (row_offset) *row_offset = g->row_offset;
+    });
+}
+
+int dg_grid_points(const dg_grid* g, dg_ecef* out) {
+    return guard([&] {
+        if (!g) raise(DG_EINVAL, "null grid");
+        set_device(g->eng);
+        const int64_t n = g->size();
+        std::vector<double> soa(3 * n);
+        CK(cudaMemcpy(soa.data(), g->x, n * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(soa.data() + n, g->y, n * 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(soa.data() + 2 * n, g->z, n * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) out[i] = dg_ecef{soa[i], soa[n + i], soa[2 * n + i]};
+    });
+}
+
+void dg_grid_destroy(dg_grid* g) { delete g; }
+
+int dg_predict_offsets(dg_engine* eng, const dg_grid* g, const dg_state* rx_i, const dg_state* rx_j,
+                       double fs, double wl, dg_pair_offsets* out) {
+    return guard([&] {
+        if (!eng || !g || !rx_i || !rx_j || !out) raise(DG_EINVAL, "null argument");
+        set_device(eng);
+        StreamGuard sg(nullptr);
+        Scratch sc(sg.st);
+        const int64_t P = g->size();
+        auto* pg = sc.alloc<PairGeom>(1);
+        auto* err = sc.alloc<int>(1);
+        auto* o = sc.alloc<dg_pair_offsets>(P);
+        const PairGeom h{*rx_i, *rx_j};
+        CK(cudaMemcpyAsync(pg, &h, sizeof h, cudaMemcpyHostToDevice, sg.st));
+        CK(cudaMemsetAsync(err, 0, sizeof(int), sg.st));
+        launch_predict_offsets(g->x, g->y, g->z, P, pg, fs, wl, o, err, sg.st);
+        check_err_flag(sc, err);
+        CK(cudaMemcpyAsync(out, o, P * sizeof(dg_pair_offsets), cudaMemcpyDeviceToHost, sg.st));
+        CK(cudaStreamSynchronize(sg.st));
+    });
+}
+
+
+int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
+                          const dg_state* rx_j, double fc, double* out) {
+    return guard([&] {
+        if (!s || !g || !rx_i || !rx_j || !out) raise(DG_EINVAL, "null argument");
+        if (g->size() == 0) raise(DG_EINVAL, "correlate_snapshot: empty grid");
+        if (!(fc > 0.0)) raise(DG_EINVAL, "wavelength_m: center_freq_hz <= 0");
+        const double wl = kC / fc;  // wavelength_m (geometry.hpp:36-39)
+        set_device(s->eng);
+        Scratch sc(s->st);
+        const int64_t P = g->size();
+        Pipeline pl;
+        pl.init(sc, P, s->N);
+        auto* pg = sc.alloc<PairGeom>(1);
+        auto* vals = sc.alloc<double>(P);
+        const int64_t n_words = (P + 31) / 32;
+        auto* bits = sc.alloc<uint32_t>(n_words);
+        const PairGeom h{*rx_i, *rx_j};
+        CK(cudaMemcpyAsync(pg, &h, sizeof h, cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
+        launch_geometry_hist(g->x, g->y, g->z, P, pg, s->fs, wl, pl.N, pl.d, pl.fdoa, pl.hist, vals,
+                             pl.overlap, pl.err, s->st);
+        const auto* y32 = static_cast<const float2*>(s->y32->p);
+        pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr,
+                                nullptr);
+        check_err_flag(sc, pl.err);
+        static const int pair_rx[2] = {0, 1};
+        auto* prx = sc.alloc<int>(2);
+        CK(cudaMemcpyAsync(prx, pair_rx, sizeof pair_rx, cudaMemcpyHostToDevice, s->st));
+        RefineCtx ctx{};
+        ctx.x = g->x;
+        ctx.y = g->y;
+        ctx.z = g->z;
+        ctx.P = P;
+        ctx.pg = pg;
+        ctx.pair_rx = prx;
+        ctx.pairs = 1;
+        ctx.R = 2;
+        ctx.y64 = static_cast<const double2*>(s->y64->p);
+        ctx.stride = s->stride;
+        ctx.N = (int)s->N;
+        ctx.fs = s->fs;
+        ctx.wl = wl;
+        ctx.raw = vals;
+        int64_t launches = 0;
+        run_refine(sc, bits, P, ctx, &launches);
+        CK(cudaMemcpyAsync(out, vals, P * sizeof(double), cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+    });
+}
+
+// ---- staged snapshots --------------------------------------------------------
+namespace {
+
+void validate_snapshots(const dg_snapshots* sn) {
+    if (!sn) raise(DG_EINVAL, "null snapshots");
+    if (sn->n_snapshots < 1) raise(DG_EINVAL, "geolocate_snapshots: no snapshots");
+    if (sn->n_receivers < 2) raise(DG_EINVAL, "correlate_snapshot_all_pairs: need >= 2 receivers");
+    if (sn->n_samples < 1) raise(DG_EINVAL, "BasebandCapture: no samples");
+    if (!(sn->sample_rate_hz > 0.0)) raise(DG_EINVAL, "BasebandCapture: sample_rate_hz <= 0");
+    if (!(sn->center_freq_hz > 0.0)) raise(DG_EINVAL, "wavelength_m: center_freq_hz <= 0");
+    if (!sn->states) raise(DG_EINVAL, "null receiver states");
+    if (!sn->captures_iq && !sn->captures_f32) raise(DG_EINVAL, "null captures");
+}
+
+}  // namespace
+
+int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) {
+    return guard([&] {
+        if (!eng) raise(DG_EINVAL, "null engine");
+        validate_snapshots(sn);
+        set_device(eng);
+        auto s = std::make_unique<dg_staged>();
+        s->eng = eng;
+        s->S = sn->n_snapshots;
+        s->R = sn->n_receivers;
+        s->N = sn->n_samples;
+        s->stride = stride_for(s->N);
+        s->fs = sn->sample_rate_hz;
+        s->fc = sn->center_freq_hz;
+        s->states.assign(sn->states, sn->states + s->S * s->R);
+        const int64_t n_caps = s->S * s->R;
+        s->y32 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(float2));
+        s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
+        auto* y32 = static_cast<float2*>(s->y32->p);
+        auto* y64 = static_cast<double2*>(s->y64->p);
+        StreamGuard sg(nullptr);
+        for (int64_t c = 0; c < n_caps; ++c) {
+            if (sn->captures_iq) {
+                if (!sn->captures_iq[c]) raise(DG_EINVAL, "null capture pointer");
+                CK(cudaMemcpyAsync(y64 + c * s->stride, sn->captures_iq[c], s->N * sizeof(double2),
+                                   cudaMemcpyHostToDevice, sg.st));
+                launch_f64_to_f32(y64 + c * s->stride, y32 + c * s->stride, s->N, sg.st);
+            } else {
+                if (!sn->captures_f32[c]) raise(DG_EINVAL, "null capture pointer");
+                CK(cudaMemcpyAsync(y32 + c * s->stride, sn->captures_f32[c], s->N * sizeof(float2),
+                                   cudaMemcpyHostToDevice, sg.st));
+                launch_f32_to_f64(y32 + c * s->stride, y64 + c * s->stride, s->N, sg.st);
+            }
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(sg.st));
+        *out = s.release();
+    });
+}
+
+void dg_staged_destroy(dg_staged* s) { delete s; }
+
+// ---- the driver --------------------------------------------------------------
+namespace {
+
+constexpr int kDetCap = 8192;
+constexpr int kRerankCap = 1024;
+
+void run_detect(const dg_grid* g, const double* v_dev, double k_sigma, int radius,
+                dg_emitter_estimate* out, int64_t capacity, int64_t* n_out, Scratch& sc,
+                int64_t* launches) {
+    // detect_emitters (correlate.hpp:127-201)
+    if (radius < 0) raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
+    const int64_t P = g->size();
+    const int n_part = 148 * 4;
+    auto* part = sc.alloc<double>(n_part);
+    auto* stats = sc.alloc<double>(3);
+    auto* cands = sc.alloc<DetCand>(kDetCap);
+    auto* n_c = sc.alloc<int>(2);
+    auto* dets = sc.alloc<dg_emitter_estimate>(kDetCap);
+    CK(cudaMemsetAsync(n_c, 0, 2 * sizeof(int), sc.st));
+    launch_mean_var(v_dev, P, part, n_part, stats, sc.st);
+    launch_local_max(v_dev, g->n_lat, g->n_lon, stats, k_sigma, cands, n_c, kDetCap, sc.st);
+    int hc = 0;
+    CK(cudaMemcpyAsync(&hc, n_c, sizeof hc, cudaMemcpyDeviceToHost, sc.st));
+    CK(cudaStreamSynchronize(sc.st));
+    *launches += 6;
+    if (hc > kDetCap)
+        raise(DG_ERUNTIME, "detect_emitters: " + std::to_string(hc) +
+                               " local maxima above threshold exceed the device list of " +
+                               std::to_string(kDetCap));
+    if (hc == 0) {
+        *n_out = 0;
+        return;
+    }
+    launch_greedy(cands, n_c, kDetCap, radius, stats, g->n_lon, dets, n_c + 1, sc.st);
+    CK(cudaGetLastError());
+    *launches += 1;
+    int nd = 0;
+    CK(cudaMemcpyAsync(&nd, n_c + 1, sizeof nd, cudaMemcpyDeviceToHost, sc.st));
+    CK(cudaStreamSynchronize(sc.st));
+    *n_out = nd;
+    if (out && capacity > 0) {
+        const int64_t m = std::min<int64_t>(nd, capacity);
+        CK(cudaMemcpyAsync(out, dets, m * sizeof(dg_emitter_estimate), cudaMemcpyDeviceToHost,
+                           sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+        for (int64_t i = 0; i < m; ++i) {
+            // lattice_coord (geodesy.hpp:160-162) with GridAxis::value (:145)
+            const int64_t ilat = (int64_t)out[i].lat_deg + g->row_offset;
+            const int64_t ilon = (int64_t)out[i].lon_deg;
+            out[i].lat_deg = g->lat_start + static_cast<double>(ilat) * g->lat_step;
+            out[i].lon_deg = g->lon_start + static_cast<double>(ilon) * g->lon_step;
+            out[i].alt_m = g->alt;
+            out[i].grid_index = ilat * g->n_lon + ilon;
+        }
+    }
+}
+
+void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt_in,
+                    dg_result* res) {
+    if (!eng || !g || !sn || !res) raise(DG_EINVAL, "null argument");
+    dg_options opt;
+    if (opt_in) {
+        opt = *opt_in;
+    } else {
+        dg_options_default(&opt);
+    }
+    const int64_t P = g->size();
+    if (P == 0) raise(DG_EINVAL, "correlate_snapshot: empty grid");
+    if (opt.exclusion_radius_cells < 0)
+        raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
+    set_device(eng);
+    const int S = (int)sn->S, R = (int)sn->R;
+    const int pairs = R * (R - 1) / 2;
+    const int SP = S * pairs;
+    const double fs = sn->fs, wl = kC / sn->fc;
+    StreamGuard sg(opt.stream);
+    cudaStream_t st = sg.st;
+    Scratch sc(st);
+    int64_t launches = 0;
+
+    cudaEvent_t ev_all0 = nullptr, ev_all1 = nullptr;
+    std::vector<cudaEvent_t> evs;
+    if (opt.profile) {
+        CK(cudaEventCreate(&ev_all0));
+        CK(cudaEventCreate(&ev_all1));
+        evs.resize(2 * SP);
+        for (auto& e : evs) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ev_all0, st));
+    }
+    struct EvFree {
+        std::vector<cudaEvent_t>* v;
+        cudaEvent_t a, b;
+        ~EvFree() {
+            for (auto e : *v) cudaEventDestroy(e);
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } ev_free{&evs, ev_all0, ev_all1};
+
+    // pair table and per-(snapshot, pair) receiver states
+    std::vector<int> prx;
+    for (int i = 0; i < R; ++i)
+        for (int j = i + 1; j < R; ++j) {
+            prx.push_back(i);
+            prx.push_back(j);
+        }
+    std::vector<PairGeom> hpg(SP);
+    for (int s = 0; s < S; ++s)
+        for (int q = 0; q < pairs; ++q)
+            hpg[s * pairs + q] = PairGeom{sn->states[s * R + prx[2 * q]], sn->states[s * R + prx[2 * q + 1]]};
+    auto* pg = sc.alloc<PairGeom>(SP);
+    auto* d_prx = sc.alloc<int>(prx.size());
+    CK(cudaMemcpyAsync(pg, hpg.data(), SP * sizeof(PairGeom), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_prx, prx.data(), prx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+
+    Pipeline pl;
+    pl.init(sc, P, sn->N);
+    const int64_t n_elems = (int64_t)SP * P;
+    auto* raw = sc.alloc<double>(n_elems);
+    const int64_t n_words = (n_elems + 31) / 32;
+    auto* bits = sc.alloc<uint32_t>(n_words);
+    CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
+    const auto* y32 = static_cast<const float2*>(sn->y32->p);
+
+    for (int s = 0; s < S; ++s)
+        for (int q = 0; q < pairs; ++q) {
+            const int sp = s * pairs + q;
+            double* out = raw + (int64_t)sp * P;
+            launch_geometry_hist(g->x, g->y, g->z, P, pg + sp, fs, wl, pl.N, pl.d, pl.fdoa, pl.hist,
+                                 out, pl.overlap, pl.err, st);
+            const float2* y1 = y32 + ((int64_t)s * R + prx[2 * q]) * sn->stride;
+            const float2* y2 = y32 + ((int64_t)s * R + prx[2 * q + 1]) * sn->stride;
+            pl.bucket_and_correlate(y1, y2, fs, out, bits, (int64_t)sp * P, st,
+                                    opt.profile ? evs[2 * sp] : nullptr,
+                                    opt.profile ? evs[2 * sp + 1] : nullptr);
+            launches += 1;
+        }
+    CK(cudaGetLastError());
+    check_err_flag(sc, pl.err);
+
+    RefineCtx ctx{};
+    ctx.x = g->x;
+    ctx.y = g->y;
+    ctx.z = g->z;
+    ctx.P = P;
+    ctx.pg = pg;
+    ctx.pair_rx = d_prx;
+    ctx.pairs = pairs;
+    ctx.R = R;
+    ctx.y64 = static_cast<const double2*>(sn->y64->p);
+    ctx.stride = sn->stride;
+    ctx.N = (int)sn->N;
+    ctx.fs = fs;
+    ctx.wl = wl;
+    ctx.raw = raw;
+    res->n_refined = run_refine(sc, bits, n_elems, ctx, &launches);
+
+    // per-snapshot grids: pair sums (correlate_snapshot_all_pairs), optional median scaling
+    double* grids = raw;
+    if (pairs > 1) {
+        grids = sc.alloc<double>((int64_t)S * P);
+        launch_combine_pairs(raw, S, pairs, P, grids, st);
+        launches += 1;
+    }
+    double* medians = nullptr;
+    if (opt.normalize_per_snapshot) {
+        medians = sc.alloc<double>(S);
+        auto* hist = sc.alloc<unsigned>(256);
+        auto* state = sc.alloc<unsigned long long>(2);
+        CK(cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned), st));
+        for (int s = 0; s < S; ++s) {
+            const unsigned long long init[2] = {0ull, (unsigned long long)(P / 2)};
+            CK(cudaMemcpyAsync(state, init, sizeof init, cudaMemcpyHostToDevice, st));
+            launch_median(grids + (int64_t)s * P, P, hist, state, medians + s, st);
+            launch_scale(grids + (int64_t)s * P, P, medians + s, st);
+            CK(cudaStreamSynchronize(st));  // `init` lives on the host stack
+            launches += 17;
+        }
+    }
+    double* acc = opt_in && res->accumulated_device ? res->accumulated_device : sc.alloc<double>(P);
+    launch_accumulate(grids, S, P, acc, st);
+    launches += 1;
+
+    // peak: FP64 max over the surface, then exact re-rank of every cell within
+    // a relative band of it (covers the FP32 error), lowest index on ties.
+    const int n_part = 148 * 4;
+    auto* part = sc.alloc<double>(n_part);
+    auto* vmax = sc.alloc<double>(1);
+    auto* cells = sc.alloc<int>(kRerankCap);
+    auto* n_cells = sc.alloc<int>(1);
+    auto* best_i = sc.alloc<long long>(1);
+    auto* best_v = sc.alloc<double>(1);
+    launch_max(acc, P, part, n_part, vmax, st);
+    launches += 2;
+    double hmax = 0.0;
+    CK(cudaMemcpyAsync(&hmax, vmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int hn = 0;
+    if (hmax > 0.0) {
+        for (double rel = 1e-5;; rel *= 0.1) {
+            CK(cudaMemsetAsync(n_cells, 0, sizeof(int), st));
+            launch_select_near(acc, P, vmax, rel, cells, n_cells, kRerankCap, st);
+            launches += 1;
+            CK(cudaMemcpyAsync(&hn, n_cells, sizeof hn, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (hn <= kRerankCap || rel < 1e-12) break;
+        }
+        launch_rerank(cells, n_cells, kRerankCap, SP, ctx, st);
+        launch_recombine_cells(cells, n_cells, kRerankCap, raw, S, pairs, P,
+                               pairs > 1 ? grids : nullptr, medians, acc, st);
+        launch_argmax_cells(cells, n_cells, kRerankCap, acc, best_i, best_v, st);
+        launches += 3;
+        long long bi = 0;
+        double bv = 0.0;
+        CK(cudaMemcpyAsync(&bi, best_i, sizeof bi, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&bv, best_v, sizeof bv, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        res->argmax_index = bi + g->row_offset * g->n_lon;
+        res->argmax_value = bv;
+    } else {
+        // all-zero surface (no overlap / silent captures): first index wins
+        res->argmax_index = g->row_offset * g->n_lon;
+        res->argmax_value = hmax;
+    }
+    res->n_reranked = std::min(hn, kRerankCap);
+    if (opt.profile) CK(cudaEventRecord(ev_all1, st));
+
+    res->n_detections = 0;
+    if (opt.detect)
+        run_detect(g, acc, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
+                   res->detections_capacity, &res->n_detections, sc, &launches);
+
+    if (res->accumulated)
+        CK(cudaMemcpyAsync(res->accumulated, acc, P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (res->per_snapshot)
+        CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+    unsigned long long ovl = 0;
+    CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    res->sum_overlap_samples = (double)ovl;
+    res->kernel_launches = launches;
+    res->correlate_launches = SP;
+    if (opt.profile) {
+        double tot = 0.0;
+        for (int i = 0; i < SP; ++i) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, evs[2 * i], evs[2 * i + 1]));
+            tot += ms;
+        }
+        res->correlate_ms = tot;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev_all0, ev_all1));
+        res->total_ms = ms;
+    }
+}
+
+}  // namespace
+
+int dg_geolocate_staged(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt,
+                        dg_result* res) {
+    return guard([&] { geolocate_impl(eng, g, sn, opt, res); });
+}
+
+int dg_geolocate_snapshots(dg_engine* eng, const dg_grid* g, const dg_snapshots* sn,
+                           const dg_options* opt, dg_result* res) {
+    return guard([&] {
+        dg_staged* staged = nullptr;
+        const int rc = dg_stage_snapshots(eng, sn, &staged);
+        if (rc != DG_OK) raise(rc, g_err);
+        std::unique_ptr<dg_staged> hold(staged);
+        geolocate_impl(eng, g, staged, opt, res);
+    });
+}
+
+int dg_detect_emitters(dg_engine* eng, const dg_grid* g, const double* values, int is_device,
+                       double k_sigma, int radius, dg_emitter_estimate* out, int64_t capacity,
+                       int64_t* n_out) {
+    return guard([&] {
+        if (!eng || !g || !values || !n_out) raise(DG_EINVAL, "null argument");
+        if (radius < 0) raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
+        set_device(eng);
+        StreamGuard sg(nullptr);
+        Scratch sc(sg.st);
+        const int64_t P = g->size();
+        const double* v = values;
+        if (!is_device) {
+            double* dv = sc.alloc<double>(P);
+            CK(cudaMemcpyAsync(dv, values, P * sizeof(double), cudaMemcpyHostToDevice, sg.st));
+            v = dv;
+        }
+        int64_t launches = 0;
+        run_detect(g, v, k_sigma, radius, out, capacity, n_out, sc, &launches);
+    });
+}
+
+int dg_plan_batches(uint64_t n_points, uint64_t batch_size, uint64_t budget, uint64_t capture_bytes,
+                    uint64_t* batch_count) {
+    // plan_batches (backend.hpp:77-93), messages verbatim
+    return guard([&] {
+        if (budget == 0) budget = 512ull << 20;
+        if (n_points < 1) raise(DG_EINVAL, "plan_batches: n_points < 1");
+        if (batch_size < 1) raise(DG_EINVAL, "plan_batches: batch_size < 1");
+        if (capture_bytes > budget)
+            raise(DG_EINVAL, "plan_batches: staged captures (" + std::to_string(capture_bytes) +
+                                 " bytes) exceed the memory budget of " + std::to_string(budget));
+        const uint64_t ws = batch_size * 24ull + capture_bytes;  // sizeof(PairOffsets)+sizeof(double)
+        if (ws > budget)
+            raise(DG_EINVAL, "plan_batches: batch working set (" + std::to_string(ws) +
+                                 " bytes at batch_size " + std::to_string(batch_size) +
+                                 ") exceeds the memory budget of " + std::to_string(budget));
+        if (batch_count) *batch_count = (n_points + batch_size - 1) / batch_size;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// Internal declarations shared by the kernels (dg_kernels.cu) and the C ABI
+// layer (dg_capi.cu). Not installed; the public boundary is include/b200geo.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "b200geo.h"
+
+namespace dg {
+
+// One warp-task of the correlator: up to 32 candidates that share one integer
+// TDOA d (so one z_d[k] = y1[k] conj(y2[k+d]) stream and one overlap range).
+struct Task {
+    int d;      // tdoa_samples
+    int start;  // offset into the d-sorted candidate list
+    int count;  // 1..32 lanes live
+    int pad;
+};
+
+// Geometry of one (snapshot, pair): receiver states for predict_pair_offsets.
+struct PairGeom {
+    dg_state rx_i, rx_j;
+};
+
+// Per-element flag: FP32 result too close to zero for the relative tolerance;
+// re-evaluated in FP64 in the reference's exact operation order.
+constexpr int kWarpsPerCta = 8;
+constexpr int kChunk = 256;  // samples per z-chunk (per warp, smem-staged)
+constexpr int kL = 16;       // phasor table length (samples per inner block)
+
+// Threshold on S / sqrt(sum |z|^2) below which an FP32 value is re-evaluated
+// exactly; see DESIGN.md "Parity" for the error model behind it.
+constexpr float kRefineTau = 0.02f;
+
+// --------------------------------------------------------------------------
+// launchers (dg_kernels.cu). All asynchronous on `st`.
+void launch_grid_ecef(const double* row_a, const double* row_z, const double* col_c,
+                      const double* col_s, int64_t n_lat, int64_t n_lon, double* x, double* y,
+                      double* z, cudaStream_t st);
+
+// geometry + histogram over grid points (geometry.hpp:51-83, bit-exact)
+void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
+                          const PairGeom* pg_dev, double fs, double wl, int N, int* d_out,
+                          double* fdoa_out, int* hist, double* s_out,
+                          unsigned long long* overlap, int* err, cudaStream_t st);
+void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
+                            const PairGeom* pg_dev, double fs, double wl, dg_pair_offsets* out,
+                            int* err, cudaStream_t st);
+// the same from caller offsets (correlate_batch path)
+void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
+                         double* fdoa_out, int* hist, double* s_out,
+                         unsigned long long* overlap, cudaStream_t st);
+void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
+                   const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st);
+void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
+                      const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
+                      double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st);
+
+// exact FP64 reference-order re-evaluation of flagged elements
+// elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)
+void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,
+                        cudaStream_t st);
+void launch_compact_flags(const uint32_t* bits, int64_t n_words, int64_t* list,
+                          unsigned long long* cursor, cudaStream_t st);
+struct RefineCtx {
+    // geolocate path (grid != nullptr) or batch path (offsets != nullptr)
+    const double *x, *y, *z;
+    int64_t P;
+    const PairGeom* pg;       // [S*pairs]
+    const int* pair_rx;       // [pairs*2] receiver indices
+    int pairs, R;
+    const dg_pair_offsets* offsets;  // batch path
+    const double2* y64;       // geolocate: [S][R][stride]; batch: [2][stride]
+    int64_t stride;           // elements between captures (>= N, multiple of 32)
+    int N;
+    double fs, wl;
+    double* raw;              // [S*pairs*P] (batch: [P])
+};
+void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st);
+
+void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
+                          cudaStream_t st);
+void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st);
+void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st);
+void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,
+                cudaStream_t st);
+void launch_select_near(const double* v, int64_t P, const double* vmax, double rel,
+                        int* list, int* count, int cap, cudaStream_t st);
+void launch_rerank(const int* cells, const int* n_cells, int cap, int S, RefineCtx ctx,
+                   cudaStream_t st);
+void launch_recombine_cells(const int* cells, const int* n_cells, int cap, const double* raw,
+                            int S, int pairs, int64_t P, double* grids, const double* medians,
+                            double* acc, cudaStream_t st);
+void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc,
+                         long long* best_idx, double* best_val, cudaStream_t st);
+// median (nth_element rank P/2) of nonnegative doubles by 4-pass radix select
+void launch_median(const double* v, int64_t P, unsigned* hist, unsigned long long* state,
+                   double* out, cudaStream_t st);
+
+// detect_emitters (correlate.hpp:127-201)
+struct DetCand {
+    double score;
+    long long key;  // ilat*1e6 + ilon (reference tie order)
+    int ilat, ilon;
+};
+void launch_mean_var(const double* v, int64_t P, double* partial, int n_partial,
+                     double* stats /* [mean, var, sigma] */, cudaStream_t st);
+void launch_local_max(const double* v, int64_t n_lat, int64_t n_lon, const double* stats,
+                      double k_sigma, DetCand* cands, int* n_cands, int cap, cudaStream_t st);
+void launch_greedy(const DetCand* cands, const int* n_cands, int cap, int radius,
+                   const double* stats, int64_t n_lon, dg_emitter_estimate* out, int* n_out,
+                   cudaStream_t st);
+
+void launch_f64_to_f32(const double2* in, float2* out, int64_t n, cudaStream_t st);
+void launch_f32_to_f64(const float2* in, double2* out, int64_t n, cudaStream_t st);
+
+}  // namespace dg

@@ -1,0 +1,992 @@
+// sm_100a kernels of the B200 direct-geolocation engine.
+//
+// Reference (read-only, /root/reference/proj/include/digeo): the hot path is
+// correlate.hpp:44-71 (Eq. 11) driven by geolocate.hpp:41-146, fed by
+// geometry.hpp:51-83 and geodesy.hpp:82-92,182-207.
+//
+// Data layout in HBM:
+//   grid      SoA double x[P], y[P], z[P]           (lat-major flat index)
+//   captures  float2  [S][R][N] (FP32 hot path) + double2 [S][R][N] (FP64 refine)
+//   per (snapshot, pair): d[P] int32, fdoa[P] f64, d-sorted candidate ids,
+//   warp tasks, raw surface double [S*pairs][P], refine bitmap 1 bit/element.
+#include <cuda_runtime.h>
+#include <float.h>
+#include <limits.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dg_internal.cuh"
+
+namespace dg {
+
+namespace {
+
+constexpr double kC = 299792458.0;      // geometry.hpp:32
+constexpr double kTwoPi = 6.283185307179586;  // 2.0 * std::numbers::pi (exact doubling)
+constexpr int kNoOverlap = INT_MIN;
+
+inline int blocks_for(int64_t n, int threads, int64_t cap = 148LL * 64) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+// ---------------------------------------------------------------------------
+// predict_geometry (geometry.hpp:51-64) in the reference's exact IEEE order:
+// r = p_rx - c; rho = sqrt((x*x + y*y) + z*z); delay = rho / c;
+// u = (1/rho) * r; doppler = -dot(u, v) / wl. No FMA contraction.
+__device__ __forceinline__ bool geometry_exact(double cx, double cy, double cz, const dg_state& rx,
+                                               double wl, double* delay, double* dop) {
+    const double rx_ = __dsub_rn(rx.position.x, cx);
+    const double ry = __dsub_rn(rx.position.y, cy);
+    const double rz = __dsub_rn(rx.position.z, cz);
+    const double rho =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(rx_, rx_), __dmul_rn(ry, ry)), __dmul_rn(rz, rz)));
+    *delay = __ddiv_rn(rho, kC);
+    const double inv = __ddiv_rn(1.0, rho);
+    const double ux = __dmul_rn(inv, rx_), uy = __dmul_rn(inv, ry), uz = __dmul_rn(inv, rz);
+    const double dot = __dadd_rn(__dadd_rn(__dmul_rn(ux, rx.velocity.x), __dmul_rn(uy, rx.velocity.y)),
+                                 __dmul_rn(uz, rx.velocity.z));
+    *dop = __ddiv_rn(-dot, wl);
+    return rho > 0.0;
+}
+
+// predict_pair_offsets (geometry.hpp:73-83): llround ties away from zero.
+__device__ __forceinline__ bool offsets_exact(double cx, double cy, double cz, const PairGeom& g,
+                                              double fs, double wl, long long* tdoa, double* fdoa) {
+    double di, fi, dj, fj;
+    const bool ok_i = geometry_exact(cx, cy, cz, g.rx_i, wl, &di, &fi);
+    const bool ok_j = geometry_exact(cx, cy, cz, g.rx_j, wl, &dj, &fj);
+    *tdoa = llround(__dmul_rn(__dsub_rn(dj, di), fs));
+    *fdoa = __dsub_rn(fj, fi);
+    return ok_i && ok_j;
+}
+
+// correlate_kernel (correlate.hpp:44-71) in the reference's exact order: one
+// FP64 phasor recurrence, ascending k, double accumulators. Used only for the
+// few elements whose FP32 value cannot meet the relative tolerance and for the
+// near-peak re-rank; cos/sin are CUDA's (<= 1 ulp apart from glibc's).
+__device__ double correlate_exact(const double2* __restrict__ y1, const double2* __restrict__ y2,
+                                  int N, long long d, double fdoa, double fs) {
+    const long long kb = d < 0 ? -d : 0;
+    const long long ke = (N - d) < N ? (N - d) : N;
+    if (kb >= ke) return 0.0;
+    const double step = __ddiv_rn(__dmul_rn(kTwoPi, fdoa), fs);
+    double rot_im, rot_re;
+    sincos(step, &rot_im, &rot_re);
+    const double phase0 = __dmul_rn(step, (double)kb);
+    double ph_im, ph_re;
+    sincos(phase0, &ph_im, &ph_re);
+    double acc_re = 0.0, acc_im = 0.0;
+    const double2* b = y2 + d;
+    for (long long k = kb; k < ke; ++k) {
+        const double2 a = y1[k];
+        const double2 bb = b[k];
+        const double b_re = bb.x, b_im = -bb.y;
+        const double p_re = __dsub_rn(__dmul_rn(a.x, b_re), __dmul_rn(a.y, b_im));
+        const double p_im = __dadd_rn(__dmul_rn(a.x, b_im), __dmul_rn(a.y, b_re));
+        acc_re = __dadd_rn(acc_re, __dsub_rn(__dmul_rn(p_re, ph_re), __dmul_rn(p_im, ph_im)));
+        acc_im = __dadd_rn(acc_im, __dadd_rn(__dmul_rn(p_re, ph_im), __dmul_rn(p_im, ph_re)));
+        const double nr = __dsub_rn(__dmul_rn(ph_re, rot_re), __dmul_rn(ph_im, rot_im));
+        ph_im = __dadd_rn(__dmul_rn(ph_re, rot_im), __dmul_rn(ph_im, rot_re));
+        ph_re = nr;
+    }
+    return __dsqrt_rn(__dadd_rn(__dmul_rn(acc_re, acc_re), __dmul_rn(acc_im, acc_im)));
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// K1: lattice ECEF (geodesy.hpp:82-92,182-207). The host supplies per-row
+// A_i = (N_i + alt) * cos(lat_i), Z_i = (N_i (1 - e2) + alt) * sin(lat_i) and
+// per-column cos/sin(lon_j) from libm, so x = A_i * cos(lon_j) etc. reproduce
+// lla_to_ecef's doubles exactly (same operands, same single rounding).
+__global__ void k_grid_ecef(const double* __restrict__ ra, const double* __restrict__ rz,
+                            const double* __restrict__ cc, const double* __restrict__ cs,
+                            int64_t n_lat, int64_t n_lon, double* __restrict__ x,
+                            double* __restrict__ y, double* __restrict__ z) {
+    const int64_t P = n_lat * n_lon;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = p / n_lon, j = p - i * n_lon;
+        const double a = ra[i];
+        x[p] = __dmul_rn(a, cc[j]);
+        y[p] = __dmul_rn(a, cs[j]);
+        z[p] = rz[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: per-point offsets (bit-exact) + TDOA histogram for the warp bucketing.
+// Candidates whose shift leaves no overlap get S = 0 here (correlate.hpp:49).
+__device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdoa, int N,
+                                           int* d_out, double* fdoa_out, int* hist,
+                                           double* s_out, unsigned long long& ovl) {
+    if (tdoa >= N || tdoa <= -N) {  // empty overlap (also catches llround overflow)
+        d_out[p] = kNoOverlap;
+        s_out[p] = 0.0;
+    } else {
+        const int d = (int)tdoa;
+        d_out[p] = d;
+        fdoa_out[p] = fdoa;
+        atomicAdd(&hist[d + N - 1], 1);
+        ovl += (unsigned long long)(N - (d < 0 ? -d : d));
+    }
+}
+
+__global__ void k_geometry_hist(const double* __restrict__ x, const double* __restrict__ y,
+                                const double* __restrict__ z, int64_t P,
+                                const PairGeom* __restrict__ pg, double fs, double wl, int N,
+                                int* __restrict__ d_out, double* __restrict__ fdoa_out,
+                                int* __restrict__ hist, double* __restrict__ s_out,
+                                unsigned long long* __restrict__ overlap, int* __restrict__ err) {
+    const PairGeom g = *pg;
+    unsigned long long ovl = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        long long tdoa;
+        double fdoa;
+        if (!offsets_exact(x[p], y[p], z[p], g, fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
+        emit_point(p, tdoa, fdoa, N, d_out, fdoa_out, hist, s_out, ovl);
+    }
+    ovl = warp_sum_u64(ovl);
+    if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
+}
+
+__global__ void k_predict_offsets(const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ z, int64_t P,
+                                  const PairGeom* __restrict__ pg, double fs, double wl,
+                                  dg_pair_offsets* __restrict__ out, int* __restrict__ err) {
+    const PairGeom g = *pg;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        long long tdoa;
+        double fdoa;
+        if (!offsets_exact(x[p], y[p], z[p], g, fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
+        dg_pair_offsets o;
+        o.tdoa_samples = tdoa;
+        o.fdoa_hz = fdoa;
+        out[p] = o;
+    }
+}
+
+__global__ void k_offsets_hist(const dg_pair_offsets* __restrict__ off, int64_t P, int N,
+                               int* __restrict__ d_out, double* __restrict__ fdoa_out,
+                               int* __restrict__ hist, double* __restrict__ s_out,
+                               unsigned long long* __restrict__ overlap) {
+    unsigned long long ovl = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const dg_pair_offsets o = off[p];
+        emit_point(p, o.tdoa_samples, o.fdoa_hz, N, d_out, fdoa_out, hist, s_out, ovl);
+    }
+    ovl = warp_sum_u64(ovl);
+    if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
+}
+
+// ---------------------------------------------------------------------------
+// Bucketing: exclusive scans of per-d counts and per-d warp-task counts, then
+// scatter candidate ids by d and cut each d-bucket into <=32-lane tasks.
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan(const int* __restrict__ hist, int nbins, int* __restrict__ off, int* __restrict__ toff,
+       int* __restrict__ cursor, int* __restrict__ n_tasks) {
+    __shared__ int ws[32], wt[32];
+    __shared__ int carry_s, carry_t;
+    if (threadIdx.x == 0) carry_s = carry_t = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < nbins; base += kScanThreads * kScanItems) {
+        int v[kScanItems], t[kScanItems];
+        int s = 0, st = 0;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            const int idx = base + threadIdx.x * kScanItems + i;
+            v[i] = idx < nbins ? hist[idx] : 0;
+            t[i] = (v[i] + 31) >> 5;
+            s += v[i];
+            st += t[i];
+        }
+        int is = s, it = st;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, is, o);
+            const int b = __shfl_up_sync(0xffffffffu, it, o);
+            if (lane >= o) {
+                is += a;
+                it += b;
+            }
+        }
+        if (lane == 31) {
+            ws[warp] = is;
+            wt[warp] = it;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int a = ws[lane], b = wt[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, a, o);
+                const int y = __shfl_up_sync(0xffffffffu, b, o);
+                if (lane >= o) {
+                    a += x;
+                    b += y;
+                }
+            }
+            ws[lane] = a;
+            wt[lane] = b;
+        }
+        __syncthreads();
+        int es = carry_s + (warp ? ws[warp - 1] : 0) + is - s;
+        int et = carry_t + (warp ? wt[warp - 1] : 0) + it - st;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            const int idx = base + threadIdx.x * kScanItems + i;
+            if (idx < nbins) {
+                off[idx] = es;
+                cursor[idx] = es;
+                toff[idx] = et;
+            }
+            es += v[i];
+            et += t[i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry_s += ws[31];
+            carry_t += wt[31];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_tasks = carry_t;
+}
+
+__global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __restrict__ cursor,
+                          int* __restrict__ sorted) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int dd = d[p];
+        if (dd == kNoOverlap) continue;
+        const int pos = atomicAdd(&cursor[dd + N - 1], 1);
+        sorted[pos] = (int)p;
+    }
+}
+
+__global__ void k_build_tasks(int* __restrict__ hist, int nbins, int N, const int* __restrict__ off,
+                              const int* __restrict__ toff, Task* __restrict__ tasks) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
+        const int cnt = hist[b];
+        if (!cnt) continue;
+        hist[b] = 0;  // ready for the next (snapshot, pair)
+        const int d = b - (N - 1);
+        const int t0 = toff[b], s0 = off[b];
+        for (int t = 0; 32 * t < cnt; ++t) {
+            Task tk;
+            tk.d = d;
+            tk.start = s0 + 32 * t;
+            tk.count = min(32, cnt - 32 * t);
+            tk.pad = 0;
+            tasks[t0 + t] = tk;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: the correlator (Eq. 11, correlate.hpp:44-71) on CUDA cores in FP32.
+//
+// One warp = one task = up to 32 candidates sharing TDOA d. Per 256-sample
+// chunk the warp stages z[k] = y1[k] conj(y2[k+d]) once in shared memory
+// (each lane produces 8 samples), then every lane — one candidate with its own
+// FDOA f — evaluates sum_k z[k] e^{j 2 pi f k} as
+//     sum_b W_b * (sum_{j<16} z[c0+16b+j] E[j]),   E[j] = e^{j 2 pi f j},
+// E held in registers, W_b = e^{j 2 pi f (c0+16b)} advanced by one complex
+// multiply per 16 samples and re-anchored each chunk from an FP64-reduced
+// phase. z is read with 16-byte broadcast LDS (2 samples, all lanes same
+// address). Chunk sums are accumulated in FP64. Cost per sample per
+// candidate: 4 FFMA + 1/2 LDS.128 + 1/2 (W update) + ~1/4 (z production).
+//
+// Elements with S < kRefineTau * sqrt(sum|z|^2) are flagged for the exact FP64
+// re-evaluation (their FP32 relative error could exceed 1e-4).
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
+            const int* __restrict__ sorted, const double* __restrict__ fdoa,
+            const float2* __restrict__ y1, const float2* __restrict__ y2, int N, double fs,
+            double* __restrict__ s_out, uint32_t* __restrict__ flag_bits, int64_t flag_base) {
+    __shared__ __align__(16) float4 zb[kWarpsPerCta][kChunk / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x * kWarpsPerCta + warp;
+    if (t >= *n_tasks) return;
+    const Task tk = tasks[t];
+    const int d = tk.d;
+    const int p = lane < tk.count ? sorted[tk.start + lane] : -1;
+    const double f = p >= 0 ? fdoa[p] / fs : 0.0;  // cycles per sample
+
+    // phasor table E[j] = e^{j 2 pi f j}, W1 = e^{j 2 pi f L}; FP64 range reduction
+    float er[kL], ei[kL];
+#pragma unroll
+    for (int j = 0; j < kL; ++j) {
+        const double x = f * (double)j;
+        sincospif((float)(2.0 * (x - rint(x))), &ei[j], &er[j]);
+    }
+    float w1r, w1i;
+    {
+        const double x = f * (double)kL;
+        sincospif((float)(2.0 * (x - rint(x))), &w1i, &w1r);
+    }
+
+    const int kb = d < 0 ? -d : 0;
+    const int ke = (N - d) < N ? (N - d) : N;
+    const int kb0 = kb & ~1;  // even chunk origin -> 16-byte aligned y1 pairs
+    float4* zw = zb[warp];
+    double acc_re = 0.0, acc_im = 0.0;
+    float z2 = 0.f;
+    const bool d_even = (d & 1) == 0;
+
+    for (int c0 = kb0; c0 < ke; c0 += kChunk) {
+        // ---- produce z for [c0, c0 + kChunk) ----
+#pragma unroll
+        for (int i = 0; i < kChunk / 64; ++i) {
+            const int q = lane + 32 * i;
+            const int k = c0 + 2 * q;
+            float2 a0, a1, b0, b1;
+            if (k >= kb && k + 1 < ke) {
+                const float4 a = *reinterpret_cast<const float4*>(y1 + k);
+                a0 = make_float2(a.x, a.y);
+                a1 = make_float2(a.z, a.w);
+                if (d_even) {
+                    const float4 b = *reinterpret_cast<const float4*>(y2 + k + d);
+                    b0 = make_float2(b.x, b.y);
+                    b1 = make_float2(b.z, b.w);
+                } else {
+                    b0 = y2[k + d];
+                    b1 = y2[k + d + 1];
+                }
+            } else {
+                const bool v0 = k >= kb && k < ke, v1 = k + 1 >= kb && k + 1 < ke;
+                a0 = v0 ? y1[k] : make_float2(0.f, 0.f);
+                b0 = v0 ? y2[k + d] : make_float2(0.f, 0.f);
+                a1 = v1 ? y1[k + 1] : make_float2(0.f, 0.f);
+                b1 = v1 ? y2[k + 1 + d] : make_float2(0.f, 0.f);
+            }
+            float4 zz;
+            zz.x = fmaf(a0.x, b0.x, a0.y * b0.y);
+            zz.y = fmaf(a0.y, b0.x, -(a0.x * b0.y));
+            zz.z = fmaf(a1.x, b1.x, a1.y * b1.y);
+            zz.w = fmaf(a1.y, b1.x, -(a1.x * b1.y));
+            z2 = fmaf(zz.x, zz.x, fmaf(zz.y, zz.y, fmaf(zz.z, zz.z, fmaf(zz.w, zz.w, z2))));
+            zw[q] = zz;
+        }
+        __syncwarp();
+
+        // ---- anchor W = e^{j 2 pi f c0} from the FP64-reduced phase ----
+        float wr, wi;
+        {
+            const double x = f * (double)c0;
+            sincospif((float)(2.0 * (x - rint(x))), &wi, &wr);
+        }
+        float ar = 0.f, ai = 0.f;
+#pragma unroll
+        for (int b = 0; b < kChunk / kL; ++b) {
+            float cr = 0.f, ci = 0.f;
+#pragma unroll
+            for (int j = 0; j < kL; j += 2) {
+                const float4 z = zw[(b * kL + j) >> 1];
+                cr = fmaf(z.x, er[j], cr);
+                cr = fmaf(-z.y, ei[j], cr);
+                ci = fmaf(z.x, ei[j], ci);
+                ci = fmaf(z.y, er[j], ci);
+                cr = fmaf(z.z, er[j + 1], cr);
+                cr = fmaf(-z.w, ei[j + 1], cr);
+                ci = fmaf(z.z, ei[j + 1], ci);
+                ci = fmaf(z.w, er[j + 1], ci);
+            }
+            ar = fmaf(wr, cr, ar);
+            ar = fmaf(-wi, ci, ar);
+            ai = fmaf(wr, ci, ai);
+            ai = fmaf(wi, cr, ai);
+            const float nr = fmaf(wr, w1r, -(wi * w1i));
+            wi = fmaf(wr, w1i, wi * w1r);
+            wr = nr;
+        }
+        acc_re += (double)ar;
+        acc_im += (double)ai;
+        __syncwarp();
+    }
+
+#pragma unroll
+    for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
+    if (p >= 0) {
+        const double s = sqrt(acc_re * acc_re + acc_im * acc_im);
+        s_out[p] = s;
+        if (s < (double)kRefineTau * sqrt((double)z2)) {
+            const int64_t e = flag_base + p;
+            atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Refinement: compact the flag bitmap and re-evaluate those elements exactly.
+__global__ void k_count_flags(const uint32_t* __restrict__ bits, int64_t n_words,
+                              unsigned long long* __restrict__ count) {
+    unsigned long long c = 0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_words;
+         w += (int64_t)gridDim.x * blockDim.x)
+        c += __popc(bits[w]);
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void k_compact_flags(const uint32_t* __restrict__ bits, int64_t n_words,
+                                int64_t* __restrict__ list, unsigned long long* __restrict__ cur) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n_words;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t b = bits[w];
+        if (!b) continue;
+        unsigned long long pos = atomicAdd(cur, (unsigned long long)__popc(b));
+        while (b) {
+            const int i = __ffs(b) - 1;
+            b &= b - 1;
+            list[pos++] = w * 32 + i;
+        }
+    }
+}
+
+__device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, int64_t p) {
+    if (c.offsets) {
+        const dg_pair_offsets o = c.offsets[p];
+        return correlate_exact(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz, c.fs);
+    }
+    const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
+    long long tdoa;
+    double fdoa;
+    offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
+    const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
+    const double2* y1 = c.y64 + (s * c.R + ri) * c.stride;
+    const double2* y2 = c.y64 + (s * c.R + rj) * c.stride;
+    return correlate_exact(y1, y2, c.N, tdoa, fdoa, c.fs);
+}
+
+__global__ void k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx c) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = list[i];
+        const int64_t sp = e / c.P, p = e - sp * c.P;
+        c.raw[e] = exact_element(c, sp, p);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Accumulation (correlate_snapshot_all_pairs + accumulate_grids order).
+__global__ void k_combine_pairs(const double* __restrict__ raw, int S, int pairs, int64_t P,
+                                double* __restrict__ grids) {
+    const int64_t total = (int64_t)S * P;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / P, p = i - s * P;
+        const double* r = raw + s * pairs * P + p;
+        double g = r[0];
+        for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[q * P]);
+        grids[i] = g;
+    }
+}
+
+__global__ void k_scale(double* __restrict__ v, int64_t P, const double* __restrict__ median) {
+    const double m = *median;
+    if (!(m > 0.0)) return;  // geolocate.hpp:120
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = __ddiv_rn(v[i], m);
+}
+
+__global__ void k_accumulate(const double* __restrict__ grids, int S, int64_t P,
+                             double* __restrict__ acc) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double a = grids[p];
+        for (int s = 1; s < S; ++s) a = __dadd_rn(a, grids[(int64_t)s * P + p]);
+        acc[p] = a;
+    }
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void k_max_partial(const double* __restrict__ v, int64_t P, double* __restrict__ part) {
+    __shared__ double sm[32];
+    double m = -DBL_MAX;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = fmax(m, v[i]);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : -DBL_MAX;
+        m = warp_max(m);
+        if (threadIdx.x == 0) part[blockIdx.x] = m;
+    }
+}
+
+__global__ void k_max_final(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double sm[32];
+    double m = -DBL_MAX;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, part[i]);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : -DBL_MAX;
+        m = warp_max(m);
+        if (threadIdx.x == 0) *out = m;
+    }
+}
+
+__global__ void k_select_near(const double* __restrict__ v, int64_t P,
+                              const double* __restrict__ vmax, double rel, int* __restrict__ list,
+                              int* __restrict__ count, int cap) {
+    const double m = *vmax;
+    const double thr = m - fabs(m) * rel;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (v[i] >= thr) {
+            const int pos = atomicAdd(count, 1);
+            if (pos < cap) list[pos] = (int)i;
+        }
+    }
+}
+
+__global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ n_cells, int cap,
+                         int SP, RefineCtx c) {
+    const int n = min(*n_cells, cap);
+    const int64_t total = (int64_t)n * SP;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ci = i / SP, sp = i - ci * SP;
+        const int64_t p = cells[ci];
+        c.raw[sp * c.P + p] = exact_element(c, sp, p);
+    }
+}
+
+__global__ void k_recombine_cells(const int* __restrict__ cells, const int* __restrict__ n_cells,
+                                  int cap, const double* __restrict__ raw, int S, int pairs,
+                                  int64_t P, double* __restrict__ grids,
+                                  const double* __restrict__ medians, double* __restrict__ acc) {
+    const int n = min(*n_cells, cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t p = cells[i];
+        double a = 0.0;
+        for (int s = 0; s < S; ++s) {
+            const double* r = raw + (int64_t)s * pairs * P + p;
+            double g = r[0];
+            for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[q * P]);
+            if (medians && medians[s] > 0.0) g = __ddiv_rn(g, medians[s]);
+            if (grids) grids[(int64_t)s * P + p] = g;
+            a = s ? __dadd_rn(a, g) : g;
+        }
+        acc[p] = a;
+    }
+}
+
+// single block: exact max over the re-ranked cells, lowest flat index on ties
+// (std::max_element keeps the first maximum)
+__global__ void k_argmax_cells(const int* __restrict__ cells, const int* __restrict__ n_cells,
+                               int cap, const double* __restrict__ acc,
+                               long long* __restrict__ best_idx, double* __restrict__ best_val) {
+    __shared__ double sv[1024];
+    __shared__ long long si[1024];
+    const int n = min(*n_cells, cap);
+    double bv = -DBL_MAX;
+    long long bi = LLONG_MAX;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const long long p = cells[i];
+        const double v = acc[p];
+        if (v > bv || (v == bv && p < bi)) {
+            bv = v;
+            bi = p;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s) {
+            const double v = sv[threadIdx.x + s];
+            const long long p = si[threadIdx.x + s];
+            if (v > sv[threadIdx.x] || (v == sv[threadIdx.x] && p < si[threadIdx.x])) {
+                sv[threadIdx.x] = v;
+                si[threadIdx.x] = p;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *best_idx = si[0];
+        *best_val = sv[0];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Median (geolocate.hpp:115-122: nth_element at size/2) by 8-bit radix select
+// over the IEEE bit patterns (order-preserving for S >= 0).
+// state[0] = prefix, state[1] = remaining rank
+__global__ void k_radix_hist(const double* __restrict__ v, int64_t P, int shift,
+                             const unsigned long long* __restrict__ state,
+                             unsigned* __restrict__ hist) {
+    __shared__ unsigned sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = state[0];
+    const unsigned long long hi_mask = shift >= 56 ? 0ull : (~0ull << (shift + 8));
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(v[i]);
+        if ((key & hi_mask) == (prefix & hi_mask)) atomicAdd(&sh[(key >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+__global__ void k_radix_pick(unsigned* __restrict__ hist, int shift,
+                             unsigned long long* __restrict__ state, double* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        unsigned long long rank = state[1], cum = 0;
+        int digit = 255;
+        for (int i = 0; i < 256; ++i) {
+            if (cum + hist[i] > rank) {
+                digit = i;
+                break;
+            }
+            cum += hist[i];
+        }
+        state[0] |= (unsigned long long)digit << shift;
+        state[1] = rank - cum;
+        if (shift == 0) *out = __longlong_as_double((long long)state[0]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// detect_emitters (correlate.hpp:127-201)
+__device__ __forceinline__ double warp_sumd(double v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// fixed-shape tree reductions (deterministic); mode 0: sum v, mode 1: sum (v-mean)^2
+__global__ void k_sum_partial(const double* __restrict__ v, int64_t P, const double* __restrict__ stats,
+                              int mode, double* __restrict__ part) {
+    __shared__ double sm[32];
+    const double mean = mode ? stats[0] : 0.0;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = v[i];
+        s += mode ? (x - mean) * (x - mean) : x;
+    }
+    s = warp_sumd(s);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+        s = warp_sumd(s);
+        if (threadIdx.x == 0) part[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_sum_final(const double* __restrict__ part, int n, int64_t P, int mode,
+                            double* __restrict__ stats) {
+    __shared__ double sm[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    s = warp_sumd(s);
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0.0;
+        s = warp_sumd(s);
+        if (threadIdx.x == 0) {
+            const double m = s / (double)P;
+            if (mode == 0) {
+                stats[0] = m;
+            } else {
+                stats[1] = m;
+                stats[2] = sqrt(m);
+            }
+        }
+    }
+}
+
+__global__ void k_local_max(const double* __restrict__ v, int64_t n_lat, int64_t n_lon,
+                            const double* __restrict__ stats, double k_sigma,
+                            DetCand* __restrict__ cands, int* __restrict__ n_cands, int cap) {
+    const double sigma = stats[2];
+    if (sigma == 0.0) return;
+    const double thr = stats[0] + k_sigma * sigma;
+    const int64_t P = n_lat * n_lon;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const double x = v[p];
+        if (x <= thr) continue;
+        const int64_t i = p / n_lon, j = p - i * n_lon;
+        bool is_max = true;
+        for (int di = -1; di <= 1 && is_max; ++di)
+            for (int dj = -1; dj <= 1 && is_max; ++dj) {
+                if (!di && !dj) continue;
+                const int64_t ni = i + di, nj = j + dj;
+                if (ni < 0 || ni >= n_lat || nj < 0 || nj >= n_lon) continue;
+                if (v[ni * n_lon + nj] > x) is_max = false;
+            }
+        if (!is_max) continue;
+        const int pos = atomicAdd(n_cands, 1);
+        if (pos < cap) {
+            DetCand c;
+            c.score = x;
+            c.key = (long long)i * 1000000LL + j;
+            c.ilat = (int)i;
+            c.ilon = (int)j;
+            cands[pos] = c;
+        }
+    }
+}
+
+// single block: sort by (score desc, key asc) then greedy Chebyshev exclusion
+__device__ __forceinline__ bool cand_before(const DetCand& a, const DetCand& b) {
+    if (a.score != b.score) return a.score > b.score;
+    return a.key < b.key;
+}
+
+__global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restrict__ n_cands,
+                         int cap, int radius, const double* __restrict__ stats, int64_t n_lon,
+                         dg_emitter_estimate* __restrict__ out, int* __restrict__ n_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    DetCand* c = reinterpret_cast<DetCand*>(smem);
+    __shared__ int n_acc, excluded;
+    const int n = min(*n_cands, cap);
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        if (i < n) {
+            c[i] = cands[i];
+        } else {
+            c[i].score = -DBL_MAX;
+            c[i].key = LLONG_MAX;
+        }
+    }
+    if (threadIdx.x == 0) n_acc = 0;
+    __syncthreads();
+    for (int k = 2; k <= m; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const bool swap = up ? cand_before(c[l], c[i]) : cand_before(c[i], c[l]);
+                    if (swap) {
+                        const DetCand t = c[i];
+                        c[i] = c[l];
+                        c[l] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // accepted entries are compacted to the front of c[] as they are found
+    for (int idx = 0; idx < n; ++idx) {
+        const DetCand cur = c[idx];
+        if (threadIdx.x == 0) excluded = 0;
+        __syncthreads();
+        for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
+            const int dl = abs(cur.ilat - c[a].ilat), dn = abs(cur.ilon - c[a].ilon);
+            if (max(dl, dn) <= radius) excluded = 1;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && !excluded) {
+            c[n_acc] = cur;  // n_acc <= idx, so this never clobbers unvisited entries
+            dg_emitter_estimate e;
+            e.lat_deg = (double)cur.ilat;  // lattice coordinates filled in on the host
+            e.lon_deg = (double)cur.ilon;
+            e.alt_m = 0.0;
+            e.grid_index = (int64_t)cur.ilat * n_lon + cur.ilon;
+            e.score = cur.score;
+            e.score_zsigma = (cur.score - stats[0]) / stats[2];
+            out[n_acc] = e;
+            ++n_acc;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_out = n_acc;
+}
+
+__global__ void k_f64_to_f32(const double2* __restrict__ in, float2* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 v = in[i];
+        out[i] = make_float2((float)v.x, (float)v.y);
+    }
+}
+
+__global__ void k_f32_to_f64(const float2* __restrict__ in, double2* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = in[i];
+        out[i] = make_double2((double)v.x, (double)v.y);
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+void launch_grid_ecef(const double* ra, const double* rz, const double* cc, const double* cs,
+                      int64_t n_lat, int64_t n_lon, double* x, double* y, double* z,
+                      cudaStream_t st) {
+    k_grid_ecef<<<blocks_for(n_lat * n_lon, 256), 256, 0, st>>>(ra, rz, cc, cs, n_lat, n_lon, x, y,
+                                                               z);
+}
+
+void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
+                          const PairGeom* pg, double fs, double wl, int N, int* d_out,
+                          double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
+                          int* err, cudaStream_t st) {
+    k_geometry_hist<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, N, d_out, fdoa_out,
+                                                        hist, s_out, overlap, err);
+}
+
+void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
+                            const PairGeom* pg, double fs, double wl, dg_pair_offsets* out, int* err,
+                            cudaStream_t st) {
+    k_predict_offsets<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, out, err);
+}
+
+void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
+                         double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
+                         cudaStream_t st) {
+    k_offsets_hist<<<blocks_for(P, 256), 256, 0, st>>>(off, P, N, d_out, fdoa_out, hist, s_out,
+                                                       overlap);
+}
+
+void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
+                   const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st) {
+    k_scan<<<1, kScanThreads, 0, st>>>(hist, nbins, off, toff, cursor, n_tasks);
+    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
+    k_build_tasks<<<blocks_for(nbins, 256), 256, 0, st>>>(hist, nbins, N, off, toff, tasks);
+}
+
+void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
+                      const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
+                      double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st) {
+    const int blocks = (max_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (blocks <= 0) return;
+    k_correlate<<<blocks, 32 * kWarpsPerCta, 0, st>>>(tasks, n_tasks, sorted, fdoa, y1, y2, N, fs,
+                                                      s_out, flag_bits, flag_base);
+}
+
+void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,
+                        cudaStream_t st) {
+    k_count_flags<<<blocks_for(n_words, 256), 256, 0, st>>>(bits, n_words, count);
+}
+
+void launch_compact_flags(const uint32_t* bits, int64_t n_words, int64_t* list,
+                          unsigned long long* cursor, cudaStream_t st) {
+    k_compact_flags<<<blocks_for(n_words, 256), 256, 0, st>>>(bits, n_words, list, cursor);
+}
+
+void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st) {
+    if (n <= 0) return;
+    k_refine<<<blocks_for(n, 128, 148LL * 128), 128, 0, st>>>(list, n, ctx);
+}
+
+void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
+                          cudaStream_t st) {
+    k_combine_pairs<<<blocks_for((int64_t)S * P, 256), 256, 0, st>>>(raw, S, pairs, P, grids);
+}
+
+void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st) {
+    k_scale<<<blocks_for(P, 256), 256, 0, st>>>(v, P, median);
+}
+
+void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st) {
+    k_accumulate<<<blocks_for(P, 256), 256, 0, st>>>(grids, S, P, acc);
+}
+
+void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,
+                cudaStream_t st) {
+    k_max_partial<<<n_partial, 256, 0, st>>>(v, P, partial);
+    k_max_final<<<1, 1024, 0, st>>>(partial, n_partial, out);
+}
+
+void launch_select_near(const double* v, int64_t P, const double* vmax, double rel, int* list,
+                        int* count, int cap, cudaStream_t st) {
+    k_select_near<<<blocks_for(P, 256), 256, 0, st>>>(v, P, vmax, rel, list, count, cap);
+}
+
+void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
+                   cudaStream_t st) {
+    k_rerank<<<blocks_for((int64_t)cap * SP, 64, 148LL * 64), 64, 0, st>>>(cells, n_cells, cap, SP,
+                                                                          ctx);
+}
+
+void launch_recombine_cells(const int* cells, const int* n_cells, int cap, const double* raw, int S,
+                            int pairs, int64_t P, double* grids, const double* medians,
+                            double* acc, cudaStream_t st) {
+    k_recombine_cells<<<blocks_for(cap, 128), 128, 0, st>>>(cells, n_cells, cap, raw, S, pairs, P,
+                                                            grids, medians, acc);
+}
+
+void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc,
+                         long long* best_idx, double* best_val, cudaStream_t st) {
+    k_argmax_cells<<<1, 1024, 0, st>>>(cells, n_cells, cap, acc, best_idx, best_val);
+}
+
+void launch_median(const double* v, int64_t P, unsigned* hist, unsigned long long* state,
+                   double* out, cudaStream_t st) {
+    // state must hold {0, P/2}; hist zeroed
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        k_radix_hist<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(v, P, shift, state, hist);
+        k_radix_pick<<<1, 256, 0, st>>>(hist, shift, state, out);
+    }
+}
+
+void launch_mean_var(const double* v, int64_t P, double* partial, int n_partial, double* stats,
+                     cudaStream_t st) {
+    k_sum_partial<<<n_partial, 256, 0, st>>>(v, P, stats, 0, partial);
+    k_sum_final<<<1, 1024, 0, st>>>(partial, n_partial, P, 0, stats);
+    k_sum_partial<<<n_partial, 256, 0, st>>>(v, P, stats, 1, partial);
+    k_sum_final<<<1, 1024, 0, st>>>(partial, n_partial, P, 1, stats);
+}
+
+void launch_local_max(const double* v, int64_t n_lat, int64_t n_lon, const double* stats,
+                      double k_sigma, DetCand* cands, int* n_cands, int cap, cudaStream_t st) {
+    k_local_max<<<blocks_for(n_lat * n_lon, 256), 256, 0, st>>>(v, n_lat, n_lon, stats, k_sigma,
+                                                               cands, n_cands, cap);
+}
+
+void launch_greedy(const DetCand* cands, const int* n_cands, int cap, int radius,
+                   const double* stats, int64_t n_lon, dg_emitter_estimate* out, int* n_out,
+                   cudaStream_t st) {
+    int m = 1;
+    while (m < cap) m <<= 1;
+    const size_t smem = (size_t)m * sizeof(DetCand);
+    cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_greedy<<<1, 1024, smem, st>>>(cands, n_cands, cap, radius, stats, n_lon, out, n_out);
+}
+
+void launch_f64_to_f32(const double2* in, float2* out, int64_t n, cudaStream_t st) {
+    k_f64_to_f32<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+}
+
+void launch_f32_to_f64(const float2* in, double2* out, int64_t n, cudaStream_t st) {
+    k_f32_to_f64<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+}
+
+}  // namespace dg

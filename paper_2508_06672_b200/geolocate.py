@@ -1,0 +1,267 @@
+"""Algorithm-1 driver — host mirror of digeo geolocate.hpp:41-146 over the C ABI.
+
+``geolocate_snapshots`` runs the whole path on the GPU in one call: per
+snapshot and receiver pair, bit-exact TDOA/FDOA for every candidate, the FP32
+correlator, FP64 re-evaluation of the elements the tolerance needs, pair sum,
+optional median normalisation, non-coherent accumulation, the exact peak
+(argmax) and ``detect_emitters``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .backend import (DEFAULT_MEMORY_BUDGET_BYTES, B200Backend, BasebandCapture,
+                      CorrelationSession, plan_batches)
+from .engine import Engine, default_engine
+from .geodesy import CandidateGrid, GeodeticCoord
+
+SPEED_OF_LIGHT_M_S = 299792458.0  # geometry.hpp:32
+GPS_L1_FREQ_HZ = 1575.42e6        # geometry.hpp:33
+
+
+def wavelength_m(center_freq_hz: float) -> float:
+    """geometry.hpp:36-39"""
+    if not (center_freq_hz > 0.0):
+        raise ValueError("wavelength_m: center_freq_hz <= 0")
+    return SPEED_OF_LIGHT_M_S / center_freq_hz
+
+
+@dataclass
+class Snapshot:
+    """scene.hpp:66-70. states: [R, 6] (ECEF position xyz, velocity xyz)."""
+    epoch_s: float
+    states: np.ndarray
+    captures: list
+
+
+@dataclass
+class CorrelationGrid:
+    """correlate.hpp:89-98"""
+    grid: CandidateGrid
+    values: np.ndarray
+
+
+@dataclass
+class EmitterEstimate:
+    """correlate.hpp:117-122"""
+    location: GeodeticCoord
+    grid_index: int
+    score: float
+    score_zsigma: float
+
+
+@dataclass
+class GeolocateOptions:
+    """geolocate.hpp:96-104 (backend_name selects this engine: "b200")."""
+    backend_name: str = "b200"
+    workers: int = 0
+    batch_size: int = 8
+    memory_budget_bytes: int = DEFAULT_MEMORY_BUDGET_BYTES
+    k_sigma: float = 5.0
+    exclusion_radius_cells: int = 5
+    normalize_per_snapshot: bool = False
+    keep_per_snapshot: bool = True   # the reference always keeps them (geolocate.hpp:108)
+    detect: bool = True
+
+
+@dataclass
+class GeolocateResult:
+    """geolocate.hpp:106-111 plus the exact peak and run statistics."""
+    grid: CandidateGrid
+    per_snapshot: list
+    accumulated: CorrelationGrid
+    detections: list
+    argmax_index: int = 0
+    argmax_value: float = 0.0
+    stats: dict = field(default_factory=dict)
+
+
+def _pair_states(a) -> _capi.dg_state:
+    v = np.asarray(a, np.float64).reshape(6)
+    return _capi.dg_state(_capi.dg_ecef(*v[:3]), _capi.dg_ecef(*v[3:]))
+
+
+def correlate_snapshot(grid: CandidateGrid, snapshot: Snapshot, pair, backend: B200Backend,
+                       batch_size: int = 8,
+                       memory_budget_bytes: int = DEFAULT_MEMORY_BUDGET_BYTES) -> CorrelationGrid:
+    """geolocate.hpp:41-75 — offsets and correlation for the whole grid on the GPU."""
+    if grid is None or grid.size() == 0:
+        raise ValueError("correlate_snapshot: empty grid")
+    i, j = pair
+    n_rx = len(snapshot.captures)
+    if i >= n_rx or j >= n_rx or i == j:
+        raise ValueError("correlate_snapshot: bad receiver pair")
+    y1, y2 = snapshot.captures[i], snapshot.captures[j]
+    wavelength_m(y1.center_freq_hz)
+    cap_bytes = (len(y1.samples) + len(y2.samples)) * 16
+    plan_batches(grid.size(), batch_size, memory_budget_bytes, cap_bytes)
+    session = backend.stage(y1, y2)
+    out = np.zeros(grid.size(), np.float64)
+    si, sj = _pair_states(snapshot.states[i]), _pair_states(snapshot.states[j])
+    check(lib.dg_correlate_snapshot(session.handle, grid.handle, C.byref(si), C.byref(sj),
+                                    float(y1.center_freq_hz),
+                                    out.ctypes.data_as(C.POINTER(C.c_double))))
+    return CorrelationGrid(grid, out)
+
+
+def predict_offsets(grid: CandidateGrid, state_i, state_j, sample_rate_hz: float,
+                    wavelength: float) -> np.ndarray:
+    """predict_pair_offsets (geometry.hpp:73-83) for every grid point, on the GPU."""
+    from .backend import PAIR_OFFSETS_DTYPE
+    out = np.zeros(grid.size(), PAIR_OFFSETS_DTYPE)
+    si, sj = _pair_states(state_i), _pair_states(state_j)
+    check(lib.dg_predict_offsets(grid.engine.handle, grid.handle, C.byref(si), C.byref(sj),
+                                 float(sample_rate_hz), float(wavelength),
+                                 out.ctypes.data_as(C.POINTER(_capi.dg_pair_offsets))))
+    return out
+
+
+class StagedSnapshots:
+    """A run's captures and states resident in HBM (float2 + double2 copies)."""
+
+    def __init__(self, states: np.ndarray, captures: np.ndarray, sample_rate_hz: float,
+                 center_freq_hz: float, engine: Engine | None = None):
+        self.engine = engine or default_engine()
+        snaps, self._keep = _snapshots_struct(states, captures, sample_rate_hz, center_freq_hz)
+        h = C.c_void_p()
+        check(lib.dg_stage_snapshots(self.engine.handle, C.byref(snaps), C.byref(h)))
+        self._h = h
+        self._keep = None  # host buffers no longer needed
+        self.shape = captures.shape
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.dg_staged_destroy(h)
+            self._h = None
+
+
+def _snapshots_struct(states, captures, fs, fc):
+    """captures: [S, R, N] complex128 (reference layout) or complex64 (DGIQ)."""
+    caps = np.asarray(captures)
+    if caps.ndim != 3:
+        raise ValueError("captures must be [n_snapshots, n_receivers, n_samples]")
+    S, R, N = caps.shape
+    st = np.ascontiguousarray(states, np.float64).reshape(S * R, 6)
+    st_arr = (_capi.dg_state * (S * R))(*[_pair_states(st[k]) for k in range(S * R)])
+    keep = [st_arr]
+    snaps = _capi.dg_snapshots()
+    snaps.n_snapshots, snaps.n_receivers, snaps.n_samples = S, R, N
+    snaps.sample_rate_hz, snaps.center_freq_hz = float(fs), float(fc)
+    snaps.states = st_arr
+    if caps.dtype == np.complex64:
+        caps = np.ascontiguousarray(caps)
+        fp = C.POINTER(C.c_float)
+        ptrs = (fp * (S * R))(*[caps[s, r].ctypes.data_as(fp) for s in range(S) for r in range(R)])
+        snaps.captures_f32 = ptrs
+    else:
+        caps = np.ascontiguousarray(caps, np.complex128)
+        dp = C.POINTER(C.c_double)
+        ptrs = (dp * (S * R))(*[caps[s, r].ctypes.data_as(dp) for s in range(S) for r in range(R)])
+        snaps.captures_iq = ptrs
+    keep += [caps, ptrs]
+    return snaps, keep
+
+
+def _options(options: GeolocateOptions, stream=None, profile=False) -> _capi.dg_options:
+    o = _capi.dg_options()
+    lib.dg_options_default(C.byref(o))
+    o.k_sigma = float(options.k_sigma)
+    o.exclusion_radius_cells = int(options.exclusion_radius_cells)
+    o.normalize_per_snapshot = int(bool(options.normalize_per_snapshot))
+    o.detect = int(bool(options.detect))
+    o.stream = stream
+    o.profile = int(bool(profile))
+    return o
+
+
+def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, want_surface=True,
+         want_per_snapshot=False, accumulated_device=None, stream=None, profile=False,
+         det_cap=4096):
+    P = grid.size()
+    res = _capi.dg_result()
+    acc = np.zeros(P, np.float64) if want_surface else None
+    per = np.zeros((n_snap, P), np.float64) if want_per_snapshot else None
+    dets = (_capi.dg_emitter_estimate * det_cap)()
+    if acc is not None:
+        res.accumulated = acc.ctypes.data_as(C.POINTER(C.c_double))
+    if per is not None:
+        res.per_snapshot = per.ctypes.data_as(C.POINTER(C.c_double))
+    if accumulated_device is not None:
+        res.accumulated_device = int(accumulated_device)
+    res.detections = dets
+    res.detections_capacity = det_cap
+    opt = _options(options, stream, profile)
+    check(call(C.byref(opt), C.byref(res)))
+    detections = [EmitterEstimate(GeodeticCoord(d.lat_deg, d.lon_deg, d.alt_m), int(d.grid_index),
+                                  d.score, d.score_zsigma)
+                  for d in dets[:min(res.n_detections, det_cap)]]
+    stats = dict(n_refined=res.n_refined, n_reranked=res.n_reranked,
+                 sum_overlap_samples=res.sum_overlap_samples, correlate_ms=res.correlate_ms,
+                 correlate_launches=res.correlate_launches, total_ms=res.total_ms,
+                 kernel_launches=res.kernel_launches, n_detections=res.n_detections)
+    per_list = [CorrelationGrid(grid, per[s]) for s in range(n_snap)] if per is not None else []
+    return GeolocateResult(grid, per_list, CorrelationGrid(grid, acc), detections,
+                           int(res.argmax_index), float(res.argmax_value), stats)
+
+
+def geolocate_arrays(grid: CandidateGrid, states: np.ndarray, captures: np.ndarray,
+                     sample_rate_hz: float, center_freq_hz: float,
+                     options: GeolocateOptions | None = None, **kw) -> GeolocateResult:
+    """Host arrays in ([S,R,6] states, [S,R,N] captures), host results out."""
+    options = options or GeolocateOptions()
+    snaps, keep = _snapshots_struct(states, captures, sample_rate_hz, center_freq_hz)
+    kw.setdefault("want_per_snapshot", options.keep_per_snapshot)
+    return _run(grid, options, captures.shape[0],
+                lambda o, r: lib.dg_geolocate_snapshots(grid.engine.handle, grid.handle,
+                                                        C.byref(snaps), o, r), **kw)
+
+
+def geolocate_staged(grid: CandidateGrid, staged: StagedSnapshots,
+                     options: GeolocateOptions | None = None, **kw) -> GeolocateResult:
+    """Inputs already resident in HBM (the bench's device-only `value`)."""
+    options = options or GeolocateOptions()
+    kw.setdefault("want_per_snapshot", False)
+    return _run(grid, options, staged.shape[0],
+                lambda o, r: lib.dg_geolocate_staged(grid.engine.handle, grid.handle,
+                                                     staged.handle, o, r), **kw)
+
+
+def geolocate_snapshots(snapshots: list, grid: CandidateGrid,
+                        options: GeolocateOptions | None = None) -> GeolocateResult:
+    """geolocate.hpp:127-146 — same inputs/outputs as the reference driver."""
+    options = options or GeolocateOptions()
+    if not snapshots:
+        raise ValueError("geolocate_snapshots: no snapshots")
+    if options.backend_name != "b200":
+        raise ValueError(f"make_backend: unknown backend '{options.backend_name}' "
+                         "(expected b200)")
+    R = len(snapshots[0].captures)
+    if R < 2:
+        raise ValueError("correlate_snapshot_all_pairs: need >= 2 receivers")
+    c0 = snapshots[0].captures[0]
+    for snap in snapshots:
+        if len(snap.captures) != R:
+            raise ValueError("geolocate_snapshots: receiver count differs between snapshots")
+        for c in snap.captures:
+            c.validate()
+            if c.sample_rate_hz != c0.sample_rate_hz:
+                raise ValueError("backend stage: sample rates differ")
+            if len(c.samples) != len(c0.samples):
+                raise ValueError("backend stage: sample counts differ")
+    f32 = all(np.asarray(c.samples).dtype == np.complex64 for s in snapshots for c in s.captures)
+    caps = np.stack([np.stack([np.asarray(c.samples) for c in s.captures]) for s in snapshots])
+    caps = caps.astype(np.complex64 if f32 else np.complex128, copy=False)
+    states = np.stack([np.asarray(s.states, np.float64).reshape(R, 6) for s in snapshots])
+    plan_batches(grid.size(), options.batch_size, options.memory_budget_bytes,
+                 2 * len(c0.samples) * 16)
+    return geolocate_arrays(grid, states, caps, c0.sample_rate_hz, c0.center_freq_hz, options)
