@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: grid-point x time-step correlations/s for the full-grid solve.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C3]
+
+One step = one full-grid solve of the workload (BASELINE.json config C3 by
+default: 2001x2001 candidates at 1 km x 50 snapshots x 50,000 samples, four
+emitters at -20 dB): bit-exact geometry, FP32 correlator, FP64 refinement,
+accumulation, exact argmax and detect_emitters, all on the GPU.
+
+* value     — device time with captures already resident in HBM (CUDA events
+              on the launching stream, max over ranks), L2 flushed between steps.
+* e2e       — the same solve through the public API with host (pinned) captures:
+              H2D of every capture and D2H of the accumulated surface inside the
+              timed region.
+* roofline  — the correlator kernel: 20 FLOP per overlapping sample (the
+              reference kernel as executed) x sum N_ov / its
+              event time, against the FP32 CUDA-core peak measured in-process.
+* cpu_baseline / --impl reference — the reference's own CPU path (oracle/_ref,
+              compiled from the unmodified reference headers) on this host's
+              cores, on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): the grid is split into contiguous latitude slabs, one per
+rank; the only exchange is the final argmax all-gather over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    # name: (half-span km, snapshots, samples, fs, emitters-kind, snr dB, seed)
+    "C1": dict(half_km=50.0, snapshots=1, samples=250_000, fs=5e6, emitters="tone", snr=-5.0,
+               seed=1),
+    "C2": dict(half_km=250.0, snapshots=10, samples=50_000, fs=5e6, emitters="chirp", snr=-10.0,
+               seed=2),
+    "C3": dict(half_km=1000.0, snapshots=50, samples=50_000, fs=5e6, emitters="four", snr=-20.0,
+               seed=3),
+    "C5": dict(half_km=2000.0, snapshots=100, samples=50_000, fs=5e6, emitters="four", snr=-20.0,
+               seed=5),
+}
+FC = 1575.42e6
+METRIC = "grid-point·time-step correlations/sec (full-grid solve)"
+UNIT = "correlations/s"
+FLOP_PER_SAMPLE = 20.0  # correlate.hpp:60-68 as executed
+
+
+def make_inputs(cfg: dict, spacing_km: float = 1.0, n_snapshots: int | None = None):
+    from paper_2508_06672_b200 import scene
+    em = {"four": scene.FOUR_EMITTERS, "tone": [("tone", 0.0, 0.0, {})],
+          "chirp": [("chirp", 0.0, 0.0, {})]}[cfg["emitters"]]
+    S = n_snapshots or cfg["snapshots"]
+    states, caps = scene.synthesize(S, cfg["samples"], cfg["fs"], em, cfg["snr"], seed=cfg["seed"])
+    h = cfg["half_km"] * scene.KM_DEG
+    bounds = (-h, h, -h, h)
+    return states, caps, bounds, spacing_km * scene.KM_DEG
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "n_samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref) — run in a child process under a watchdog
+# because the reference's ParallelBatchedBackend can deadlock.
+def ref_worker(args):
+    from oracle.bindings import RefLib
+    ref = RefLib()
+    cfg = WORKLOADS[args.config]
+    states, caps, bounds, spacing = make_inputs(cfg, args.sample_km, args.sample_snapshots)
+    workers = os.cpu_count() or 1
+    times = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = ref.geolocate(states, caps, cfg["fs"], FC, bounds, spacing, 0.0, backend="parallel",
+                            workers=workers, batch_size=4096)
+        times.append(time.perf_counter() - t0)
+    P = len(res["accumulated"])
+    print(json.dumps({"times": times[args.warmup:], "points": P,
+                      "snapshots": int(caps.shape[0]), "workers": workers,
+                      "argmax": int(np.argmax(res["accumulated"]))}))
+
+
+def run_ref_child(args, steps, warmup, sample_km, sample_snapshots, timeout):
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-worker", "--config", args.config,
+           "--steps", str(steps), "--warmup", str(warmup), "--sample-km", str(sample_km),
+           "--sample-snapshots", str(sample_snapshots)]
+    hangs = 0
+    for _attempt in range(2):
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        except subprocess.TimeoutExpired:
+            hangs += 1
+            continue
+        if out.returncode == 0:
+            d = json.loads(out.stdout.strip().splitlines()[-1])
+            d["hangs"] = hangs
+            return d
+        raise RuntimeError(out.stderr[-2000:])
+    raise RuntimeError(f"reference CPU path hung {hangs} times (TaskPool race, SURVEY.md §5)")
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    d = run_ref_child(args, args.steps, args.warmup, args.sample_km, args.sample_snapshots,
+                      timeout=1800)
+    sec = statistics.mean(d["times"])
+    value = d["points"] * d["snapshots"] / sec
+    sample = (f"{args.config} footprint at {args.sample_km:g} km stride ({d['points']} points) x "
+              f"{d['snapshots']} snapshots, reference geolocate_snapshots with "
+              f"ParallelBatchedBackend({d['workers']}) batch 4096; {cpu_model()}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": d["workers"], "kind": "reference",
+                         "sample": sample, "hangs": d["hangs"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def b200_arm(args, rank, world):
+    import torch
+
+    import paper_2508_06672_b200 as b2
+    from paper_2508_06672_b200._capi import lib
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    cfg = WORKLOADS[args.config]
+    states, caps, bounds, spacing = make_inputs(cfg, args.spacing_km)
+    S, R, N = caps.shape
+    eng = b2.default_engine(dev)
+    full = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing, 0.0, engine=eng)
+    n_lat = full.lat.count
+    r0, r1 = rank * n_lat // world, (rank + 1) * n_lat // world
+    grid = full.slab(r0, r1)
+    P_total, P = full.size(), grid.size()
+    staged = b2.StagedSnapshots(states, caps, cfg["fs"], FC, engine=eng)
+    opts = b2.GeolocateOptions(k_sigma=5.0, exclusion_radius_cells=5, detect=(world == 1))
+    stream = torch.cuda.current_stream()
+    acc_dev = torch.empty(P, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def solve(profile=False):
+        res = b2.geolocate_staged(grid, staged, opts, want_surface=False,
+                                  accumulated_device=acc_dev.data_ptr(),
+                                  stream=stream.cuda_stream, profile=profile)
+        best = (res.argmax_value, res.argmax_index)
+        if dist is not None:  # the one exchange: global argmax over slabs
+            t = torch.tensor([res.argmax_value, float(res.argmax_index)], dtype=torch.float64,
+                             device="cuda")
+            allt = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            cand = [(float(a[0]), int(a[1])) for a in allt]
+            best = max(cand, key=lambda vi: (vi[0], -vi[1]))
+        return res, best
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    stats = []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # outside the events: L2 starts cold every step
+            ev[k][0].record(stream)
+            res, best = solve(profile=True)
+            ev[k][1].record(stream)
+            stats.append(res.stats)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    ms_step = sum(ms) / len(ms)
+    if dist is not None:
+        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = P_total * S / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (the correlator), this rank's launches
+    corr_ms = statistics.mean(s["correlate_ms"] for s in stats)
+    ovl = stats[0]["sum_overlap_samples"]
+    achieved = FLOP_PER_SAMPLE * ovl / (corr_ms * 1e-3) / 1e12
+    peak = ctypes_peak(lib, dev)
+    launches = sum(s["kernel_launches"] for s in stats) // len(stats)
+
+    # e2e: host (pinned) captures in, accumulated surface out, through the public API
+    pinned = torch.empty(caps.shape, dtype=torch.complex128, pin_memory=True).numpy()
+    pinned[...] = caps
+    e2e_t = []
+    for k in range(args.warmup + args.steps):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = b2.geolocate_arrays(grid, states, pinned, cfg["fs"], FC, opts, want_surface=True,
+                                want_per_snapshot=False)
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            e2e_t.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e_t)
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": P_total * S / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(caps.nbytes + states.nbytes),
+           "d2h_bytes_per_step": int(P * 8 + 4096 * 48),
+           "ms_per_step": e2e_s * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            d = run_ref_child(args, 1, 0, args.sample_km, args.cpu_sample_snapshots, timeout=900)
+            cpu = {"value": d["points"] * d["snapshots"] / d["times"][0], "unit": UNIT,
+                   "cores": d["workers"], "kind": "reference",
+                   "sample": (f"{args.config} footprint at {args.sample_km:g} km stride "
+                              f"({d['points']} points) x {d['snapshots']} snapshots, reference "
+                              f"geolocate_snapshots, ParallelBatchedBackend({d['workers']}) batch "
+                              f"4096, {d['times'][0]:.1f} s; {cpu_model()}"),
+                   "hangs": d["hangs"]}
+        except Exception as e:  # the baseline is reported, never the product
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (paper_2508_06672_b200.scene: 4 emitters, LEO receiver pair, "
+                    "complex Gaussian noise)",
+            "config": {"workload": args.config, "grid": f"{full.lat.count}x{full.lon.count}",
+                       "points": P_total, "snapshots": S, "samples": N,
+                       "spacing_km": args.spacing_km, "parallelism": f"grid lat-slabs x{world}",
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "precision": "FP32 correlator, FP64 geometry/accumulation/refine"},
+            "e2e": e2e,
+            "roofline": {"bound": "fp32", "kernel": "k_correlate", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": None,
+                         "peak_source": "dg_fp32_peak_tflops FFMA probe in this process",
+                         "flop_per_sample": FLOP_PER_SAMPLE, "sum_overlap_samples": ovl,
+                         "correlate_ms_per_step": corr_ms},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches * args.steps,
+            "argmax": {"index": best[1], "value": best[0]},
+            "refined_elements": stats[0]["n_refined"],
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def ctypes_peak(lib, dev):
+    import ctypes as C
+    v = C.c_double()
+    rc = lib.dg_fp32_peak_tflops(dev, C.byref(v))
+    return v.value if rc == 0 else None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--spacing-km", type=float, default=1.0)
+    ap.add_argument("--sample-km", type=float, default=20.0,
+                    help="reference CPU sample: same footprint at a coarser stride")
+    ap.add_argument("--sample-snapshots", type=int, default=5,
+                    help="snapshots per reference-arm step")
+    ap.add_argument("--cpu-sample-snapshots", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args()
+    if args.ref_worker:
+        return ref_worker(args)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    if world != args.gpus and rank == 0:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    return b200_arm(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -198,6 +198,10 @@ int dg_detect_emitters(dg_engine* engine, const dg_grid* grid, const double* val
 int dg_plan_batches(uint64_t n_points, uint64_t batch_size, uint64_t memory_budget_bytes,
                     uint64_t capture_bytes_total, uint64_t* batch_count);
 
+/* Measured FP32 CUDA-core peak (FFMA, register operands, full occupancy) of
+ * `device` in TFLOP/s: the roofline denominator bench.py reports against. */
+int dg_fp32_peak_tflops(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif
