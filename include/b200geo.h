@@ -201,6 +201,8 @@ int dg_plan_batches(uint64_t n_points, uint64_t batch_size, uint64_t memory_budg
 /* Measured FP32 CUDA-core peak (FFMA, register operands, full occupancy) of
  * `device` in TFLOP/s: the roofline denominator bench.py reports against. */
 int dg_fp32_peak_tflops(int device, double* tflops);
+/* The same issued as packed FP32x2 FMAs (fma.rn.f32x2 / SASS FFMA2). */
+int dg_fp32x2_peak_tflops(int device, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -106,7 +106,6 @@ struct StreamGuard {
     }
 };
 
-int64_t stride_for(int64_t n) { return (n + 31) & ~int64_t(31); }
 
 // geodesy.hpp:31-38
 constexpr double kA = 6378137.0;
@@ -253,11 +252,13 @@ std::unique_ptr<dg_session> make_session(dg_engine* eng, int64_t n1, double fs1,
     auto s = std::make_unique<dg_session>();
     s->eng = eng;
     s->N = n1;
-    s->stride = stride_for(n1);
+    s->stride = capture_stride(n1);
     s->fs = fs1;
     s->y32 = std::make_unique<DevMem>(2 * s->stride * sizeof(float2));
     s->y64 = std::make_unique<DevMem>(2 * s->stride * sizeof(double2));
     CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, s->st));
+    CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, s->st));
     return s;
 }
 
@@ -288,6 +289,12 @@ int dg_engine_create(int device, dg_engine** out) {
         CK(cudaGetDeviceProperties(&prop, device));
         if (prop.major != 10)
             raise(DG_ERUNTIME, std::string("b200: sm_100a build cannot run on ") + prop.name);
+        // keep freed stream-ordered scratch (per-run surfaces, GBs at C3/C5)
+        // mapped in the pool instead of returning it to the driver at every sync
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         auto e = std::make_unique<dg_engine>();
         e->device = device;
         e->sm_count = prop.multiProcessorCount;
@@ -312,8 +319,8 @@ int dg_stage(dg_engine* eng, const double* y1, int64_t n1, double fs1, const dou
              double fs2, dg_session** out) {
     return guard([&] {
         auto s = make_session(eng, n1, fs1, n2, fs2);
-        auto* y64 = static_cast<double2*>(s->y64->p);
-        auto* y32 = static_cast<float2*>(s->y32->p);
+        auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
+        auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
         CK(cudaMemcpyAsync(y64, y1, n1 * sizeof(double2), cudaMemcpyHostToDevice, s->st));
         CK(cudaMemcpyAsync(y64 + s->stride, y2, n1 * sizeof(double2), cudaMemcpyHostToDevice, s->st));
         launch_f64_to_f32(y64, y32, n1, s->st);
@@ -327,8 +334,8 @@ int dg_stage_f32(dg_engine* eng, const float* y1, int64_t n1, double fs1, const 
                  int64_t n2, double fs2, dg_session** out) {
     return guard([&] {
         auto s = make_session(eng, n1, fs1, n2, fs2);
-        auto* y64 = static_cast<double2*>(s->y64->p);
-        auto* y32 = static_cast<float2*>(s->y32->p);
+        auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
+        auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
         CK(cudaMemcpyAsync(y32, y1, n1 * sizeof(float2), cudaMemcpyHostToDevice, s->st));
         CK(cudaMemcpyAsync(y32 + s->stride, y2, n1 * sizeof(float2), cudaMemcpyHostToDevice, s->st));
         launch_f32_to_f64(y32, y64, n1, s->st);
@@ -358,12 +365,12 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
         CK(cudaMemcpyAsync(off, batch, n * sizeof(dg_pair_offsets), cudaMemcpyHostToDevice, s->st));
         launch_offsets_hist(off, n, pl.N, pl.d, pl.fdoa, pl.hist, vals, pl.overlap, s->st);
-        const auto* y32 = static_cast<const float2*>(s->y32->p);
+        const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr, nullptr);
         RefineCtx ctx{};
         ctx.P = n;
         ctx.offsets = off;
-        ctx.y64 = static_cast<const double2*>(s->y64->p);
+        ctx.y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
         ctx.stride = s->stride;
         ctx.N = (int)s->N;
         ctx.fs = s->fs;
@@ -570,7 +577,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
         launch_geometry_hist(g->x, g->y, g->z, P, pg, s->fs, wl, pl.N, pl.d, pl.fdoa, pl.hist, vals,
                              pl.overlap, pl.err, s->st);
-        const auto* y32 = static_cast<const float2*>(s->y32->p);
+        const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr,
                                 nullptr);
         check_err_flag(sc, pl.err);
@@ -586,7 +593,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         ctx.pair_rx = prx;
         ctx.pairs = 1;
         ctx.R = 2;
-        ctx.y64 = static_cast<const double2*>(s->y64->p);
+        ctx.y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
         ctx.stride = s->stride;
         ctx.N = (int)s->N;
         ctx.fs = s->fs;
@@ -625,16 +632,18 @@ int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) 
         s->S = sn->n_snapshots;
         s->R = sn->n_receivers;
         s->N = sn->n_samples;
-        s->stride = stride_for(s->N);
+        s->stride = capture_stride(s->N);
         s->fs = sn->sample_rate_hz;
         s->fc = sn->center_freq_hz;
         s->states.assign(sn->states, sn->states + s->S * s->R);
         const int64_t n_caps = s->S * s->R;
         s->y32 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(float2));
         s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
-        auto* y32 = static_cast<float2*>(s->y32->p);
-        auto* y64 = static_cast<double2*>(s->y64->p);
+        auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
+        auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
         StreamGuard sg(nullptr);
+        CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, sg.st));
+        CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, sg.st));
         for (int64_t c = 0; c < n_caps; ++c) {
             if (sn->captures_iq) {
                 if (!sn->captures_iq[c]) raise(DG_EINVAL, "null capture pointer");
@@ -778,7 +787,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     const int64_t n_words = (n_elems + 31) / 32;
     auto* bits = sc.alloc<uint32_t>(n_words);
     CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
-    const auto* y32 = static_cast<const float2*>(sn->y32->p);
+    const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
 
     for (int s = 0; s < S; ++s)
         for (int q = 0; q < pairs; ++q) {
@@ -805,7 +814,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     ctx.pair_rx = d_prx;
     ctx.pairs = pairs;
     ctx.R = R;
-    ctx.y64 = static_cast<const double2*>(sn->y64->p);
+    ctx.y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
     ctx.stride = sn->stride;
     ctx.N = (int)sn->N;
     ctx.fs = fs;

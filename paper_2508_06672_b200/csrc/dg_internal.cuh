@@ -26,7 +26,16 @@ struct PairGeom {
 // Per-element flag: FP32 result too close to zero for the relative tolerance;
 // re-evaluated in FP64 in the reference's exact operation order.
 constexpr int kWarpsPerCta = 8;
-constexpr int kChunk = 256;  // samples per z-chunk (per warp, smem-staged)
+constexpr int kChunk = 256;  // samples per z-chunk (per warp, TMA-staged in smem)
+
+// Device capture layout: every capture sits in a zero-filled slot of `stride`
+// elements starting kCapturePad elements in, with >= kCaptureTail zeros after
+// it, so the correlator's chunked bulk copies never leave the allocation.
+constexpr int64_t kCapturePad = 32;
+constexpr int64_t kCaptureTail = 512;
+inline int64_t capture_stride(int64_t n) {
+    return (kCapturePad + n + kCaptureTail + 31) & ~int64_t(31);
+}
 constexpr int kL = 16;       // phasor table length (samples per inner block)
 
 // Threshold on S / sqrt(sum |z|^2) below which an FP32 value is re-evaluated

@@ -297,140 +297,6 @@ __global__ void k_build_tasks(int* __restrict__ hist, int nbins, int N, const in
 }
 
 // ---------------------------------------------------------------------------
-// K3: the correlator (Eq. 11, correlate.hpp:44-71) on CUDA cores in FP32.
-//
-// One warp = one task = up to 32 candidates sharing TDOA d. Per 256-sample
-// chunk the warp stages z[k] = y1[k] conj(y2[k+d]) once in shared memory
-// (each lane produces 8 samples), then every lane — one candidate with its own
-// FDOA f — evaluates sum_k z[k] e^{j 2 pi f k} as
-//     sum_b W_b * (sum_{j<16} z[c0+16b+j] E[j]),   E[j] = e^{j 2 pi f j},
-// E held in registers, W_b = e^{j 2 pi f (c0+16b)} advanced by one complex
-// multiply per 16 samples and re-anchored each chunk from an FP64-reduced
-// phase. z is read with 16-byte broadcast LDS (2 samples, all lanes same
-// address). Chunk sums are accumulated in FP64. Cost per sample per
-// candidate: 4 FFMA + 1/2 LDS.128 + 1/2 (W update) + ~1/4 (z production).
-//
-// Elements with S < kRefineTau * sqrt(sum|z|^2) are flagged for the exact FP64
-// re-evaluation (their FP32 relative error could exceed 1e-4).
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
-k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
-            const int* __restrict__ sorted, const double* __restrict__ fdoa,
-            const float2* __restrict__ y1, const float2* __restrict__ y2, int N, double fs,
-            double* __restrict__ s_out, uint32_t* __restrict__ flag_bits, int64_t flag_base) {
-    __shared__ __align__(16) float4 zb[kWarpsPerCta][kChunk / 2];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x * kWarpsPerCta + warp;
-    if (t >= *n_tasks) return;
-    const Task tk = tasks[t];
-    const int d = tk.d;
-    const int p = lane < tk.count ? sorted[tk.start + lane] : -1;
-    const double f = p >= 0 ? fdoa[p] / fs : 0.0;  // cycles per sample
-
-    // phasor table E[j] = e^{j 2 pi f j}, W1 = e^{j 2 pi f L}; FP64 range reduction
-    float er[kL], ei[kL];
-#pragma unroll
-    for (int j = 0; j < kL; ++j) {
-        const double x = f * (double)j;
-        sincospif((float)(2.0 * (x - rint(x))), &ei[j], &er[j]);
-    }
-    float w1r, w1i;
-    {
-        const double x = f * (double)kL;
-        sincospif((float)(2.0 * (x - rint(x))), &w1i, &w1r);
-    }
-
-    const int kb = d < 0 ? -d : 0;
-    const int ke = (N - d) < N ? (N - d) : N;
-    const int kb0 = kb & ~1;  // even chunk origin -> 16-byte aligned y1 pairs
-    float4* zw = zb[warp];
-    double acc_re = 0.0, acc_im = 0.0;
-    float z2 = 0.f;
-    const bool d_even = (d & 1) == 0;
-
-    for (int c0 = kb0; c0 < ke; c0 += kChunk) {
-        // ---- produce z for [c0, c0 + kChunk) ----
-#pragma unroll
-        for (int i = 0; i < kChunk / 64; ++i) {
-            const int q = lane + 32 * i;
-            const int k = c0 + 2 * q;
-            float2 a0, a1, b0, b1;
-            if (k >= kb && k + 1 < ke) {
-                const float4 a = *reinterpret_cast<const float4*>(y1 + k);
-                a0 = make_float2(a.x, a.y);
-                a1 = make_float2(a.z, a.w);
-                if (d_even) {
-                    const float4 b = *reinterpret_cast<const float4*>(y2 + k + d);
-                    b0 = make_float2(b.x, b.y);
-                    b1 = make_float2(b.z, b.w);
-                } else {
-                    b0 = y2[k + d];
-                    b1 = y2[k + d + 1];
-                }
-            } else {
-                const bool v0 = k >= kb && k < ke, v1 = k + 1 >= kb && k + 1 < ke;
-                a0 = v0 ? y1[k] : make_float2(0.f, 0.f);
-                b0 = v0 ? y2[k + d] : make_float2(0.f, 0.f);
-                a1 = v1 ? y1[k + 1] : make_float2(0.f, 0.f);
-                b1 = v1 ? y2[k + 1 + d] : make_float2(0.f, 0.f);
-            }
-            float4 zz;
-            zz.x = fmaf(a0.x, b0.x, a0.y * b0.y);
-            zz.y = fmaf(a0.y, b0.x, -(a0.x * b0.y));
-            zz.z = fmaf(a1.x, b1.x, a1.y * b1.y);
-            zz.w = fmaf(a1.y, b1.x, -(a1.x * b1.y));
-            z2 = fmaf(zz.x, zz.x, fmaf(zz.y, zz.y, fmaf(zz.z, zz.z, fmaf(zz.w, zz.w, z2))));
-            zw[q] = zz;
-        }
-        __syncwarp();
-
-        // ---- anchor W = e^{j 2 pi f c0} from the FP64-reduced phase ----
-        float wr, wi;
-        {
-            const double x = f * (double)c0;
-            sincospif((float)(2.0 * (x - rint(x))), &wi, &wr);
-        }
-        float ar = 0.f, ai = 0.f;
-#pragma unroll
-        for (int b = 0; b < kChunk / kL; ++b) {
-            float cr = 0.f, ci = 0.f;
-#pragma unroll
-            for (int j = 0; j < kL; j += 2) {
-                const float4 z = zw[(b * kL + j) >> 1];
-                cr = fmaf(z.x, er[j], cr);
-                cr = fmaf(-z.y, ei[j], cr);
-                ci = fmaf(z.x, ei[j], ci);
-                ci = fmaf(z.y, er[j], ci);
-                cr = fmaf(z.z, er[j + 1], cr);
-                cr = fmaf(-z.w, ei[j + 1], cr);
-                ci = fmaf(z.z, ei[j + 1], ci);
-                ci = fmaf(z.w, er[j + 1], ci);
-            }
-            ar = fmaf(wr, cr, ar);
-            ar = fmaf(-wi, ci, ar);
-            ai = fmaf(wr, ci, ai);
-            ai = fmaf(wi, cr, ai);
-            const float nr = fmaf(wr, w1r, -(wi * w1i));
-            wi = fmaf(wr, w1i, wi * w1r);
-            wr = nr;
-        }
-        acc_re += (double)ar;
-        acc_im += (double)ai;
-        __syncwarp();
-    }
-
-#pragma unroll
-    for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
-    if (p >= 0) {
-        const double s = sqrt(acc_re * acc_re + acc_im * acc_im);
-        s_out[p] = s;
-        if (s < (double)kRefineTau * sqrt((double)z2)) {
-            const int64_t e = flag_base + p;
-            atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Refinement: compact the flag bitmap and re-evaluate those elements exactly.
 __global__ void k_count_flags(const uint32_t* __restrict__ bits, int64_t n_words,
                               unsigned long long* __restrict__ count) {
@@ -880,15 +746,6 @@ void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor
     k_scan<<<1, kScanThreads, 0, st>>>(hist, nbins, off, toff, cursor, n_tasks);
     k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
     k_build_tasks<<<blocks_for(nbins, 256), 256, 0, st>>>(hist, nbins, N, off, toff, tasks);
-}
-
-void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
-                      const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
-                      double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st) {
-    const int blocks = (max_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (blocks <= 0) return;
-    k_correlate<<<blocks, 32 * kWarpsPerCta, 0, st>>>(tasks, n_tasks, sorted, fdoa, y1, y2, N, fs,
-                                                      s_out, flag_bits, flag_base);
 }
 
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,

@@ -68,6 +68,11 @@ def scene_case(name):
 
 if __name__ == "__main__":
     print(b2.default_engine().descriptor())
+    import ctypes as C
+    from paper_2508_06672_b200._capi import lib
+    v = C.c_double()
+    lib.dg_fp32_peak_tflops(0, C.byref(v)); print("FFMA peak TFLOP/s", v.value)
+    lib.dg_fp32x2_peak_tflops(0, C.byref(v)); print("FFMA2 peak TFLOP/s", v.value)
     # grid + offsets bit-exact
     grid = b2.build_candidate_grid(b2.LatLonBounds(-1.0, 1.0, 10.0, 11.0), 0.25, 120.0)
     nl, nn, pts = ref.build_grid((-1.0, 1.0, 10.0, 11.0), 0.25, 120.0)
