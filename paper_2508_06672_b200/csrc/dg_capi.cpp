@@ -872,10 +872,11 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
             CK(cudaStreamSynchronize(st));
             if (hn <= kRerankCap || rel < 1e-12) break;
         }
-        launch_rerank(cells, n_cells, kRerankCap, SP, ctx, st);
-        launch_recombine_cells(cells, n_cells, kRerankCap, raw, S, pairs, P,
-                               pairs > 1 ? grids : nullptr, medians, acc, st);
-        launch_argmax_cells(cells, n_cells, kRerankCap, acc, best_i, best_v, st);
+        auto* ex = sc.alloc<double>((int64_t)kRerankCap * SP);
+        auto* acc_ex = sc.alloc<double>(kRerankCap);
+        launch_rerank(cells, n_cells, kRerankCap, SP, ctx, ex, st);
+        launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, st);
+        launch_argmax_cells(cells, n_cells, kRerankCap, acc_ex, best_i, best_v, st);
         launches += 3;
         long long bi = 0;
         double bv = 0.0;

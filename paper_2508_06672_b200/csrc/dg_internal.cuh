@@ -96,12 +96,11 @@ void launch_max(const double* v, int64_t P, double* partial, int n_partial, doub
                 cudaStream_t st);
 void launch_select_near(const double* v, int64_t P, const double* vmax, double rel,
                         int* list, int* count, int cap, cudaStream_t st);
-void launch_rerank(const int* cells, const int* n_cells, int cap, int S, RefineCtx ctx,
-                   cudaStream_t st);
-void launch_recombine_cells(const int* cells, const int* n_cells, int cap, const double* raw,
-                            int S, int pairs, int64_t P, double* grids, const double* medians,
-                            double* acc, cudaStream_t st);
-void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc,
+void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
+                   double* ex /* [cap][SP] */, cudaStream_t st);
+void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
+                            const double* medians, double* acc_ex, cudaStream_t st);
+void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc_ex,
                          long long* best_idx, double* best_val, cudaStream_t st);
 // median (nth_element rank P/2) of nonnegative doubles by 4-pass radix select
 void launch_median(const double* v, int64_t P, unsigned* hist, unsigned long long* state,

@@ -429,42 +429,43 @@ __global__ void k_select_near(const double* __restrict__ v, int64_t P,
     }
 }
 
+// Exact re-evaluation of the near-peak candidates into a private buffer
+// ex[ci * SP + sp] (the returned surfaces are left untouched so they stay
+// independent of how the grid is partitioned).
 __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ n_cells, int cap,
-                         int SP, RefineCtx c) {
+                         int SP, RefineCtx c, double* __restrict__ ex) {
     const int n = min(*n_cells, cap);
     const int64_t total = (int64_t)n * SP;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t ci = i / SP, sp = i - ci * SP;
-        const int64_t p = cells[ci];
-        c.raw[sp * c.P + p] = exact_element(c, sp, p);
+        ex[i] = exact_element(c, sp, cells[ci]);
     }
 }
 
-__global__ void k_recombine_cells(const int* __restrict__ cells, const int* __restrict__ n_cells,
-                                  int cap, const double* __restrict__ raw, int S, int pairs,
-                                  int64_t P, double* __restrict__ grids,
-                                  const double* __restrict__ medians, double* __restrict__ acc) {
+// per candidate: pair sums (correlate_snapshot_all_pairs), optional median
+// scaling, accumulation over snapshots in order (accumulate_grids)
+__global__ void k_recombine_cells(const int* __restrict__ n_cells, int cap,
+                                  const double* __restrict__ ex, int S, int pairs,
+                                  const double* __restrict__ medians, double* __restrict__ acc_ex) {
     const int n = min(*n_cells, cap);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int64_t p = cells[i];
+        const double* r = ex + (int64_t)i * S * pairs;
         double a = 0.0;
         for (int s = 0; s < S; ++s) {
-            const double* r = raw + (int64_t)s * pairs * P + p;
-            double g = r[0];
-            for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[q * P]);
+            double g = r[s * pairs];
+            for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[s * pairs + q]);
             if (medians && medians[s] > 0.0) g = __ddiv_rn(g, medians[s]);
-            if (grids) grids[(int64_t)s * P + p] = g;
             a = s ? __dadd_rn(a, g) : g;
         }
-        acc[p] = a;
+        acc_ex[i] = a;
     }
 }
 
 // single block: exact max over the re-ranked cells, lowest flat index on ties
 // (std::max_element keeps the first maximum)
 __global__ void k_argmax_cells(const int* __restrict__ cells, const int* __restrict__ n_cells,
-                               int cap, const double* __restrict__ acc,
+                               int cap, const double* __restrict__ acc_ex,
                                long long* __restrict__ best_idx, double* __restrict__ best_val) {
     __shared__ double sv[1024];
     __shared__ long long si[1024];
@@ -473,7 +474,7 @@ __global__ void k_argmax_cells(const int* __restrict__ cells, const int* __restr
     long long bi = LLONG_MAX;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const long long p = cells[i];
-        const double v = acc[p];
+        const double v = acc_ex[i];
         if (v > bv || (v == bv && p < bi)) {
             bv = v;
             bi = p;
@@ -788,21 +789,20 @@ void launch_select_near(const double* v, int64_t P, const double* vmax, double r
 }
 
 void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
-                   cudaStream_t st) {
+                   double* ex, cudaStream_t st) {
     k_rerank<<<blocks_for((int64_t)cap * SP, 64, 148LL * 64), 64, 0, st>>>(cells, n_cells, cap, SP,
-                                                                          ctx);
+                                                                          ctx, ex);
 }
 
-void launch_recombine_cells(const int* cells, const int* n_cells, int cap, const double* raw, int S,
-                            int pairs, int64_t P, double* grids, const double* medians,
-                            double* acc, cudaStream_t st) {
-    k_recombine_cells<<<blocks_for(cap, 128), 128, 0, st>>>(cells, n_cells, cap, raw, S, pairs, P,
-                                                            grids, medians, acc);
+void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
+                            const double* medians, double* acc_ex, cudaStream_t st) {
+    k_recombine_cells<<<blocks_for(cap, 128), 128, 0, st>>>(n_cells, cap, ex, S, pairs, medians,
+                                                            acc_ex);
 }
 
-void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc,
+void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc_ex,
                          long long* best_idx, double* best_val, cudaStream_t st) {
-    k_argmax_cells<<<1, 1024, 0, st>>>(cells, n_cells, cap, acc, best_idx, best_val);
+    k_argmax_cells<<<1, 1024, 0, st>>>(cells, n_cells, cap, acc_ex, best_idx, best_val);
 }
 
 void launch_median(const double* v, int64_t P, unsigned* hist, unsigned long long* state,
