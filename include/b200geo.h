@@ -152,6 +152,10 @@ typedef struct {
     int detect;                 /* run detect_emitters on the accumulated surface */
     void* stream;               /* cudaStream_t to launch on; NULL = private stream */
     int profile;                /* record per-kernel CUDA events into dg_result stats */
+    int patch_peak;             /* write the exact FP64 values of the re-ranked near-peak
+                                   cells into the HOST surfaces (default 1) so max_element on
+                                   them is the exact argmax; 0 keeps every cell the FP32-path
+                                   value, bit-identical under any grid partition */
 } dg_options;
 
 typedef struct {

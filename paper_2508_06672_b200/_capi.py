@@ -48,7 +48,7 @@ class dg_snapshots(C.Structure):
 class dg_options(C.Structure):
     _fields_ = [("k_sigma", C.c_double), ("exclusion_radius_cells", C.c_int),
                 ("normalize_per_snapshot", C.c_int), ("detect", C.c_int),
-                ("stream", C.c_void_p), ("profile", C.c_int)]
+                ("stream", C.c_void_p), ("profile", C.c_int), ("patch_peak", C.c_int)]
 
 
 class dg_result(C.Structure):

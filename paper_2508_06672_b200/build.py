@@ -71,7 +71,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         _run(cmd)
         objs.append(obj)
     tmp = OUT + ".tmp"
-    _run([nvcc, "-shared", *ARCH, "-o", tmp, *objs])
+    _run([nvcc, "-shared", *ARCH, "-Xlinker", "-soname=libb200geo.so", "-o", tmp, *objs])
     os.replace(tmp, OUT)
     return OUT
 

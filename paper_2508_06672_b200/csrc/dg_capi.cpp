@@ -275,6 +275,7 @@ void dg_options_default(dg_options* o) {
     o->k_sigma = 5.0;
     o->exclusion_radius_cells = 5;
     o->detect = 1;
+    o->patch_peak = 1;
 }
 
 int dg_engine_create(int device, dg_engine** out) {
@@ -863,6 +864,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     CK(cudaMemcpyAsync(&hmax, vmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     int hn = 0;
+    double *acc_ex = nullptr, *grid_ex = nullptr;
     if (hmax > 0.0) {
         for (double rel = 1e-5;; rel *= 0.1) {
             CK(cudaMemsetAsync(n_cells, 0, sizeof(int), st));
@@ -873,9 +875,10 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
             if (hn <= kRerankCap || rel < 1e-12) break;
         }
         auto* ex = sc.alloc<double>((int64_t)kRerankCap * SP);
-        auto* acc_ex = sc.alloc<double>(kRerankCap);
+        acc_ex = sc.alloc<double>(kRerankCap);
+        grid_ex = sc.alloc<double>((int64_t)kRerankCap * S);
         launch_rerank(cells, n_cells, kRerankCap, SP, ctx, ex, st);
-        launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, st);
+        launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, grid_ex, st);
         launch_argmax_cells(cells, n_cells, kRerankCap, acc_ex, best_i, best_v, st);
         launches += 3;
         long long bi = 0;
@@ -906,6 +909,22 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     unsigned long long ovl = 0;
     CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (opt.patch_peak && acc_ex && res->n_reranked > 0 && (res->accumulated || res->per_snapshot)) {
+        // exact FP64 values of the re-ranked cells into the host copies
+        const int n = (int)res->n_reranked;
+        std::vector<int> hc(n);
+        std::vector<double> ha(n), hg((size_t)n * S);
+        CK(cudaMemcpyAsync(hc.data(), cells, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ha.data(), acc_ex, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hg.data(), grid_ex, (size_t)n * S * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int i = 0; i < n; ++i) {
+            if (res->accumulated) res->accumulated[hc[i]] = ha[i];
+            if (res->per_snapshot)
+                for (int s = 0; s < S; ++s) res->per_snapshot[(int64_t)s * P + hc[i]] = hg[(size_t)i * S + s];
+        }
+    }
     res->sum_overlap_samples = (double)ovl;
     res->kernel_launches = launches;
     res->correlate_launches = SP;

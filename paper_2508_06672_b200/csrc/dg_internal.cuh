@@ -99,7 +99,8 @@ void launch_select_near(const double* v, int64_t P, const double* vmax, double r
 void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
                    double* ex /* [cap][SP] */, cudaStream_t st);
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
-                            const double* medians, double* acc_ex, cudaStream_t st);
+                            const double* medians, double* acc_ex, double* grid_ex /* [cap][S] */,
+                            cudaStream_t st);
 void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc_ex,
                          long long* best_idx, double* best_val, cudaStream_t st);
 // median (nth_element rank P/2) of nonnegative doubles by 4-pass radix select

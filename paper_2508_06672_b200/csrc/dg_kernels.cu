@@ -447,7 +447,8 @@ __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ 
 // scaling, accumulation over snapshots in order (accumulate_grids)
 __global__ void k_recombine_cells(const int* __restrict__ n_cells, int cap,
                                   const double* __restrict__ ex, int S, int pairs,
-                                  const double* __restrict__ medians, double* __restrict__ acc_ex) {
+                                  const double* __restrict__ medians, double* __restrict__ acc_ex,
+                                  double* __restrict__ grid_ex) {
     const int n = min(*n_cells, cap);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const double* r = ex + (int64_t)i * S * pairs;
@@ -456,6 +457,7 @@ __global__ void k_recombine_cells(const int* __restrict__ n_cells, int cap,
             double g = r[s * pairs];
             for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[s * pairs + q]);
             if (medians && medians[s] > 0.0) g = __ddiv_rn(g, medians[s]);
+            grid_ex[(int64_t)i * S + s] = g;
             a = s ? __dadd_rn(a, g) : g;
         }
         acc_ex[i] = a;
@@ -795,9 +797,10 @@ void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, Refine
 }
 
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
-                            const double* medians, double* acc_ex, cudaStream_t st) {
+                            const double* medians, double* acc_ex, double* grid_ex,
+                            cudaStream_t st) {
     k_recombine_cells<<<blocks_for(cap, 128), 128, 0, st>>>(n_cells, cap, ex, S, pairs, medians,
-                                                            acc_ex);
+                                                            acc_ex, grid_ex);
 }
 
 void launch_argmax_cells(const int* cells, const int* n_cells, int cap, const double* acc_ex,

@@ -67,6 +67,7 @@ class GeolocateOptions:
     normalize_per_snapshot: bool = False
     keep_per_snapshot: bool = True   # the reference always keeps them (geolocate.hpp:108)
     detect: bool = True
+    patch_peak: bool = True  # exact FP64 values at the re-ranked near-peak cells of host surfaces
 
 
 @dataclass
@@ -181,6 +182,7 @@ def _options(options: GeolocateOptions, stream=None, profile=False) -> _capi.dg_
     o.detect = int(bool(options.detect))
     o.stream = stream
     o.profile = int(bool(profile))
+    o.patch_peak = int(bool(options.patch_peak))
     return o
 
 

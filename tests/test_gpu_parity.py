@@ -279,7 +279,8 @@ def test_geolocate_scene_vs_reference(b2, ref, name):
     # argmax: bit-exact index and bit-identical exact value
     assert res.argmax_index == int(np.argmax(want["accumulated"])) == want_g["argmax"]
     assert res.argmax_value == float.fromhex(want_g["argmax_value"])
-    assert acc[res.argmax_index] == pytest.approx(res.argmax_value, rel=REL_TOL)
+    assert acc[res.argmax_index] == res.argmax_value  # patch_peak: exact value in the surface
+    assert int(np.argmax(acc)) == res.argmax_index
     # detections: identical cells and order
     assert [d.grid_index for d in res.detections] == want_g["detections"] == \
         [d["grid_index"] for d in want["detections"]]
@@ -344,7 +345,7 @@ def test_slab_sharding_bit_identical(b2, ref):
     from paper_2508_06672_b200.sharding import merge_argmax, slab_rows
     sc = load_scene(ref, "DESK_FOURJAM")
     grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
-    opts = b2.GeolocateOptions(detect=False)
+    opts = b2.GeolocateOptions(detect=False, patch_peak=False)
     full = b2.geolocate_arrays(grid, sc.states, sc.captures, sc.fs, sc.fc, opts)
     for world in (2, 3, 8):
         parts, peaks = [], []
