@@ -315,7 +315,10 @@ def b200_arm(args, rank, world):
             "e2e": e2e,
             "roofline": {"bound": "fp32", "kernel": "k_correlate", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None,
+                         "frac_mac_8flop": achieved * 8.0 / FLOP_PER_SAMPLE / peak,
+                         "traffic": ncu_traffic(),
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per "
+                                           "k_correlate launch, profiles/r01_ncu_correlate.txt",
                          "peak_source": "dg_fp32_peak_tflops FFMA probe in this process",
                          "flop_per_sample": FLOP_PER_SAMPLE, "sum_overlap_samples": ovl,
                          "correlate_ms_per_step": corr_ms},
@@ -328,6 +331,21 @@ def b200_arm(args, rank, world):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def ncu_traffic():
+    """DRAM bytes per correlator launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_correlate.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[parts[-2]]
+                vals[parts[0]] = float(parts[-1]) * scale
+        return sum(vals.values()) if len(vals) == 2 else None
+    except OSError:
+        return None
 
 
 def ctypes_peak(lib, dev):
