@@ -185,7 +185,7 @@ struct Pipeline {
         P = P_;
         N = (int)N_;
         nbins = 2 * N - 1;
-        const int64_t mt = P / 32 + std::min<int64_t>(P, nbins) + 1;
+        const int64_t mt = P / correlate_task_size() + std::min<int64_t>(P, nbins) + 1;
         max_tasks = (int)std::min<int64_t>(mt, INT32_MAX);
         d = sc.alloc<int>(P);
         sorted = sc.alloc<int>(P);

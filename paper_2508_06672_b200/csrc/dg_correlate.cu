@@ -91,9 +91,11 @@ struct alignas(16) WarpSmemT {
 
 }  // namespace
 
-// LB: phasor-table length (samples per block); CH: samples per staged chunk.
-template <int LB, int CH>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 2)
+// NC: candidates per lane (a warp task holds up to 32*NC candidates of one d);
+// LB: phasor-table length (samples per block); CH: samples per staged chunk;
+// WPC: warps per CTA; MINB: CTAs per SM the register budget is sized for.
+template <int NC, int LB, int CH, int WPC, int MINB>
+__global__ void __launch_bounds__(32 * WPC, MINB)
 k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
             const int* __restrict__ sorted, const double* __restrict__ fdoa,
             const float2* __restrict__ y1, const float2* __restrict__ y2, int N, double fs,
@@ -102,12 +104,18 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
-    const int t = blockIdx.x * kWarpsPerCta + warp;
+    const int t = blockIdx.x * WPC + warp;
     if (t >= *n_tasks) return;
     const Task tk = tasks[t];
     const int d = tk.d;
-    const int p = lane < tk.count ? sorted[tk.start + lane] : -1;
-    const double f = p >= 0 ? fdoa[p] / fs : 0.0;  // cycles per sample
+    int p[NC];
+    double f[NC];  // cycles per sample
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int slot = lane + 32 * c;
+        p[c] = slot < tk.count ? sorted[tk.start + slot] : -1;
+        f[c] = p[c] >= 0 ? fdoa[p[c]] / fs : 0.0;
+    }
 
     const int kb = d < 0 ? -d : 0;
     const int ke = (N - d) < N ? (N - d) : N;
@@ -131,30 +139,32 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
     };
     if (lane == 0) issue(0, 0);
 
-    // phasor table E[j] = e^{j 2 pi f j} and the block step W1 = e^{j 2 pi f LB},
+    // phasor tables E[j] = e^{j 2 pi f j} and block steps W1 = e^{j 2 pi f LB},
     // FP64 range reduction, then single-precision sincospi of the fraction
-    float er[LB], ei[LB];
+    float er[NC][LB], ei[NC][LB], w1r[NC], w1i[NC];
 #pragma unroll
-    for (int j = 0; j < LB; ++j) {
-        const double x = f * (double)j;
-        sincospif((float)(2.0 * (x - rint(x))), &ei[j], &er[j]);
-    }
-    float w1r, w1i;
-    {
-        const double x = f * (double)LB;
-        sincospif((float)(2.0 * (x - rint(x))), &w1i, &w1r);
+    for (int c = 0; c < NC; ++c) {
+#pragma unroll
+        for (int j = 0; j < LB; ++j) {
+            const double x = f[c] * (double)j;
+            sincospif((float)(2.0 * (x - rint(x))), &ei[c][j], &er[c][j]);
+        }
+        const double x = f[c] * (double)LB;
+        sincospif((float)(2.0 * (x - rint(x))), &w1i[c], &w1r[c]);
     }
 
-    double acc_re = 0.0, acc_im = 0.0;
+    double acc_re[NC], acc_im[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc_re[c] = acc_im[c] = 0.0;
     float z2 = 0.f;
-    for (int c = 0; c < n_chunks; ++c) {
-        const int buf = c & 1;
-        const int c0 = kb0 + c * CH;
-        if (lane == 0 && c + 1 < n_chunks) {
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int buf = ch & 1;
+        const int c0 = kb0 + ch * CH;
+        if (lane == 0 && ch + 1 < n_chunks) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(c + 1, buf ^ 1);
+            issue(ch + 1, buf ^ 1);
         }
-        mbar_wait(&ws.bar[buf], (c >> 1) & 1);
+        mbar_wait(&ws.bar[buf], (ch >> 1) & 1);
 
         // ---- z = y1 conj(y2), zero outside [kb, ke); written over y1 in place ----
         float4* zq = reinterpret_cast<float4*>(ws.y1[buf]);
@@ -178,48 +188,68 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
 
         // ---- blocks in reverse, Horner: H = (((C_last) W1 + C_last-1) W1 + ...) ----
         //      chunk sum = W(c0) * H,  C_b = sum_j z[c0 + LB b + j] E[j]
-        float hr = 0.f, hi = 0.f;
+        float hr[NC], hi[NC];
 #pragma unroll
-        for (int b = CH / LB - 1; b >= 0; --b) {
-            float2 A0 = make_float2(0.f, 0.f), B0 = A0, A1 = A0, B1 = A0;
+        for (int c = 0; c < NC; ++c) hr[c] = hi[c] = 0.f;
+        constexpr int QB = LB / 2;        // z quads (2 samples each) per block
+        constexpr int NB = CH / LB;       // blocks per chunk
+        float4 znext = zq[(NB - 1) * QB];  // rolling one-quad-ahead prefetch
 #pragma unroll
-            for (int j = 0; j < LB; j += 4) {
-                const float4 za = zq[(b * LB + j) >> 1];
-                const float4 zb = zq[(b * LB + j + 2) >> 1];
-                A0 = ffma2(make_float2(za.x, za.y), er[j], A0);
-                B0 = ffma2(make_float2(za.x, za.y), ei[j], B0);
-                A1 = ffma2(make_float2(za.z, za.w), er[j + 1], A1);
-                B1 = ffma2(make_float2(za.z, za.w), ei[j + 1], B1);
-                A0 = ffma2(make_float2(zb.x, zb.y), er[j + 2], A0);
-                B0 = ffma2(make_float2(zb.x, zb.y), ei[j + 2], B0);
-                A1 = ffma2(make_float2(zb.z, zb.w), er[j + 3], A1);
-                B1 = ffma2(make_float2(zb.z, zb.w), ei[j + 3], B1);
+        for (int b = NB - 1; b >= 0; --b) {
+            float2 A[NC], B[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) A[c] = B[c] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int jj = 0; jj < QB; ++jj) {
+                const float4 zz = znext;
+                if (jj + 1 < QB)
+                    znext = zq[b * QB + jj + 1];
+                else if (b > 0)
+                    znext = zq[(b - 1) * QB];
+                const int j = 2 * jj;
+                const float2 z0 = make_float2(zz.x, zz.y), z1 = make_float2(zz.z, zz.w);
+                // each z pair feeds 2*NC consecutive FFMA2 (operand reuse)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    A[c] = ffma2(z0, er[c][j], A[c]);
+                    B[c] = ffma2(z0, ei[c][j], B[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    A[c] = ffma2(z1, er[c][j + 1], A[c]);
+                    B[c] = ffma2(z1, ei[c][j + 1], B[c]);
+                }
             }
-            // C = A + jB with A = A0 + A1, B = B0 + B1
-            const float cr = (A0.x + A1.x) - (B0.y + B1.y);
-            const float ci = (A0.y + A1.y) + (B0.x + B1.x);
-            const float nr = fmaf(hr, w1r, fmaf(-hi, w1i, cr));
-            hi = fmaf(hr, w1i, fmaf(hi, w1r, ci));
-            hr = nr;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const float cr = A[c].x - B[c].y, ci = A[c].y + B[c].x;  // C = A + jB
+                const float nr = fmaf(hr[c], w1r[c], fmaf(-hi[c], w1i[c], cr));
+                hi[c] = fmaf(hr[c], w1i[c], fmaf(hi[c], w1r[c], ci));
+                hr[c] = nr;
+            }
         }
         // anchor W = e^{j 2 pi f c0} from the FP64-reduced phase
-        float wr, wi;
-        {
-            const double x = f * (double)c0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            float wr, wi;
+            const double x = f[c] * (double)c0;
             sincospif((float)(2.0 * (x - rint(x))), &wi, &wr);
+            acc_re[c] += (double)fmaf(wr, hr[c], -(wi * hi[c]));
+            acc_im[c] += (double)fmaf(wr, hi[c], wi * hr[c]);
         }
-        acc_re += (double)fmaf(wr, hr, -(wi * hi));
-        acc_im += (double)fmaf(wr, hi, wi * hr);
         __syncwarp();  // this stage's buffers are free for the next bulk copy
     }
 
 #pragma unroll
     for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
-    if (p >= 0) {
-        const double s = sqrt(acc_re * acc_re + acc_im * acc_im);
-        s_out[p] = s;
-        if (s < (double)kRefineTau * sqrt((double)z2)) {
-            const int64_t e = flag_base + p;
+    const double thr = (double)kRefineTau * sqrt((double)z2);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (p[c] < 0) continue;
+        const double s = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
+        s_out[p[c]] = s;
+        if (s < thr) {
+            const int64_t e = flag_base + p[c];
             atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
         }
     }
@@ -227,19 +257,20 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
 
 namespace {
 
-template <int LB, int CH>
-void launch_variant(int blocks, cudaStream_t st, const Task* tasks, const int* n_tasks,
+template <int NC, int LB, int CH, int WPC, int MINB>
+void launch_variant(int n_tasks_max, cudaStream_t st, const Task* tasks, const int* n_tasks,
                     const int* sorted, const double* fdoa, const float2* y1, const float2* y2,
                     int N, double fs, double* s_out, uint32_t* flag_bits, int64_t flag_base) {
-    const size_t smem = sizeof(WarpSmemT<CH>) * kWarpsPerCta;
+    auto kern = k_correlate<NC, LB, CH, WPC, MINB>;
+    const size_t smem = sizeof(WarpSmemT<CH>) * WPC;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_correlate<LB, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    k_correlate<LB, CH><<<blocks, 32 * kWarpsPerCta, smem, st>>>(
-        tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out, flag_bits, flag_base);
+    const int blocks = (n_tasks_max + WPC - 1) / WPC;
+    kern<<<blocks, 32 * WPC, smem, st>>>(tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
+                                         flag_bits, flag_base);
 }
 
 int variant_from_env() {
@@ -249,24 +280,44 @@ int variant_from_env() {
 
 }  // namespace
 
+int correlate_task_size() {
+    static const int v = variant_from_env();
+    return v == 1 || v == 2 ? 32 : 64;
+}
+
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
                       double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st) {
-    const int blocks = (max_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (blocks <= 0) return;
+    if (max_tasks <= 0) return;
     static const int variant = variant_from_env();
     switch (variant) {
-        case 1:
-            launch_variant<32, 256>(blocks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
-                                    flag_bits, flag_base);
+        case 1:  // one candidate per lane (r01b)
+            launch_variant<1, 16, 256, 8, 2>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
             break;
         case 2:
-            launch_variant<16, 512>(blocks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
-                                    flag_bits, flag_base);
+            launch_variant<1, 16, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
             break;
-        default:
-            launch_variant<16, 256>(blocks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
-                                    flag_bits, flag_base);
+        case 4:
+            launch_variant<2, 8, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                            fs, s_out, flag_bits, flag_base);
+            break;
+        case 5:
+            launch_variant<2, 16, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
+            break;
+        case 6:
+            launch_variant<2, 12, 192, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
+            break;
+        case 7:
+            launch_variant<2, 12, 192, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
+            break;
+        default:  // two candidates per lane, 3 CTAs x 4 warps per SM, 148 registers
+            launch_variant<2, 16, 256, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
+                                             fs, s_out, flag_bits, flag_base);
     }
 }
 

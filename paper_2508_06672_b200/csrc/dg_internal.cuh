@@ -9,7 +9,8 @@
 
 namespace dg {
 
-// One warp-task of the correlator: up to 32 candidates that share one integer
+// One warp-task of the correlator: up to correlate_task_size() candidates (32 per
+// lane-slot) that share one integer
 // TDOA d (so one z_d[k] = y1[k] conj(y2[k+d]) stream and one overlap range).
 struct Task {
     int d;      // tdoa_samples
@@ -25,7 +26,6 @@ struct PairGeom {
 
 // Per-element flag: FP32 result too close to zero for the relative tolerance;
 // re-evaluated in FP64 in the reference's exact operation order.
-constexpr int kWarpsPerCta = 8;
 constexpr int kChunk = 256;  // samples per z-chunk (per warp, TMA-staged in smem)
 
 // Device capture layout: every capture sits in a zero-filled slot of `stride`
@@ -62,6 +62,8 @@ void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_ou
                          unsigned long long* overlap, cudaStream_t st);
 void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
                    const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st);
+// candidates per warp task of the active correlator variant (32 x candidates/lane)
+int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
                       double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st);

@@ -195,8 +195,8 @@ constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 8;
 
 __global__ void __launch_bounds__(kScanThreads)
-k_scan(const int* __restrict__ hist, int nbins, int* __restrict__ off, int* __restrict__ toff,
-       int* __restrict__ cursor, int* __restrict__ n_tasks) {
+k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
+       int* __restrict__ toff, int* __restrict__ cursor, int* __restrict__ n_tasks) {
     __shared__ int ws[32], wt[32];
     __shared__ int carry_s, carry_t;
     if (threadIdx.x == 0) carry_s = carry_t = 0;
@@ -209,7 +209,7 @@ k_scan(const int* __restrict__ hist, int nbins, int* __restrict__ off, int* __re
         for (int i = 0; i < kScanItems; ++i) {
             const int idx = base + threadIdx.x * kScanItems + i;
             v[i] = idx < nbins ? hist[idx] : 0;
-            t[i] = (v[i] + 31) >> 5;
+            t[i] = (v[i] + ts - 1) / ts;
             s += v[i];
             st += t[i];
         }
@@ -277,19 +277,20 @@ __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __re
     }
 }
 
-__global__ void k_build_tasks(int* __restrict__ hist, int nbins, int N, const int* __restrict__ off,
-                              const int* __restrict__ toff, Task* __restrict__ tasks) {
+__global__ void k_build_tasks(int* __restrict__ hist, int nbins, int N, int ts,
+                              const int* __restrict__ off, const int* __restrict__ toff,
+                              Task* __restrict__ tasks) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
         const int cnt = hist[b];
         if (!cnt) continue;
         hist[b] = 0;  // ready for the next (snapshot, pair)
         const int d = b - (N - 1);
         const int t0 = toff[b], s0 = off[b];
-        for (int t = 0; 32 * t < cnt; ++t) {
+        for (int t = 0; ts * t < cnt; ++t) {
             Task tk;
             tk.d = d;
-            tk.start = s0 + 32 * t;
-            tk.count = min(32, cnt - 32 * t);
+            tk.start = s0 + ts * t;
+            tk.count = min(ts, cnt - ts * t);
             tk.pad = 0;
             tasks[t0 + t] = tk;
         }
@@ -746,9 +747,10 @@ void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_ou
 
 void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
                    const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st) {
-    k_scan<<<1, kScanThreads, 0, st>>>(hist, nbins, off, toff, cursor, n_tasks);
+    const int ts = correlate_task_size();
+    k_scan<<<1, kScanThreads, 0, st>>>(hist, nbins, ts, off, toff, cursor, n_tasks);
     k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
-    k_build_tasks<<<blocks_for(nbins, 256), 256, 0, st>>>(hist, nbins, N, off, toff, tasks);
+    k_build_tasks<<<blocks_for(nbins, 256), 256, 0, st>>>(hist, nbins, N, ts, off, toff, tasks);
 }
 
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,
