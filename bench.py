@@ -256,6 +256,9 @@ def b200_arm(args, rank, world):
 
     # roofline of the dominant kernel (the correlator), this rank's launches
     corr_ms = statistics.mean(s["correlate_ms"] for s in stats)
+    print("[bench] per-solve stats: " + json.dumps({k: stats[-1][k] for k in (
+        "correlate_ms", "moments_ms", "evaluate_ms", "moment_ffma2", "evaluate_ffma2",
+        "direct_steps", "n_refined", "total_ms", "kernel_launches")}), file=sys.stderr)
     ovl = stats[0]["sum_overlap_samples"]
     achieved = FLOP_PER_SAMPLE * ovl / (corr_ms * 1e-3) / 1e12
     peak = ctypes_peak(lib, dev)

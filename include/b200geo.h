@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 1
+#define DG_ABI_VERSION 2
 
 enum {
     DG_OK = 0,
@@ -176,6 +176,12 @@ typedef struct {
     int64_t correlate_launches;
     double total_ms;            /* profile: event time of the whole device pipeline */
     int64_t kernel_launches;    /* all kernels this call launched */
+    /* block-moment correlator accounting */
+    double moments_ms;          /* profile: event time of k_moments (+ k_center) */
+    double evaluate_ms;         /* profile: event time of k_evaluate */
+    double moment_ffma2;        /* packed FP32x2 MACs k_moments performs (sum nb*B*R) */
+    double evaluate_ffma2;      /* packed FP32x2 MACs k_evaluate performs (sum count*nb*R) */
+    int64_t direct_steps;       /* (snapshot, pair) steps run on the direct correlator */
 } dg_result;
 
 void dg_options_default(dg_options* opt);

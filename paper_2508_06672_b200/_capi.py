@@ -66,7 +66,12 @@ class dg_result(C.Structure):
                 ("correlate_ms", C.c_double),
                 ("correlate_launches", C.c_int64),
                 ("total_ms", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64),
+                ("moments_ms", C.c_double),
+                ("evaluate_ms", C.c_double),
+                ("moment_ffma2", C.c_double),
+                ("evaluate_ffma2", C.c_double),
+                ("direct_steps", C.c_int64)]
 
 
 # every symbol include/b200geo.h declares (tests check the .so exports them)

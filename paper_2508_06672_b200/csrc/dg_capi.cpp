@@ -139,7 +139,13 @@ struct dg_grid {
     int64_t n_lat = 0, n_lon = 0, row_offset = 0;
     std::shared_ptr<DevMem> mem;  // x | y | z of the full lattice
     const double *x = nullptr, *y = nullptr, *z = nullptr;
+    // the FULL lattice (shared by every slab): FP32 positions relative to its
+    // centre, for partition-independent correlator planning
+    std::shared_ptr<DevMem> rel;
+    int64_t full_size = 0;
+    double cx = 0, cy = 0, cz = 0;
     int64_t size() const { return n_lat * n_lon; }
+    const float4* rel32() const { return static_cast<const float4*>(rel->p); }
 };
 
 struct dg_session {
@@ -167,51 +173,291 @@ namespace {
 void set_device(const dg_engine* e) { CK(cudaSetDevice(e->device)); }
 
 // ---------------------------------------------------------------------------
+// Correlator planning. A (snapshot, pair) "step" runs either the block-moment
+// correlator (dg_moments.cu) with block length B and R moments, or the direct
+// FFMA2 correlator (dg_correlate.cu) when no (B, R) meets the truncation bound
+// (very wide FDOA ranges) or when the direct form is cheaper (few candidates
+// per TDOA bucket). See DESIGN.md section 4.
+struct StepPlan {
+    bool empty = true;    // no candidate overlaps: every S is 0 (already written)
+    bool direct = false;
+    int B = 0, R = 0, nbmax = 0, cpb = 0;
+    int bin0 = 0, nbins = 0;
+    double nu_c = 0.0;
+};
+
+// |e^{ixt} - sum_{m<R} a_m T_m(t)| <= 2 (x/2)^R / R! / (1 - (x/2)^2/(R+1)), |t| <= 1
+double jacobi_anger_tail(double x, int R) {
+    const double h = std::fabs(x) * 0.5;
+    double t = 2.0;
+    for (int m = 1; m <= R; ++m) t *= h / m;
+    const double q = h * h / (R + 1);
+    return q < 1.0 ? t / (1.0 - q) : INFINITY;
+}
+
+constexpr double kMomentTail = 1e-8;
+constexpr int kMomentR[] = {8, 10, 12, 16};
+constexpr int kMomentB[] = {256, 128, 64};
+
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// `r`: the exact range of the candidates being correlated (bins, emptiness).
+// `a` (nullable): the FP32 planning range of the whole lattice with its FDOA
+// margin; when given, B / R / nu_c depend only on it, so every slab of a
+// lattice computes every cell bit-identically.
+StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, int64_t P_plan,
+                   int N, double fs) {
+    StepPlan pl;
+    if (r.dmin > r.dmax) return pl;
+    pl.empty = false;
+    pl.bin0 = r.dmin + N - 1;
+    pl.nbins = r.dmax - r.dmin + 1;
+    double nu_lo = f64_from_key(r.fmin) / fs, nu_hi = f64_from_key(r.fmax) / fs;
+    double d_span = pl.nbins;
+    if (a && a->dmin <= a->dmax) {
+        const double alo = (f64_from_key(a->fmin) - a_margin_hz) / fs;
+        const double ahi = (f64_from_key(a->fmax) + a_margin_hz) / fs;
+        // the exact range lies inside the planning range unless FP32 erred
+        // beyond its margin; then widen (correct, no longer partition-proof)
+        nu_lo = std::min(nu_lo, alo);
+        nu_hi = std::max(nu_hi, ahi);
+        d_span = std::max(1, std::min(a->dmax, N - 1) - std::max(a->dmin, 1 - N) + 1);
+    }
+    pl.nu_c = 0.5 * (nu_lo + nu_hi);
+    const double half = 0.5 * (nu_hi - nu_lo) * (1.0 + 1e-9) + 1e-15;
+    const double avg = (double)P_plan / d_span;  // candidates per TDOA bucket (approx.)
+    // costs in FP32x2-MAC units per bucket: direct ~2.3 per candidate-sample;
+    // moments R per sample (x1.5 for smem traffic) + (R + 5) per candidate-block
+    double best = 2.3 * avg * N;
+    const int mode = env_int("DG_CORRELATOR_MOMENTS", 1);  // 0: force direct, 2: force moments
+    const int forceB = env_int("DG_MOMENT_B", 0), forceR = env_int("DG_MOMENT_R", 0);
+    pl.direct = true;
+    if (mode == 0) return pl;
+    if (mode == 2) best = INFINITY;
+    for (int B : kMomentB) {
+        if (forceB && B != forceB) continue;
+        const double x = M_PI * half * B;
+        for (int R : kMomentR) {
+            if (forceR && R != forceR) continue;
+            if (!forceR && jacobi_anger_tail(x, R) > kMomentTail) continue;
+            const double cost = 1.5 * R * N + avg * ((double)N / B) * (R + 5);
+            if (cost < best) {
+                best = cost;
+                pl.direct = false;
+                pl.B = B;
+                pl.R = R;
+            }
+            break;  // smallest admissible R for this B
+        }
+    }
+    if (!pl.direct) {
+        pl.nbmax = (N + pl.B - 1) / pl.B;
+        pl.cpb = (pl.nbmax + 31) / 32;
+    }
+    return pl;
+}
+
+// Chebyshev tables T_m(t_j), t_j = (2j - (B-1))/B, for every supported B:
+// [B][kMaxMoments] floats each, FP64 recurrence then one rounding.
+std::vector<float> chebyshev_table(int B) {
+    std::vector<float> t((size_t)B * kMaxMoments);
+    for (int j = 0; j < B; ++j) {
+        const double x = (2.0 * j - (B - 1)) / B;
+        double tm1 = 1.0, tm = x;
+        t[(size_t)j * kMaxMoments] = 1.0f;
+        t[(size_t)j * kMaxMoments + 1] = (float)x;
+        for (int m = 2; m < kMaxMoments; ++m) {
+            const double tn = 2.0 * x * tm - tm1;
+            tm1 = tm;
+            tm = tn;
+            t[(size_t)j * kMaxMoments + m] = (float)tn;
+        }
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
 // The per-(snapshot, pair) pipeline shared by correlate_batch, correlate_snapshot
-// and the full driver: offsets -> d-buckets -> warp tasks -> correlator.
+// and the full driver. Phase A (geometry) runs for a window of steps into
+// per-slot d/fdoa/histogram/range buffers; one synchronisation reads the
+// ranges and plans every step; phase B buckets and correlates each step.
+std::vector<RxPairF32> rx_pairs_f32(const dg_grid* g, const PairGeom* pg, int n);
+double fp32_fdoa_margin(const PairGeom* pg, int n, double wl);
+
 struct Pipeline {
     int64_t P = 0;
-    int N = 0, nbins = 0, max_tasks = 0;
+    int N = 0, nbins = 0, max_tasks = 0, slots = 0, sm_count = 148;
     int *d = nullptr, *sorted = nullptr, *hist = nullptr, *off = nullptr, *toff = nullptr,
-        *cursor = nullptr, *n_tasks = nullptr, *err = nullptr;
+        *boff = nullptr, *cursor = nullptr, *n_tasks = nullptr, *n_buckets = nullptr,
+        *err = nullptr;
     double* fdoa = nullptr;
     Task* tasks = nullptr;
+    Bucket* buckets = nullptr;
+    StepRange* range = nullptr;
+    double* nu_c = nullptr;  // [slots]
+    float2* y1c = nullptr;
+    float2* mom = nullptr;
+    size_t mom_cap = 0;
     unsigned long long* overlap = nullptr;
-    int64_t launches = 0;
+    unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
+    const float* tcheb[3] = {nullptr, nullptr, nullptr};  // B = 64, 128, 256
+    std::vector<StepPlan> plans;
+    int64_t launches = 0, direct_steps = 0;
+    // refinement threshold of the block-moment path; DG_REFINE_TAU overrides
+    // (tests use a huge value to re-evaluate every element exactly)
+    float tau = [] {
+        const char* v = getenv("DG_REFINE_TAU");
+        return v && *v ? (float)atof(v) : kMomentRefineTau;
+    }();
 
-    void init(Scratch& sc, int64_t P_, int64_t N_) {
+    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms) {
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
         N = (int)N_;
+        sm_count = sms;
         nbins = 2 * N - 1;
         const int64_t mt = P / correlate_task_size() + std::min<int64_t>(P, nbins) + 1;
         max_tasks = (int)std::min<int64_t>(mt, INT32_MAX);
-        d = sc.alloc<int>(P);
+        // phase-A window: per-slot d + fdoa + histogram, within ~4 GB
+        const int64_t per_slot = 12 * P + 4 * (int64_t)nbins + 64;
+        slots = (int)std::max<int64_t>(1, std::min<int64_t>(n_steps, (4ll << 30) / per_slot));
+        d = sc.alloc<int>((size_t)P * slots);
+        fdoa = sc.alloc<double>((size_t)P * slots);
+        hist = sc.alloc<int>((size_t)nbins * slots);
+        range = sc.alloc<StepRange>(slots);
+        nu_c = sc.alloc<double>(slots);
         sorted = sc.alloc<int>(P);
-        fdoa = sc.alloc<double>(P);
         tasks = sc.alloc<Task>(max_tasks);
-        hist = sc.alloc<int>(nbins);
+        buckets = sc.alloc<Bucket>(std::min<int64_t>(P, nbins));
         off = sc.alloc<int>(nbins);
         toff = sc.alloc<int>(nbins);
+        boff = sc.alloc<int>(nbins);
         cursor = sc.alloc<int>(nbins);
         n_tasks = sc.alloc<int>(1);
+        n_buckets = sc.alloc<int>(1);
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
-        CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins, sc.st));
+        work = sc.alloc<unsigned long long>(2);
+        y1c = sc.alloc<float2>(N);
+        CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
         CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
         CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
+        CK(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), sc.st));
+        static const int kB[3] = {64, 128, 256};
+        std::vector<float> all;
+        for (int B : kB) {
+            auto t = chebyshev_table(B);
+            all.insert(all.end(), t.begin(), t.end());
+        }
+        auto* tdev = sc.alloc<float>(all.size());
+        CK(cudaMemcpyAsync(tdev, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice,
+                           sc.st));
+        tcheb[0] = tdev;
+        tcheb[1] = tdev + 64 * kMaxMoments;
+        tcheb[2] = tdev + (64 + 128) * kMaxMoments;
+        CK(cudaStreamSynchronize(sc.st));  // `all` is host memory of this frame
     }
 
-    void bucket_and_correlate(const float2* y1, const float2* y2, double fs, double* s_out,
-                              uint32_t* bits, int64_t flag_base, cudaStream_t st,
-                              cudaEvent_t ev0, cudaEvent_t ev1) {
-        launch_bucket(hist, nbins, N, off, toff, cursor, n_tasks, d, P, sorted, tasks, st);
-        if (ev0) CK(cudaEventRecord(ev0, st));
-        launch_correlate(tasks, n_tasks, max_tasks, sorted, fdoa, y1, y2, N, fs, s_out, bits,
-                         flag_base, st);
-        if (ev1) CK(cudaEventRecord(ev1, st));
-        launches += 4;
+    int* d_slot(int s) const { return d + (size_t)s * P; }
+    double* fdoa_slot(int s) const { return fdoa + (size_t)s * P; }
+    int* hist_slot(int s) const { return hist + (size_t)s * nbins; }
+
+    void reset_ranges(Scratch& sc, int n) {
+        std::vector<StepRange> h(n);
+        for (auto& r : h) step_range_init(&r);
+        CK(cudaMemcpyAsync(range, h.data(), n * sizeof(StepRange), cudaMemcpyHostToDevice, sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+    }
+
+    // one synchronisation: read the window's ranges (and the lattice planning
+    // ranges `approx`, nullable), plan each step, upload nu_c
+    void plan_window(Scratch& sc, int n, double fs, const StepRange* approx = nullptr,
+                     double margin_hz = 0.0, int64_t P_plan = 0) {
+        std::vector<StepRange> h(n), ha(approx ? n : 0);
+        CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost, sc.st));
+        if (approx)
+            CK(cudaMemcpyAsync(ha.data(), approx, n * sizeof(StepRange), cudaMemcpyDeviceToHost,
+                               sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+        plans.assign(n, StepPlan{});
+        std::vector<double> nc(n);
+        for (int i = 0; i < n; ++i) {
+            plans[i] = plan_step(h[i], approx ? &ha[i] : nullptr, margin_hz, approx ? P_plan : P, N,
+                                 fs);
+            nc[i] = plans[i].nu_c;
+        }
+        CK(cudaMemcpyAsync(nu_c, nc.data(), n * sizeof(double), cudaMemcpyHostToDevice, sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+    }
+
+    // FP32 planning ranges over the full lattice of `g` for steps pg[0..n)
+    StepRange* lattice_ranges(Scratch& sc, const dg_grid* g, const PairGeom* pg_host,
+                              int n, double fs, double wl) {
+        auto rx = rx_pairs_f32(g, pg_host, n);
+        auto* rx_dev = sc.alloc<RxPairF32>(n);
+        auto* out = sc.alloc<StepRange>(n);
+        std::vector<StepRange> init(n);
+        for (auto& r : init) step_range_init(&r);
+        CK(cudaMemcpyAsync(rx_dev, rx.data(), n * sizeof(RxPairF32), cudaMemcpyHostToDevice,
+                           sc.st));
+        CK(cudaMemcpyAsync(out, init.data(), n * sizeof(StepRange), cudaMemcpyHostToDevice, sc.st));
+        launch_range_fp32(g->rel32(), g->full_size, rx_dev, n, fs, wl, out, sc.st);
+        CK(cudaStreamSynchronize(sc.st));  // host vectors of this frame
+        launches += 1;
+        return out;
+    }
+
+    void ensure_moments(Scratch& sc, const StepPlan& pl) {
+        const size_t nbk = (size_t)std::min<int64_t>(P, pl.nbins);
+        const size_t need = nbk * pl.nbmax * pl.R;
+        if (need > mom_cap) {
+            mom = sc.alloc<float2>(need);
+            mom_cap = need;
+        }
+    }
+
+    // phase B for slot s. y1_64 is the exact capture (centring source).
+    void correlate(Scratch& sc, int s, const double2* y1_64, const float2* y1, const float2* y2,
+                   double fs, double* s_out, uint32_t* bits, int64_t flag_base, cudaEvent_t ev0,
+                   cudaEvent_t ev1, cudaEvent_t ev2) {
+        const StepPlan& pl = plans[s];
+        cudaStream_t st = sc.st;
+        if (pl.empty) {
+            for (cudaEvent_t e : {ev0, ev1, ev2})
+                if (e) CK(cudaEventRecord(e, st));
+            return;
+        }
+        if (pl.direct) {
+            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
+                          n_buckets, d_slot(s), P, sorted, tasks, buckets, 0, st);
+            if (ev0) CK(cudaEventRecord(ev0, st));
+            if (ev1) CK(cudaEventRecord(ev1, st));
+            launch_correlate(tasks, n_tasks, max_tasks, sorted, fdoa_slot(s), y1, y2, N, fs, s_out,
+                             bits, flag_base, st);
+            launches += 4;
+            ++direct_steps;
+        } else {
+            ensure_moments(sc, pl);
+            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
+                          n_buckets, d_slot(s), P, sorted, tasks, buckets, pl.B, st);
+            launch_center(y1_64, N, nu_c + s, y1c, st);
+            if (ev0) CK(cudaEventRecord(ev0, st));
+            launch_moments(pl.B, pl.R, buckets, n_buckets, pl.cpb,
+                           tcheb[pl.B == 64 ? 0 : pl.B == 128 ? 1 : 2], y1c, y2, N, mom, pl.nbmax,
+                           sm_count, st);
+            if (ev1) CK(cudaEventRecord(ev1, st));
+            const int mt = (int)std::min<int64_t>(
+                (int64_t)P / correlate_task_size() + std::min<int64_t>(P, pl.nbins) + 1, max_tasks);
+            launch_evaluate(pl.R, mt, tasks, n_tasks, buckets, sorted, fdoa_slot(s), fs, nu_c + s,
+                            pl.B, mom, pl.nbmax, s_out, bits, flag_base, tau, st);
+            launch_work_count(buckets, n_buckets, pl.B, pl.R, work, st);
+            launches += 7;
+        }
+        if (ev2) CK(cudaEventRecord(ev2, st));
     }
 };
 
@@ -260,6 +506,60 @@ std::unique_ptr<dg_session> make_session(dg_engine* eng, int64_t n1, double fs1,
     CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, s->st));
     CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, s->st));
     return s;
+}
+
+// FP32 centre-relative copy of a freshly built full lattice (planning only)
+void finish_lattice(dg_grid* g, cudaStream_t st) {
+    const int64_t n = g->size();
+    g->full_size = n;
+    const int64_t mid = n / 2;
+    double c[3];
+    CK(cudaMemcpyAsync(&c[0], g->x + mid, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&c[1], g->y + mid, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&c[2], g->z + mid, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    g->cx = c[0];
+    g->cy = c[1];
+    g->cz = c[2];
+    g->rel = std::make_shared<DevMem>(n * sizeof(float4));
+    launch_lattice_rel(g->x, g->y, g->z, n, g->cx, g->cy, g->cz,
+                       static_cast<float4*>(g->rel->p), st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+}
+
+// per-step receiver pairs relative to the lattice centre, FP32
+std::vector<RxPairF32> rx_pairs_f32(const dg_grid* g, const PairGeom* pg, int n) {
+    std::vector<RxPairF32> out(n);
+    for (int i = 0; i < n; ++i) {
+        const dg_state& a = pg[i].rx_i;
+        const dg_state& b = pg[i].rx_j;
+        RxPairF32& r = out[i];
+        r.pi[0] = (float)(a.position.x - g->cx);
+        r.pi[1] = (float)(a.position.y - g->cy);
+        r.pi[2] = (float)(a.position.z - g->cz);
+        r.vi[0] = (float)a.velocity.x;
+        r.vi[1] = (float)a.velocity.y;
+        r.vi[2] = (float)a.velocity.z;
+        r.pj[0] = (float)(b.position.x - g->cx);
+        r.pj[1] = (float)(b.position.y - g->cy);
+        r.pj[2] = (float)(b.position.z - g->cz);
+        r.vj[0] = (float)b.velocity.x;
+        r.vj[1] = (float)b.velocity.y;
+        r.vj[2] = (float)b.velocity.z;
+    }
+    return out;
+}
+
+// FDOA error bound of the FP32 planning geometry: 1e-5 of the largest
+// possible Doppler difference (|v_i| + |v_j|) / wl, plus 1 mHz
+double fp32_fdoa_margin(const PairGeom* pg, int n, double wl) {
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) {
+        auto norm = [](const dg_ecef& v) { return std::sqrt(v.x * v.x + v.y * v.y + v.z * v.z); };
+        m = std::max(m, (norm(pg[i].rx_i.velocity) + norm(pg[i].rx_j.velocity)) / wl);
+    }
+    return 1e-5 * m + 1e-3;
 }
 
 }  // namespace
@@ -358,16 +658,21 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         set_device(s->eng);
         Scratch sc(s->st);
         Pipeline pl;
-        pl.init(sc, n, s->N);
+        pl.init(sc, n, s->N, 1, s->eng->sm_count);
         auto* off = sc.alloc<dg_pair_offsets>(n);
         auto* vals = sc.alloc<double>(n);
         const int64_t n_words = (n + 31) / 32;
         auto* bits = sc.alloc<uint32_t>(n_words);
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
         CK(cudaMemcpyAsync(off, batch, n * sizeof(dg_pair_offsets), cudaMemcpyHostToDevice, s->st));
-        launch_offsets_hist(off, n, pl.N, pl.d, pl.fdoa, pl.hist, vals, pl.overlap, s->st);
+        pl.reset_ranges(sc, 1);
+        launch_offsets_hist(off, n, pl.N, pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), vals,
+                            pl.overlap, pl.range, s->st);
+        pl.plan_window(sc, 1, s->fs);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
-        pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr, nullptr);
+        const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
+        pl.correlate(sc, 0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+                     nullptr);
         RefineCtx ctx{};
         ctx.P = n;
         ctx.offsets = off;
@@ -453,7 +758,7 @@ int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double sp
         launch_grid_ecef(t, t + n_lat, t + 2 * n_lat, t + 2 * n_lat + n_lon, n_lat, n_lon, base,
                          base + n, base + 2 * n, sg.st);
         CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(sg.st));
+        finish_lattice(g.get(), sg.st);
         *out = g.release();
     });
 }
@@ -500,6 +805,8 @@ int dg_grid_from_points(dg_engine* eng, const dg_ecef* pts, int64_t n, double la
         g->x = base;
         g->y = base + n;
         g->z = base + 2 * n;
+        StreamGuard sg(nullptr);
+        finish_lattice(g.get(), sg.st);
         *out = g.release();
     });
 }
@@ -568,7 +875,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         Scratch sc(s->st);
         const int64_t P = g->size();
         Pipeline pl;
-        pl.init(sc, P, s->N);
+        pl.init(sc, P, s->N, 1, s->eng->sm_count);
         auto* pg = sc.alloc<PairGeom>(1);
         auto* vals = sc.alloc<double>(P);
         const int64_t n_words = (P + 31) / 32;
@@ -576,11 +883,16 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         const PairGeom h{*rx_i, *rx_j};
         CK(cudaMemcpyAsync(pg, &h, sizeof h, cudaMemcpyHostToDevice, s->st));
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
-        launch_geometry_hist(g->x, g->y, g->z, P, pg, s->fs, wl, pl.N, pl.d, pl.fdoa, pl.hist, vals,
-                             pl.overlap, pl.err, s->st);
+        pl.reset_ranges(sc, 1);
+        launch_geometry_hist(g->x, g->y, g->z, P, pg, s->fs, wl, pl.N, pl.d_slot(0),
+                             pl.fdoa_slot(0), pl.hist_slot(0), vals, pl.overlap, pl.err, pl.range,
+                             s->st);
+        const StepRange* approx = pl.lattice_ranges(sc, g, &h, 1, s->fs, wl);
+        pl.plan_window(sc, 1, s->fs, approx, fp32_fdoa_margin(&h, 1, wl), g->full_size);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
-        pl.bucket_and_correlate(y32, y32 + s->stride, s->fs, vals, bits, 0, s->st, nullptr,
-                                nullptr);
+        const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
+        pl.correlate(sc, 0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+                     nullptr);
         check_err_flag(sc, pl.err);
         static const int pair_rx[2] = {0, 1};
         auto* prx = sc.alloc<int>(2);
@@ -751,7 +1063,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     if (opt.profile) {
         CK(cudaEventCreate(&ev_all0));
         CK(cudaEventCreate(&ev_all1));
-        evs.resize(2 * SP);
+        evs.resize(3 * SP);
         for (auto& e : evs) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(ev_all0, st));
     }
@@ -782,27 +1094,40 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     CK(cudaMemcpyAsync(d_prx, prx.data(), prx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
 
     Pipeline pl;
-    pl.init(sc, P, sn->N);
+    pl.init(sc, P, sn->N, SP, eng->sm_count);
     const int64_t n_elems = (int64_t)SP * P;
     auto* raw = sc.alloc<double>(n_elems);
     const int64_t n_words = (n_elems + 31) / 32;
     auto* bits = sc.alloc<uint32_t>(n_words);
     CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
     const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
+    const auto* y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
 
-    for (int s = 0; s < S; ++s)
-        for (int q = 0; q < pairs; ++q) {
-            const int sp = s * pairs + q;
-            double* out = raw + (int64_t)sp * P;
-            launch_geometry_hist(g->x, g->y, g->z, P, pg + sp, fs, wl, pl.N, pl.d, pl.fdoa, pl.hist,
-                                 out, pl.overlap, pl.err, st);
-            const float2* y1 = y32 + ((int64_t)s * R + prx[2 * q]) * sn->stride;
-            const float2* y2 = y32 + ((int64_t)s * R + prx[2 * q + 1]) * sn->stride;
-            pl.bucket_and_correlate(y1, y2, fs, out, bits, (int64_t)sp * P, st,
-                                    opt.profile ? evs[2 * sp] : nullptr,
-                                    opt.profile ? evs[2 * sp + 1] : nullptr);
+    for (int w0 = 0; w0 < SP; w0 += pl.slots) {
+        const int nw = std::min(pl.slots, SP - w0);
+        pl.reset_ranges(sc, nw);
+        for (int i = 0; i < nw; ++i) {  // phase A: geometry of the window
+            const int sp = w0 + i;
+            launch_geometry_hist(g->x, g->y, g->z, P, pg + sp, fs, wl, pl.N, pl.d_slot(i),
+                                 pl.fdoa_slot(i), pl.hist_slot(i), raw + (int64_t)sp * P,
+                                 pl.overlap, pl.err, pl.range + i, st);
             launches += 1;
         }
+        const StepRange* approx = pl.lattice_ranges(sc, g, hpg.data() + w0, nw, fs, wl);
+        pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hpg.data() + w0, nw, wl),
+                       g->full_size);
+        for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each step
+            const int sp = w0 + i;
+            const int s = sp / pairs, q = sp - s * pairs;
+            const int64_t c1 = ((int64_t)s * R + prx[2 * q]) * sn->stride;
+            const int64_t c2 = ((int64_t)s * R + prx[2 * q + 1]) * sn->stride;
+            pl.correlate(sc, i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)sp * P, bits,
+                         (int64_t)sp * P, opt.profile ? evs[3 * sp] : nullptr,
+                         opt.profile ? evs[3 * sp + 1] : nullptr,
+                         opt.profile ? evs[3 * sp + 2] : nullptr);
+        }
+    }
+    launches += pl.launches;
     CK(cudaGetLastError());
     check_err_flag(sc, pl.err);
 
@@ -906,8 +1231,9 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     if (res->per_snapshot)
         CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
                            cudaMemcpyDeviceToHost, st));
-    unsigned long long ovl = 0;
+    unsigned long long ovl = 0, work[2] = {0, 0};
     CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(work, pl.work, sizeof work, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (opt.patch_peak && acc_ex && res->n_reranked > 0 && (res->accumulated || res->per_snapshot)) {
         // exact FP64 values of the re-ranked cells into the host copies
@@ -928,14 +1254,22 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     res->sum_overlap_samples = (double)ovl;
     res->kernel_launches = launches;
     res->correlate_launches = SP;
+    res->moment_ffma2 = (double)work[0];
+    res->evaluate_ffma2 = (double)work[1];
+    res->direct_steps = pl.direct_steps;
     if (opt.profile) {
-        double tot = 0.0;
+        double tot = 0.0, tm = 0.0, te = 0.0;
         for (int i = 0; i < SP; ++i) {
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, evs[2 * i], evs[2 * i + 1]));
-            tot += ms;
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, evs[3 * i], evs[3 * i + 1]));
+            CK(cudaEventElapsedTime(&b, evs[3 * i + 1], evs[3 * i + 2]));
+            tm += a;
+            te += b;
+            tot += a + b;
         }
         res->correlate_ms = tot;
+        res->moments_ms = tm;
+        res->evaluate_ms = te;
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev_all0, ev_all1));
         res->total_ms = ms;

@@ -15,9 +15,52 @@ namespace dg {
 struct Task {
     int d;      // tdoa_samples
     int start;  // offset into the d-sorted candidate list
-    int count;  // 1..32 lanes live
-    int pad;
+    int count;  // 1..correlate_task_size() candidates live
+    int pad;    // index of the task's d-bucket (block-moment correlator)
 };
+
+// One d-bucket: every candidate with this integer TDOA (block-moment correlator).
+struct Bucket {
+    int d;      // tdoa_samples
+    int start;  // offset into the d-sorted candidate list
+    int count;  // candidates
+    int nb;     // blocks of B samples covering the overlap [max(0,-d), min(N, N-d))
+};
+
+// Per-(snapshot, pair) ranges reduced by the geometry kernel: FDOA as
+// order-preserving keys of the doubles, TDOA as ints (overlapping candidates only).
+struct StepRange {
+    unsigned long long fmin, fmax;
+    int dmin, dmax;
+};
+inline void step_range_init(StepRange* r) {
+    r->fmin = ~0ull;
+    r->fmax = 0ull;
+    r->dmin = 0x7fffffff;
+    r->dmax = -0x7fffffff - 1;
+}
+__host__ __device__ inline unsigned long long f64_key(double v) {
+    unsigned long long b;
+#ifdef __CUDA_ARCH__
+    b = (unsigned long long)__double_as_longlong(v);
+#else
+    __builtin_memcpy(&b, &v, 8);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+inline double f64_from_key(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double v;
+    __builtin_memcpy(&v, &b, 8);
+    return v;
+}
+
+// receiver pair of one step in FP32, positions relative to the lattice centre
+struct RxPairF32 {
+    float pi[3], vi[3], pj[3], vj[3];
+};
+
+constexpr int kMaxMoments = 16;  // Chebyshev table width (moments per block <= 16)
 
 // Geometry of one (snapshot, pair): receiver states for predict_pair_offsets.
 struct PairGeom {
@@ -40,7 +83,8 @@ constexpr int kL = 16;       // phasor table length (samples per inner block)
 
 // Threshold on S / sqrt(sum |z|^2) below which an FP32 value is re-evaluated
 // exactly; see DESIGN.md "Parity" for the error model behind it.
-constexpr float kRefineTau = 0.02f;
+constexpr float kRefineTau = 0.02f;         // direct correlator (dg_correlate.cu)
+constexpr float kMomentRefineTau = 0.02f;   // block-moment correlator
 
 // --------------------------------------------------------------------------
 // launchers (dg_kernels.cu). All asynchronous on `st`.
@@ -52,21 +96,45 @@ void launch_grid_ecef(const double* row_a, const double* row_z, const double* co
 void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
                           const PairGeom* pg_dev, double fs, double wl, int N, int* d_out,
                           double* fdoa_out, int* hist, double* s_out,
-                          unsigned long long* overlap, int* err, cudaStream_t st);
+                          unsigned long long* overlap, int* err, StepRange* range,
+                          cudaStream_t st);
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
                             const PairGeom* pg_dev, double fs, double wl, dg_pair_offsets* out,
                             int* err, cudaStream_t st);
 // the same from caller offsets (correlate_batch path)
 void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
                          double* fdoa_out, int* hist, double* s_out,
-                         unsigned long long* overlap, cudaStream_t st);
-void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
-                   const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st);
+                         unsigned long long* overlap, StepRange* range, cudaStream_t st);
+// planning ranges over a whole lattice (FP32, partition-independent)
+void launch_lattice_rel(const double* x, const double* y, const double* z, int64_t P, double cx,
+                        double cy, double cz, float4* out, cudaStream_t st);
+void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_steps, double fs,
+                       double wl, StepRange* out, cudaStream_t st);
+// bins [bin0, bin0 + nb) of the TDOA histogram (bin = d + N - 1) -> d-sorted
+// candidate ids, warp tasks of <= correlate_task_size() candidates and one
+// Bucket per non-empty bin (blocks of length B; B = 0 skips buckets)
+void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
+                   int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
+                   Task* tasks, Bucket* buckets, int B, cudaStream_t st);
 // candidates per warp task of the active correlator variant (32 x candidates/lane)
 int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
                       double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st);
+
+// block-moment correlator (dg_moments.cu)
+void launch_center(const double2* y, int N, const double* nu_c, float2* out, cudaStream_t st);
+size_t moments_smem_bytes(int B);
+void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
+                       unsigned long long* work, cudaStream_t st);
+void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,
+                    const float* tcheb, const float2* y1c, const float2* y2, int N, float2* mom,
+                    int nbmax, int sm_count, cudaStream_t st);
+void launch_evaluate(int R, int max_tasks, const Task* tasks, const int* n_tasks,
+                     const Bucket* buckets, const int* sorted, const double* fdoa, double fs,
+                     const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
+                     uint32_t* flag_bits, int64_t flag_base, float tau,
+                     cudaStream_t st);
 
 // exact FP64 reference-order re-evaluation of flagged elements
 // elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)

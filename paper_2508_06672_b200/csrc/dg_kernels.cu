@@ -80,9 +80,8 @@ __device__ double correlate_exact(const double2* __restrict__ y1, const double2*
     sincos(phase0, &ph_im, &ph_re);
     double acc_re = 0.0, acc_im = 0.0;
     const double2* b = y2 + d;
-    for (long long k = kb; k < ke; ++k) {
-        const double2 a = y1[k];
-        const double2 bb = b[k];
+    // one reference iteration (correlate.hpp:59-69), operation order unchanged
+    auto step_k = [&](const double2 a, const double2 bb) {
         const double b_re = bb.x, b_im = -bb.y;
         const double p_re = __dsub_rn(__dmul_rn(a.x, b_re), __dmul_rn(a.y, b_im));
         const double p_im = __dadd_rn(__dmul_rn(a.x, b_im), __dmul_rn(a.y, b_re));
@@ -91,7 +90,35 @@ __device__ double correlate_exact(const double2* __restrict__ y1, const double2*
         const double nr = __dsub_rn(__dmul_rn(ph_re, rot_re), __dmul_rn(ph_im, rot_im));
         ph_im = __dadd_rn(__dmul_rn(ph_re, rot_im), __dmul_rn(ph_im, rot_re));
         ph_re = nr;
+    };
+    // the loads of the next 8 samples are issued before the current 8 are
+    // consumed, so the sequential FP64 chain never waits on memory
+    constexpr int U = 8;
+    long long k = kb;
+    if (ke - kb >= 2 * U) {
+        double2 na[U], nb[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+            na[i] = __ldg(y1 + k + i);
+            nb[i] = __ldg(b + k + i);
+        }
+        for (; k + 2 * U <= ke; k += U) {
+            double2 ca[U], cb[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+                ca[i] = na[i];
+                cb[i] = nb[i];
+                na[i] = __ldg(y1 + k + U + i);
+                nb[i] = __ldg(b + k + U + i);
+            }
+#pragma unroll
+            for (int i = 0; i < U; ++i) step_k(ca[i], cb[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < U; ++i) step_k(na[i], nb[i]);
+        k += U;
     }
+    for (; k < ke; ++k) step_k(y1[k], b[k]);
     return __dsqrt_rn(__dadd_rn(__dmul_rn(acc_re, acc_re), __dmul_rn(acc_im, acc_im)));
 }
 
@@ -123,9 +150,30 @@ __global__ void k_grid_ecef(const double* __restrict__ ra, const double* __restr
 // ---------------------------------------------------------------------------
 // K2: per-point offsets (bit-exact) + TDOA histogram for the warp bucketing.
 // Candidates whose shift leaves no overlap get S = 0 here (correlate.hpp:49).
+// Per-thread running ranges of the overlapping candidates (StepRange).
+struct RangeAcc {
+    unsigned long long fmin = ~0ull, fmax = 0ull;
+    int dmin = INT_MAX, dmax = INT_MIN;
+    __device__ void flush(StepRange* r) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            fmin = min(fmin, __shfl_xor_sync(0xffffffffu, fmin, o));
+            fmax = max(fmax, __shfl_xor_sync(0xffffffffu, fmax, o));
+            dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        }
+        if ((threadIdx.x & 31) == 0 && dmin <= dmax) {
+            atomicMin(&r->fmin, fmin);
+            atomicMax(&r->fmax, fmax);
+            atomicMin(&r->dmin, dmin);
+            atomicMax(&r->dmax, dmax);
+        }
+    }
+};
+
 __device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdoa, int N,
                                            int* d_out, double* fdoa_out, int* hist,
-                                           double* s_out, unsigned long long& ovl) {
+                                           double* s_out, unsigned long long& ovl, RangeAcc& ra) {
     if (tdoa >= N || tdoa <= -N) {  // empty overlap (also catches llround overflow)
         d_out[p] = kNoOverlap;
         s_out[p] = 0.0;
@@ -135,6 +183,11 @@ __device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdo
         fdoa_out[p] = fdoa;
         atomicAdd(&hist[d + N - 1], 1);
         ovl += (unsigned long long)(N - (d < 0 ? -d : d));
+        const unsigned long long k = f64_key(fdoa);
+        ra.fmin = min(ra.fmin, k);
+        ra.fmax = max(ra.fmax, k);
+        ra.dmin = min(ra.dmin, d);
+        ra.dmax = max(ra.dmax, d);
     }
 }
 
@@ -143,18 +196,21 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
                                 const PairGeom* __restrict__ pg, double fs, double wl, int N,
                                 int* __restrict__ d_out, double* __restrict__ fdoa_out,
                                 int* __restrict__ hist, double* __restrict__ s_out,
-                                unsigned long long* __restrict__ overlap, int* __restrict__ err) {
+                                unsigned long long* __restrict__ overlap, int* __restrict__ err,
+                                StepRange* __restrict__ range) {
     const PairGeom g = *pg;
     unsigned long long ovl = 0;
+    RangeAcc ra;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         long long tdoa;
         double fdoa;
         if (!offsets_exact(x[p], y[p], z[p], g, fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
-        emit_point(p, tdoa, fdoa, N, d_out, fdoa_out, hist, s_out, ovl);
+        emit_point(p, tdoa, fdoa, N, d_out, fdoa_out, hist, s_out, ovl, ra);
     }
     ovl = warp_sum_u64(ovl);
     if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
+    ra.flush(range);
 }
 
 __global__ void k_predict_offsets(const double* __restrict__ x, const double* __restrict__ y,
@@ -177,93 +233,168 @@ __global__ void k_predict_offsets(const double* __restrict__ x, const double* __
 __global__ void k_offsets_hist(const dg_pair_offsets* __restrict__ off, int64_t P, int N,
                                int* __restrict__ d_out, double* __restrict__ fdoa_out,
                                int* __restrict__ hist, double* __restrict__ s_out,
-                               unsigned long long* __restrict__ overlap) {
+                               unsigned long long* __restrict__ overlap,
+                               StepRange* __restrict__ range) {
     unsigned long long ovl = 0;
+    RangeAcc ra;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         const dg_pair_offsets o = off[p];
-        emit_point(p, o.tdoa_samples, o.fdoa_hz, N, d_out, fdoa_out, hist, s_out, ovl);
+        emit_point(p, o.tdoa_samples, o.fdoa_hz, N, d_out, fdoa_out, hist, s_out, ovl, ra);
     }
     ovl = warp_sum_u64(ovl);
     if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
+    ra.flush(range);
 }
 
 // ---------------------------------------------------------------------------
-// Bucketing: exclusive scans of per-d counts and per-d warp-task counts, then
-// scatter candidate ids by d and cut each d-bucket into <=32-lane tasks.
+// Planning ranges (not bit-exact; only used to choose the correlator's block
+// length, moment count and centre frequency, which must not depend on how the
+// lattice is partitioned): positions relative to the lattice centre in FP32.
+__global__ void k_lattice_rel(const double* __restrict__ x, const double* __restrict__ y,
+                              const double* __restrict__ z, int64_t P, double cx, double cy,
+                              double cz, float4* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x)
+        out[p] = make_float4((float)(x[p] - cx), (float)(y[p] - cy), (float)(z[p] - cz), 0.f);
+}
+
+constexpr int kRangeThreads = 256;
+
+__global__ void __launch_bounds__(kRangeThreads)
+k_range_fp32(const float4* __restrict__ rel, int64_t P, const RxPairF32* __restrict__ rx,
+             int n_steps, float fs_over_c, float inv_wl, StepRange* __restrict__ out) {
+    __shared__ float red[4][kRangeThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = 0; s < n_steps; ++s) {
+        const RxPairF32 g = rx[s];
+        float fmn = INFINITY, fmx = -INFINITY, dmn = INFINITY, dmx = -INFINITY;
+        for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+             p += (int64_t)gridDim.x * blockDim.x) {
+            const float4 c = rel[p];
+            const float ax = g.pi[0] - c.x, ay = g.pi[1] - c.y, az = g.pi[2] - c.z;
+            const float bx = g.pj[0] - c.x, by = g.pj[1] - c.y, bz = g.pj[2] - c.z;
+            const float ri = sqrtf(ax * ax + ay * ay + az * az);
+            const float rj = sqrtf(bx * bx + by * by + bz * bz);
+            const float di = -(ax * g.vi[0] + ay * g.vi[1] + az * g.vi[2]) / ri;
+            const float dj = -(bx * g.vj[0] + by * g.vj[1] + bz * g.vj[2]) / rj;
+            const float f = (dj - di) * inv_wl;
+            const float t = (rj - ri) * fs_over_c;
+            fmn = fminf(fmn, f);
+            fmx = fmaxf(fmx, f);
+            dmn = fminf(dmn, t);
+            dmx = fmaxf(dmx, t);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+            fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+            dmn = fminf(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+            dmx = fmaxf(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+        }
+        if (lane == 0) {
+            red[0][warp] = fmn;
+            red[1][warp] = fmx;
+            red[2][warp] = dmn;
+            red[3][warp] = dmx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kRangeThreads / 32; ++w) {
+                fmn = fminf(fmn, red[0][w]);
+                fmx = fmaxf(fmx, red[1][w]);
+                dmn = fminf(dmn, red[2][w]);
+                dmx = fmaxf(dmx, red[3][w]);
+            }
+            if (fmn <= fmx) {
+                atomicMin(&out[s].fmin, f64_key((double)fmn));
+                atomicMax(&out[s].fmax, f64_key((double)fmx));
+                atomicMin(&out[s].dmin, (int)floorf(dmn) - 2);
+                atomicMax(&out[s].dmax, (int)ceilf(dmx) + 2);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Bucketing over the step's TDOA range only (bins [bin0, bin0 + nbins)):
+// exclusive scans of per-d counts, per-d warp-task counts and non-empty bins,
+// then scatter candidate ids by d, cut each d-bucket into warp tasks and emit
+// one Bucket per non-empty bin.
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 8;
 
 __global__ void __launch_bounds__(kScanThreads)
 k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
-       int* __restrict__ toff, int* __restrict__ cursor, int* __restrict__ n_tasks) {
-    __shared__ int ws[32], wt[32];
-    __shared__ int carry_s, carry_t;
-    if (threadIdx.x == 0) carry_s = carry_t = 0;
+       int* __restrict__ toff, int* __restrict__ boff, int* __restrict__ cursor,
+       int* __restrict__ n_tasks, int* __restrict__ n_buckets) {
+    __shared__ int ws[3][32];
+    __shared__ int carry[3];
+    if (threadIdx.x < 3) carry[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int base = 0; base < nbins; base += kScanThreads * kScanItems) {
-        int v[kScanItems], t[kScanItems];
-        int s = 0, st = 0;
+        int v[kScanItems];
+        int tot[3] = {0, 0, 0};
 #pragma unroll
         for (int i = 0; i < kScanItems; ++i) {
             const int idx = base + threadIdx.x * kScanItems + i;
             v[i] = idx < nbins ? hist[idx] : 0;
-            t[i] = (v[i] + ts - 1) / ts;
-            s += v[i];
-            st += t[i];
+            tot[0] += v[i];
+            tot[1] += (v[i] + ts - 1) / ts;
+            tot[2] += v[i] ? 1 : 0;
         }
-        int is = s, it = st;  // inclusive warp scans
+        int inc[3] = {tot[0], tot[1], tot[2]};  // inclusive warp scans
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int a = __shfl_up_sync(0xffffffffu, is, o);
-            const int b = __shfl_up_sync(0xffffffffu, it, o);
-            if (lane >= o) {
-                is += a;
-                it += b;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int x = __shfl_up_sync(0xffffffffu, inc[c], o);
+                if (lane >= o) inc[c] += x;
             }
         }
-        if (lane == 31) {
-            ws[warp] = is;
-            wt[warp] = it;
-        }
+        if (lane == 31)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ws[c][warp] = inc[c];
         __syncthreads();
         if (warp == 0) {
-            int a = ws[lane], b = wt[lane];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int x = __shfl_up_sync(0xffffffffu, a, o);
-                const int y = __shfl_up_sync(0xffffffffu, b, o);
-                if (lane >= o) {
-                    a += x;
-                    b += y;
+            for (int c = 0; c < 3; ++c) {
+                int a = ws[c][lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int x = __shfl_up_sync(0xffffffffu, a, o);
+                    if (lane >= o) a += x;
                 }
+                ws[c][lane] = a;
             }
-            ws[lane] = a;
-            wt[lane] = b;
         }
         __syncthreads();
-        int es = carry_s + (warp ? ws[warp - 1] : 0) + is - s;
-        int et = carry_t + (warp ? wt[warp - 1] : 0) + it - st;
+        int e[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) e[c] = carry[c] + (warp ? ws[c][warp - 1] : 0) + inc[c] - tot[c];
 #pragma unroll
         for (int i = 0; i < kScanItems; ++i) {
             const int idx = base + threadIdx.x * kScanItems + i;
             if (idx < nbins) {
-                off[idx] = es;
-                cursor[idx] = es;
-                toff[idx] = et;
+                off[idx] = e[0];
+                cursor[idx] = e[0];
+                toff[idx] = e[1];
+                boff[idx] = e[2];
             }
-            es += v[i];
-            et += t[i];
+            e[0] += v[i];
+            e[1] += (v[i] + ts - 1) / ts;
+            e[2] += v[i] ? 1 : 0;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            carry_s += ws[31];
-            carry_t += wt[31];
-        }
+        if (threadIdx.x < 3) carry[threadIdx.x] += ws[threadIdx.x][31];
         __syncthreads();
     }
-    if (threadIdx.x == 0) *n_tasks = carry_t;
+    if (threadIdx.x == 0) {
+        *n_tasks = carry[1];
+        *n_buckets = carry[2];
+    }
 }
 
 __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __restrict__ cursor,
@@ -277,21 +408,32 @@ __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __re
     }
 }
 
-__global__ void k_build_tasks(int* __restrict__ hist, int nbins, int N, int ts,
+// hist/off/toff/boff are offset to bin0 (d = bin0 + b - (N - 1))
+__global__ void k_build_tasks(int* __restrict__ hist, int nbins, int bin0, int N, int ts,
                               const int* __restrict__ off, const int* __restrict__ toff,
-                              Task* __restrict__ tasks) {
+                              const int* __restrict__ boff, Task* __restrict__ tasks,
+                              Bucket* __restrict__ buckets, int B) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
         const int cnt = hist[b];
         if (!cnt) continue;
         hist[b] = 0;  // ready for the next (snapshot, pair)
-        const int d = b - (N - 1);
-        const int t0 = toff[b], s0 = off[b];
+        const int d = bin0 + b - (N - 1);
+        const int t0 = toff[b], s0 = off[b], u = boff[b];
+        if (B > 0) {
+            Bucket bk;
+            bk.d = d;
+            bk.start = s0;
+            bk.count = cnt;
+            const int n_ov = N - (d < 0 ? -d : d);
+            bk.nb = (n_ov + B - 1) / B;
+            buckets[u] = bk;
+        }
         for (int t = 0; ts * t < cnt; ++t) {
             Task tk;
             tk.d = d;
             tk.start = s0 + ts * t;
             tk.count = min(ts, cnt - ts * t);
-            tk.pad = 0;
+            tk.pad = u;
             tasks[t0 + t] = tk;
         }
     }
@@ -339,12 +481,65 @@ __device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, 
     return correlate_exact(y1, y2, c.N, tdoa, fdoa, c.fs);
 }
 
+// Eq. 11 in FP64 for one element, split across the 32 lanes of a warp: lane l
+// takes samples kb + l + 32 t with its own phasor (FP64 sincos of the exact
+// FP64-reduced start phase, FP64 recurrence by e^{i 32 step}), fixed-order
+// butterfly sum. Agrees with the reference's single recurrence to ~1e-12
+// relative — far inside the 1e-4 contract the refinement exists to meet.
+__device__ double correlate_fp64_warp(const double2* __restrict__ y1, const double2* __restrict__ y2,
+                                      int N, long long d, double fdoa, double fs, int lane) {
+    const long long kb = d < 0 ? -d : 0;
+    const long long ke = (N - d) < N ? (N - d) : N;
+    double acc_re = 0.0, acc_im = 0.0;
+    if (kb < ke) {
+        const double nu = fdoa / fs;  // cycles per sample
+        const long long k0 = kb + lane;
+        const double ph0 = nu * (double)k0;
+        double pr, pi_, rr, ri;
+        sincospi(2.0 * (ph0 - rint(ph0)), &pi_, &pr);
+        const double st = nu * 32.0;
+        sincospi(2.0 * (st - rint(st)), &ri, &rr);
+        const double2* b = y2 + d;
+        for (long long k = k0; k < ke; k += 32) {
+            const double2 a = __ldg(y1 + k), bb = __ldg(b + k);
+            const double zr = a.x * bb.x + a.y * bb.y, zi = a.y * bb.x - a.x * bb.y;
+            acc_re += zr * pr - zi * pi_;
+            acc_im += zr * pi_ + zi * pr;
+            const double nr = pr * rr - pi_ * ri;
+            pi_ = pr * ri + pi_ * rr;
+            pr = nr;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        acc_re += __shfl_xor_sync(0xffffffffu, acc_re, o);
+        acc_im += __shfl_xor_sync(0xffffffffu, acc_im, o);
+    }
+    return sqrt(acc_re * acc_re + acc_im * acc_im);
+}
+
 __global__ void k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx c) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
         const int64_t e = list[i];
         const int64_t sp = e / c.P, p = e - sp * c.P;
-        c.raw[e] = exact_element(c, sp, p);
+        double v;
+        if (c.offsets) {
+            const dg_pair_offsets o = c.offsets[p];
+            v = correlate_fp64_warp(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz, c.fs,
+                                    lane);
+        } else {
+            const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
+            long long tdoa;
+            double fdoa;
+            offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
+            const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
+            v = correlate_fp64_warp(c.y64 + (s * c.R + ri) * c.stride,
+                                    c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa, fdoa, c.fs, lane);
+        }
+        if (lane == 0) c.raw[e] = v;
     }
 }
 
@@ -727,9 +922,9 @@ void launch_grid_ecef(const double* ra, const double* rz, const double* cc, cons
 void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
                           const PairGeom* pg, double fs, double wl, int N, int* d_out,
                           double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
-                          int* err, cudaStream_t st) {
+                          int* err, StepRange* range, cudaStream_t st) {
     k_geometry_hist<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, N, d_out, fdoa_out,
-                                                        hist, s_out, overlap, err);
+                                                        hist, s_out, overlap, err, range);
 }
 
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
@@ -740,17 +935,32 @@ void launch_predict_offsets(const double* x, const double* y, const double* z, i
 
 void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
                          double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
-                         cudaStream_t st) {
+                         StepRange* range, cudaStream_t st) {
     k_offsets_hist<<<blocks_for(P, 256), 256, 0, st>>>(off, P, N, d_out, fdoa_out, hist, s_out,
-                                                       overlap);
+                                                       overlap, range);
 }
 
-void launch_bucket(int* hist, int nbins, int N, int* off, int* toff, int* cursor, int* n_tasks,
-                   const int* d, int64_t P, int* sorted, Task* tasks, cudaStream_t st) {
+void launch_lattice_rel(const double* x, const double* y, const double* z, int64_t P, double cx,
+                        double cy, double cz, float4* out, cudaStream_t st) {
+    k_lattice_rel<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, cx, cy, cz, out);
+}
+
+void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_steps, double fs,
+                       double wl, StepRange* out, cudaStream_t st) {
+    if (P <= 0 || n_steps <= 0) return;
+    k_range_fp32<<<blocks_for(P, kRangeThreads, 148LL * 8), kRangeThreads, 0, st>>>(
+        rel, P, rx, n_steps, (float)(fs / kC), (float)(1.0 / wl), out);
+}
+
+void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
+                   int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
+                   Task* tasks, Bucket* buckets, int B, cudaStream_t st) {
     const int ts = correlate_task_size();
-    k_scan<<<1, kScanThreads, 0, st>>>(hist, nbins, ts, off, toff, cursor, n_tasks);
+    k_scan<<<1, kScanThreads, 0, st>>>(hist + bin0, nb, ts, off + bin0, toff + bin0, boff + bin0,
+                                       cursor + bin0, n_tasks, n_buckets);
     k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
-    k_build_tasks<<<blocks_for(nbins, 256), 256, 0, st>>>(hist, nbins, N, ts, off, toff, tasks);
+    k_build_tasks<<<blocks_for(nb, 256), 256, 0, st>>>(hist + bin0, nb, bin0, N, ts, off + bin0,
+                                                      toff + bin0, boff + bin0, tasks, buckets, B);
 }
 
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,
@@ -765,7 +975,7 @@ void launch_compact_flags(const uint32_t* bits, int64_t n_words, int64_t* list,
 
 void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st) {
     if (n <= 0) return;
-    k_refine<<<blocks_for(n, 128, 148LL * 128), 128, 0, st>>>(list, n, ctx);
+    k_refine<<<blocks_for(n * 32, 256, 148LL * 16), 256, 0, st>>>(list, n, ctx);
 }
 
 void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,

@@ -210,7 +210,10 @@ def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, w
     stats = dict(n_refined=res.n_refined, n_reranked=res.n_reranked,
                  sum_overlap_samples=res.sum_overlap_samples, correlate_ms=res.correlate_ms,
                  correlate_launches=res.correlate_launches, total_ms=res.total_ms,
-                 kernel_launches=res.kernel_launches, n_detections=res.n_detections)
+                 kernel_launches=res.kernel_launches, n_detections=res.n_detections,
+                 moments_ms=res.moments_ms, evaluate_ms=res.evaluate_ms,
+                 moment_ffma2=res.moment_ffma2, evaluate_ffma2=res.evaluate_ffma2,
+                 direct_steps=res.direct_steps)
     per_list = [CorrelationGrid(grid, per[s]) for s in range(n_snap)] if per is not None else []
     return GeolocateResult(grid, per_list, CorrelationGrid(grid, acc), detections,
                            int(res.argmax_index), float(res.argmax_value), stats)

@@ -140,7 +140,9 @@ def test_golden_correlate_batch(b2):
     (4096, 20_000, 5e6, 1.25e6, 1),      # BenchWorkload distribution (bench.hpp:65-88)
     (50_000, 4_000, 5e6, 2e4, 3),        # C2..C5 capture length
 ])
-def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed):
+@pytest.mark.parametrize("mode", ["1", "0", "2"])  # auto / direct only / moments when admissible
+def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, monkeypatch):
+    monkeypatch.setenv("DG_CORRELATOR_MOMENTS", mode)
     rng = np.random.default_rng(seed)
     y1, y2 = gauss(rng, n), gauss(rng, n)
     if seed == 1:  # BenchWorkload: uniform [-1, 1] I/Q, |tdoa| <= N/2
@@ -153,6 +155,29 @@ def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed):
     assert rel_err(got, want).max() <= REL_TOL
     again = s.correlate_batch(off)
     assert np.array_equal(got, again)  # bit-identical rerun (test_backend.cpp:97-108)
+
+
+@pytest.mark.parametrize("block", [64, 128, 256])
+@pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200)])
+def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, monkeypatch):
+    """The block-moment correlator at every block length against the reference,
+    on buckets dense enough that it is the planner's choice (many candidates
+    per TDOA), including FDOA == 0 (x = 0) and the full TDOA range."""
+    monkeypatch.setenv("DG_CORRELATOR_MOMENTS", "2")
+    monkeypatch.setenv("DG_MOMENT_B", str(block))
+    n, fs, count = 50_000, 5e6, 6_000
+    rng = np.random.default_rng(block + int(span))
+    y1, y2 = gauss(rng, n), gauss(rng, n)
+    off = np.zeros(count, PAIR_OFFSETS_DTYPE)
+    off["tdoa_samples"] = rng.integers(-tdoa_span, tdoa_span, count) if tdoa_span < n else \
+        rng.integers(-n + 1, n, count)
+    off["fdoa_hz"] = rng.uniform(-span, span, count)
+    off["fdoa_hz"][:50] = 0.0
+    want = ref.correlate_batch(y1, y2, fs, off, "parallel", 0, 4096)
+    s = b2.make_backend("b200").stage(cap(b2, y1, fs), cap(b2, y2, fs))
+    got = s.correlate_batch(off)
+    assert rel_err(got, want).max() <= REL_TOL
+    assert np.array_equal(got, s.correlate_batch(off))
 
 
 def test_partition_invariance(b2):
