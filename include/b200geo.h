@@ -213,6 +213,8 @@ int dg_plan_batches(uint64_t n_points, uint64_t batch_size, uint64_t memory_budg
 int dg_fp32_peak_tflops(int device, double* tflops);
 /* The same issued as packed FP32x2 FMAs (fma.rn.f32x2 / SASS FFMA2). */
 int dg_fp32x2_peak_tflops(int device, double* tflops);
+/* FP64 DFMA peak (geometry, refinement and re-rank run in FP64). */
+int dg_fp64_peak_tflops(int device, double* tflops);
 
 #ifdef __cplusplus
 }

@@ -82,7 +82,7 @@ EXPORTS = (
     "dg_grid_info", "dg_grid_points", "dg_grid_destroy", "dg_predict_offsets",
     "dg_correlate_snapshot", "dg_options_default", "dg_geolocate_snapshots",
     "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_detect_emitters",
-    "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops",
+    "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
 _vp = C.c_void_p
@@ -126,6 +126,7 @@ def _load():
                                C.POINTER(dg_emitter_estimate), C.c_int64, _i64p],
         "dg_fp32_peak_tflops": [C.c_int, _dp],
         "dg_fp32x2_peak_tflops": [C.c_int, _dp],
+        "dg_fp64_peak_tflops": [C.c_int, _dp],
         "dg_plan_batches": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                             C.POINTER(C.c_uint64)],
     }

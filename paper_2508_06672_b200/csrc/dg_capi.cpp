@@ -196,6 +196,7 @@ double jacobi_anger_tail(double x, int R) {
 }
 
 constexpr double kMomentTail = 1e-8;
+constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of moments
 constexpr int kMomentR[] = {8, 10, 12, 16};
 constexpr int kMomentB[] = {256, 128, 64};
 
@@ -243,7 +244,8 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
         for (int R : kMomentR) {
             if (forceR && R != forceR) continue;
             if (!forceR && jacobi_anger_tail(x, R) > kMomentTail) continue;
-            const double cost = 1.5 * R * N + avg * ((double)N / B) * (R + 5);
+            if (evaluate_smem_bytes((N + B - 1) / B, R) > kEvalSmemMax) break;
+            const double cost = 1.5 * R * N + avg * ((double)N / B) * (R + 3);
             if (cost < best) {
                 best = cost;
                 pl.direct = false;
@@ -292,7 +294,7 @@ struct Pipeline {
     int N = 0, nbins = 0, max_tasks = 0, slots = 0, sm_count = 148;
     int *d = nullptr, *sorted = nullptr, *hist = nullptr, *off = nullptr, *toff = nullptr,
         *boff = nullptr, *cursor = nullptr, *n_tasks = nullptr, *n_buckets = nullptr,
-        *err = nullptr;
+        *err = nullptr, *queue = nullptr;
     double* fdoa = nullptr;
     Task* tasks = nullptr;
     Bucket* buckets = nullptr;
@@ -339,6 +341,7 @@ struct Pipeline {
         cursor = sc.alloc<int>(nbins);
         n_tasks = sc.alloc<int>(1);
         n_buckets = sc.alloc<int>(1);
+        queue = sc.alloc<int>(1);
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
         work = sc.alloc<unsigned long long>(2);
@@ -450,10 +453,10 @@ struct Pipeline {
                            tcheb[pl.B == 64 ? 0 : pl.B == 128 ? 1 : 2], y1c, y2, N, mom, pl.nbmax,
                            sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
-            const int mt = (int)std::min<int64_t>(
-                (int64_t)P / correlate_task_size() + std::min<int64_t>(P, pl.nbins) + 1, max_tasks);
-            launch_evaluate(pl.R, mt, tasks, n_tasks, buckets, sorted, fdoa_slot(s), fs, nu_c + s,
-                            pl.B, mom, pl.nbmax, s_out, bits, flag_base, tau, st);
+            CK(cudaMemsetAsync(queue, 0, sizeof(int), st));
+            launch_evaluate(pl.R, buckets, n_buckets, queue, (int)std::min<int64_t>(P, pl.nbins),
+                            sorted, fdoa_slot(s), fs, nu_c + s, pl.B, mom, pl.nbmax, s_out, bits,
+                            flag_base, tau, sm_count, st);
             launch_work_count(buckets, n_buckets, pl.B, pl.R, work, st);
             launches += 7;
         }

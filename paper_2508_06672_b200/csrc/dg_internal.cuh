@@ -130,10 +130,12 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
 void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,
                     const float* tcheb, const float2* y1c, const float2* y2, int N, float2* mom,
                     int nbmax, int sm_count, cudaStream_t st);
-void launch_evaluate(int R, int max_tasks, const Task* tasks, const int* n_tasks,
-                     const Bucket* buckets, const int* sorted, const double* fdoa, double fs,
+// per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue)
+size_t evaluate_smem_bytes(int nbmax, int R);
+void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+                     int max_buckets, const int* sorted, const double* fdoa, double fs,
                      const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                     uint32_t* flag_bits, int64_t flag_base, float tau,
+                     uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
                      cudaStream_t st);
 
 // exact FP64 reference-order re-evaluation of flagged elements

@@ -54,6 +54,9 @@ __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
 }
 
 constexpr int kChunkBlocks = 32;  // blocks per k_moments work item (one per lane)
+
+// two staging buffers of one bucket's moments
+inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * sizeof(float2); }
 constexpr int kMomThreads = 256;
 
 // table + max(z chunk, per-warp partial moments)
@@ -154,7 +157,9 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
                 s.x += v.x;
                 s.y += v.y;
             }
-            dst[o] = s;
+            // odd moments are stored times i, so a candidate's block value is
+            // one real-weighted sum  C_b = sum_m c_m M'_m  (k_evaluate)
+            dst[o] = (m & 1) ? make_float2(-s.y, s.x) : s;
         }
     }
 }
@@ -206,104 +211,183 @@ __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
     }
 }
 
-template <int R, int G>
-__global__ void __launch_bounds__(128, 4)
-k_evaluate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
-           const Bucket* __restrict__ buckets, const int* __restrict__ sorted,
-           const double* __restrict__ fdoa, double fs, const double* __restrict__ nu_c_p, int B,
-           const float2* __restrict__ mom, int nbmax,
-           double* __restrict__ s_out, uint32_t* __restrict__ flag_bits, int64_t flag_base,
-           float tau) {
-    constexpr int NC = 2;
-    const int lane = threadIdx.x & 31;
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (t >= *n_tasks) return;
-    const Task tk = tasks[t];
-    const int u = tk.pad;
-    const Bucket bk = buckets[u];
-    const int nb = bk.nb;
-    const double nu_c = *nu_c_p;
+// ---- TMA helpers (1-D bulk copy global -> shared, mbarrier completion) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
-    int p[NC];
-    double nu[NC];
-    float cf[NC][R];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const int slot = lane + 32 * c;
-        p[c] = slot < tk.count ? sorted[tk.start + slot] : -1;
-        nu[c] = p[c] >= 0 ? fdoa[p[c]] / fs - nu_c : 0.0;
-        double jv[R];
-        bessel_j<R>(3.141592653589793 * nu[c] * (double)B, jv);
-        // a_m = (2 - delta_m0) i^m J_m: even m -> real part sign (+,-,+,...),
-        // odd m -> imaginary part sign (+,-,...)
-#pragma unroll
-        for (int m = 0; m < R; ++m) {
-            const double sg = ((m >> 1) & 1) ? -1.0 : 1.0;
-            cf[c][m] = (float)((m == 0 ? 1.0 : 2.0) * sg * jv[m]);
+__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {  // elementwise
+    float2 d;
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+constexpr int kEvalWarps = 4;
+constexpr int kEvalNC = 2;                              // candidates per lane
+constexpr int kEvalPass = 32 * kEvalWarps * kEvalNC;   // candidates per CTA pass
+
+// One CTA per d-bucket (dynamic queue), the bucket's moments staged in shared
+// memory by one TMA bulk copy (double-buffered: the next bucket's copy runs
+// under this bucket's evaluation); each lane evaluates kEvalNC candidates:
+//   C_b = sum_m c_m M'_m[b]                       (R FFMA2, broadcast LDS.128)
+//   group g of G blocks:  A += Re(W_j) C_b, V += Im(W_j) C_b, e += C_b o C_b
+//   H_g = A + iV;  acc += e^{i 2 pi nu B G g} H_g   (anchor from an FP64 phase)
+// W_j = e^{i 2 pi nu B j} (j < G) are rounded once from FP64 phases.
+template <int R, int G>
+__global__ void __launch_bounds__(32 * kEvalWarps, 4)
+k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
+           int* __restrict__ queue, const int* __restrict__ sorted,
+           const double* __restrict__ fdoa, double fs, const double* __restrict__ nu_c_p, int B,
+           const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
+           uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
+    extern __shared__ float4 smem4[];
+    float4* mbuf[2] = {smem4, smem4 + (size_t)nbmax * R / 2};
+    __shared__ uint64_t bar[2];
+    __shared__ int next_u[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nbk = *n_buckets;
+    const double nu_c = *nu_c_p;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const int u0 = atomicAdd(queue, 1);
+        next_u[0] = u0;
+        if (u0 < nbk) {
+            const uint32_t bytes = (uint32_t)buckets[u0].nb * R * sizeof(float2);
+            mbar_expect_tx(&bar[0], bytes);
+            tma_load_1d(mbuf[0], mom + (size_t)u0 * nbmax * R, bytes, &bar[0]);
         }
     }
+    __syncthreads();
+    uint32_t phase[2] = {0u, 0u};
+    for (int it = 0;; ++it) {
+        const int buf = it & 1;
+        const int u = next_u[buf];
+        if (u >= nbk) break;
+        if (tid == 0) {  // claim and prefetch the next bucket into the other buffer
+            const int un = atomicAdd(queue, 1);
+            next_u[buf ^ 1] = un;
+            if (un < nbk) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint32_t bytes = (uint32_t)buckets[un].nb * R * sizeof(float2);
+                mbar_expect_tx(&bar[buf ^ 1], bytes);
+                tma_load_1d(mbuf[buf ^ 1], mom + (size_t)un * nbmax * R, bytes, &bar[buf ^ 1]);
+            }
+        }
+        const Bucket bk = buckets[u];
+        const int nb = bk.nb;
+        mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
+        const float4* mb = mbuf[buf];
 
-    // W_j = e^{i 2 pi nu B j}, j < G: each rounded once from an FP64 phase, so
-    // the group sum sum_j W_j C_{gG+j} has no recurrence error
-    float wtr[NC][G], wti[NC][G];
+        for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
+            int p[kEvalNC];
+            double nu[kEvalNC];
+            float cf[kEvalNC][R];
+            float wtr[kEvalNC][G], wti[kEvalNC][G];
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
+            for (int c = 0; c < kEvalNC; ++c) {
+                const int slot = base + 32 * c + lane;
+                p[c] = slot < bk.count ? sorted[bk.start + slot] : -1;
+                nu[c] = p[c] >= 0 ? fdoa[p[c]] / fs - nu_c : 0.0;
+                double jv[R];
+                bessel_j<R>(3.141592653589793 * nu[c] * (double)B, jv);
+                // a_m M_m = (2 - delta_m0) (-1)^(m/2) J_m M'_m  (M' = i^(m mod 2) M)
 #pragma unroll
-        for (int j = 0; j < G; ++j) cis_cycles(nu[c] * (double)B * (double)j, &wtr[c][j], &wti[c][j]);
-
-    double acc_re[NC], acc_im[NC], en[NC];
+                for (int m = 0; m < R; ++m)
+                    cf[c][m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc_re[c] = acc_im[c] = en[c] = 0.0;
-    const float4* mb = reinterpret_cast<const float4*>(mom + (size_t)u * nbmax * R);
-    const int ng = (nb + G - 1) / G;
-    for (int g = 0; g < ng; ++g) {
-        float hr[NC], hi[NC], ge[NC];
+                for (int j = 0; j < G; ++j)
+                    cis_cycles(nu[c] * (double)B * (double)j, &wtr[c][j], &wti[c][j]);
+            }
+            double acc_re[kEvalNC], acc_im[kEvalNC], en[kEvalNC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) hr[c] = hi[c] = ge[c] = 0.f;
+            for (int c = 0; c < kEvalNC; ++c) acc_re[c] = acc_im[c] = en[c] = 0.0;
+            const int ng = (nb + G - 1) / G;
+            for (int g = 0; g < ng; ++g) {
+                float2 A[kEvalNC], V[kEvalNC], E2[kEvalNC];
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-            const int b = g * G + j;
-            if (b < nb) {
-                float4 mv[R / 2];
+                for (int c = 0; c < kEvalNC; ++c)
+                    A[c] = V[c] = E2[c] = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int q = 0; q < R / 2; ++q) mv[q] = __ldg(mb + (size_t)b * (R / 2) + q);
+                for (int j = 0; j < G; ++j) {
+                    const int b = g * G + j;
+                    if (b < nb) {
+                        float4 mv[R / 2];
 #pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    // C_b = E + iO, smallest terms first (the c_m decay with m)
-                    float2 E = make_float2(0.f, 0.f), O = make_float2(0.f, 0.f);
+                        for (int q = 0; q < R / 2; ++q) mv[q] = mb[b * (R / 2) + q];
 #pragma unroll
-                    for (int q = R / 2 - 1; q >= 0; --q) {
-                        E = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], E);
-                        O = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], O);
+                        for (int c = 0; c < kEvalNC; ++c) {
+                            // smallest terms first (the c_m decay with m)
+                            float2 C = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int q = R / 2 - 1; q >= 0; --q) {
+                                C = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], C);
+                                C = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], C);
+                            }
+                            A[c] = ffma2(C, wtr[c][j], A[c]);
+                            V[c] = ffma2(C, wti[c][j], V[c]);
+                            E2[c] = ffma2v(C, C, E2[c]);
+                        }
                     }
-                    const float cr = E.x - O.y, ci = E.y + O.x;
-                    hr[c] = fmaf(wtr[c][j], cr, fmaf(-wti[c][j], ci, hr[c]));
-                    hi[c] = fmaf(wtr[c][j], ci, fmaf(wti[c][j], cr, hi[c]));
-                    ge[c] = fmaf(cr, cr, fmaf(ci, ci, ge[c]));
+                }
+#pragma unroll
+                for (int c = 0; c < kEvalNC; ++c) {
+                    const float hr = A[c].x - V[c].y, hi = A[c].y + V[c].x;
+                    float ar, ai;
+                    cis_cycles(nu[c] * (double)(g * G) * (double)B, &ar, &ai);
+                    acc_re[c] += (double)fmaf(ar, hr, -(ai * hi));
+                    acc_im[c] += (double)fmaf(ar, hi, ai * hr);
+                    en[c] += (double)(E2[c].x + E2[c].y);
+                }
+            }
+            // FP32 error scale of this candidate: sqrt(sum_b |C_b|^2) (DESIGN.md
+            // section 5); below tau of it the value is re-evaluated in FP64
+#pragma unroll
+            for (int c = 0; c < kEvalNC; ++c) {
+                if (p[c] < 0) continue;
+                const double sv = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
+                s_out[p[c]] = sv;
+                if (sv < (double)tau * sqrt(en[c])) {
+                    const int64_t e = flag_base + p[c];
+                    atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
             }
         }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            float ar, ai;
-            cis_cycles(nu[c] * (double)(g * G) * (double)B, &ar, &ai);
-            acc_re[c] += (double)fmaf(ar, hr[c], -(ai * hi[c]));
-            acc_im[c] += (double)fmaf(ar, hi[c], ai * hr[c]);
-            en[c] += (double)ge[c];
-        }
-    }
-
-    // FP32 error scale of this candidate: sqrt(sum_b |C_b|^2) (DESIGN.md
-    // section 5); below tau of it the value is re-evaluated in FP64
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (p[c] < 0) continue;
-        const double s = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
-        s_out[p[c]] = s;
-        if (s < (double)tau * sqrt(en[c])) {
-            const int64_t e = flag_base + p[c];
-            atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
-        }
+        __syncthreads();  // everyone is done with mbuf[buf] and has read next_u
     }
 }
 
@@ -356,15 +440,21 @@ void moments_b(int R, const Bucket* buckets, const int* n_buckets, int cpb, cons
 }
 
 template <int R>
-void evaluate_variant(int max_tasks, const Task* tasks, const int* n_tasks, const Bucket* buckets,
+void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                       const int* sorted, const double* fdoa, double fs, const double* nu_c, int B,
-                      const float2* mom, int nbmax, double* s_out,
-                      uint32_t* flag_bits, int64_t flag_base, float tau, cudaStream_t st) {
-    constexpr int kWarps = 4;
-    const int blocks = (max_tasks + kWarps - 1) / kWarps;
-    k_evaluate<R, 8><<<blocks, 32 * kWarps, 0, st>>>(tasks, n_tasks, buckets, sorted, fdoa, fs,
-                                                     nu_c, B, mom, nbmax, s_out,
-                                                     flag_bits, flag_base, tau);
+                      const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
+                      int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
+    auto kern = k_evaluate<R, 8>;
+    const size_t smem = evaluate_smem(nbmax, R);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    int grid = sm_count * 4;
+    if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
+    kern<<<grid, 32 * kEvalWarps, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c,
+                                              B, mom, nbmax, s_out, flag_bits, flag_base, tau);
 }
 
 }  // namespace
@@ -393,17 +483,23 @@ void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, i
     }
 }
 
-void launch_evaluate(int R, int max_tasks, const Task* tasks, const int* n_tasks,
-                     const Bucket* buckets, const int* sorted, const double* fdoa, double fs,
-                     const double* nu_c, int B, const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits, int64_t flag_base, float tau,
+size_t evaluate_smem_bytes(int nbmax, int R) { return evaluate_smem(nbmax, R); }
+
+void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+                     int max_buckets, const int* sorted, const double* fdoa, double fs,
+                     const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
+                     uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
                      cudaStream_t st) {
-    if (max_tasks <= 0) return;
+#define DG_EVAL_CASE(RR)                                                                    \
+    evaluate_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
+                         mom, nbmax, s_out, flag_bits, flag_base, tau, sm_count, st)
     switch (R) {
-        case 8: evaluate_variant<8>(max_tasks, tasks, n_tasks, buckets, sorted, fdoa, fs, nu_c, B, mom, nbmax, s_out, flag_bits, flag_base, tau, st); break;
-        case 10: evaluate_variant<10>(max_tasks, tasks, n_tasks, buckets, sorted, fdoa, fs, nu_c, B, mom, nbmax, s_out, flag_bits, flag_base, tau, st); break;
-        case 12: evaluate_variant<12>(max_tasks, tasks, n_tasks, buckets, sorted, fdoa, fs, nu_c, B, mom, nbmax, s_out, flag_bits, flag_base, tau, st); break;
-        default: evaluate_variant<16>(max_tasks, tasks, n_tasks, buckets, sorted, fdoa, fs, nu_c, B, mom, nbmax, s_out, flag_bits, flag_base, tau, st); break;
+        case 8: DG_EVAL_CASE(8); break;
+        case 10: DG_EVAL_CASE(10); break;
+        case 12: DG_EVAL_CASE(12); break;
+        default: DG_EVAL_CASE(16); break;
     }
+#undef DG_EVAL_CASE
 }
 
 }  // namespace dg

@@ -49,6 +49,21 @@ __global__ void __launch_bounds__(256) k_ffma2_peak(float* out, float b, float c
     if (s == 12345.678f) out[0] = s;
 }
 
+__global__ void __launch_bounds__(256) k_dfma_peak(float* out, float bf, float cf) {
+    const double b = bf, c = cf;
+    double a[kChains];
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) a[i] = threadIdx.x * 1e-7 + i;
+    for (int it = 0; it < kIters / 8; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) a[i] = fma(a[i], b, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kChains; ++i) s += a[i];
+    if (s == 12345.678) out[0] = (float)s;
+}
+
 template <class K>
 double time_probe(K kernel, int blocks, int threads, float* out) {
     cudaEvent_t e0, e1;
@@ -117,5 +132,23 @@ extern "C" int dg_fp32_peak_tflops(int device, double* tflops) {
     if (err != cudaSuccess) return DG_ERUNTIME;
     const double flops = 2.0 * kChains * (double)kIters * blocks * threads;
     *tflops = flops / (best * 1e-3) / 1e12;
+    return DG_OK;
+}
+
+/* FP64 TFLOP/s of independent DFMA chains: the ceiling of the exact geometry,
+ * refinement and re-rank kernels. */
+extern "C" int dg_fp64_peak_tflops(int device, double* tflops) {
+    if (!tflops) return DG_EINVAL;
+    if (cudaSetDevice(device) != cudaSuccess) return DG_ERUNTIME;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    float* out = nullptr;
+    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return DG_ENOMEM;
+    const int blocks = sms * 8, threads = 256;
+    const double ms = time_probe(k_dfma_peak, blocks, threads, out);
+    const cudaError_t err = cudaGetLastError();
+    cudaFree(out);
+    if (err != cudaSuccess) return DG_ERUNTIME;
+    *tflops = 2.0 * kChains * (double)(kIters / 8) * blocks * threads / (ms * 1e-3) / 1e12;
     return DG_OK;
 }
