@@ -197,6 +197,23 @@ int dg_geolocate_staged(dg_engine* engine, const dg_grid* grid, const dg_staged*
                         const dg_options* opt, dg_result* result);
 void dg_staged_destroy(dg_staged* staged);
 
+/* The two halves of geolocate_snapshots, for snapshot-sharded multi-GPU runs
+ * (DESIGN.md section 7). dg_correlate_steps: snapshots [s_begin, s_end) over
+ * the whole grid — correlate_snapshot_all_pairs (geolocate.hpp:79-94) and the
+ * optional normalize_by_median (:115-122) — into grids_device
+ * [(s_end-s_begin)][P] and medians_device [s_end-s_begin] (device, caller-
+ * owned; medians only when opt->normalize_per_snapshot). Fills n_refined,
+ * sum_overlap_samples, correlate/moments/evaluate stats of `result`.
+ * dg_accumulate_peak: accumulate_grids (correlate.hpp:102-113) of
+ * grids_device [S][P_grid] (all snapshots, this grid or slab) in snapshot
+ * order, the exact argmax and detect_emitters; outputs as dg_geolocate_staged. */
+int dg_correlate_steps(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
+                       int64_t s_begin, int64_t s_end, const dg_options* opt,
+                       double* grids_device, double* medians_device, dg_result* result);
+int dg_accumulate_peak(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
+                       const double* grids_device, const double* medians_device,
+                       const dg_options* opt, dg_result* result);
+
 /* detect_emitters (correlate.hpp:127-201) on a caller-provided surface over a
  * grid lattice (host or device pointer; is_device selects). */
 int dg_detect_emitters(dg_engine* engine, const dg_grid* grid, const double* values, int is_device,

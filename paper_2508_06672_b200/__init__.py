@@ -11,8 +11,8 @@ from .engine import Engine, default_engine  # noqa: F401
 from .geodesy import (CandidateGrid, GeodeticCoord, GridAxis, LatLonBounds,  # noqa: F401
                       build_candidate_grid, grid_from_points)
 from .geolocate import (CorrelationGrid, EmitterEstimate, GeolocateOptions,  # noqa: F401
-                        GeolocateResult, Snapshot, StagedSnapshots, correlate_snapshot,
-                        geolocate_arrays, geolocate_snapshots, geolocate_staged,
-                        predict_offsets, wavelength_m)
+                        GeolocateResult, Snapshot, StagedSnapshots, accumulate_peak,
+                        correlate_snapshot, correlate_steps, geolocate_arrays,
+                        geolocate_snapshots, geolocate_staged, predict_offsets, wavelength_m)
 
 __version__ = "0.1.0"

@@ -81,7 +81,8 @@ EXPORTS = (
     "dg_correlate_batch", "dg_build_candidate_grid", "dg_grid_slab", "dg_grid_from_points",
     "dg_grid_info", "dg_grid_points", "dg_grid_destroy", "dg_predict_offsets",
     "dg_correlate_snapshot", "dg_options_default", "dg_geolocate_snapshots",
-    "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_detect_emitters",
+    "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_correlate_steps",
+    "dg_accumulate_peak", "dg_detect_emitters",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -122,6 +123,10 @@ def _load():
                                    C.POINTER(dg_result)],
         "dg_stage_snapshots": [_vp, C.POINTER(dg_snapshots), C.POINTER(_vp)],
         "dg_geolocate_staged": [_vp, _vp, _vp, C.POINTER(dg_options), C.POINTER(dg_result)],
+        "dg_correlate_steps": [_vp, _vp, _vp, C.c_int64, C.c_int64, C.POINTER(dg_options), _vp,
+                               _vp, C.POINTER(dg_result)],
+        "dg_accumulate_peak": [_vp, _vp, _vp, _vp, _vp, C.POINTER(dg_options),
+                               C.POINTER(dg_result)],
         "dg_detect_emitters": [_vp, _vp, _vp, C.c_int, C.c_double, C.c_int,
                                C.POINTER(dg_emitter_estimate), C.c_int64, _i64p],
         "dg_fp32_peak_tflops": [C.c_int, _dp],

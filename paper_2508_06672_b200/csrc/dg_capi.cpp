@@ -90,12 +90,16 @@ struct Scratch {
     }
 };
 
+// the caller's stream, else the engine's persistent stream (a fresh stream per
+// call would defeat the stream-ordered memory pool's reuse), else a private one
 struct StreamGuard {
     cudaStream_t st = nullptr;
     bool own = false;
-    explicit StreamGuard(void* user) {
+    explicit StreamGuard(void* user, cudaStream_t fallback = nullptr) {
         if (user) {
             st = static_cast<cudaStream_t>(user);
+        } else if (fallback) {
+            st = fallback;
         } else {
             CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
             own = true;
@@ -131,6 +135,10 @@ void validate_geodetic(double lat, double lon, double alt) {
 struct dg_engine {
     int device = 0;
     int sm_count = 148;
+    cudaStream_t stream = nullptr;  // default stream of calls that pass none
+    ~dg_engine() {
+        if (stream) cudaStreamDestroy(stream);
+    }
 };
 
 struct dg_grid {
@@ -244,7 +252,9 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
         for (int R : kMomentR) {
             if (forceR && R != forceR) continue;
             if (!forceR && jacobi_anger_tail(x, R) > kMomentTail) continue;
-            if (evaluate_smem_bytes((N + B - 1) / B, R) > kEvalSmemMax) break;
+            if (evaluate_smem_bytes(((N + B - 1) / B + kEvalG - 1) / kEvalG * kEvalG, R) >
+                kEvalSmemMax)
+                break;
             const double cost = 1.5 * R * N + avg * ((double)N / B) * (R + 3);
             if (cost < best) {
                 best = cost;
@@ -256,8 +266,8 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
         }
     }
     if (!pl.direct) {
-        pl.nbmax = (N + pl.B - 1) / pl.B;
-        pl.cpb = (pl.nbmax + 31) / 32;
+        pl.nbmax = ((N + pl.B - 1) / pl.B + kEvalG - 1) / kEvalG * kEvalG;
+        pl.cpb = (pl.nbmax + chunk_blocks(pl.B) - 1) / chunk_blocks(pl.B);
     }
     return pl;
 }
@@ -345,7 +355,7 @@ struct Pipeline {
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
         work = sc.alloc<unsigned long long>(2);
-        y1c = sc.alloc<float2>(N);
+        y1c = sc.alloc<float2>(N + 64);  // k_moments' bulk copies may round past N
         CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
         CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
         CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
@@ -602,6 +612,7 @@ int dg_engine_create(int device, dg_engine** out) {
         auto e = std::make_unique<dg_engine>();
         e->device = device;
         e->sm_count = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         *out = e.release();
     });
 }
@@ -750,7 +761,7 @@ int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double sp
         g->x = base;
         g->y = base + n;
         g->z = base + 2 * n;
-        StreamGuard sg(nullptr);
+        StreamGuard sg(nullptr, eng->stream);
         Scratch sc(sg.st);
         double* t = sc.alloc<double>(2 * n_lat + 2 * n_lon);
         CK(cudaMemcpyAsync(t, ra.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
@@ -808,7 +819,7 @@ int dg_grid_from_points(dg_engine* eng, const dg_ecef* pts, int64_t n, double la
         g->x = base;
         g->y = base + n;
         g->z = base + 2 * n;
-        StreamGuard sg(nullptr);
+        StreamGuard sg(nullptr, eng->stream);
         finish_lattice(g.get(), sg.st);
         *out = g.release();
     });
@@ -850,7 +861,7 @@ int dg_predict_offsets(dg_engine* eng, const dg_grid* g, const dg_state* rx_i, c
     return guard([&] {
         if (!eng || !g || !rx_i || !rx_j || !out) raise(DG_EINVAL, "null argument");
         set_device(eng);
-        StreamGuard sg(nullptr);
+        StreamGuard sg(nullptr, eng->stream);
         Scratch sc(sg.st);
         const int64_t P = g->size();
         auto* pg = sc.alloc<PairGeom>(1);
@@ -957,7 +968,7 @@ int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) 
         s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
         auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
         auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
-        StreamGuard sg(nullptr);
+        StreamGuard sg(nullptr, eng->stream);
         CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, sg.st));
         CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, sg.st));
         for (int64_t c = 0; c < n_caps; ++c) {
@@ -1038,142 +1049,206 @@ void run_detect(const dg_grid* g, const double* v_dev, double k_sigma, int radiu
     }
 }
 
-void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt_in,
-                    dg_result* res) {
-    if (!eng || !g || !sn || !res) raise(DG_EINVAL, "null argument");
+// Everything a run shares: pairs, per-(snapshot, pair) receiver states.
+struct RunGeo {
+    int S = 0, R = 0, pairs = 0, SP = 0;
+    double fs = 0, wl = 0;
+    std::vector<int> prx;
+    std::vector<PairGeom> hpg;
+    PairGeom* pg = nullptr;  // device [SP]
+    int* d_prx = nullptr;    // device [2 * pairs]
+};
+
+RunGeo make_geo(Scratch& sc, const dg_staged* sn) {
+    RunGeo r;
+    r.S = (int)sn->S;
+    r.R = (int)sn->R;
+    r.pairs = r.R * (r.R - 1) / 2;
+    r.SP = r.S * r.pairs;
+    r.fs = sn->fs;
+    r.wl = kC / sn->fc;
+    for (int i = 0; i < r.R; ++i)
+        for (int j = i + 1; j < r.R; ++j) {
+            r.prx.push_back(i);
+            r.prx.push_back(j);
+        }
+    r.hpg.resize(r.SP);
+    for (int s = 0; s < r.S; ++s)
+        for (int q = 0; q < r.pairs; ++q)
+            r.hpg[s * r.pairs + q] = PairGeom{sn->states[s * r.R + r.prx[2 * q]],
+                                              sn->states[s * r.R + r.prx[2 * q + 1]]};
+    r.pg = sc.alloc<PairGeom>(r.SP);
+    r.d_prx = sc.alloc<int>(r.prx.size());
+    CK(cudaMemcpyAsync(r.pg, r.hpg.data(), r.SP * sizeof(PairGeom), cudaMemcpyHostToDevice, sc.st));
+    CK(cudaMemcpyAsync(r.d_prx, r.prx.data(), r.prx.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       sc.st));
+    CK(cudaStreamSynchronize(sc.st));  // host vectors may move with the struct
+    return r;
+}
+
+RefineCtx refine_ctx(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, double* raw) {
+    RefineCtx ctx{};
+    ctx.x = g->x;
+    ctx.y = g->y;
+    ctx.z = g->z;
+    ctx.P = g->size();
+    ctx.pg = geo.pg;
+    ctx.pair_rx = geo.d_prx;
+    ctx.pairs = geo.pairs;
+    ctx.R = geo.R;
+    ctx.y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
+    ctx.stride = sn->stride;
+    ctx.N = (int)sn->N;
+    ctx.fs = geo.fs;
+    ctx.wl = geo.wl;
+    ctx.raw = raw;
+    return ctx;
+}
+
+dg_options options_or_default(const dg_options* o) {
     dg_options opt;
-    if (opt_in) {
-        opt = *opt_in;
+    if (o) {
+        opt = *o;
     } else {
         dg_options_default(&opt);
     }
-    const int64_t P = g->size();
-    if (P == 0) raise(DG_EINVAL, "correlate_snapshot: empty grid");
-    if (opt.exclusion_radius_cells < 0)
-        raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
-    set_device(eng);
-    const int S = (int)sn->S, R = (int)sn->R;
-    const int pairs = R * (R - 1) / 2;
-    const int SP = S * pairs;
-    const double fs = sn->fs, wl = kC / sn->fc;
-    StreamGuard sg(opt.stream);
-    cudaStream_t st = sg.st;
-    Scratch sc(st);
-    int64_t launches = 0;
+    return opt;
+}
 
-    cudaEvent_t ev_all0 = nullptr, ev_all1 = nullptr;
+// Snapshots [s0, s1) over the whole grid g: geometry, correlation of every
+// pair, exact refinement, pair sums (correlate_snapshot_all_pairs) and the
+// optional median scaling -> grids [(s1-s0)][P] (device), medians [s1-s0].
+// This is the step-sharded half of geolocate_snapshots.
+void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                          const RunGeo& geo, int s0, int s1, const dg_options& opt, double* grids,
+                          double* medians, Scratch& sc, dg_result* res) {
+    const int64_t P = g->size();
+    const int pairs = geo.pairs, R = geo.R;
+    const int ns = s1 - s0, SPl = ns * pairs;
+    const double fs = geo.fs, wl = geo.wl;
+    cudaStream_t st = sc.st;
+    int64_t launches = 0;
+    if (ns <= 0) return;
+
     std::vector<cudaEvent_t> evs;
     if (opt.profile) {
-        CK(cudaEventCreate(&ev_all0));
-        CK(cudaEventCreate(&ev_all1));
-        evs.resize(3 * SP);
+        evs.resize(3 * SPl);
         for (auto& e : evs) CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(ev_all0, st));
     }
     struct EvFree {
         std::vector<cudaEvent_t>* v;
-        cudaEvent_t a, b;
         ~EvFree() {
             for (auto e : *v) cudaEventDestroy(e);
-            if (a) cudaEventDestroy(a);
-            if (b) cudaEventDestroy(b);
         }
-    } ev_free{&evs, ev_all0, ev_all1};
-
-    // pair table and per-(snapshot, pair) receiver states
-    std::vector<int> prx;
-    for (int i = 0; i < R; ++i)
-        for (int j = i + 1; j < R; ++j) {
-            prx.push_back(i);
-            prx.push_back(j);
-        }
-    std::vector<PairGeom> hpg(SP);
-    for (int s = 0; s < S; ++s)
-        for (int q = 0; q < pairs; ++q)
-            hpg[s * pairs + q] = PairGeom{sn->states[s * R + prx[2 * q]], sn->states[s * R + prx[2 * q + 1]]};
-    auto* pg = sc.alloc<PairGeom>(SP);
-    auto* d_prx = sc.alloc<int>(prx.size());
-    CK(cudaMemcpyAsync(pg, hpg.data(), SP * sizeof(PairGeom), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_prx, prx.data(), prx.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    } ev_free{&evs};
 
     Pipeline pl;
-    pl.init(sc, P, sn->N, SP, eng->sm_count);
-    const int64_t n_elems = (int64_t)SP * P;
-    auto* raw = sc.alloc<double>(n_elems);
+    pl.init(sc, P, sn->N, SPl, eng->sm_count);
+    const int64_t n_elems = (int64_t)SPl * P;
+    double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
     const int64_t n_words = (n_elems + 31) / 32;
     auto* bits = sc.alloc<uint32_t>(n_words);
     CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
     const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
     const auto* y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
+    const int sp0 = s0 * pairs;  // global (snapshot, pair) index of local step 0
 
-    for (int w0 = 0; w0 < SP; w0 += pl.slots) {
-        const int nw = std::min(pl.slots, SP - w0);
+    for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
+        const int nw = std::min(pl.slots, SPl - w0);
         pl.reset_ranges(sc, nw);
         for (int i = 0; i < nw; ++i) {  // phase A: geometry of the window
-            const int sp = w0 + i;
-            launch_geometry_hist(g->x, g->y, g->z, P, pg + sp, fs, wl, pl.N, pl.d_slot(i),
-                                 pl.fdoa_slot(i), pl.hist_slot(i), raw + (int64_t)sp * P,
-                                 pl.overlap, pl.err, pl.range + i, st);
+            const int lsp = w0 + i;
+            launch_geometry_hist(g->x, g->y, g->z, P, geo.pg + sp0 + lsp, fs, wl, pl.N,
+                                 pl.d_slot(i), pl.fdoa_slot(i), pl.hist_slot(i),
+                                 raw + (int64_t)lsp * P, pl.overlap, pl.err, pl.range + i, st);
             launches += 1;
         }
-        const StepRange* approx = pl.lattice_ranges(sc, g, hpg.data() + w0, nw, fs, wl);
-        pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hpg.data() + w0, nw, wl),
-                       g->full_size);
+        const PairGeom* hw = geo.hpg.data() + sp0 + w0;
+        const StepRange* approx = pl.lattice_ranges(sc, g, hw, nw, fs, wl);
+        pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size);
         for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each step
-            const int sp = w0 + i;
+            const int lsp = w0 + i, sp = sp0 + lsp;
             const int s = sp / pairs, q = sp - s * pairs;
-            const int64_t c1 = ((int64_t)s * R + prx[2 * q]) * sn->stride;
-            const int64_t c2 = ((int64_t)s * R + prx[2 * q + 1]) * sn->stride;
-            pl.correlate(sc, i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)sp * P, bits,
-                         (int64_t)sp * P, opt.profile ? evs[3 * sp] : nullptr,
-                         opt.profile ? evs[3 * sp + 1] : nullptr,
-                         opt.profile ? evs[3 * sp + 2] : nullptr);
+            const int64_t c1 = ((int64_t)s * R + geo.prx[2 * q]) * sn->stride;
+            const int64_t c2 = ((int64_t)s * R + geo.prx[2 * q + 1]) * sn->stride;
+            pl.correlate(sc, i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)lsp * P, bits,
+                         (int64_t)lsp * P, opt.profile ? evs[3 * lsp] : nullptr,
+                         opt.profile ? evs[3 * lsp + 1] : nullptr,
+                         opt.profile ? evs[3 * lsp + 2] : nullptr);
         }
     }
     launches += pl.launches;
     CK(cudaGetLastError());
     check_err_flag(sc, pl.err);
 
-    RefineCtx ctx{};
-    ctx.x = g->x;
-    ctx.y = g->y;
-    ctx.z = g->z;
-    ctx.P = P;
-    ctx.pg = pg;
-    ctx.pair_rx = d_prx;
-    ctx.pairs = pairs;
-    ctx.R = R;
-    ctx.y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
-    ctx.stride = sn->stride;
-    ctx.N = (int)sn->N;
-    ctx.fs = fs;
-    ctx.wl = wl;
-    ctx.raw = raw;
+    // exact refinement; element e = local step * P + p
+    RefineCtx ctx = refine_ctx(g, sn, geo, raw);
+    ctx.pg = geo.pg + sp0;
+    ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
     res->n_refined = run_refine(sc, bits, n_elems, ctx, &launches);
 
-    // per-snapshot grids: pair sums (correlate_snapshot_all_pairs), optional median scaling
-    double* grids = raw;
     if (pairs > 1) {
-        grids = sc.alloc<double>((int64_t)S * P);
-        launch_combine_pairs(raw, S, pairs, P, grids, st);
+        launch_combine_pairs(raw, ns, pairs, P, grids, st);
         launches += 1;
     }
-    double* medians = nullptr;
     if (opt.normalize_per_snapshot) {
-        medians = sc.alloc<double>(S);
         auto* hist = sc.alloc<unsigned>(256);
-        auto* state = sc.alloc<unsigned long long>(2);
+        auto* state = sc.alloc<unsigned long long>(2 * ns);
+        std::vector<unsigned long long> init(2 * ns);
+        for (int s = 0; s < ns; ++s) {
+            init[2 * s] = 0ull;
+            init[2 * s + 1] = (unsigned long long)(P / 2);
+        }
+        CK(cudaMemcpyAsync(state, init.data(), init.size() * sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned), st));
-        for (int s = 0; s < S; ++s) {
-            const unsigned long long init[2] = {0ull, (unsigned long long)(P / 2)};
-            CK(cudaMemcpyAsync(state, init, sizeof init, cudaMemcpyHostToDevice, st));
-            launch_median(grids + (int64_t)s * P, P, hist, state, medians + s, st);
+        for (int s = 0; s < ns; ++s) {
+            launch_median(grids + (int64_t)s * P, P, hist, state + 2 * s, medians + s, st);
             launch_scale(grids + (int64_t)s * P, P, medians + s, st);
-            CK(cudaStreamSynchronize(st));  // `init` lives on the host stack
             launches += 17;
         }
+        CK(cudaStreamSynchronize(st));  // `init` is host memory of this frame
     }
-    double* acc = opt_in && res->accumulated_device ? res->accumulated_device : sc.alloc<double>(P);
+
+    unsigned long long ovl = 0, work[2] = {0, 0};
+    CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(work, pl.work, sizeof work, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    res->sum_overlap_samples = (double)ovl;
+    res->kernel_launches += launches;
+    res->correlate_launches = SPl;
+    res->moment_ffma2 = (double)work[0];
+    res->evaluate_ffma2 = (double)work[1];
+    res->direct_steps = pl.direct_steps;
+    if (opt.profile) {
+        double tm = 0.0, te = 0.0;
+        for (int i = 0; i < SPl; ++i) {
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, evs[3 * i], evs[3 * i + 1]));
+            CK(cudaEventElapsedTime(&b, evs[3 * i + 1], evs[3 * i + 2]));
+            tm += a;
+            te += b;
+        }
+        res->moments_ms = tm;
+        res->evaluate_ms = te;
+        res->correlate_ms = tm + te;
+    }
+}
+
+// Accumulation over ALL S snapshots of grid g (a slab or the full lattice)
+// from per-snapshot grids [S][P] (device), then the exact peak (near-peak
+// cells re-evaluated in FP64 for every (snapshot, pair)), detection and the
+// host copies — the other half of geolocate_snapshots.
+void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunGeo& geo,
+               const double* grids, const double* medians, const dg_options& opt,
+               bool acc_dev_allowed, dg_result* res, Scratch& sc) {
+    (void)eng;
+    const int64_t P = g->size();
+    const int S = geo.S, SP = geo.SP, pairs = geo.pairs;
+    cudaStream_t st = sc.st;
+    int64_t launches = 0;
+    double* acc = acc_dev_allowed && res->accumulated_device ? res->accumulated_device
+                                                             : sc.alloc<double>(P);
     launch_accumulate(grids, S, P, acc, st);
     launches += 1;
 
@@ -1202,6 +1277,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
             CK(cudaStreamSynchronize(st));
             if (hn <= kRerankCap || rel < 1e-12) break;
         }
+        RefineCtx ctx = refine_ctx(g, sn, geo, nullptr);
         auto* ex = sc.alloc<double>((int64_t)kRerankCap * SP);
         acc_ex = sc.alloc<double>(kRerankCap);
         grid_ex = sc.alloc<double>((int64_t)kRerankCap * S);
@@ -1222,7 +1298,6 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
         res->argmax_value = hmax;
     }
     res->n_reranked = std::min(hn, kRerankCap);
-    if (opt.profile) CK(cudaEventRecord(ev_all1, st));
 
     res->n_detections = 0;
     if (opt.detect)
@@ -1234,9 +1309,6 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     if (res->per_snapshot)
         CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
                            cudaMemcpyDeviceToHost, st));
-    unsigned long long ovl = 0, work[2] = {0, 0};
-    CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(work, pl.work, sizeof work, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (opt.patch_peak && acc_ex && res->n_reranked > 0 && (res->accumulated || res->per_snapshot)) {
         // exact FP64 values of the re-ranked cells into the host copies
@@ -1251,35 +1323,92 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
         for (int i = 0; i < n; ++i) {
             if (res->accumulated) res->accumulated[hc[i]] = ha[i];
             if (res->per_snapshot)
-                for (int s = 0; s < S; ++s) res->per_snapshot[(int64_t)s * P + hc[i]] = hg[(size_t)i * S + s];
+                for (int s = 0; s < S; ++s)
+                    res->per_snapshot[(int64_t)s * P + hc[i]] = hg[(size_t)i * S + s];
         }
     }
-    res->sum_overlap_samples = (double)ovl;
-    res->kernel_launches = launches;
-    res->correlate_launches = SP;
-    res->moment_ffma2 = (double)work[0];
-    res->evaluate_ffma2 = (double)work[1];
-    res->direct_steps = pl.direct_steps;
+    res->kernel_launches += launches;
+}
+
+void check_run(const dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options& opt,
+               const void* res) {
+    if (!eng || !g || !sn || !res) raise(DG_EINVAL, "null argument");
+    if (g->size() == 0) raise(DG_EINVAL, "correlate_snapshot: empty grid");
+    if (opt.exclusion_radius_cells < 0)
+        raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
+}
+
+void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt_in,
+                    dg_result* res) {
+    const dg_options opt = options_or_default(opt_in);
+    check_run(eng, g, sn, opt, res);
+    set_device(eng);
+    StreamGuard sg(opt.stream, eng->stream);
+    Scratch sc(sg.st);
+    res->kernel_launches = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (opt.profile) {
-        double tot = 0.0, tm = 0.0, te = 0.0;
-        for (int i = 0; i < SP; ++i) {
-            float a = 0.f, b = 0.f;
-            CK(cudaEventElapsedTime(&a, evs[3 * i], evs[3 * i + 1]));
-            CK(cudaEventElapsedTime(&b, evs[3 * i + 1], evs[3 * i + 2]));
-            tm += a;
-            te += b;
-            tot += a + b;
-        }
-        res->correlate_ms = tot;
-        res->moments_ms = tm;
-        res->evaluate_ms = te;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, sc.st));
+    }
+    const RunGeo geo = make_geo(sc, sn);
+    const int64_t P = g->size();
+    auto* grids = sc.alloc<double>((int64_t)geo.S * P);
+    double* medians = opt.normalize_per_snapshot ? sc.alloc<double>(geo.S) : nullptr;
+    correlate_steps_impl(eng, g, sn, geo, 0, geo.S, opt, grids, medians, sc, res);
+    peak_impl(eng, g, sn, geo, grids, medians, opt, opt_in != nullptr, res, sc);
+    if (opt.profile) {
+        CK(cudaEventRecord(e1, sc.st));
+        CK(cudaEventSynchronize(e1));
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev_all0, ev_all1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
         res->total_ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
     }
 }
 
 }  // namespace
+
+int dg_correlate_steps(dg_engine* eng, const dg_grid* g, const dg_staged* sn, int64_t s_begin,
+                       int64_t s_end, const dg_options* opt_in, double* grids_device,
+                       double* medians_device, dg_result* res) {
+    return guard([&] {
+        const dg_options opt = options_or_default(opt_in);
+        check_run(eng, g, sn, opt, res);
+        if (s_begin < 0 || s_end > sn->S || s_begin > s_end)
+            raise(DG_EINVAL, "dg_correlate_steps: bad snapshot range");
+        if (!grids_device) raise(DG_EINVAL, "dg_correlate_steps: null grids");
+        if (opt.normalize_per_snapshot && !medians_device)
+            raise(DG_EINVAL, "dg_correlate_steps: normalisation needs a medians buffer");
+        set_device(eng);
+        StreamGuard sg(opt.stream, eng->stream);
+        Scratch sc(sg.st);
+        res->kernel_launches = 0;
+        const RunGeo geo = make_geo(sc, sn);
+        correlate_steps_impl(eng, g, sn, geo, (int)s_begin, (int)s_end, opt, grids_device,
+                             medians_device, sc, res);
+    });
+}
+
+int dg_accumulate_peak(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                       const double* grids_device, const double* medians_device,
+                       const dg_options* opt_in, dg_result* res) {
+    return guard([&] {
+        const dg_options opt = options_or_default(opt_in);
+        check_run(eng, g, sn, opt, res);
+        if (!grids_device) raise(DG_EINVAL, "dg_accumulate_peak: null grids");
+        set_device(eng);
+        StreamGuard sg(opt.stream, eng->stream);
+        Scratch sc(sg.st);
+        res->kernel_launches = 0;
+        const RunGeo geo = make_geo(sc, sn);
+        peak_impl(eng, g, sn, geo, grids_device,
+                  opt.normalize_per_snapshot ? medians_device : nullptr, opt, opt_in != nullptr,
+                  res, sc);
+    });
+}
 
 int dg_geolocate_staged(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt,
                         dg_result* res) {
@@ -1304,7 +1433,7 @@ int dg_detect_emitters(dg_engine* eng, const dg_grid* g, const double* values, i
         if (!eng || !g || !values || !n_out) raise(DG_EINVAL, "null argument");
         if (radius < 0) raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
         set_device(eng);
-        StreamGuard sg(nullptr);
+        StreamGuard sg(nullptr, eng->stream);
         Scratch sc(sg.st);
         const int64_t P = g->size();
         const double* v = values;

@@ -60,7 +60,10 @@ struct RxPairF32 {
     float pi[3], vi[3], pj[3], vj[3];
 };
 
-constexpr int kMaxMoments = 16;  // Chebyshev table width (moments per block <= 16)
+constexpr int kMaxMoments = 16;
+constexpr int kEvalG = 8;  // blocks per exact-phase group in k_evaluate (moment rows padded to it)
+// blocks per k_moments work item (shared-memory budget: two items' worth per SM)
+__host__ __device__ constexpr int chunk_blocks(int B) { return B >= 256 ? 16 : 32; }  // Chebyshev table width (moments per block <= 16)
 
 // Geometry of one (snapshot, pair): receiver states for predict_pair_offsets.
 struct PairGeom {
@@ -124,7 +127,6 @@ void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, cons
 
 // block-moment correlator (dg_moments.cu)
 void launch_center(const double2* y, int N, const double* nu_c, float2* out, cudaStream_t st);
-size_t moments_smem_bytes(int B);
 void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
                        unsigned long long* work, cudaStream_t st);
 void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,

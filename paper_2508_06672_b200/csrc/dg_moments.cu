@@ -53,19 +53,13 @@ __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
     sincospif((float)(2.0 * (x - rint(x))), s, c);
 }
 
-constexpr int kChunkBlocks = 32;  // blocks per k_moments work item (one per lane)
+static_assert(chunk_blocks(256) % kEvalG == 0 && chunk_blocks(64) % kEvalG == 0,
+              "padding stays inside the last chunk");
+__host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) / kEvalG * kEvalG; }
 
 // two staging buffers of one bucket's moments
 inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * sizeof(float2); }
 constexpr int kMomThreads = 256;
-
-// table + max(z chunk, per-warp partial moments)
-constexpr size_t moments_smem(int B) {
-    return (size_t)B * kMaxMoments * sizeof(float) +
-           sizeof(float2) * ((size_t)kChunkBlocks * (B + 1) > (size_t)8 * 32 * (kMaxMoments + 1)
-                                 ? (size_t)kChunkBlocks * (B + 1)
-                                 : (size_t)8 * 32 * (kMaxMoments + 1));
-}
 
 __global__ void k_center(const double2* __restrict__ y, int N, const double* __restrict__ nu_c,
                          float2* __restrict__ out) {
@@ -79,6 +73,62 @@ __global__ void k_center(const double2* __restrict__ y, int N, const double* __r
     }
 }
 
+// TMA helpers (1-D bulk copy global -> shared, mbarrier completion)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Moments of one d-bucket, a chunk of CB = chunk_blocks(B) blocks per work
+// item (items strided over a persistent grid). Per item:
+//   stage  y1c[k0 ..) and y2[k0+d ..) arrive by TMA bulk copy (issued while
+//          the previous item computed its moments)
+//   z      = y1c conj(y2) from the stage into a padded [block][B+1] buffer
+//   M_m[b] lane = block (x 32/CB lanes splitting j), warp = slice of j, FFMA2
+//          with the Chebyshev row broadcast from shared memory; partials
+//          summed in a fixed order (shuffle, then 8 warps through smem)
+template <int B, int R>
+struct MomLayout {
+    static constexpr int CB = chunk_blocks(B);
+    static constexpr int LPB = 32 / CB;             // lanes per block
+    static constexpr int RP = (R + 3) / 4 * 4;      // table row (floats)
+    static constexpr int ZS = B + 1;                // padded z row
+    static constexpr int CS = CB * B;               // samples per chunk
+    static constexpr size_t zbuf = ((size_t)CB * ZS > (size_t)8 * CB * (R + 1)
+                                        ? (size_t)CB * ZS
+                                        : (size_t)8 * CB * (R + 1)) + 1 & ~(size_t)1;
+    static constexpr size_t table_floats = (size_t)B / 2 * RP;  // rows j < B/2
+    static constexpr size_t smem = table_floats * sizeof(float) +
+                                   sizeof(float2) * (zbuf + 2 * ((size_t)CS + 8));
+};
+
 template <int B, int R>
 __global__ void __launch_bounds__(kMomThreads, 2)
 k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets, int cpb,
@@ -86,81 +136,138 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
           const float2* __restrict__ y2, int N, float2* __restrict__ mom, int nbmax) {
     static_assert(B % 64 == 0 && B <= 256, "block length");
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
-    constexpr int RQ = (R + 3) / 4;          // float4 rows of the table actually read
-    constexpr int ZS = B + 1;                // padded z row (conflict-free column reads)
-    constexpr int JW = B / 8;                // samples per warp in the moment pass
+    using L = MomLayout<B, R>;
+    constexpr int CB = L::CB, LPB = L::LPB, RP = L::RP, ZS = L::ZS, CS = L::CS;
+    constexpr int PW = B / 16;          // sample pairs (j, B-1-j) per warp
+    constexpr int PL = PW / LPB;        // ... per lane
     extern __shared__ float4 smem4[];
-    float* ts = reinterpret_cast<float*>(smem4);                    // [B][kMaxMoments]
-    float2* zs = reinterpret_cast<float2*>(ts + B * kMaxMoments);   // [32][ZS]
+    float* ts = reinterpret_cast<float*>(smem4);                       // [B/2][RP]
+    float2* zs = reinterpret_cast<float2*>(ts + L::table_floats);      // z / partials
+    float2* s1 = zs + L::zbuf;                                         // stage y1c [CS + 8]
+    float2* s2 = s1 + CS + 8;                                          // stage y2  [CS + 8]
+    __shared__ uint64_t bar;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < B * kMaxMoments; i += kMomThreads) ts[i] = tcheb[i];
-
+    const int blk = lane % CB, half = lane / CB;
     const int nitems = *n_buckets * cpb;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        const int u = item / cpb, c = item - u * cpb;
+    // next item at or after `it` (stride gridDim.x) whose chunk overlaps its bucket
+    auto next_valid = [&](int it) {
+        for (; it < nitems; it += gridDim.x) {
+            const int u = it / cpb;
+            if ((it - u * cpb) * CB < buckets[u].nb) return it;
+        }
+        return nitems;
+    };
+    auto issue = [&](int it) {  // thread 0: TMA of the item's y1c / y2 ranges
+        const int u = it / cpb;
         const Bucket bk = buckets[u];
-        const int b0 = c * kChunkBlocks;
-        if (b0 >= bk.nb) continue;  // uniform: this chunk is past the overlap
-        const int d = bk.d;
-        const int kb = d < 0 ? -d : 0;
-        const int ke = d > 0 ? N - d : N;
+        const int d = bk.d, kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
+        const int k0 = kb + (it - u * cpb) * CS;
+        const int cnt = min(CS, ke - k0);
+        const int a1 = k0 & ~1, a2 = (k0 + d) & ~1;
+        const uint32_t n1 = (uint32_t)(((k0 - a1 + cnt) * 8 + 15) & ~15);
+        const uint32_t n2 = (uint32_t)(((k0 + d - a2 + cnt) * 8 + 15) & ~15);
+        mbar_expect_tx(&bar, n1 + n2);
+        tma_load_1d(s1, y1c + a1, n1, &bar);
+        tma_load_1d(s2, y2 + a2, n2, &bar);
+    };
+
+    for (int i = tid; i < B / 2 * RP; i += kMomThreads)
+        ts[i] = tcheb[(i / RP) * kMaxMoments + (i % RP)];
+    int item = next_valid(blockIdx.x);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (item < nitems) issue(item);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (; item < nitems;) {
+        const int u = item / cpb;
+        const Bucket bk = buckets[u];
+        const int b0 = (item - u * cpb) * CB;
+        const int d = bk.d, kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
         const int k0 = kb + b0 * B;
-        __syncthreads();  // table loaded / previous item's reduction consumed
+        const int sh1 = k0 & 1, sh2 = (k0 + d) & 1;
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
 
         // ---- z = y1c conj(y2[k+d]) for the chunk, zero past the overlap ----
-#pragma unroll 4
-        for (int i = tid; i < kChunkBlocks * B; i += kMomThreads) {
-            const int k = k0 + i;
+        const int lim = ke - k0;
+#pragma unroll 8
+        for (int i = tid; i < CS; i += kMomThreads) {
             float2 zz = make_float2(0.f, 0.f);
-            if (k < ke) {
-                const float2 a = y1c[k], b = y2[k + d];
+            if (i < lim) {
+                const float2 a = s1[i + sh1], b = s2[i + sh2];
                 zz.x = fmaf(a.x, b.x, a.y * b.y);
                 zz.y = fmaf(a.y, b.x, -(a.x * b.y));
             }
             zs[(i / B) * ZS + (i % B)] = zz;
         }
-        __syncthreads();
+        __syncthreads();  // stage consumed, z complete
+        const int nitem = next_valid(item + gridDim.x);
+        if (tid == 0 && nitem < nitems) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(nitem);  // lands while this item's moments are computed
+        }
 
-        // ---- lane = block, warp = slice of j: partial moments on FFMA2 ----
+        // ---- partial moments on FFMA2, folded: T_m(-t) = (-1)^m T_m(t), so the
+        // pair (j, B-1-j) contributes T_m(t_j) (z_j + z_{B-1-j}) to even m and
+        // T_m(t_j) (z_j - z_{B-1-j}) to odd m: R/2 FFMA2 per sample ----
         float2 acc[R];
 #pragma unroll
         for (int m = 0; m < R; ++m) acc[m] = make_float2(0.f, 0.f);
-        const float2* zrow = zs + lane * ZS + warp * JW;
-        const float4* trow = reinterpret_cast<const float4*>(ts + warp * JW * kMaxMoments);
+        const int p0 = warp * PW + half * PL;
+        const float2* zrow = zs + blk * ZS;
+        const float4* trow = reinterpret_cast<const float4*>(ts + p0 * RP);
 #pragma unroll 4
-        for (int j = 0; j < JW; ++j) {
-            const float2 zv = zrow[j];
+        for (int q0 = 0; q0 < PL; ++q0) {
+            const float2 za = zrow[p0 + q0], zb = zrow[B - 1 - p0 - q0];
+            const float2 ue = make_float2(za.x + zb.x, za.y + zb.y);
+            const float2 vo = make_float2(za.x - zb.x, za.y - zb.y);
 #pragma unroll
-            for (int q = 0; q < RQ; ++q) {
-                const float4 t = trow[j * (kMaxMoments / 4) + q];
-                if (4 * q + 0 < R) acc[4 * q + 0] = ffma2(zv, t.x, acc[4 * q + 0]);
-                if (4 * q + 1 < R) acc[4 * q + 1] = ffma2(zv, t.y, acc[4 * q + 1]);
-                if (4 * q + 2 < R) acc[4 * q + 2] = ffma2(zv, t.z, acc[4 * q + 2]);
-                if (4 * q + 3 < R) acc[4 * q + 3] = ffma2(zv, t.w, acc[4 * q + 3]);
+            for (int q = 0; q < RP / 4; ++q) {
+                const float4 t = trow[q0 * (RP / 4) + q];
+                if (4 * q + 0 < R) acc[4 * q + 0] = ffma2(ue, t.x, acc[4 * q + 0]);
+                if (4 * q + 1 < R) acc[4 * q + 1] = ffma2(vo, t.y, acc[4 * q + 1]);
+                if (4 * q + 2 < R) acc[4 * q + 2] = ffma2(ue, t.z, acc[4 * q + 2]);
+                if (4 * q + 3 < R) acc[4 * q + 3] = ffma2(vo, t.w, acc[4 * q + 3]);
+            }
+        }
+        if (LPB == 2) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                acc[m].x += __shfl_xor_sync(0xffffffffu, acc[m].x, 16);
+                acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, 16);
             }
         }
         __syncthreads();  // every warp is done reading zs
         // partials -> smem [warp][block][R+1] (reuses the z buffer), fixed-order sum
         float2* red = zs;
+        if (half == 0) {
 #pragma unroll
-        for (int m = 0; m < R; ++m) red[(warp * 32 + lane) * (R + 1) + m] = acc[m];
+            for (int m = 0; m < R; ++m) red[(warp * CB + blk) * (R + 1) + m] = acc[m];
+        }
         __syncthreads();
-        const int nbc = min(kChunkBlocks, bk.nb - b0);
+        // blocks past nb up to a multiple of kEvalG are all-zero (z = 0 there):
+        // written too, so k_evaluate runs whole groups without a bounds check
+        const int nbc = min(CB, pad_blocks(bk.nb) - b0);
         float2* dst = mom + ((size_t)u * nbmax + b0) * R;
         for (int o = tid; o < nbc * R; o += kMomThreads) {
             const int b = o / R, m = o - b * R;
-            float2 s = red[b * (R + 1) + m];
+            float2 sm = red[b * (R + 1) + m];
 #pragma unroll
             for (int w = 1; w < 8; ++w) {
-                const float2 v = red[(w * 32 + b) * (R + 1) + m];
-                s.x += v.x;
-                s.y += v.y;
+                const float2 v = red[(w * CB + b) * (R + 1) + m];
+                sm.x += v.x;
+                sm.y += v.y;
             }
             // odd moments are stored times i, so a candidate's block value is
             // one real-weighted sum  C_b = sum_m c_m M'_m  (k_evaluate)
-            dst[o] = (m & 1) ? make_float2(-s.y, s.x) : s;
+            dst[o] = (m & 1) ? make_float2(-sm.y, sm.x) : sm;
         }
+        __syncthreads();  // partials consumed before the next item's z
+        item = nitem;
     }
 }
 
@@ -211,36 +318,6 @@ __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
     }
 }
 
-// ---- TMA helpers (1-D bulk copy global -> shared, mbarrier completion) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {  // elementwise
     float2 d;
     asm("{.reg .b64 ra, rb, rc, rd;\n\t"
@@ -258,12 +335,15 @@ constexpr int kEvalWarps = 4;
 constexpr int kEvalNC = 2;                              // candidates per lane
 constexpr int kEvalPass = 32 * kEvalWarps * kEvalNC;   // candidates per CTA pass
 
-// One CTA per d-bucket (dynamic queue), the bucket's moments staged in shared
-// memory by one TMA bulk copy (double-buffered: the next bucket's copy runs
-// under this bucket's evaluation); each lane evaluates kEvalNC candidates:
+// One CTA per d-bucket from a dynamic queue; the bucket's moments are staged
+// in shared memory by one TMA bulk copy into a double buffer run as a
+// producer/consumer pipeline (full/empty mbarriers): thread 0 claims and
+// prefetches bucket k+1 while the warps evaluate bucket k, and each warp
+// releases a buffer on its own, so no warp waits for the others at a bucket
+// boundary. Each lane evaluates kEvalNC candidates:
 //   C_b = sum_m c_m M'_m[b]                       (R FFMA2, broadcast LDS.128)
 //   group g of G blocks:  A += Re(W_j) C_b, V += Im(W_j) C_b, e += C_b o C_b
-//   H_g = A + iV;  acc += e^{i 2 pi nu B G g} H_g   (anchor from an FP64 phase)
+//   acc += a_g (A + iV),  a_{g+1} = a_g e^{i 2 pi nu B G}   (FP64 recurrence)
 // W_j = e^{i 2 pi nu B j} (j < G) are rounded once from FP64 phases.
 template <int R, int G>
 __global__ void __launch_bounds__(32 * kEvalWarps, 4)
@@ -273,51 +353,53 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
            const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
            uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
     extern __shared__ float4 smem4[];
-    float4* mbuf[2] = {smem4, smem4 + (size_t)nbmax * R / 2};
-    __shared__ uint64_t bar[2];
-    __shared__ int next_u[2];
+    __shared__ uint64_t full[2], empty[2];
+    __shared__ int slot_u[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nbk = *n_buckets;
     const double nu_c = *nu_c_p;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const int u0 = atomicAdd(queue, 1);
-        next_u[0] = u0;
-        if (u0 < nbk) {
-            const uint32_t bytes = (uint32_t)buckets[u0].nb * R * sizeof(float2);
-            mbar_expect_tx(&bar[0], bytes);
-            tma_load_1d(mbuf[0], mom + (size_t)u0 * nbmax * R, bytes, &bar[0]);
+    const size_t buf_f4 = (size_t)nbmax * R / 2;
+
+    auto produce = [&](int k) {  // thread 0 only
+        const int sl = k & 1;
+        if (k >= 2) mbar_wait(&empty[sl], ((k >> 1) - 1) & 1);
+        const int u = atomicAdd(queue, 1);
+        slot_u[sl] = u;
+        if (u < nbk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t bytes = (uint32_t)pad_blocks(buckets[u].nb) * R * sizeof(float2);
+            mbar_expect_tx(&full[sl], bytes);
+            tma_load_1d(smem4 + sl * buf_f4, mom + (size_t)u * nbmax * R, bytes, &full[sl]);
+        } else {
+            mbar_arrive(&full[sl]);  // end of queue: complete the phase with no data
         }
+    };
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], kEvalWarps);
+        mbar_init(&empty[1], kEvalWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t phase[2] = {0u, 0u};
-    for (int it = 0;; ++it) {
-        const int buf = it & 1;
-        const int u = next_u[buf];
+    if (tid == 0) produce(0);
+
+    for (int k = 0;; ++k) {
+        if (tid == 0) produce(k + 1);
+        const int sl = k & 1;
+        mbar_wait(&full[sl], (k >> 1) & 1);
+        const int u = slot_u[sl];
         if (u >= nbk) break;
-        if (tid == 0) {  // claim and prefetch the next bucket into the other buffer
-            const int un = atomicAdd(queue, 1);
-            next_u[buf ^ 1] = un;
-            if (un < nbk) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint32_t bytes = (uint32_t)buckets[un].nb * R * sizeof(float2);
-                mbar_expect_tx(&bar[buf ^ 1], bytes);
-                tma_load_1d(mbuf[buf ^ 1], mom + (size_t)un * nbmax * R, bytes, &bar[buf ^ 1]);
-            }
-        }
         const Bucket bk = buckets[u];
         const int nb = bk.nb;
-        mbar_wait(&bar[buf], phase[buf]);
-        phase[buf] ^= 1u;
-        const float4* mb = mbuf[buf];
+        const float4* mb = smem4 + sl * buf_f4;
 
         for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
             int p[kEvalNC];
             double nu[kEvalNC];
             float cf[kEvalNC][R];
             float wtr[kEvalNC][G], wti[kEvalNC][G];
+            double sr[kEvalNC], si[kEvalNC];  // e^{i 2 pi nu B G}
 #pragma unroll
             for (int c = 0; c < kEvalNC; ++c) {
                 const int slot = base + 32 * c + lane;
@@ -332,32 +414,38 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
 #pragma unroll
                 for (int j = 0; j < G; ++j)
                     cis_cycles(nu[c] * (double)B * (double)j, &wtr[c][j], &wti[c][j]);
+                const double x = nu[c] * (double)B * (double)G;
+                sincospi(2.0 * (x - rint(x)), &si[c], &sr[c]);
             }
-            double acc_re[kEvalNC], acc_im[kEvalNC], en[kEvalNC];
+            double acc_re[kEvalNC], acc_im[kEvalNC], en[kEvalNC], ar[kEvalNC], ai[kEvalNC];
 #pragma unroll
-            for (int c = 0; c < kEvalNC; ++c) acc_re[c] = acc_im[c] = en[c] = 0.0;
-            const int ng = (nb + G - 1) / G;
-            for (int g = 0; g < ng; ++g) {
+            for (int c = 0; c < kEvalNC; ++c) {
+                acc_re[c] = acc_im[c] = en[c] = ai[c] = 0.0;
+                ar[c] = 1.0;
+            }
+            const int ng = pad_blocks(nb) / G;
+            const float4* mg = mb;
+            for (int g = 0; g < ng; ++g, mg += G * (R / 2)) {
                 float2 A[kEvalNC], V[kEvalNC], E2[kEvalNC];
 #pragma unroll
                 for (int c = 0; c < kEvalNC; ++c)
                     A[c] = V[c] = E2[c] = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
-                    const int b = g * G + j;
-                    if (b < nb) {
+                    {
                         float4 mv[R / 2];
 #pragma unroll
-                        for (int q = 0; q < R / 2; ++q) mv[q] = mb[b * (R / 2) + q];
+                        for (int q = 0; q < R / 2; ++q) mv[q] = mg[j * (R / 2) + q];
 #pragma unroll
                         for (int c = 0; c < kEvalNC; ++c) {
-                            // smallest terms first (the c_m decay with m)
-                            float2 C = make_float2(0.f, 0.f);
+                            // two chains (odd / even m), smallest terms first
+                            float2 Co = make_float2(0.f, 0.f), Ce = make_float2(0.f, 0.f);
 #pragma unroll
                             for (int q = R / 2 - 1; q >= 0; --q) {
-                                C = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], C);
-                                C = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], C);
+                                Co = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], Co);
+                                Ce = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], Ce);
                             }
+                            const float2 C = make_float2(Ce.x + Co.x, Ce.y + Co.y);
                             A[c] = ffma2(C, wtr[c][j], A[c]);
                             V[c] = ffma2(C, wti[c][j], V[c]);
                             E2[c] = ffma2v(C, C, E2[c]);
@@ -366,12 +454,13 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                 }
 #pragma unroll
                 for (int c = 0; c < kEvalNC; ++c) {
-                    const float hr = A[c].x - V[c].y, hi = A[c].y + V[c].x;
-                    float ar, ai;
-                    cis_cycles(nu[c] * (double)(g * G) * (double)B, &ar, &ai);
-                    acc_re[c] += (double)fmaf(ar, hr, -(ai * hi));
-                    acc_im[c] += (double)fmaf(ar, hi, ai * hr);
+                    const double hr = (double)(A[c].x - V[c].y), hi = (double)(A[c].y + V[c].x);
+                    acc_re[c] = fma(ar[c], hr, fma(-ai[c], hi, acc_re[c]));
+                    acc_im[c] = fma(ar[c], hi, fma(ai[c], hr, acc_im[c]));
                     en[c] += (double)(E2[c].x + E2[c].y);
+                    const double nr = fma(ar[c], sr[c], -ai[c] * si[c]);
+                    ai[c] = fma(ar[c], si[c], ai[c] * sr[c]);
+                    ar[c] = nr;
                 }
             }
             // FP32 error scale of this candidate: sqrt(sum_b |C_b|^2) (DESIGN.md
@@ -387,20 +476,21 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                 }
             }
         }
-        __syncthreads();  // everyone is done with mbuf[buf] and has read next_u
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[sl]);
     }
 }
 
-// algorithmic work of one step (FP32x2 MACs): moments sum nb*B*R, evaluation
-// sum count*nb*R — the numerators of the roofline in bench.py
+// algorithmic work of one step (FP32x2 MACs): moments sum nb*(B/2)*R (folded
+// pairs), evaluation sum count*nb*(R+3) — the numerators of bench.py's roofline
 __global__ void k_work_count(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
                              int B, int R, unsigned long long* __restrict__ work) {
     unsigned long long a = 0, b = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < *n_buckets;
          u += gridDim.x * blockDim.x) {
         const Bucket bk = buckets[u];
-        a += (unsigned long long)bk.nb * B * R;
-        b += (unsigned long long)bk.count * bk.nb * R;
+        a += (unsigned long long)bk.nb * (B / 2) * R;             // folded pair MACs
+        b += (unsigned long long)bk.count * bk.nb * (R + 3);      // C_b, A, V, |C_b|^2
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -418,12 +508,14 @@ void moments_variant(const Bucket* buckets, const int* n_buckets, int cpb, const
                      const float2* y1c, const float2* y2, int N, float2* mom, int nbmax,
                      int grid, cudaStream_t st) {
     auto kern = k_moments<B, R>;
-    const size_t smem = moments_smem(B);
-    static bool attr = false;
-    if (!attr) {
+    const size_t smem = MomLayout<B, R>::smem;
+    static const int per_sm = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+        int n = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kMomThreads, smem);
+        return n > 0 ? n : 1;
+    }();
+    grid *= per_sm;
     kern<<<grid, kMomThreads, smem, st>>>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax);
 }
 
@@ -444,7 +536,7 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
                       const int* sorted, const double* fdoa, double fs, const double* nu_c, int B,
                       const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
                       int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
-    auto kern = k_evaluate<R, 8>;
+    auto kern = k_evaluate<R, kEvalG>;
     const size_t smem = evaluate_smem(nbmax, R);
     static size_t attr = 0;
     if (smem > attr) {
@@ -470,12 +562,11 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
     k_work_count<<<64, 256, 0, st>>>(buckets, n_buckets, B, R, work);
 }
 
-size_t moments_smem_bytes(int B) { return moments_smem(B); }
 
 void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,
                     const float* tcheb, const float2* y1c, const float2* y2, int N, float2* mom,
                     int nbmax, int sm_count, cudaStream_t st) {
-    const int grid = sm_count * 2;
+    const int grid = sm_count;  // x resident CTAs per SM (moments_variant)
     switch (B) {
         case 64: moments_b<64>(R, buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
         case 128: moments_b<128>(R, buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;

@@ -241,6 +241,42 @@ def geolocate_staged(grid: CandidateGrid, staged: StagedSnapshots,
                                                      staged.handle, o, r), **kw)
 
 
+def correlate_steps(grid: CandidateGrid, staged: StagedSnapshots, s_begin: int, s_end: int,
+                    grids_device: int, medians_device: int | None = None,
+                    options: GeolocateOptions | None = None, stream=None,
+                    profile: bool = False) -> dict:
+    """Per-snapshot surfaces of snapshots [s_begin, s_end) over the whole grid
+    into a device buffer [(s_end - s_begin)][P] (float64, e.g. a torch tensor's
+    data_ptr()): correlate_snapshot_all_pairs (+ normalize_by_median) of
+    geolocate.hpp:79-122 — the snapshot-sharded half of geolocate_snapshots."""
+    options = options or GeolocateOptions()
+    res = _capi.dg_result()
+    opt = _options(options, stream, profile)
+    check(lib.dg_correlate_steps(grid.engine.handle, grid.handle, staged.handle, int(s_begin),
+                                 int(s_end), C.byref(opt), C.c_void_p(int(grids_device)),
+                                 C.c_void_p(int(medians_device)) if medians_device else None,
+                                 C.byref(res)))
+    return dict(n_refined=res.n_refined, sum_overlap_samples=res.sum_overlap_samples,
+                correlate_ms=res.correlate_ms, moments_ms=res.moments_ms,
+                evaluate_ms=res.evaluate_ms, moment_ffma2=res.moment_ffma2,
+                evaluate_ffma2=res.evaluate_ffma2, direct_steps=res.direct_steps,
+                kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
+
+
+def accumulate_peak(grid: CandidateGrid, staged: StagedSnapshots, grids_device: int,
+                    medians_device: int | None = None, options: GeolocateOptions | None = None,
+                    **kw) -> GeolocateResult:
+    """accumulate_grids + exact argmax (+ detect_emitters) of per-snapshot
+    surfaces [S][P_grid] already on the device, for a grid or a slab of one."""
+    options = options or GeolocateOptions()
+    kw.setdefault("want_per_snapshot", False)
+    med = C.c_void_p(int(medians_device)) if medians_device else None
+    return _run(grid, options, staged.shape[0],
+                lambda o, r: lib.dg_accumulate_peak(grid.engine.handle, grid.handle,
+                                                    staged.handle, C.c_void_p(int(grids_device)),
+                                                    med, o, r), **kw)
+
+
 def geolocate_snapshots(snapshots: list, grid: CandidateGrid,
                         options: GeolocateOptions | None = None) -> GeolocateResult:
     """geolocate.hpp:127-146 — same inputs/outputs as the reference driver."""

@@ -1,13 +1,22 @@
-"""Multi-GPU sharding of the candidate grid (one process per GPU).
+"""Multi-GPU sharding of a geolocation run (one process per GPU).
 
-The grid is split into contiguous latitude slabs (lat-major flat index, so a
-slab is a contiguous flat range and slab order equals global order). Every
-rank stages all snapshots' captures, solves its slab with no communication,
-and the only exchange is the final peak: an all-gather of each rank's exact
-(value, flat index), reduced to the global maximum with the reference's
-lowest-index tie-break (std::max_element). The accumulated
-surface can optionally be gathered to one rank for detect_emitters, which
-needs global mean/sigma and the 3x3 neighbourhoods across slab edges.
+The work of a run is (snapshot, pair) steps, each over the whole candidate
+grid, and every step is independent. Sharding the *grid* would
+repeat each step's per-TDOA-bucket block moments on every GPU (a slab still
+crosses almost every TDOA contour), so the run is sharded by *snapshot*:
+
+1. rank r correlates snapshots [s0_r, s1_r) over the whole grid
+   (dg_correlate_steps): geometry, block moments, candidate evaluation, exact
+   refinement, pair sums, optional median scaling — no communication;
+2. one all-to-all moves every per-snapshot surface to the owner of its
+   latitude slab (contiguous flat range, so slab order equals global order):
+   rank j receives [S][slab_j] in snapshot order;
+3. rank j accumulates its slab over all S snapshots in the reference's order
+   (dg_accumulate_peak), so each cell's accumulated value is bit-identical to
+   the single-GPU solve, and finds the slab's exact peak;
+4. the only other exchanges are the peak (all-gather of (value, flat index),
+   first-maximum tie-break = std::max_element) and, for detect_emitters, the
+   accumulated surface (global mean/sigma, 3x3 neighbourhoods across slabs).
 
 torch.distributed is the plumbing: NCCL over NVLink on GPUs, gloo in the CPU
 tests (tests/test_sharding.py).
@@ -20,6 +29,13 @@ def slab_rows(n_lat: int, rank: int, world: int) -> tuple[int, int]:
     if world < 1 or not (0 <= rank < world):
         raise ValueError(f"slab_rows: bad rank {rank} of {world}")
     return rank * n_lat // world, (rank + 1) * n_lat // world
+
+
+def step_range(n_snapshots: int, rank: int, world: int) -> tuple[int, int]:
+    """Snapshots [s0, s1) correlated by `rank`; balanced to within one."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError(f"step_range: bad rank {rank} of {world}")
+    return rank * n_snapshots // world, (rank + 1) * n_snapshots // world
 
 
 def merge_argmax(pairs):
@@ -49,15 +65,37 @@ def exchange_argmax(value: float, index: int, device="cpu", group=None):
     return merge_argmax((float(a.item()), int(b.item())) for a, b in zip(vs, ix))
 
 
-def gather_surface(local, sizes, dst: int = 0, group=None):
-    """Concatenate per-rank slab surfaces (1-D float64 tensors of `sizes[r]`
-    elements) in rank order on every rank (all_gather with padding to the
-    largest slab); returns the full surface."""
+def exchange_steps(local, n_snapshots: int, n_lat: int, n_lon: int, group=None):
+    """All-to-all of per-snapshot surfaces: `local` is [s1-s0][n_lat*n_lon]
+    (this rank's snapshots, full grid); returns [n_snapshots][slab] for this
+    rank's latitude slab, snapshots in global order."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    s0, s1 = step_range(n_snapshots, rank, world)
+    if tuple(local.shape) != (s1 - s0, n_lat * n_lon):
+        raise ValueError("exchange_steps: local surfaces have the wrong shape")
+    cols = [tuple(c * n_lon for c in slab_rows(n_lat, j, world)) for j in range(world)]
+    send = torch.cat([local[:, a:b].reshape(-1) for a, b in cols]) if local.numel() else \
+        local.new_empty(0)
+    send_split = [(s1 - s0) * (b - a) for a, b in cols]
+    mine = cols[rank][1] - cols[rank][0]
+    steps = [step_range(n_snapshots, i, world) for i in range(world)]
+    recv_split = [(b - a) * mine for a, b in steps]
+    recv = local.new_empty(sum(recv_split))
+    dist.all_to_all_single(recv, send.contiguous(), recv_split, send_split, group=group)
+    return recv.view(n_snapshots, mine)
+
+
+def gather_vector(local, sizes, group=None):
+    """Concatenate per-rank 1-D tensors of `sizes[r]` elements in rank order on
+    every rank (all_gather with padding to the largest)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    m = max(sizes)
+    m = max(max(sizes), 1)
     buf = torch.zeros(m, dtype=local.dtype, device=local.device)
     buf[: local.numel()] = local
     parts = [torch.empty_like(buf) for _ in range(world)]
@@ -65,41 +103,67 @@ def gather_surface(local, sizes, dst: int = 0, group=None):
     return torch.cat([parts[r][: sizes[r]] for r in range(world)])
 
 
-def geolocate_sharded(grid, states, captures, sample_rate_hz, center_freq_hz, options=None,
-                      gather=True, group=None):
-    """Solve the full grid across the ranks of the default process group.
+gather_surface = gather_vector  # the accumulated slabs -> full surface
 
-    Returns (argmax_value, argmax_index, full_surface_or_None, detections) on
-    every rank; detections are computed on the gathered surface (rank-local GPU).
+
+def geolocate_sharded(grid, staged, options=None, gather=True, group=None, stream=None,
+                      profile=False):
+    """Solve the full grid over the ranks of `group` (snapshot-sharded).
+
+    `staged`: every rank's StagedSnapshots of the whole run (captures are
+    small next to the surfaces). Returns (argmax_value, argmax_index,
+    full_surface_or_None, detections, correlation stats of this rank) on
+    every rank.
     """
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
     from . import _capi
-    from .geolocate import EmitterEstimate, GeolocateOptions, geolocate_staged, StagedSnapshots
     from .geodesy import GeodeticCoord
+    from .geolocate import EmitterEstimate, GeolocateOptions, accumulate_peak, correlate_steps
 
     options = options or GeolocateOptions()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    r0, r1 = slab_rows(grid.lat.count, rank, world)
+    S = staged.shape[0]
+    n_lat, n_lon = grid.lat.count, grid.lon.count
+    s0, s1 = step_range(S, rank, world)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    local = torch.empty((s1 - s0, grid.size()), dtype=torch.float64, device=dev)
+    med = torch.empty(max(s1 - s0, 1), dtype=torch.float64, device=dev)
+    norm = bool(options.normalize_per_snapshot)
+    stats = dict(n_refined=0, sum_overlap_samples=0.0, correlate_ms=0.0, moments_ms=0.0,
+                 evaluate_ms=0.0, moment_ffma2=0.0, evaluate_ffma2=0.0, direct_steps=0,
+                 kernel_launches=0, correlate_launches=0)
+    if s1 > s0:
+        stats = correlate_steps(grid, staged, s0, s1, local.data_ptr(),
+                                med.data_ptr() if norm else None, options, stream=stream,
+                                profile=profile)
+    slab_all = exchange_steps(local, S, n_lat, n_lon, group=group)
+    medians = None
+    if norm:
+        medians = gather_vector(med[: s1 - s0], [b - a for a, b in
+                                                 (step_range(S, r, world) for r in range(world))],
+                                group=group)
+    r0, r1 = slab_rows(n_lat, rank, world)
     slab = grid.slab(r0, r1)
-    staged = StagedSnapshots(states, captures, sample_rate_hz, center_freq_hz, engine=grid.engine)
-    local = torch.empty(max(slab.size(), 1), dtype=torch.float64, device="cuda")
+    acc = torch.empty(max(slab.size(), 1), dtype=torch.float64, device=dev)
     opts = GeolocateOptions(**{**options.__dict__, "detect": False})
     if slab.size() > 0:
-        res = geolocate_staged(slab, staged, opts, want_surface=False,
-                               accumulated_device=local.data_ptr())
+        res = accumulate_peak(slab, staged, slab_all.data_ptr(),
+                              medians.data_ptr() if medians is not None else None, opts,
+                              want_surface=False, accumulated_device=acc.data_ptr(),
+                              stream=stream)
         peak = (res.argmax_value, res.argmax_index)
     else:
         peak = (0.0, -1)
-    value, index = exchange_argmax(peak[0], peak[1], device=local.device, group=group)
+    value, index = exchange_argmax(peak[0], peak[1], device=dev, group=group)
     full, dets = None, []
     if gather:
-        sizes = [(slab_rows(grid.lat.count, r, world)[1] - slab_rows(grid.lat.count, r, world)[0])
-                 * grid.lon.count for r in range(world)]
-        full = gather_surface(local[: slab.size()], sizes, group=group)
+        sizes = [(b - a) * n_lon for a, b in (slab_rows(n_lat, r, world) for r in range(world))]
+        full = gather_vector(acc[: slab.size()], sizes, group=group)
         if options.detect:
-            import ctypes as C
             cap = 4096
             out = (_capi.dg_emitter_estimate * cap)()
             n = C.c_int64()
@@ -110,4 +174,4 @@ def geolocate_sharded(grid, states, captures, sample_rate_hz, center_freq_hz, op
             dets = [EmitterEstimate(GeodeticCoord(e.lat_deg, e.lon_deg, e.alt_m),
                                     int(e.grid_index), e.score, e.score_zsigma)
                     for e in out[: min(n.value, cap)]]
-    return value, index, full, dets
+    return value, index, full, dets, stats

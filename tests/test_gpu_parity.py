@@ -383,6 +383,44 @@ def test_slab_sharding_bit_identical(b2, ref):
         assert merge_argmax(peaks) == (full.argmax_value, full.argmax_index)
 
 
+@pytest.mark.parametrize("normalize", [False, True])
+def test_step_sharding_bit_identical(b2, ref, normalize):
+    """The snapshot-sharded solve (dg_correlate_steps per rank, the all-to-all
+    to latitude slabs emulated in process, dg_accumulate_peak per slab) gives
+    the single-GPU accumulated surface bit for bit and the same exact peak."""
+    import torch
+
+    from paper_2508_06672_b200.sharding import merge_argmax, slab_rows, step_range
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    opts = b2.GeolocateOptions(detect=False, patch_peak=False, normalize_per_snapshot=normalize)
+    full = b2.geolocate_arrays(grid, sc.states, sc.captures, sc.fs, sc.fc, opts)
+    staged = b2.StagedSnapshots(sc.states, sc.captures, sc.fs, sc.fc)
+    S, P, n_lon = sc.states.shape[0], grid.size(), grid.lon.count
+    for world in (2, 3, 4):
+        local, meds = [], []
+        for r in range(world):
+            s0, s1 = step_range(S, r, world)
+            t = torch.empty((s1 - s0, P), dtype=torch.float64, device="cuda")
+            m = torch.empty(max(s1 - s0, 1), dtype=torch.float64, device="cuda")
+            if s1 > s0:
+                b2.correlate_steps(grid, staged, s0, s1, t.data_ptr(),
+                                   m.data_ptr() if normalize else None, opts)
+            local.append(t)
+            meds.append(m[: s1 - s0])
+        medians = torch.cat(meds) if normalize else None
+        parts, peaks = [], []
+        for j in range(world):
+            r0, r1 = slab_rows(grid.lat.count, j, world)
+            slab_all = torch.cat([t[:, r0 * n_lon:r1 * n_lon] for t in local]).contiguous()
+            res = b2.accumulate_peak(grid.slab(r0, r1), staged, slab_all.data_ptr(),
+                                     medians.data_ptr() if normalize else None, opts)
+            parts.append(res.accumulated.values)
+            peaks.append((res.argmax_value, res.argmax_index))
+        assert np.array_equal(np.concatenate(parts), full.accumulated.values)
+        assert merge_argmax(peaks) == (full.argmax_value, full.argmax_index)
+
+
 def test_silent_captures(b2):
     grid = b2.build_candidate_grid(b2.LatLonBounds(-0.1, 0.1, -0.1, 0.1), 0.05)
     states = np.zeros((2, 2, 6))

@@ -8,8 +8,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2508_06672_b200.sharding import (exchange_argmax, gather_surface, merge_argmax,
-                                            slab_rows)
+from paper_2508_06672_b200.sharding import (exchange_argmax, exchange_steps, gather_surface,
+                                            merge_argmax, slab_rows, step_range)
 
 
 def test_slab_rows_partition():
@@ -22,6 +22,14 @@ def test_slab_rows_partition():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         slab_rows(10, 2, 2)
+
+
+def test_step_range_partition():
+    for S in (1, 3, 10, 50, 100):
+        for world in (1, 2, 3, 4, 8):
+            rng = [step_range(S, r, world) for r in range(world)]
+            assert rng[0][0] == 0 and rng[-1][1] == S
+            assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
 
 
 def test_merge_argmax_tie_break():
@@ -54,7 +62,13 @@ def _worker(rank, world, port, q):
         sizes = [(slab_rows(n_lat, r, world)[1] - slab_rows(n_lat, r, world)[0]) * n_lon
                  for r in range(world)]
         got = gather_surface(local, sizes)
-        q.put((rank, peak, bool(torch.equal(got, full))))
+        # snapshot-sharded surfaces -> latitude slabs, snapshots in order
+        S = 5
+        allsteps = torch.arange(S * n_lat * n_lon, dtype=torch.float64).view(S, -1)
+        s0, s1 = step_range(S, rank, world)
+        slab = exchange_steps(allsteps[s0:s1].clone(), S, n_lat, n_lon)
+        ok_steps = bool(torch.equal(slab, allsteps[:, r0 * n_lon:r1 * n_lon]))
+        q.put((rank, peak, bool(torch.equal(got, full)) and ok_steps))
     finally:
         dist.destroy_process_group()
 
