@@ -267,7 +267,6 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
     }
     if (!pl.direct) {
         pl.nbmax = ((N + pl.B - 1) / pl.B + kEvalG - 1) / kEvalG * kEvalG;
-        pl.cpb = (pl.nbmax + chunk_blocks(pl.B) - 1) / chunk_blocks(pl.B);
     }
     return pl;
 }
@@ -310,7 +309,9 @@ struct Pipeline {
     Bucket* buckets = nullptr;
     StepRange* range = nullptr;
     double* nu_c = nullptr;  // [slots]
-    float2* y1c = nullptr;
+    float2 *y1c = nullptr, *y2p = nullptr, *y2op = nullptr;
+    int padf = 0;     // zero padding in front of y2p / y2op
+    int* ubin = nullptr;  // bucket of each TDOA bin of the step, or -1
     float2* mom = nullptr;
     size_t mom_cap = 0;
     unsigned long long* overlap = nullptr;
@@ -355,7 +356,16 @@ struct Pipeline {
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
         work = sc.alloc<unsigned long long>(2);
-        y1c = sc.alloc<float2>(N + 64);  // k_moments' bulk copies may round past N
+        // centred y1 (k_moments' row copies may run one block past N) and y2 in
+        // zero-padded arrays, as is and shifted by one sample: its window copies
+        // reach from N samples before to N + 320 samples after the data
+        padf = (N + 65) & ~1;  // even: window copies start 16-byte aligned
+        const size_t ylen = (size_t)padf + 2 * (size_t)N + 640;
+        y1c = sc.alloc<float2>(N + 320);
+        y2p = sc.alloc<float2>(2 * ylen);
+        y2op = y2p + ylen;
+        CK(cudaMemsetAsync(y2p, 0, 2 * ylen * sizeof(float2), sc.st));
+        ubin = sc.alloc<int>(nbins);
         CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
         CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
         CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
@@ -446,7 +456,7 @@ struct Pipeline {
         }
         if (pl.direct) {
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
-                          n_buckets, d_slot(s), P, sorted, tasks, buckets, 0, st);
+                          n_buckets, d_slot(s), P, sorted, tasks, buckets, ubin, 0, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             if (ev1) CK(cudaEventRecord(ev1, st));
             launch_correlate(tasks, n_tasks, max_tasks, sorted, fdoa_slot(s), y1, y2, N, fs, s_out,
@@ -456,12 +466,12 @@ struct Pipeline {
         } else {
             ensure_moments(sc, pl);
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
-                          n_buckets, d_slot(s), P, sorted, tasks, buckets, pl.B, st);
-            launch_center(y1_64, N, nu_c + s, y1c, st);
+                          n_buckets, d_slot(s), P, sorted, tasks, buckets, ubin, pl.B, st);
+            launch_center(y1_64, y2, N, nu_c + s, y1c, y2p, y2op, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
-            launch_moments(pl.B, pl.R, buckets, n_buckets, pl.cpb,
-                           tcheb[pl.B == 64 ? 0 : pl.B == 128 ? 1 : 2], y1c, y2, N, mom, pl.nbmax,
-                           sm_count, st);
+            launch_moments(pl.B, pl.R, buckets, ubin, pl.bin0, pl.nbins, N,
+                           tcheb[pl.B == 64 ? 0 : pl.B == 128 ? 1 : 2], y1c, y2p, y2op, padf,
+                           mom, pl.nbmax, sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
             CK(cudaMemsetAsync(queue, 0, sizeof(int), st));
             launch_evaluate(pl.R, buckets, n_buckets, queue, (int)std::min<int64_t>(P, pl.nbins),

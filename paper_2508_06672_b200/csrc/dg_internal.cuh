@@ -60,10 +60,8 @@ struct RxPairF32 {
     float pi[3], vi[3], pj[3], vj[3];
 };
 
-constexpr int kMaxMoments = 16;
+constexpr int kMaxMoments = 16;  // Chebyshev table width (moments per block <= 16)
 constexpr int kEvalG = 8;  // blocks per exact-phase group in k_evaluate (moment rows padded to it)
-// blocks per k_moments work item (shared-memory budget: two items' worth per SM)
-__host__ __device__ constexpr int chunk_blocks(int B) { return B >= 256 ? 16 : 32; }  // Chebyshev table width (moments per block <= 16)
 
 // Geometry of one (snapshot, pair): receiver states for predict_pair_offsets.
 struct PairGeom {
@@ -118,7 +116,7 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 // Bucket per non-empty bin (blocks of length B; B = 0 skips buckets)
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
                    int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int B, cudaStream_t st);
+                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st);
 // candidates per warp task of the active correlator variant (32 x candidates/lane)
 int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
@@ -126,12 +124,16 @@ void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, cons
                       double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st);
 
 // block-moment correlator (dg_moments.cu)
-void launch_center(const double2* y, int N, const double* nu_c, float2* out, cudaStream_t st);
+void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
+                   float2* y2p, float2* y2op, int padf, cudaStream_t st);
 void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
                        unsigned long long* work, cudaStream_t st);
-void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,
-                    const float* tcheb, const float2* y1c, const float2* y2, int N, float2* mom,
-                    int nbmax, int sm_count, cudaStream_t st);
+// moments of every bucket of a step (blocks aligned to absolute sample index);
+// ubin[bin - bin0] = bucket of a TDOA bin or -1
+void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
+                    int N, const float* tcheb, const float2* y1c, const float2* y2p,
+                    const float2* y2op, int padf, float2* mom, int nbmax, int sm_count,
+                    cudaStream_t st);
 // per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue)
 size_t evaluate_smem_bytes(int nbmax, int R);
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,

@@ -412,9 +412,10 @@ __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __re
 __global__ void k_build_tasks(int* __restrict__ hist, int nbins, int bin0, int N, int ts,
                               const int* __restrict__ off, const int* __restrict__ toff,
                               const int* __restrict__ boff, Task* __restrict__ tasks,
-                              Bucket* __restrict__ buckets, int B) {
+                              Bucket* __restrict__ buckets, int* __restrict__ ubin, int B) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
         const int cnt = hist[b];
+        if (B > 0) ubin[b] = cnt ? boff[b] : -1;
         if (!cnt) continue;
         hist[b] = 0;  // ready for the next (snapshot, pair)
         const int d = bin0 + b - (N - 1);
@@ -424,8 +425,10 @@ __global__ void k_build_tasks(int* __restrict__ hist, int nbins, int bin0, int N
             bk.d = d;
             bk.start = s0;
             bk.count = cnt;
-            const int n_ov = N - (d < 0 ? -d : d);
-            bk.nb = (n_ov + B - 1) / B;
+            // blocks aligned to absolute sample index (k_moments): those meeting
+            // the overlap [kb, ke)
+            const int kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
+            bk.nb = (ke - 1) / B - kb / B + 1;
             buckets[u] = bk;
         }
         for (int t = 0; ts * t < cnt; ++t) {
@@ -954,13 +957,13 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
                    int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int B, cudaStream_t st) {
+                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st) {
     const int ts = correlate_task_size();
     k_scan<<<1, kScanThreads, 0, st>>>(hist + bin0, nb, ts, off + bin0, toff + bin0, boff + bin0,
                                        cursor + bin0, n_tasks, n_buckets);
     k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
     k_build_tasks<<<blocks_for(nb, 256), 256, 0, st>>>(hist + bin0, nb, bin0, N, ts, off + bin0,
-                                                      toff + bin0, boff + bin0, tasks, buckets, B);
+                                                      toff + bin0, boff + bin0, tasks, buckets, ubin, B);
 }
 
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,

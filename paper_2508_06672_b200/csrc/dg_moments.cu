@@ -53,23 +53,30 @@ __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
     sincospif((float)(2.0 * (x - rint(x))), s, c);
 }
 
-static_assert(chunk_blocks(256) % kEvalG == 0 && chunk_blocks(64) % kEvalG == 0,
-              "padding stays inside the last chunk");
 __host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) / kEvalG * kEvalG; }
 
 // two staging buffers of one bucket's moments
 inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * sizeof(float2); }
-constexpr int kMomThreads = 256;
+constexpr int kMomThreads = 512;
+constexpr int kMomWarps = kMomThreads / 32;
 
-__global__ void k_center(const double2* __restrict__ y, int N, const double* __restrict__ nu_c,
-                         float2* __restrict__ out) {
+// y1c[k] = fp32(y1[k] e^{i 2 pi nu_c k}) (FP64 math), and y2 into zero-padded
+// arrays (data at offset padf) as is and shifted by one sample
+// (y2op[padf + k] = y2[k + 1]), so k_moments' window copies always start at
+// an even (16-byte aligned) sample and never leave the allocation.
+__global__ void k_center(const double2* __restrict__ y, const float2* __restrict__ y2, int N,
+                         const double* __restrict__ nu_c, float2* __restrict__ y1c,
+                         float2* __restrict__ y2p, float2* __restrict__ y2op, int padf) {
     const double nc = *nu_c;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         const double ph = nc * (double)k;
         double s, c;
         sincospi(2.0 * (ph - rint(ph)), &s, &c);
         const double2 v = y[k];
-        out[k] = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
+        y1c[k] = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
+        const float2 w = y2[k];
+        y2p[padf + k] = w;
+        y2op[padf + k - 1] = w;  // padf >= 1
     }
 }
 
@@ -106,168 +113,168 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-// Moments of one d-bucket, a chunk of CB = chunk_blocks(B) blocks per work
-// item (items strided over a persistent grid). Per item:
-//   stage  y1c[k0 ..) and y2[k0+d ..) arrive by TMA bulk copy (issued while
-//          the previous item computed its moments)
-//   z      = y1c conj(y2) from the stage into a padded [block][B+1] buffer
-//   M_m[b] lane = block (x 32/CB lanes splitting j), warp = slice of j, FFMA2
-//          with the Chebyshev row broadcast from shared memory; partials
-//          summed in a fixed order (shuffle, then 8 warps through smem)
+// Moments of all d-buckets, blocks aligned to ABSOLUTE sample index (block b
+// covers y1 samples [bB, (b+1)B); a bucket uses the blocks meeting its
+// overlap, masked to it), so buckets with neighbouring d share the same y1
+// rows and overlapping y2 windows. Work item = (group of kMomGroup
+// consecutive TDOA values starting at an even d0, chunk of kMomCB absolute
+// blocks); persistent grid, one 16-warp CTA per SM:
+//   stage   per block row: y1c[bB .. +B) and the y2 window [bB+d0 .. +B+G+2)
+//           (even copy and one-sample-shifted copy, zero-padded arrays) by
+//           per-row TMA bulk copies, rows padded so that lane = block LDS.128
+//           reads are conflict-free; double-buffered with full/empty mbarriers
+//           (item k+1 lands while item k is computed; no __syncthreads)
+//   compute warp w = TDOA values d0+2w (lanes 0-15) and d0+2w+1 (lanes 16-31),
+//           lane = block; each lane runs its whole block: z = y1c conj(y2)
+//           in registers, folded by T_m(-t) = (-1)^m T_m(t) (R/2 FFMA2 per
+//           sample), Chebyshev rows broadcast; moments written directly
+// L2 -> SM traffic is (B + 2(B + G)) samples per block for G buckets instead of
+// 2B per bucket.
+constexpr int kMomCB = 16;     // blocks per item
+constexpr int kMomGroup = 32;  // TDOA values per item (2 per warp)
+
 template <int B, int R>
 struct MomLayout {
-    static constexpr int CB = chunk_blocks(B);
-    static constexpr int LPB = 32 / CB;             // lanes per block
-    static constexpr int RP = (R + 3) / 4 * 4;      // table row (floats)
-    static constexpr int ZS = B + 1;                // padded z row
-    static constexpr int CS = CB * B;               // samples per chunk
-    static constexpr size_t zbuf = ((size_t)CB * ZS > (size_t)8 * CB * (R + 1)
-                                        ? (size_t)CB * ZS
-                                        : (size_t)8 * CB * (R + 1)) + 1 & ~(size_t)1;
-    static constexpr size_t table_floats = (size_t)B / 2 * RP;  // rows j < B/2
-    static constexpr size_t smem = table_floats * sizeof(float) +
-                                   sizeof(float2) * (zbuf + 2 * ((size_t)CS + 8));
+    static constexpr int RP = (R + 3) / 4 * 4;          // table row (floats)
+    static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
+    static constexpr int RS2 = ((B + kMomGroup + 2 + 13) / 16) * 16 + 2;  // y2 window row
+    static constexpr int W2 = B + kMomGroup + 2;        // y2 window samples copied
+    static constexpr size_t table_floats = (size_t)B / 2 * RP;
+    static constexpr size_t stage_f2 = (size_t)kMomCB * (RS1 + 2 * RS2);  // one buffer
+    static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
+                                   2 * stage_f2 * sizeof(float2);
+    static_assert(RS2 % 16 == 2 && RS2 >= W2, "y2 row padding");
 };
 
+__device__ __forceinline__ float2 cmulc(float4 a, float4 b, int hi) {  // a * conj(b), one sample
+    const float ax = hi ? a.z : a.x, ay = hi ? a.w : a.y;
+    const float bx = hi ? b.z : b.x, by = hi ? b.w : b.y;
+    return make_float2(fmaf(ax, bx, ay * by), fmaf(ay, bx, -(ax * by)));
+}
+
 template <int B, int R>
-__global__ void __launch_bounds__(kMomThreads, 2)
-k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets, int cpb,
-          const float* __restrict__ tcheb, const float2* __restrict__ y1c,
-          const float2* __restrict__ y2, int N, float2* __restrict__ mom, int nbmax) {
+__global__ void __launch_bounds__(kMomThreads, 1)
+k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int bin0,
+          int nbins, int bin_lo, int ngroups, int cpb, const float* __restrict__ tcheb,
+          const float2* __restrict__ y1c, const float2* __restrict__ y2p,
+          const float2* __restrict__ y2op, int padf, int N, float2* __restrict__ mom,
+          int nbmax) {
     static_assert(B % 64 == 0 && B <= 256, "block length");
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
+    static_assert(kMomThreads == 512 && kMomGroup == 2 * kMomWarps && kMomCB == 16, "mapping");
     using L = MomLayout<B, R>;
-    constexpr int CB = L::CB, LPB = L::LPB, RP = L::RP, ZS = L::ZS, CS = L::CS;
-    constexpr int PW = B / 16;          // sample pairs (j, B-1-j) per warp
-    constexpr int PL = PW / LPB;        // ... per lane
+    constexpr int RP = L::RP, RS1 = L::RS1, RS2 = L::RS2, W2 = L::W2;
     extern __shared__ float4 smem4[];
-    float* ts = reinterpret_cast<float*>(smem4);                       // [B/2][RP]
-    float2* zs = reinterpret_cast<float2*>(ts + L::table_floats);      // z / partials
-    float2* s1 = zs + L::zbuf;                                         // stage y1c [CS + 8]
-    float2* s2 = s1 + CS + 8;                                          // stage y2  [CS + 8]
-    __shared__ uint64_t bar;
+    float* ts = reinterpret_cast<float*>(smem4);  // [B/2][RP]
+    float2* stage = reinterpret_cast<float2*>(reinterpret_cast<char*>(smem4) +
+                                              ((L::table_floats * sizeof(float) + 15) & ~15));
+    __shared__ uint64_t full[2], empty[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int blk = lane % CB, half = lane / CB;
-    const int nitems = *n_buckets * cpb;
-    // next item at or after `it` (stride gridDim.x) whose chunk overlaps its bucket
-    auto next_valid = [&](int it) {
-        for (; it < nitems; it += gridDim.x) {
-            const int u = it / cpb;
-            if ((it - u * cpb) * CB < buckets[u].nb) return it;
+    const int blk = lane & 15, hb = lane >> 4;
+    const int nitems = ngroups * cpb;
+    const int nblk_abs = (N + B - 1) / B;
+
+    auto issue = [&](int it, int buf) {  // warp 0: TMA rows of item `it` into `buf`
+        const int g = it / cpb, c = it - g * cpb;
+        const int d0 = bin_lo + g * kMomGroup - (N - 1);
+        const int nrow = max(0, min(kMomCB, nblk_abs - c * kMomCB));
+        float2* st = stage + (size_t)buf * L::stage_f2;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0) mbar_expect_tx(&full[buf], (uint32_t)(nrow * (B + 2 * W2) * sizeof(float2)));
+        __syncwarp();
+        for (int i = lane; i < 3 * nrow; i += 32) {
+            const int r = i / 3, which = i - 3 * r;
+            const int k0 = (c * kMomCB + r) * B;
+            if (which == 0)
+                tma_load_1d(st + r * RS1, y1c + k0, B * sizeof(float2), &full[buf]);
+            else
+                tma_load_1d(st + kMomCB * RS1 + (which - 1) * kMomCB * RS2 + r * RS2,
+                            (which == 1 ? y2p : y2op) + padf + k0 + d0, W2 * sizeof(float2),
+                            &full[buf]);
         }
-        return nitems;
-    };
-    auto issue = [&](int it) {  // thread 0: TMA of the item's y1c / y2 ranges
-        const int u = it / cpb;
-        const Bucket bk = buckets[u];
-        const int d = bk.d, kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
-        const int k0 = kb + (it - u * cpb) * CS;
-        const int cnt = min(CS, ke - k0);
-        const int a1 = k0 & ~1, a2 = (k0 + d) & ~1;
-        const uint32_t n1 = (uint32_t)(((k0 - a1 + cnt) * 8 + 15) & ~15);
-        const uint32_t n2 = (uint32_t)(((k0 + d - a2 + cnt) * 8 + 15) & ~15);
-        mbar_expect_tx(&bar, n1 + n2);
-        tma_load_1d(s1, y1c + a1, n1, &bar);
-        tma_load_1d(s2, y2 + a2, n2, &bar);
     };
 
     for (int i = tid; i < B / 2 * RP; i += kMomThreads)
         ts[i] = tcheb[(i / RP) * kMaxMoments + (i % RP)];
-    int item = next_valid(blockIdx.x);
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], kMomWarps);
+        mbar_init(&empty[1], kMomWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (item < nitems) issue(item);
     }
     __syncthreads();
-    uint32_t phase = 0;
-    for (; item < nitems;) {
-        const int u = item / cpb;
-        const Bucket bk = buckets[u];
-        const int b0 = (item - u * cpb) * CB;
-        const int d = bk.d, kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
-        const int k0 = kb + b0 * B;
-        const int sh1 = k0 & 1, sh2 = (k0 + d) & 1;
-        mbar_wait(&bar, phase);
-        phase ^= 1u;
-
-        // ---- z = y1c conj(y2[k+d]) for the chunk, zero past the overlap ----
-        const int lim = ke - k0;
-#pragma unroll 8
-        for (int i = tid; i < CS; i += kMomThreads) {
-            float2 zz = make_float2(0.f, 0.f);
-            if (i < lim) {
-                const float2 a = s1[i + sh1], b = s2[i + sh2];
-                zz.x = fmaf(a.x, b.x, a.y * b.y);
-                zz.y = fmaf(a.y, b.x, -(a.x * b.y));
+    int item = blockIdx.x;
+    if (warp == 0 && item < nitems) issue(item, 0);
+    for (int k = 0; item < nitems; ++k, item += gridDim.x) {
+        const int buf = k & 1;
+        const int nitem = item + gridDim.x;
+        if (warp == 0 && nitem < nitems) {
+            if (k >= 1) mbar_wait(&empty[buf ^ 1], ((k - 1) >> 1) & 1);  // item k-1 done
+            issue(nitem, buf ^ 1);
+        }
+        const int g = item / cpb, c = item - g * cpb;
+        const int t = 2 * warp + hb;                   // TDOA slot in the group
+        const int bin = bin_lo + g * kMomGroup + t;
+        const int u = (bin >= bin0 && bin < bin0 + nbins) ? ubin[bin - bin0] : -1;
+        const int d = bin - (N - 1);
+        const int kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
+        const int bf = kb / B, bl = (ke - 1) / B;      // the bucket's absolute block range
+        const int babs = c * kMomCB + blk;
+        const bool active = u >= 0 && babs >= bf && babs <= bl;
+        mbar_wait(&full[buf], (k >> 1) & 1);
+        if (active) {
+            const float2* st = stage + (size_t)buf * L::stage_f2;
+            const float2* r1 = st + blk * RS1;
+            // y2 samples [bB + d ..): offset t in the even window, t - 1 in the odd one
+            const float2* r2 = st + kMomCB * RS1 + (t & 1) * kMomCB * RS2 + blk * RS2 + (t & ~1);
+            const int lo = kb - babs * B, hi = ke - babs * B;  // valid j in [lo, hi)
+            float2 acc[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) acc[m] = make_float2(0.f, 0.f);
+#pragma unroll 2
+            for (int j = 0; j < B / 2; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
+                const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
+                const float4 f2 = *reinterpret_cast<const float4*>(r2 + j);
+                const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
+                const float4 g2 = *reinterpret_cast<const float4*>(r2 + B - 2 - j);
+                const float2 zero = make_float2(0.f, 0.f);
+                const float2 z0 = (j >= lo && j < hi) ? cmulc(f1, f2, 0) : zero;
+                const float2 z1 = (j + 1 >= lo && j + 1 < hi) ? cmulc(f1, f2, 1) : zero;
+                const float2 w1 = (B - 2 - j >= lo && B - 2 - j < hi) ? cmulc(g1, g2, 0) : zero;
+                const float2 w0 = (B - 1 - j >= lo && B - 1 - j < hi) ? cmulc(g1, g2, 1) : zero;
+                // pair j: (z0, w0); pair j+1: (z1, w1)
+                const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
+                const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
+                const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
+                const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
+                const float4* t0 = reinterpret_cast<const float4*>(ts + j * RP);
+                const float4* t1 = reinterpret_cast<const float4*>(ts + (j + 1) * RP);
+#pragma unroll
+                for (int qq = 0; qq < RP / 4; ++qq) {
+                    const float4 a = t0[qq], bq = t1[qq];
+                    if (4 * qq + 0 < R) acc[4 * qq + 0] = ffma2(u1, bq.x, ffma2(u0, a.x, acc[4 * qq + 0]));
+                    if (4 * qq + 1 < R) acc[4 * qq + 1] = ffma2(v1, bq.y, ffma2(v0, a.y, acc[4 * qq + 1]));
+                    if (4 * qq + 2 < R) acc[4 * qq + 2] = ffma2(u1, bq.z, ffma2(u0, a.z, acc[4 * qq + 2]));
+                    if (4 * qq + 3 < R) acc[4 * qq + 3] = ffma2(v1, bq.w, ffma2(v0, a.w, acc[4 * qq + 3]));
+                }
             }
-            zs[(i / B) * ZS + (i % B)] = zz;
-        }
-        __syncthreads();  // stage consumed, z complete
-        const int nitem = next_valid(item + gridDim.x);
-        if (tid == 0 && nitem < nitems) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(nitem);  // lands while this item's moments are computed
-        }
-
-        // ---- partial moments on FFMA2, folded: T_m(-t) = (-1)^m T_m(t), so the
-        // pair (j, B-1-j) contributes T_m(t_j) (z_j + z_{B-1-j}) to even m and
-        // T_m(t_j) (z_j - z_{B-1-j}) to odd m: R/2 FFMA2 per sample ----
-        float2 acc[R];
+            // odd moments are stored times i, so a candidate's block value is one
+            // real-weighted sum  C_b = sum_m c_m M'_m  (k_evaluate)
+            const int rb = babs - bf;
+            float2* dst = mom + ((size_t)u * nbmax + rb) * R;
 #pragma unroll
-        for (int m = 0; m < R; ++m) acc[m] = make_float2(0.f, 0.f);
-        const int p0 = warp * PW + half * PL;
-        const float2* zrow = zs + blk * ZS;
-        const float4* trow = reinterpret_cast<const float4*>(ts + p0 * RP);
-#pragma unroll 4
-        for (int q0 = 0; q0 < PL; ++q0) {
-            const float2 za = zrow[p0 + q0], zb = zrow[B - 1 - p0 - q0];
-            const float2 ue = make_float2(za.x + zb.x, za.y + zb.y);
-            const float2 vo = make_float2(za.x - zb.x, za.y - zb.y);
-#pragma unroll
-            for (int q = 0; q < RP / 4; ++q) {
-                const float4 t = trow[q0 * (RP / 4) + q];
-                if (4 * q + 0 < R) acc[4 * q + 0] = ffma2(ue, t.x, acc[4 * q + 0]);
-                if (4 * q + 1 < R) acc[4 * q + 1] = ffma2(vo, t.y, acc[4 * q + 1]);
-                if (4 * q + 2 < R) acc[4 * q + 2] = ffma2(ue, t.z, acc[4 * q + 2]);
-                if (4 * q + 3 < R) acc[4 * q + 3] = ffma2(vo, t.w, acc[4 * q + 3]);
+            for (int m = 0; m < R; ++m)
+                dst[m] = (m & 1) ? make_float2(-acc[m].y, acc[m].x) : acc[m];
+            if (babs == bl) {  // zero rows up to a multiple of kEvalG (k_evaluate's groups)
+                const int nb = bl - bf + 1;
+                for (int z = nb * R; z < pad_blocks(nb) * R; ++z)
+                    mom[(size_t)u * nbmax * R + z] = make_float2(0.f, 0.f);
             }
         }
-        if (LPB == 2) {
-#pragma unroll
-            for (int m = 0; m < R; ++m) {
-                acc[m].x += __shfl_xor_sync(0xffffffffu, acc[m].x, 16);
-                acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, 16);
-            }
-        }
-        __syncthreads();  // every warp is done reading zs
-        // partials -> smem [warp][block][R+1] (reuses the z buffer), fixed-order sum
-        float2* red = zs;
-        if (half == 0) {
-#pragma unroll
-            for (int m = 0; m < R; ++m) red[(warp * CB + blk) * (R + 1) + m] = acc[m];
-        }
-        __syncthreads();
-        // blocks past nb up to a multiple of kEvalG are all-zero (z = 0 there):
-        // written too, so k_evaluate runs whole groups without a bounds check
-        const int nbc = min(CB, pad_blocks(bk.nb) - b0);
-        float2* dst = mom + ((size_t)u * nbmax + b0) * R;
-        for (int o = tid; o < nbc * R; o += kMomThreads) {
-            const int b = o / R, m = o - b * R;
-            float2 sm = red[b * (R + 1) + m];
-#pragma unroll
-            for (int w = 1; w < 8; ++w) {
-                const float2 v = red[(w * CB + b) * (R + 1) + m];
-                sm.x += v.x;
-                sm.y += v.y;
-            }
-            // odd moments are stored times i, so a candidate's block value is
-            // one real-weighted sum  C_b = sum_m c_m M'_m  (k_evaluate)
-            dst[o] = (m & 1) ? make_float2(-sm.y, sm.x) : sm;
-        }
-        __syncthreads();  // partials consumed before the next item's z
-        item = nitem;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);
     }
 }
 
@@ -503,31 +510,40 @@ __global__ void k_work_count(const Bucket* __restrict__ buckets, const int* __re
     }
 }
 
+struct MomArgs {
+    const Bucket* buckets;
+    const int* ubin;
+    int bin0, nbins, bin_lo, ngroups, cpb;
+    const float* tcheb;
+    const float2 *y1c, *y2p, *y2op;
+    int padf, N;
+    float2* mom;
+    int nbmax;
+};
+
 template <int B, int R>
-void moments_variant(const Bucket* buckets, const int* n_buckets, int cpb, const float* tcheb,
-                     const float2* y1c, const float2* y2, int N, float2* mom, int nbmax,
-                     int grid, cudaStream_t st) {
+void moments_variant(const MomArgs& a, int sm_count, cudaStream_t st) {
     auto kern = k_moments<B, R>;
     const size_t smem = MomLayout<B, R>::smem;
-    static const int per_sm = [&] {
+    static const bool attr = [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int n = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kMomThreads, smem);
-        return n > 0 ? n : 1;
+        return true;
     }();
-    grid *= per_sm;
-    kern<<<grid, kMomThreads, smem, st>>>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax);
+    (void)attr;
+    const int items = a.ngroups * a.cpb;
+    const int grid = items < sm_count ? (items > 0 ? items : 1) : sm_count;
+    kern<<<grid, kMomThreads, smem, st>>>(a.buckets, a.ubin, a.bin0, a.nbins, a.bin_lo, a.ngroups,
+                                          a.cpb, a.tcheb, a.y1c, a.y2p, a.y2op, a.padf, a.N,
+                                          a.mom, a.nbmax);
 }
 
 template <int B>
-void moments_b(int R, const Bucket* buckets, const int* n_buckets, int cpb, const float* tcheb,
-               const float2* y1c, const float2* y2, int N, float2* mom, int nbmax,
-               int grid, cudaStream_t st) {
+void moments_b(int R, const MomArgs& a, int sm_count, cudaStream_t st) {
     switch (R) {
-        case 8: moments_variant<B, 8>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
-        case 10: moments_variant<B, 10>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
-        case 12: moments_variant<B, 12>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
-        default: moments_variant<B, 16>(buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
+        case 8: moments_variant<B, 8>(a, sm_count, st); break;
+        case 10: moments_variant<B, 10>(a, sm_count, st); break;
+        case 12: moments_variant<B, 12>(a, sm_count, st); break;
+        default: moments_variant<B, 16>(a, sm_count, st); break;
     }
 }
 
@@ -551,10 +567,11 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
 
 }  // namespace
 
-void launch_center(const double2* y, int N, const double* nu_c, float2* out, cudaStream_t st) {
+void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
+                   float2* y2p, float2* y2op, int padf, cudaStream_t st) {
     int blocks = (N + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    k_center<<<blocks, 256, 0, st>>>(y, N, nu_c, out);
+    k_center<<<blocks, 256, 0, st>>>(y, y2, N, nu_c, y1c, y2p, y2op, padf);
 }
 
 void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
@@ -563,14 +580,31 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
 }
 
 
-void launch_moments(int B, int R, const Bucket* buckets, const int* n_buckets, int cpb,
-                    const float* tcheb, const float2* y1c, const float2* y2, int N, float2* mom,
-                    int nbmax, int sm_count, cudaStream_t st) {
-    const int grid = sm_count;  // x resident CTAs per SM (moments_variant)
+void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
+                    int N, const float* tcheb, const float2* y1c, const float2* y2p,
+                    const float2* y2op, int padf, float2* mom, int nbmax, int sm_count,
+                    cudaStream_t st) {
+    MomArgs a;
+    a.buckets = buckets;
+    a.ubin = ubin;
+    a.bin0 = bin0;
+    a.nbins = nbins;
+    // groups of kMomGroup TDOA values starting at an even d (16-byte aligned y2 windows)
+    a.bin_lo = ((bin0 - (N - 1)) & 1) ? bin0 - 1 : bin0;
+    a.ngroups = (bin0 + nbins - a.bin_lo + kMomGroup - 1) / kMomGroup;
+    a.cpb = ((N + B - 1) / B + kMomCB - 1) / kMomCB;
+    a.tcheb = tcheb;
+    a.y1c = y1c;
+    a.y2p = y2p;
+    a.y2op = y2op;
+    a.padf = padf;
+    a.N = N;
+    a.mom = mom;
+    a.nbmax = nbmax;
     switch (B) {
-        case 64: moments_b<64>(R, buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
-        case 128: moments_b<128>(R, buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
-        default: moments_b<256>(R, buckets, n_buckets, cpb, tcheb, y1c, y2, N, mom, nbmax, grid, st); break;
+        case 64: moments_b<64>(R, a, sm_count, st); break;
+        case 128: moments_b<128>(R, a, sm_count, st); break;
+        default: moments_b<256>(R, a, sm_count, st); break;
     }
 }
 
