@@ -58,15 +58,21 @@ int guard(F&& f) {
     }
 }
 
-// owning device allocation (synchronous free; objects that outlive a call)
+// owning device allocation for objects that outlive a call (staged captures,
+// lattices): taken from the device's stream-ordered pool, which keeps freed
+// memory mapped (release threshold set at engine creation), so re-staging a
+// run every call costs no cudaMalloc/cudaFree device synchronisation.
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
     explicit DevMem(size_t n) : bytes(n) {
-        if (n) CK(cudaMalloc(&p, n));
+        if (n) {
+            CK(cudaMallocAsync(&p, n, cudaStreamPerThread));
+            CK(cudaStreamSynchronize(cudaStreamPerThread));
+        }
     }
     ~DevMem() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, cudaStreamPerThread);
     }
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
