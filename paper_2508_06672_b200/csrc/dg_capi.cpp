@@ -211,8 +211,8 @@ double jacobi_anger_tail(double x, int R) {
 
 constexpr double kMomentTail = 1e-8;
 constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of moments
-constexpr int kMomentR[] = {8, 10, 12, 16};
-constexpr int kMomentB[] = {256, 128, 64};
+constexpr int kMomentR[] = {8, 10, 12, 14, 16};
+constexpr int kMomentB[] = {512, 256, 128, 64};
 
 int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -315,14 +315,17 @@ struct Pipeline {
     Bucket* buckets = nullptr;
     StepRange* range = nullptr;
     double* nu_c = nullptr;  // [slots]
-    float2 *y1c = nullptr, *y2p = nullptr, *y2op = nullptr;
+    float2 *y1c = nullptr, *y2p = nullptr;
     int padf = 0;     // zero padding in front of y2p / y2op
     int* ubin = nullptr;  // bucket of each TDOA bin of the step, or -1
     float2* mom = nullptr;
     size_t mom_cap = 0;
     unsigned long long* overlap = nullptr;
     unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
-    const float* tcheb[3] = {nullptr, nullptr, nullptr};  // B = 64, 128, 256
+    const float* tcheb[4] = {nullptr, nullptr, nullptr, nullptr};  // B = 64, 128, 256, 512
+    const float* tcheb_for(int B) const {
+        return tcheb[B == 64 ? 0 : B == 128 ? 1 : B == 256 ? 2 : 3];
+    }
     std::vector<StepPlan> plans;
     int64_t launches = 0, direct_steps = 0;
     // refinement threshold of the block-moment path; DG_REFINE_TAU overrides
@@ -362,21 +365,20 @@ struct Pipeline {
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
         work = sc.alloc<unsigned long long>(2);
-        // centred y1 (k_moments' row copies may run one block past N) and y2 in
-        // zero-padded arrays, as is and shifted by one sample: its window copies
-        // reach from N samples before to N + 320 samples after the data
+        // centred y1 (k_moments' row copies may run one block past N) and y2 in a
+        // zero-padded array: its window copies reach from N samples before to
+        // N + 1200 samples after the data
         padf = (N + 65) & ~1;  // even: window copies start 16-byte aligned
-        const size_t ylen = (size_t)padf + 2 * (size_t)N + 640;
-        y1c = sc.alloc<float2>(N + 320);
-        y2p = sc.alloc<float2>(2 * ylen);
-        y2op = y2p + ylen;
-        CK(cudaMemsetAsync(y2p, 0, 2 * ylen * sizeof(float2), sc.st));
+        const size_t ylen = (size_t)padf + 2 * (size_t)N + 1280;
+        y1c = sc.alloc<float2>(N + 576);
+        y2p = sc.alloc<float2>(ylen);
+        CK(cudaMemsetAsync(y2p, 0, ylen * sizeof(float2), sc.st));
         ubin = sc.alloc<int>(nbins);
         CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
         CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
         CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
         CK(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), sc.st));
-        static const int kB[3] = {64, 128, 256};
+        static const int kB[4] = {64, 128, 256, 512};
         std::vector<float> all;
         for (int B : kB) {
             auto t = chebyshev_table(B);
@@ -388,6 +390,7 @@ struct Pipeline {
         tcheb[0] = tdev;
         tcheb[1] = tdev + 64 * kMaxMoments;
         tcheb[2] = tdev + (64 + 128) * kMaxMoments;
+        tcheb[3] = tdev + (64 + 128 + 256) * kMaxMoments;
         CK(cudaStreamSynchronize(sc.st));  // `all` is host memory of this frame
     }
 
@@ -473,11 +476,10 @@ struct Pipeline {
             ensure_moments(sc, pl);
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
                           n_buckets, d_slot(s), P, sorted, tasks, buckets, ubin, pl.B, st);
-            launch_center(y1_64, y2, N, nu_c + s, y1c, y2p, y2op, padf, st);
+            launch_center(y1_64, y2, N, nu_c + s, y1c, y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             launch_moments(pl.B, pl.R, buckets, ubin, pl.bin0, pl.nbins, N,
-                           tcheb[pl.B == 64 ? 0 : pl.B == 128 ? 1 : 2], y1c, y2p, y2op, padf,
-                           mom, pl.nbmax, sm_count, st);
+                           tcheb_for(pl.B), y1c, y2p, padf, mom, pl.nbmax, sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
             CK(cudaMemsetAsync(queue, 0, sizeof(int), st));
             launch_evaluate(pl.R, buckets, n_buckets, queue, (int)std::min<int64_t>(P, pl.nbins),

@@ -125,15 +125,14 @@ void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, cons
 
 // block-moment correlator (dg_moments.cu)
 void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
-                   float2* y2p, float2* y2op, int padf, cudaStream_t st);
+                   float2* y2p, int padf, cudaStream_t st);
 void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
                        unsigned long long* work, cudaStream_t st);
 // moments of every bucket of a step (blocks aligned to absolute sample index);
 // ubin[bin - bin0] = bucket of a TDOA bin or -1
 void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
-                    int N, const float* tcheb, const float2* y1c, const float2* y2p,
-                    const float2* y2op, int padf, float2* mom, int nbmax, int sm_count,
-                    cudaStream_t st);
+                    int N, const float* tcheb, const float2* y1c, const float2* y2p, int padf,
+                    float2* mom, int nbmax, int sm_count, cudaStream_t st);
 // per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue)
 size_t evaluate_smem_bytes(int nbmax, int R);
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,

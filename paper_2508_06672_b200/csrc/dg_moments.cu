@@ -60,13 +60,12 @@ inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * s
 constexpr int kMomThreads = 512;
 constexpr int kMomWarps = kMomThreads / 32;
 
-// y1c[k] = fp32(y1[k] e^{i 2 pi nu_c k}) (FP64 math), and y2 into zero-padded
-// arrays (data at offset padf) as is and shifted by one sample
-// (y2op[padf + k] = y2[k + 1]), so k_moments' window copies always start at
-// an even (16-byte aligned) sample and never leave the allocation.
+// y1c[k] = fp32(y1[k] e^{i 2 pi nu_c k}) (FP64 math), and y2 into a zero-padded
+// array (data at the even offset padf), so k_moments' window copies start
+// 16-byte aligned and never leave the allocation.
 __global__ void k_center(const double2* __restrict__ y, const float2* __restrict__ y2, int N,
                          const double* __restrict__ nu_c, float2* __restrict__ y1c,
-                         float2* __restrict__ y2p, float2* __restrict__ y2op, int padf) {
+                         float2* __restrict__ y2p, int padf) {
     const double nc = *nu_c;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         const double ph = nc * (double)k;
@@ -76,7 +75,6 @@ __global__ void k_center(const double2* __restrict__ y, const float2* __restrict
         y1c[k] = make_float2((float)(v.x * c - v.y * s), (float)(v.x * s + v.y * c));
         const float2 w = y2[k];
         y2p[padf + k] = w;
-        y2op[padf + k - 1] = w;  // padf >= 1
     }
 }
 
@@ -116,34 +114,35 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 // Moments of all d-buckets, blocks aligned to ABSOLUTE sample index (block b
 // covers y1 samples [bB, (b+1)B); a bucket uses the blocks meeting its
 // overlap, masked to it), so buckets with neighbouring d share the same y1
-// rows and overlapping y2 windows. Work item = (group of kMomGroup
-// consecutive TDOA values starting at an even d0, chunk of kMomCB absolute
-// blocks); persistent grid, one 16-warp CTA per SM:
+// rows and overlapping y2 windows. Work item = (group of G consecutive TDOA
+// values starting at an even d0, chunk of CB absolute blocks); persistent
+// grid, one 16-warp CTA per SM:
 //   stage   per block row: y1c[bB .. +B) and the y2 window [bB+d0 .. +B+G+2)
-//           (even copy and one-sample-shifted copy, zero-padded arrays) by
-//           per-row TMA bulk copies, rows padded so that lane = block LDS.128
-//           reads are conflict-free; double-buffered with full/empty mbarriers
-//           (item k+1 lands while item k is computed; no __syncthreads)
-//   compute warp w = TDOA values d0+2w (lanes 0-15) and d0+2w+1 (lanes 16-31),
-//           lane = block; each lane runs its whole block: z = y1c conj(y2)
-//           in registers, folded by T_m(-t) = (-1)^m T_m(t) (R/2 FFMA2 per
-//           sample), Chebyshev rows broadcast; moments written directly
-// L2 -> SM traffic is (B + 2(B + G)) samples per block for G buckets instead of
+//           (zero-padded array) by per-row TMA bulk copies, rows padded so the
+//           lane = block reads are conflict-free (y1: LDS.128 across 8-lane
+//           quarters; y2 at any shift: LDS.64 across 16-lane halves);
+//           double-buffered with full/empty mbarriers (item k+1 lands while
+//           item k is computed; no __syncthreads)
+//   compute warp w = TDOA values d0 + BPW w + (lane / CB), lane % CB = block;
+//           each lane runs its whole block: z = y1c conj(y2) in registers,
+//           folded by T_m(-t) = (-1)^m T_m(t) (R/2 FFMA2 per sample),
+//           Chebyshev rows broadcast; moments written directly
+// L2 -> SM traffic is (B + (B + G)) samples per block for G buckets instead of
 // 2B per bucket.
-constexpr int kMomCB = 16;     // blocks per item
-constexpr int kMomGroup = 32;  // TDOA values per item (2 per warp)
-
 template <int B, int R>
 struct MomLayout {
+    static constexpr int CB = B >= 512 ? 8 : 16;       // blocks per item
+    static constexpr int BPW = 32 / CB;                // TDOA values per warp
+    static constexpr int G = BPW * kMomWarps;           // TDOA values per item
     static constexpr int RP = (R + 3) / 4 * 4;          // table row (floats)
     static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
-    static constexpr int RS2 = ((B + kMomGroup + 2 + 13) / 16) * 16 + 2;  // y2 window row
-    static constexpr int W2 = B + kMomGroup + 2;        // y2 window samples copied
+    static constexpr int W2 = B + G + 2;                // y2 window samples copied
+    static constexpr int RS2 = (W2 + 13) / 16 * 16 + 2; // y2 row: 2 float2 mod 16
     static constexpr size_t table_floats = (size_t)B / 2 * RP;
-    static constexpr size_t stage_f2 = (size_t)kMomCB * (RS1 + 2 * RS2);  // one buffer
+    static constexpr size_t stage_f2 = (size_t)CB * (RS1 + RS2);  // one buffer
     static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
                                    2 * stage_f2 * sizeof(float2);
-    static_assert(RS2 % 16 == 2 && RS2 >= W2, "y2 row padding");
+    static_assert(RS2 % 16 == 2 && RS2 >= W2 && W2 % 2 == 0, "y2 row padding");
 };
 
 __device__ __forceinline__ float2 cmulc(float4 a, float4 b, int hi) {  // a * conj(b), one sample
@@ -156,13 +155,13 @@ template <int B, int R>
 __global__ void __launch_bounds__(kMomThreads, 1)
 k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int bin0,
           int nbins, int bin_lo, int ngroups, int cpb, const float* __restrict__ tcheb,
-          const float2* __restrict__ y1c, const float2* __restrict__ y2p,
-          const float2* __restrict__ y2op, int padf, int N, float2* __restrict__ mom,
-          int nbmax) {
-    static_assert(B % 64 == 0 && B <= 256, "block length");
+          const float2* __restrict__ y1c, const float2* __restrict__ y2p, int padf, int N,
+          float2* __restrict__ mom, int nbmax) {
+    static_assert(B % 64 == 0 && B <= 512, "block length");
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
-    static_assert(kMomThreads == 512 && kMomGroup == 2 * kMomWarps && kMomCB == 16, "mapping");
+    static_assert(kMomThreads == 512, "mapping");
     using L = MomLayout<B, R>;
+    constexpr int CB = L::CB, BPW = L::BPW, G = L::G;
     constexpr int RP = L::RP, RS1 = L::RS1, RS2 = L::RS2, W2 = L::W2;
     extern __shared__ float4 smem4[];
     float* ts = reinterpret_cast<float*>(smem4);  // [B/2][RP]
@@ -171,27 +170,29 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
     __shared__ uint64_t full[2], empty[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int blk = lane & 15, hb = lane >> 4;
+    // a 16-lane half-warp = 8 blocks x 2 TDOA values, so the y2 LDS.64 at shifts
+    // t, t+1 fill each other's bank gaps (row stride 4 banks mod 32)
+    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & 7);
+    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane >> 3);
     const int nitems = ngroups * cpb;
     const int nblk_abs = (N + B - 1) / B;
 
     auto issue = [&](int it, int buf) {  // warp 0: TMA rows of item `it` into `buf`
         const int g = it / cpb, c = it - g * cpb;
-        const int d0 = bin_lo + g * kMomGroup - (N - 1);
-        const int nrow = max(0, min(kMomCB, nblk_abs - c * kMomCB));
+        const int d0 = bin_lo + g * G - (N - 1);
+        const int nrow = max(0, min(CB, nblk_abs - c * CB));
         float2* st = stage + (size_t)buf * L::stage_f2;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (lane == 0) mbar_expect_tx(&full[buf], (uint32_t)(nrow * (B + 2 * W2) * sizeof(float2)));
+        if (lane == 0) mbar_expect_tx(&full[buf], (uint32_t)(nrow * (B + W2) * sizeof(float2)));
         __syncwarp();
-        for (int i = lane; i < 3 * nrow; i += 32) {
-            const int r = i / 3, which = i - 3 * r;
-            const int k0 = (c * kMomCB + r) * B;
-            if (which == 0)
+        for (int i = lane; i < 2 * nrow; i += 32) {
+            const int r = i >> 1;
+            const int k0 = (c * CB + r) * B;
+            if ((i & 1) == 0)
                 tma_load_1d(st + r * RS1, y1c + k0, B * sizeof(float2), &full[buf]);
             else
-                tma_load_1d(st + kMomCB * RS1 + (which - 1) * kMomCB * RS2 + r * RS2,
-                            (which == 1 ? y2p : y2op) + padf + k0 + d0, W2 * sizeof(float2),
-                            &full[buf]);
+                tma_load_1d(st + CB * RS1 + r * RS2, y2p + padf + k0 + d0,
+                            W2 * sizeof(float2), &full[buf]);
         }
     };
 
@@ -215,20 +216,20 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
             issue(nitem, buf ^ 1);
         }
         const int g = item / cpb, c = item - g * cpb;
-        const int t = 2 * warp + hb;                   // TDOA slot in the group
-        const int bin = bin_lo + g * kMomGroup + t;
+        const int t = BPW * warp + hb;                 // TDOA slot in the group
+        const int bin = bin_lo + g * G + t;
         const int u = (bin >= bin0 && bin < bin0 + nbins) ? ubin[bin - bin0] : -1;
         const int d = bin - (N - 1);
         const int kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
         const int bf = kb / B, bl = (ke - 1) / B;      // the bucket's absolute block range
-        const int babs = c * kMomCB + blk;
+        const int babs = c * CB + blk;
         const bool active = u >= 0 && babs >= bf && babs <= bl;
         mbar_wait(&full[buf], (k >> 1) & 1);
         if (active) {
             const float2* st = stage + (size_t)buf * L::stage_f2;
             const float2* r1 = st + blk * RS1;
-            // y2 samples [bB + d ..): offset t in the even window, t - 1 in the odd one
-            const float2* r2 = st + kMomCB * RS1 + (t & 1) * kMomCB * RS2 + blk * RS2 + (t & ~1);
+            // y2 samples [bB + d ..) start at offset t of the window row
+            const float2* r2 = st + CB * RS1 + blk * RS2 + t;
             const int lo = kb - babs * B, hi = ke - babs * B;  // valid j in [lo, hi)
             float2 acc[R];
 #pragma unroll
@@ -236,9 +237,10 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
 #pragma unroll 2
             for (int j = 0; j < B / 2; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
                 const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
-                const float4 f2 = *reinterpret_cast<const float4*>(r2 + j);
                 const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
-                const float4 g2 = *reinterpret_cast<const float4*>(r2 + B - 2 - j);
+                const float2 fa = r2[j], fb = r2[j + 1], ga = r2[B - 2 - j], gb = r2[B - 1 - j];
+                const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
+                const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
                 const float2 zero = make_float2(0.f, 0.f);
                 const float2 z0 = (j >= lo && j < hi) ? cmulc(f1, f2, 0) : zero;
                 const float2 z1 = (j + 1 >= lo && j + 1 < hi) ? cmulc(f1, f2, 1) : zero;
@@ -445,14 +447,13 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                         for (int q = 0; q < R / 2; ++q) mv[q] = mg[j * (R / 2) + q];
 #pragma unroll
                         for (int c = 0; c < kEvalNC; ++c) {
-                            // two chains (odd / even m), smallest terms first
-                            float2 Co = make_float2(0.f, 0.f), Ce = make_float2(0.f, 0.f);
+                            // one chain, smallest terms first (the c_m decay with m)
+                            float2 C = make_float2(0.f, 0.f);
 #pragma unroll
                             for (int q = R / 2 - 1; q >= 0; --q) {
-                                Co = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], Co);
-                                Ce = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], Ce);
+                                C = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], C);
+                                C = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], C);
                             }
-                            const float2 C = make_float2(Ce.x + Co.x, Ce.y + Co.y);
                             A[c] = ffma2(C, wtr[c][j], A[c]);
                             V[c] = ffma2(C, wti[c][j], V[c]);
                             E2[c] = ffma2v(C, C, E2[c]);
@@ -515,14 +516,19 @@ struct MomArgs {
     const int* ubin;
     int bin0, nbins, bin_lo, ngroups, cpb;
     const float* tcheb;
-    const float2 *y1c, *y2p, *y2op;
+    const float2 *y1c, *y2p;
     int padf, N;
     float2* mom;
     int nbmax;
 };
 
 template <int B, int R>
-void moments_variant(const MomArgs& a, int sm_count, cudaStream_t st) {
+void moments_variant(MomArgs a, int sm_count, cudaStream_t st) {
+    using L = MomLayout<B, R>;
+    // groups of G TDOA values starting at an even d (16-byte aligned y2 windows)
+    a.bin_lo = ((a.bin0 - (a.N - 1)) & 1) ? a.bin0 - 1 : a.bin0;
+    a.ngroups = (a.bin0 + a.nbins - a.bin_lo + L::G - 1) / L::G;
+    a.cpb = ((a.N + B - 1) / B + L::CB - 1) / L::CB;
     auto kern = k_moments<B, R>;
     const size_t smem = MomLayout<B, R>::smem;
     static const bool attr = [&] {
@@ -533,8 +539,8 @@ void moments_variant(const MomArgs& a, int sm_count, cudaStream_t st) {
     const int items = a.ngroups * a.cpb;
     const int grid = items < sm_count ? (items > 0 ? items : 1) : sm_count;
     kern<<<grid, kMomThreads, smem, st>>>(a.buckets, a.ubin, a.bin0, a.nbins, a.bin_lo, a.ngroups,
-                                          a.cpb, a.tcheb, a.y1c, a.y2p, a.y2op, a.padf, a.N,
-                                          a.mom, a.nbmax);
+                                          a.cpb, a.tcheb, a.y1c, a.y2p, a.padf, a.N, a.mom,
+                                          a.nbmax);
 }
 
 template <int B>
@@ -543,6 +549,7 @@ void moments_b(int R, const MomArgs& a, int sm_count, cudaStream_t st) {
         case 8: moments_variant<B, 8>(a, sm_count, st); break;
         case 10: moments_variant<B, 10>(a, sm_count, st); break;
         case 12: moments_variant<B, 12>(a, sm_count, st); break;
+        case 14: moments_variant<B, 14>(a, sm_count, st); break;
         default: moments_variant<B, 16>(a, sm_count, st); break;
     }
 }
@@ -568,10 +575,10 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
 }  // namespace
 
 void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
-                   float2* y2p, float2* y2op, int padf, cudaStream_t st) {
+                   float2* y2p, int padf, cudaStream_t st) {
     int blocks = (N + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    k_center<<<blocks, 256, 0, st>>>(y, y2, N, nu_c, y1c, y2p, y2op, padf);
+    k_center<<<blocks, 256, 0, st>>>(y, y2, N, nu_c, y1c, y2p, padf);
 }
 
 void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
@@ -581,22 +588,16 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
 
 
 void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
-                    int N, const float* tcheb, const float2* y1c, const float2* y2p,
-                    const float2* y2op, int padf, float2* mom, int nbmax, int sm_count,
-                    cudaStream_t st) {
+                    int N, const float* tcheb, const float2* y1c, const float2* y2p, int padf,
+                    float2* mom, int nbmax, int sm_count, cudaStream_t st) {
     MomArgs a;
     a.buckets = buckets;
     a.ubin = ubin;
     a.bin0 = bin0;
     a.nbins = nbins;
-    // groups of kMomGroup TDOA values starting at an even d (16-byte aligned y2 windows)
-    a.bin_lo = ((bin0 - (N - 1)) & 1) ? bin0 - 1 : bin0;
-    a.ngroups = (bin0 + nbins - a.bin_lo + kMomGroup - 1) / kMomGroup;
-    a.cpb = ((N + B - 1) / B + kMomCB - 1) / kMomCB;
     a.tcheb = tcheb;
     a.y1c = y1c;
     a.y2p = y2p;
-    a.y2op = y2op;
     a.padf = padf;
     a.N = N;
     a.mom = mom;
@@ -604,7 +605,8 @@ void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bi
     switch (B) {
         case 64: moments_b<64>(R, a, sm_count, st); break;
         case 128: moments_b<128>(R, a, sm_count, st); break;
-        default: moments_b<256>(R, a, sm_count, st); break;
+        case 256: moments_b<256>(R, a, sm_count, st); break;
+        default: moments_b<512>(R, a, sm_count, st); break;
     }
 }
 
@@ -622,6 +624,7 @@ void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* qu
         case 8: DG_EVAL_CASE(8); break;
         case 10: DG_EVAL_CASE(10); break;
         case 12: DG_EVAL_CASE(12); break;
+        case 14: DG_EVAL_CASE(14); break;
         default: DG_EVAL_CASE(16); break;
     }
 #undef DG_EVAL_CASE
