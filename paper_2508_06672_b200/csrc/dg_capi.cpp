@@ -408,9 +408,11 @@ struct Pipeline {
     // one synchronisation: read the window's ranges (and the lattice planning
     // ranges `approx`, nullable), plan each step, upload nu_c
     void plan_window(Scratch& sc, int n, double fs, const StepRange* approx = nullptr,
-                     double margin_hz = 0.0, int64_t P_plan = 0) {
+                     double margin_hz = 0.0, int64_t P_plan = 0, bool exact_ranges = true) {
         std::vector<StepRange> h(n), ha(approx ? n : 0);
-        CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost, sc.st));
+        if (exact_ranges)
+            CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost,
+                               sc.st));
         if (approx)
             CK(cudaMemcpyAsync(ha.data(), approx, n * sizeof(StepRange), cudaMemcpyDeviceToHost,
                                sc.st));
@@ -418,6 +420,11 @@ struct Pipeline {
         plans.assign(n, StepPlan{});
         std::vector<double> nc(n);
         for (int i = 0; i < n; ++i) {
+            if (!exact_ranges) {  // the planning range bounds the bins (TDOA +-2 samples)
+                h[i] = ha[i];
+                h[i].dmin = std::max(h[i].dmin, 1 - N);
+                h[i].dmax = std::min(h[i].dmax, N - 1);
+            }
             plans[i] = plan_step(h[i], approx ? &ha[i] : nullptr, margin_hz, approx ? P_plan : P, N,
                                  fs);
             nc[i] = plans[i].nu_c;
@@ -1173,17 +1180,16 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
 
     for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
         const int nw = std::min(pl.slots, SPl - w0);
-        pl.reset_ranges(sc, nw);
-        for (int i = 0; i < nw; ++i) {  // phase A: geometry of the window
-            const int lsp = w0 + i;
-            launch_geometry_hist(g->x, g->y, g->z, P, geo.pg + sp0 + lsp, fs, wl, pl.N,
-                                 pl.d_slot(i), pl.fdoa_slot(i), pl.hist_slot(i),
-                                 raw + (int64_t)lsp * P, pl.overlap, pl.err, pl.range + i, st);
-            launches += 1;
-        }
+        // phase A: geometry of the whole window in one pass (planned from the
+        // FP32 lattice ranges, which bound the exact TDOA bins)
+        launch_geometry_steps(g->x, g->y, g->z, P, geo.pg + sp0 + w0, nw, fs, wl, pl.N,
+                              pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins,
+                              raw + (int64_t)w0 * P, pl.overlap, pl.err, st);
+        launches += (nw + 63) / 64;
         const PairGeom* hw = geo.hpg.data() + sp0 + w0;
         const StepRange* approx = pl.lattice_ranges(sc, g, hw, nw, fs, wl);
-        pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size);
+        pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size,
+                       /*exact_ranges=*/false);
         for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each step
             const int lsp = w0 + i, sp = sp0 + lsp;
             const int s = sp / pairs, q = sp - s * pairs;

@@ -99,6 +99,12 @@ void launch_geometry_hist(const double* x, const double* y, const double* z, int
                           double* fdoa_out, int* hist, double* s_out,
                           unsigned long long* overlap, int* err, StepRange* range,
                           cudaStream_t st);
+// every step of a window in one pass: d/fdoa/surface slices of stride P,
+// histograms of stride nbins (no exact ranges; see k_geometry_steps)
+void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
+                           const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
+                           double* fdoa_out, int* hist, int nbins, double* s_out,
+                           unsigned long long* overlap, int* err, cudaStream_t st);
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
                             const PairGeom* pg_dev, double fs, double wl, dg_pair_offsets* out,
                             int* err, cudaStream_t st);

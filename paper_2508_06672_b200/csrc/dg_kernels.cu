@@ -103,6 +103,10 @@ __device__ double correlate_exact(const double2* __restrict__ y1, const double2*
             nb[i] = __ldg(b + k + i);
         }
         for (; k + 2 * U <= ke; k += U) {
+            // pull the lines 32 groups ahead into L1 so the register prefetch
+            // below never waits on L2/HBM (one 128-B line per U samples)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(y1 + k + 32 * U));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(b + k + 32 * U));
             double2 ca[U], cb[U];
 #pragma unroll
             for (int i = 0; i < U; ++i) {
@@ -211,6 +215,42 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
     ovl = warp_sum_u64(ovl);
     if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
     ra.flush(range);
+}
+
+// Phase A of a window of steps in one pass: each thread loads its candidate
+// once and predicts the offsets of every step of the window (receiver states
+// staged in shared memory), writing d[s][P], fdoa[s][P], the per-step TDOA
+// histograms and S = 0 for candidates without overlap. The exact ranges are
+// not reduced here: the window is planned from the FP32 lattice ranges
+// (k_range_fp32), whose TDOA range (+-2 samples) bounds the bins.
+constexpr int kGeoStepsMax = 64;  // steps per launch (shared-memory receiver table)
+
+__global__ void __launch_bounds__(256)
+k_geometry_steps(const double* __restrict__ x, const double* __restrict__ y,
+                 const double* __restrict__ z, int64_t P, const PairGeom* __restrict__ pg, int n,
+                 double fs, double wl, int N, int* __restrict__ d_out,
+                 double* __restrict__ fdoa_out, int* __restrict__ hist, int nbins,
+                 double* __restrict__ s_out, unsigned long long* __restrict__ overlap,
+                 int* __restrict__ err) {
+    __shared__ PairGeom sg[kGeoStepsMax];
+    for (int i = threadIdx.x; i < n * (int)(sizeof(PairGeom) / 8); i += blockDim.x)
+        reinterpret_cast<double*>(sg)[i] = reinterpret_cast<const double*>(pg)[i];
+    __syncthreads();
+    unsigned long long ovl = 0;
+    RangeAcc ra;  // unused: planning ranges come from the FP32 pass
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const double cx = x[p], cy = y[p], cz = z[p];
+        for (int s = 0; s < n; ++s) {
+            long long tdoa;
+            double fdoa;
+            if (!offsets_exact(cx, cy, cz, sg[s], fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
+            emit_point(p, tdoa, fdoa, N, d_out + (int64_t)s * P, fdoa_out + (int64_t)s * P,
+                       hist + (int64_t)s * nbins, s_out + (int64_t)s * P, ovl, ra);
+        }
+    }
+    ovl = warp_sum_u64(ovl);
+    if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
 }
 
 __global__ void k_predict_offsets(const double* __restrict__ x, const double* __restrict__ y,
@@ -399,12 +439,22 @@ k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
 
 __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __restrict__ cursor,
                           int* __restrict__ sorted) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int dd = d[p];
-        if (dd == kNoOverlap) continue;
-        const int pos = atomicAdd(&cursor[dd + N - 1], 1);
-        sorted[pos] = (int)p;
+    // four independent cursor atomics in flight per thread (latency-bound)
+    constexpr int U = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < P; p0 += U * stride) {
+        int dd[U], pos[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * stride;
+            dd[u] = p < P ? d[p] : kNoOverlap;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            pos[u] = dd[u] != kNoOverlap ? atomicAdd(&cursor[dd[u] + N - 1], 1) : -1;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pos[u] >= 0) sorted[pos[u]] = (int)(p0 + u * stride);
     }
 }
 
@@ -928,6 +978,18 @@ void launch_geometry_hist(const double* x, const double* y, const double* z, int
                           int* err, StepRange* range, cudaStream_t st) {
     k_geometry_hist<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, N, d_out, fdoa_out,
                                                         hist, s_out, overlap, err, range);
+}
+
+void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
+                           const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
+                           double* fdoa_out, int* hist, int nbins, double* s_out,
+                           unsigned long long* overlap, int* err, cudaStream_t st) {
+    for (int s0 = 0; s0 < n; s0 += kGeoStepsMax) {
+        const int m = n - s0 < kGeoStepsMax ? n - s0 : kGeoStepsMax;
+        k_geometry_steps<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
+            x, y, z, P, pg + s0, m, fs, wl, N, d_out + (int64_t)s0 * P, fdoa_out + (int64_t)s0 * P,
+            hist + (int64_t)s0 * nbins, nbins, s_out + (int64_t)s0 * P, overlap, err);
+    }
 }
 
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
