@@ -58,6 +58,7 @@ __host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) 
 // two staging buffers of one bucket's moments
 inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * sizeof(float2); }
 constexpr int kMomThreads = 512;
+constexpr int kMomRun = 16;  // sample pairs per first-level FP32 sum in k_moments
 constexpr int kMomWarps = kMomThreads / 32;
 
 // y1c[k] = fp32(y1[k] e^{i 2 pi nu_c k}) (FP64 math), and y2 into a zero-padded
@@ -231,35 +232,48 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
             // y2 samples [bB + d ..) start at offset t of the window row
             const float2* r2 = st + CB * RS1 + blk * RS2 + t;
             const int lo = kb - babs * B, hi = ke - babs * B;  // valid j in [lo, hi)
+            // two-level accumulation: sums of 16 pairs, then their sum, so the
+            // FP32 rounding of coherent partial sums stays ~16x below one
+            // sequential 256-pair run
             float2 acc[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) acc[m] = make_float2(0.f, 0.f);
-#pragma unroll 2
-            for (int j = 0; j < B / 2; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
-                const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
-                const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
-                const float2 fa = r2[j], fb = r2[j + 1], ga = r2[B - 2 - j], gb = r2[B - 1 - j];
-                const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
-                const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
-                const float2 zero = make_float2(0.f, 0.f);
-                const float2 z0 = (j >= lo && j < hi) ? cmulc(f1, f2, 0) : zero;
-                const float2 z1 = (j + 1 >= lo && j + 1 < hi) ? cmulc(f1, f2, 1) : zero;
-                const float2 w1 = (B - 2 - j >= lo && B - 2 - j < hi) ? cmulc(g1, g2, 0) : zero;
-                const float2 w0 = (B - 1 - j >= lo && B - 1 - j < hi) ? cmulc(g1, g2, 1) : zero;
-                // pair j: (z0, w0); pair j+1: (z1, w1)
-                const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
-                const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
-                const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
-                const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
-                const float4* t0 = reinterpret_cast<const float4*>(ts + j * RP);
-                const float4* t1 = reinterpret_cast<const float4*>(ts + (j + 1) * RP);
+            for (int j0 = 0; j0 < B / 2; j0 += kMomRun) {
+                float2 part[R];
 #pragma unroll
-                for (int qq = 0; qq < RP / 4; ++qq) {
-                    const float4 a = t0[qq], bq = t1[qq];
-                    if (4 * qq + 0 < R) acc[4 * qq + 0] = ffma2(u1, bq.x, ffma2(u0, a.x, acc[4 * qq + 0]));
-                    if (4 * qq + 1 < R) acc[4 * qq + 1] = ffma2(v1, bq.y, ffma2(v0, a.y, acc[4 * qq + 1]));
-                    if (4 * qq + 2 < R) acc[4 * qq + 2] = ffma2(u1, bq.z, ffma2(u0, a.z, acc[4 * qq + 2]));
-                    if (4 * qq + 3 < R) acc[4 * qq + 3] = ffma2(v1, bq.w, ffma2(v0, a.w, acc[4 * qq + 3]));
+                for (int m = 0; m < R; ++m) part[m] = make_float2(0.f, 0.f);
+#pragma unroll 2
+                for (int j = j0; j < j0 + kMomRun; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
+                    const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
+                    const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
+                    const float2 fa = r2[j], fb = r2[j + 1], ga = r2[B - 2 - j], gb = r2[B - 1 - j];
+                    const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
+                    const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
+                    const float2 zero = make_float2(0.f, 0.f);
+                    const float2 z0 = (j >= lo && j < hi) ? cmulc(f1, f2, 0) : zero;
+                    const float2 z1 = (j + 1 >= lo && j + 1 < hi) ? cmulc(f1, f2, 1) : zero;
+                    const float2 w1 = (B - 2 - j >= lo && B - 2 - j < hi) ? cmulc(g1, g2, 0) : zero;
+                    const float2 w0 = (B - 1 - j >= lo && B - 1 - j < hi) ? cmulc(g1, g2, 1) : zero;
+                    // pair j: (z0, w0); pair j+1: (z1, w1)
+                    const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
+                    const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
+                    const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
+                    const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
+                    const float4* t0 = reinterpret_cast<const float4*>(ts + j * RP);
+                    const float4* t1 = reinterpret_cast<const float4*>(ts + (j + 1) * RP);
+#pragma unroll
+                    for (int qq = 0; qq < RP / 4; ++qq) {
+                        const float4 a = t0[qq], bq = t1[qq];
+                        if (4 * qq + 0 < R) part[4 * qq + 0] = ffma2(u1, bq.x, ffma2(u0, a.x, part[4 * qq + 0]));
+                        if (4 * qq + 1 < R) part[4 * qq + 1] = ffma2(v1, bq.y, ffma2(v0, a.y, part[4 * qq + 1]));
+                        if (4 * qq + 2 < R) part[4 * qq + 2] = ffma2(u1, bq.z, ffma2(u0, a.z, part[4 * qq + 2]));
+                        if (4 * qq + 3 < R) part[4 * qq + 3] = ffma2(v1, bq.w, ffma2(v0, a.w, part[4 * qq + 3]));
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    acc[m].x += part[m].x;
+                    acc[m].y += part[m].y;
                 }
             }
             // odd moments are stored times i, so a candidate's block value is one
@@ -402,6 +416,17 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
         const Bucket bk = buckets[u];
         const int nb = bk.nb;
         const float4* mb = smem4 + sl * buf_f4;
+        // Q = ||M_0||_2 of the bucket: the scale of the moments' own FP32
+        // rounding, which every candidate of a coherent bucket inherits
+        // (DESIGN.md section 6); per warp, fixed-order reduction
+        float q2 = 0.f;
+        for (int b = lane; b < nb; b += 32) {
+            const float4 v = mb[b * (R / 2)];
+            q2 = fmaf(v.x, v.x, fmaf(v.y, v.y, q2));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+        const double qscale = sqrt((double)q2);
 
         for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
             int p[kEvalNC];
@@ -471,14 +496,15 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                     ar[c] = nr;
                 }
             }
-            // FP32 error scale of this candidate: sqrt(sum_b |C_b|^2) (DESIGN.md
-            // section 5); below tau of it the value is re-evaluated in FP64
+            // FP32 error scale of this candidate: max(sqrt(sum_b |C_b|^2), Q)
+            // (DESIGN.md section 6); below tau of it the value is re-evaluated
+            // in FP64
 #pragma unroll
             for (int c = 0; c < kEvalNC; ++c) {
                 if (p[c] < 0) continue;
                 const double sv = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
                 s_out[p[c]] = sv;
-                if (sv < (double)tau * sqrt(en[c])) {
+                if (sv < (double)tau * fmax(sqrt(en[c]), qscale)) {
                     const int64_t e = flag_base + p[c];
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
