@@ -151,7 +151,9 @@ typedef struct {
     int normalize_per_snapshot; /* median normalisation (geolocate.hpp:115-122) */
     int detect;                 /* run detect_emitters on the accumulated surface */
     void* stream;               /* cudaStream_t to launch on; NULL = private stream */
-    int profile;                /* record per-kernel CUDA events into dg_result stats */
+    int profile;                /* record per-kernel CUDA events into dg_result stats
+                                   (steps then run serialised on one stream, so each
+                                   kernel's event time is its own) */
     int patch_peak;             /* write the exact FP64 values of the re-ranked near-peak
                                    cells into the HOST surfaces (default 1) so max_element on
                                    them is the exact argmax; 0 keeps every cell the FP32-path

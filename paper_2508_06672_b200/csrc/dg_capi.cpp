@@ -304,24 +304,38 @@ std::vector<float> chebyshev_table(int B) {
 std::vector<RxPairF32> rx_pairs_f32(const dg_grid* g, const PairGeom* pg, int n);
 double fp32_fdoa_margin(const PairGeom* pg, int n, double wl);
 
-struct Pipeline {
-    int64_t P = 0;
-    int N = 0, nbins = 0, max_tasks = 0, slots = 0, sm_count = 148;
-    int *d = nullptr, *sorted = nullptr, *hist = nullptr, *off = nullptr, *toff = nullptr,
-        *boff = nullptr, *cursor = nullptr, *n_tasks = nullptr, *n_buckets = nullptr,
-        *err = nullptr, *queue = nullptr;
-    double* fdoa = nullptr;
+// Per-step working set of the bucket/moments/evaluate stages. Two lanes on two
+// streams let step i+1's latency-bound bucketing (scan, scatter, task build)
+// and moments overlap step i's evaluation.
+struct Lane {
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int *sorted = nullptr, *off = nullptr, *toff = nullptr, *boff = nullptr, *cursor = nullptr,
+        *n_tasks = nullptr, *n_buckets = nullptr, *queue = nullptr, *ubin = nullptr;
     Task* tasks = nullptr;
     Bucket* buckets = nullptr;
-    StepRange* range = nullptr;
-    double* nu_c = nullptr;  // [slots]
     float2 *y1c = nullptr, *y2p = nullptr;
-    int padf = 0;     // zero padding in front of y2p / y2op
-    int* ubin = nullptr;  // bucket of each TDOA bin of the step, or -1
     float2* mom = nullptr;
     size_t mom_cap = 0;
-    unsigned long long* overlap = nullptr;
     unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
+    cudaEvent_t done = nullptr;
+    ~Lane() {
+        if (done) cudaEventDestroy(done);
+        if (own_stream && st) cudaStreamDestroy(st);
+    }
+};
+
+struct Pipeline {
+    int64_t P = 0;
+    int N = 0, nbins = 0, max_tasks = 0, slots = 0, sm_count = 148, n_lanes = 1;
+    int *d = nullptr, *hist = nullptr, *err = nullptr;
+    double* fdoa = nullptr;
+    StepRange* range = nullptr;
+    double* nu_c = nullptr;  // [slots]
+    int padf = 0;            // zero padding in front of each lane's y2p
+    Lane lanes[2];
+    cudaEvent_t window_ready = nullptr;
+    unsigned long long* overlap = nullptr;
     const float* tcheb[4] = {nullptr, nullptr, nullptr, nullptr};  // B = 64, 128, 256, 512
     const float* tcheb_for(int B) const {
         return tcheb[B == 64 ? 0 : B == 128 ? 1 : B == 256 ? 2 : 3];
@@ -335,7 +349,13 @@ struct Pipeline {
         return v && *v ? (float)atof(v) : kMomentRefineTau;
     }();
 
-    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms) {
+    ~Pipeline() {
+        if (window_ready) cudaEventDestroy(window_ready);
+    }
+
+    // lanes: 2 overlap consecutive steps; 1 serialises them (profiled runs, so
+    // each kernel's CUDA-event time is its own)
+    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms, int max_lanes = 2) {
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
@@ -352,32 +372,44 @@ struct Pipeline {
         hist = sc.alloc<int>((size_t)nbins * slots);
         range = sc.alloc<StepRange>(slots);
         nu_c = sc.alloc<double>(slots);
-        sorted = sc.alloc<int>(P);
-        tasks = sc.alloc<Task>(max_tasks);
-        buckets = sc.alloc<Bucket>(std::min<int64_t>(P, nbins));
-        off = sc.alloc<int>(nbins);
-        toff = sc.alloc<int>(nbins);
-        boff = sc.alloc<int>(nbins);
-        cursor = sc.alloc<int>(nbins);
-        n_tasks = sc.alloc<int>(1);
-        n_buckets = sc.alloc<int>(1);
-        queue = sc.alloc<int>(1);
         err = sc.alloc<int>(1);
         overlap = sc.alloc<unsigned long long>(1);
-        work = sc.alloc<unsigned long long>(2);
+        CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
+        CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
+        CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
         // centred y1 (k_moments' row copies may run one block past N) and y2 in a
         // zero-padded array: its window copies reach from N samples before to
         // N + 1200 samples after the data
         padf = (N + 65) & ~1;  // even: window copies start 16-byte aligned
         const size_t ylen = (size_t)padf + 2 * (size_t)N + 1280;
-        y1c = sc.alloc<float2>(N + 576);
-        y2p = sc.alloc<float2>(ylen);
-        CK(cudaMemsetAsync(y2p, 0, ylen * sizeof(float2), sc.st));
-        ubin = sc.alloc<int>(nbins);
-        CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
-        CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
-        CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
-        CK(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), sc.st));
+        n_lanes = n_steps > 1 ? std::max(1, std::min(2, max_lanes)) : 1;
+        for (int l = 0; l < n_lanes; ++l) {
+            Lane& L = lanes[l];
+            if (l == 0) {
+                L.st = sc.st;
+            } else {
+                CK(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+                L.own_stream = true;
+            }
+            CK(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+            L.sorted = sc.alloc<int>(P);
+            L.tasks = sc.alloc<Task>(max_tasks);
+            L.buckets = sc.alloc<Bucket>(std::min<int64_t>(P, nbins));
+            L.off = sc.alloc<int>(nbins);
+            L.toff = sc.alloc<int>(nbins);
+            L.boff = sc.alloc<int>(nbins);
+            L.cursor = sc.alloc<int>(nbins);
+            L.ubin = sc.alloc<int>(nbins);
+            L.n_tasks = sc.alloc<int>(1);
+            L.n_buckets = sc.alloc<int>(1);
+            L.queue = sc.alloc<int>(1);
+            L.work = sc.alloc<unsigned long long>(2);
+            L.y1c = sc.alloc<float2>(N + 576);
+            L.y2p = sc.alloc<float2>(ylen);
+            CK(cudaMemsetAsync(L.y2p, 0, ylen * sizeof(float2), sc.st));
+            CK(cudaMemsetAsync(L.work, 0, 2 * sizeof(unsigned long long), sc.st));
+        }
+        CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
         static const int kB[4] = {64, 128, 256, 512};
         std::vector<float> all;
         for (int B : kB) {
@@ -406,7 +438,8 @@ struct Pipeline {
     }
 
     // one synchronisation: read the window's ranges (and the lattice planning
-    // ranges `approx`, nullable), plan each step, upload nu_c
+    // ranges `approx`, nullable), plan each step, upload nu_c, size the moment
+    // buffers; the lanes then wait for `window_ready` (main stream)
     void plan_window(Scratch& sc, int n, double fs, const StepRange* approx = nullptr,
                      double margin_hz = 0.0, int64_t P_plan = 0, bool exact_ranges = true) {
         std::vector<StepRange> h(n), ha(approx ? n : 0);
@@ -419,6 +452,7 @@ struct Pipeline {
         CK(cudaStreamSynchronize(sc.st));
         plans.assign(n, StepPlan{});
         std::vector<double> nc(n);
+        size_t need = 0;
         for (int i = 0; i < n; ++i) {
             if (!exact_ranges) {  // the planning range bounds the bins (TDOA +-2 samples)
                 h[i] = ha[i];
@@ -428,9 +462,38 @@ struct Pipeline {
             plans[i] = plan_step(h[i], approx ? &ha[i] : nullptr, margin_hz, approx ? P_plan : P, N,
                                  fs);
             nc[i] = plans[i].nu_c;
+            const StepPlan& pl = plans[i];
+            if (!pl.empty && !pl.direct)
+                need = std::max(need, (size_t)std::min<int64_t>(P, pl.nbins) * pl.nbmax * pl.R);
         }
+        for (int l = 0; l < n_lanes; ++l)
+            if (need > lanes[l].mom_cap) {
+                lanes[l].mom = sc.alloc<float2>(need);
+                lanes[l].mom_cap = need;
+            }
         CK(cudaMemcpyAsync(nu_c, nc.data(), n * sizeof(double), cudaMemcpyHostToDevice, sc.st));
         CK(cudaStreamSynchronize(sc.st));
+        CK(cudaEventRecord(window_ready, sc.st));
+        for (int l = 1; l < n_lanes; ++l) CK(cudaStreamWaitEvent(lanes[l].st, window_ready, 0));
+    }
+
+    // the main stream waits for every lane (end of a window / of the call)
+    void join(Scratch& sc) {
+        for (int l = 1; l < n_lanes; ++l) {
+            CK(cudaEventRecord(lanes[l].done, lanes[l].st));
+            CK(cudaStreamWaitEvent(sc.st, lanes[l].done, 0));
+        }
+    }
+
+    unsigned long long work_total(Scratch& sc, int which) {
+        unsigned long long t = 0;
+        for (int l = 0; l < n_lanes; ++l) {
+            unsigned long long w[2] = {0, 0};
+            CK(cudaMemcpyAsync(w, lanes[l].work, sizeof w, cudaMemcpyDeviceToHost, sc.st));
+            CK(cudaStreamSynchronize(sc.st));
+            t += w[which];
+        }
+        return t;
     }
 
     // FP32 planning ranges over the full lattice of `g` for steps pg[0..n)
@@ -450,49 +513,44 @@ struct Pipeline {
         return out;
     }
 
-    void ensure_moments(Scratch& sc, const StepPlan& pl) {
-        const size_t nbk = (size_t)std::min<int64_t>(P, pl.nbins);
-        const size_t need = nbk * pl.nbmax * pl.R;
-        if (need > mom_cap) {
-            mom = sc.alloc<float2>(need);
-            mom_cap = need;
-        }
-    }
-
-    // phase B for slot s. y1_64 is the exact capture (centring source).
-    void correlate(Scratch& sc, int s, const double2* y1_64, const float2* y1, const float2* y2,
-                   double fs, double* s_out, uint32_t* bits, int64_t flag_base, cudaEvent_t ev0,
+    // phase B for slot s on lane s % n_lanes. y1_64 is the exact capture
+    // (centring source).
+    void correlate(int s, const double2* y1_64, const float2* y1, const float2* y2, double fs,
+                   double* s_out, uint32_t* bits, int64_t flag_base, cudaEvent_t ev0,
                    cudaEvent_t ev1, cudaEvent_t ev2) {
         const StepPlan& pl = plans[s];
-        cudaStream_t st = sc.st;
+        Lane& L = lanes[s % n_lanes];
+        cudaStream_t st = L.st;
         if (pl.empty) {
             for (cudaEvent_t e : {ev0, ev1, ev2})
                 if (e) CK(cudaEventRecord(e, st));
             return;
         }
         if (pl.direct) {
-            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
-                          n_buckets, d_slot(s), P, sorted, tasks, buckets, ubin, 0, st);
+            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
+                          L.n_tasks, L.n_buckets, d_slot(s), P, L.sorted, L.tasks, L.buckets,
+                          L.ubin, 0, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             if (ev1) CK(cudaEventRecord(ev1, st));
-            launch_correlate(tasks, n_tasks, max_tasks, sorted, fdoa_slot(s), y1, y2, N, fs, s_out,
-                             bits, flag_base, st);
+            launch_correlate(L.tasks, L.n_tasks, max_tasks, L.sorted, fdoa_slot(s), y1, y2, N, fs,
+                             s_out, bits, flag_base, st);
             launches += 4;
             ++direct_steps;
         } else {
-            ensure_moments(sc, pl);
-            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, off, toff, boff, cursor, n_tasks,
-                          n_buckets, d_slot(s), P, sorted, tasks, buckets, ubin, pl.B, st);
-            launch_center(y1_64, y2, N, nu_c + s, y1c, y2p, padf, st);
+            launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
+                          L.n_tasks, L.n_buckets, d_slot(s), P, L.sorted, L.tasks, L.buckets,
+                          L.ubin, pl.B, st);
+            launch_center(y1_64, y2, N, nu_c + s, L.y1c, L.y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
-            launch_moments(pl.B, pl.R, buckets, ubin, pl.bin0, pl.nbins, N,
-                           tcheb_for(pl.B), y1c, y2p, padf, mom, pl.nbmax, sm_count, st);
+            launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
+                           L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
-            CK(cudaMemsetAsync(queue, 0, sizeof(int), st));
-            launch_evaluate(pl.R, buckets, n_buckets, queue, (int)std::min<int64_t>(P, pl.nbins),
-                            sorted, fdoa_slot(s), fs, nu_c + s, pl.B, mom, pl.nbmax, s_out, bits,
-                            flag_base, tau, sm_count, st);
-            launch_work_count(buckets, n_buckets, pl.B, pl.R, work, st);
+            CK(cudaMemsetAsync(L.queue, 0, sizeof(int), st));
+            launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
+                            (int)std::min<int64_t>(P, pl.nbins), L.sorted, fdoa_slot(s), fs,
+                            nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
+                            sm_count, st);
+            launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, L.work, st);
             launches += 7;
         }
         if (ev2) CK(cudaEventRecord(ev2, st));
@@ -710,7 +768,7 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         pl.plan_window(sc, 1, s->fs);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
-        pl.correlate(sc, 0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+        pl.correlate(0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
                      nullptr);
         RefineCtx ctx{};
         ctx.P = n;
@@ -930,7 +988,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         pl.plan_window(sc, 1, s->fs, approx, fp32_fdoa_margin(&h, 1, wl), g->full_size);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
-        pl.correlate(sc, 0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+        pl.correlate(0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
                      nullptr);
         check_err_flag(sc, pl.err);
         static const int pair_rx[2] = {0, 1};
@@ -1168,7 +1226,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     } ev_free{&evs};
 
     Pipeline pl;
-    pl.init(sc, P, sn->N, SPl, eng->sm_count);
+    pl.init(sc, P, sn->N, SPl, eng->sm_count, opt.profile ? 1 : 2);
     const int64_t n_elems = (int64_t)SPl * P;
     double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
     const int64_t n_words = (n_elems + 31) / 32;
@@ -1195,11 +1253,12 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
             const int s = sp / pairs, q = sp - s * pairs;
             const int64_t c1 = ((int64_t)s * R + geo.prx[2 * q]) * sn->stride;
             const int64_t c2 = ((int64_t)s * R + geo.prx[2 * q + 1]) * sn->stride;
-            pl.correlate(sc, i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)lsp * P, bits,
+            pl.correlate(i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)lsp * P, bits,
                          (int64_t)lsp * P, opt.profile ? evs[3 * lsp] : nullptr,
                          opt.profile ? evs[3 * lsp + 1] : nullptr,
                          opt.profile ? evs[3 * lsp + 2] : nullptr);
         }
+        pl.join(sc);  // the next window reuses the d / fdoa / histogram slots
     }
     launches += pl.launches;
     CK(cudaGetLastError());
@@ -1234,9 +1293,8 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         CK(cudaStreamSynchronize(st));  // `init` is host memory of this frame
     }
 
-    unsigned long long ovl = 0, work[2] = {0, 0};
+    unsigned long long ovl = 0, work[2] = {pl.work_total(sc, 0), pl.work_total(sc, 1)};
     CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(work, pl.work, sizeof work, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     res->sum_overlap_samples = (double)ovl;
     res->kernel_launches += launches;
