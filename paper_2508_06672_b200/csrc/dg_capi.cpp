@@ -1363,7 +1363,7 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
         auto* ex = sc.alloc<double>((int64_t)kRerankCap * SP);
         acc_ex = sc.alloc<double>(kRerankCap);
         grid_ex = sc.alloc<double>((int64_t)kRerankCap * S);
-        launch_rerank(cells, n_cells, kRerankCap, SP, ctx, ex, st);
+        launch_rerank(cells, n_cells, kRerankCap, hn, SP, ctx, ex, st);
         launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, grid_ex, st);
         launch_argmax_cells(cells, n_cells, kRerankCap, acc_ex, best_i, best_v, st);
         launches += 3;

@@ -177,8 +177,9 @@ void launch_max(const double* v, int64_t P, double* partial, int n_partial, doub
                 cudaStream_t st);
 void launch_select_near(const double* v, int64_t P, const double* vmax, double rel,
                         int* list, int* count, int cap, cudaStream_t st);
-void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
-                   double* ex /* [cap][SP] */, cudaStream_t st);
+// n_items_hint: host-side count of near-peak cells (sizes the launch)
+void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
+                   RefineCtx ctx, double* ex, cudaStream_t st);
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
                             const double* medians, double* acc_ex, double* grid_ex /* [cap][S] */,
                             cudaStream_t st);

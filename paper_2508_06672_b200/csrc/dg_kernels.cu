@@ -10,6 +10,8 @@
 //   per (snapshot, pair): d[P] int32, fdoa[P] f64, d-sorted candidate ids,
 //   warp tasks, raw surface double [S*pairs][P], refine bitmap 1 bit/element.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <float.h>
 #include <limits.h>
 #include <math.h>
@@ -681,12 +683,17 @@ __global__ void k_select_near(const double* __restrict__ v, int64_t P,
 // Exact re-evaluation of the near-peak candidates into a private buffer
 // ex[ci * SP + sp] (the returned surfaces are left untouched so they stay
 // independent of how the grid is partitioned).
+// Each (cell, snapshot-pair) is one sequential FP64 chain of N_ov iterations
+// (the reference's order, bit-exact). With few items, one item per warp (lane
+// 0 only) spreads the chains over SM sub-partitions so each runs at its own
+// FP64 pipe's rate instead of sharing it: `stride` threads per item.
 __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ n_cells, int cap,
-                         int SP, RefineCtx c, double* __restrict__ ex) {
+                         int SP, RefineCtx c, double* __restrict__ ex, int stride) {
     const int n = min(*n_cells, cap);
     const int64_t total = (int64_t)n * SP;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t % stride) return;
+    for (int64_t i = t / stride; i < total; i += (int64_t)gridDim.x * blockDim.x / stride) {
         const int64_t ci = i / SP, sp = i - ci * SP;
         ex[i] = exact_element(c, sp, cells[ci]);
     }
@@ -1067,10 +1074,12 @@ void launch_select_near(const double* v, int64_t P, const double* vmax, double r
     k_select_near<<<blocks_for(P, 256), 256, 0, st>>>(v, P, vmax, rel, list, count, cap);
 }
 
-void launch_rerank(const int* cells, const int* n_cells, int cap, int SP, RefineCtx ctx,
-                   double* ex, cudaStream_t st) {
-    k_rerank<<<blocks_for((int64_t)cap * SP, 64, 148LL * 64), 64, 0, st>>>(cells, n_cells, cap, SP,
-                                                                          ctx, ex);
+void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
+                   RefineCtx ctx, double* ex, cudaStream_t st) {
+    const int64_t items = (int64_t)std::min(n_items_hint, cap) * SP;
+    const int stride = items <= 148 * 16 ? 32 : 1;  // one chain per warp when they fit
+    k_rerank<<<blocks_for((int64_t)cap * SP * stride, 64, 148LL * 64), 64, 0, st>>>(
+        cells, n_cells, cap, SP, ctx, ex, stride);
 }
 
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,

@@ -445,11 +445,22 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     cf[c][m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
+                // W_j = W_1^j by an FP64 recurrence from one FP64 sincospi (error
+                // ~1e-15), each rounded once to FP32; e^{i 2 pi nu B G} = W_G
+                const double x1 = nu[c] * (double)B;
+                double w1r, w1i;
+                sincospi(2.0 * (x1 - rint(x1)), &w1i, &w1r);
+                double pr = 1.0, pi_ = 0.0;
 #pragma unroll
-                for (int j = 0; j < G; ++j)
-                    cis_cycles(nu[c] * (double)B * (double)j, &wtr[c][j], &wti[c][j]);
-                const double x = nu[c] * (double)B * (double)G;
-                sincospi(2.0 * (x - rint(x)), &si[c], &sr[c]);
+                for (int j = 0; j < G; ++j) {
+                    wtr[c][j] = (float)pr;
+                    wti[c][j] = (float)pi_;
+                    const double nr = fma(pr, w1r, -pi_ * w1i);
+                    pi_ = fma(pr, w1i, pi_ * w1r);
+                    pr = nr;
+                }
+                sr[c] = pr;
+                si[c] = pi_;
             }
             double acc_re[kEvalNC], acc_im[kEvalNC], en[kEvalNC], ar[kEvalNC], ai[kEvalNC];
 #pragma unroll
