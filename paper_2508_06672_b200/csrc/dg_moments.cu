@@ -55,8 +55,10 @@ __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
 
 __host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) / kEvalG * kEvalG; }
 
-// two staging buffers of one bucket's moments
-inline size_t evaluate_smem(int nbmax, int R) { return 2 * (size_t)nbmax * R * sizeof(float2); }
+constexpr int kEvalStages = 3;  // bucket-moment buffers in k_evaluate's TMA ring
+inline size_t evaluate_smem(int nbmax, int R) {
+    return kEvalStages * (size_t)nbmax * R * sizeof(float2);
+}
 constexpr int kMomThreads = 512;
 constexpr int kMomRun = 16;  // sample pairs per first-level FP32 sum in k_moments
 constexpr int kMomWarps = kMomThreads / 32;
@@ -102,6 +104,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
 }
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
@@ -376,16 +389,25 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
            const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
            uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
     extern __shared__ float4 smem4[];
-    __shared__ uint64_t full[2], empty[2];
-    __shared__ int slot_u[2];
+    __shared__ uint64_t full[kEvalStages], empty[kEvalStages];
+    __shared__ int slot_u[kEvalStages];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nbk = *n_buckets;
     const double nu_c = *nu_c_p;
     const size_t buf_f4 = (size_t)nbmax * R / 2;
 
-    auto produce = [&](int k) {  // thread 0 only
-        const int sl = k & 1;
-        if (k >= 2) mbar_wait(&empty[sl], ((k >> 1) - 1) & 1);
+    // thread 0 only: claim bucket k into its ring slot. The slot is free once
+    // every warp released item k - kEvalStages; `block` = wait for that,
+    // otherwise give up (returns false) so the producer never idles a warp.
+    auto produce = [&](int k, bool block) -> bool {
+        const int sl = k % kEvalStages;
+        if (k >= kEvalStages) {
+            const uint32_t par = ((k / kEvalStages) - 1) & 1;
+            if (block)
+                mbar_wait(&empty[sl], par);
+            else if (!mbar_test(&empty[sl], par))
+                return false;
+        }
         const int u = atomicAdd(queue, 1);
         slot_u[sl] = u;
         if (u < nbk) {
@@ -396,21 +418,29 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
         } else {
             mbar_arrive(&full[sl]);  // end of queue: complete the phase with no data
         }
+        return true;
     };
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], kEvalWarps);
-        mbar_init(&empty[1], kEvalWarps);
+        for (int i = 0; i < kEvalStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kEvalWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) produce(0);
+    int produced = 0;  // thread 0: buckets claimed so far
+    if (tid == 0)
+        for (; produced < kEvalStages; ++produced) produce(produced, false);
 
     for (int k = 0;; ++k) {
-        if (tid == 0) produce(k + 1);
-        const int sl = k & 1;
-        mbar_wait(&full[sl], (k >> 1) & 1);
+        // the ring runs up to kEvalStages buckets ahead; thread 0 blocks only
+        // if bucket k itself is not claimed yet
+        if (tid == 0) {
+            for (; produced <= k; ++produced) produce(produced, true);
+            while (produced < k + kEvalStages && produce(produced, false)) ++produced;
+        }
+        const int sl = k % kEvalStages;
+        mbar_wait(&full[sl], (k / kEvalStages) & 1);
         const int u = slot_u[sl];
         if (u >= nbk) break;
         const Bucket bk = buckets[u];

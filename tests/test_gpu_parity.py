@@ -421,6 +421,21 @@ def test_step_sharding_bit_identical(b2, ref, normalize):
         assert merge_argmax(peaks) == (full.argmax_value, full.argmax_index)
 
 
+def test_lane_pipeline_bit_identical(b2, ref):
+    """Steps overlapped on two streams (default) and serialised on one (the
+    profiled mode) give the same surfaces bit for bit."""
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    staged = b2.StagedSnapshots(sc.states, sc.captures, sc.fs, sc.fc)
+    opts = b2.GeolocateOptions(detect=False)
+    a = b2.geolocate_staged(grid, staged, opts, want_per_snapshot=True)
+    b = b2.geolocate_staged(grid, staged, opts, want_per_snapshot=True, profile=True)
+    for x, y in zip(a.per_snapshot, b.per_snapshot):
+        assert np.array_equal(x.values, y.values)
+    assert np.array_equal(a.accumulated.values, b.accumulated.values)
+    assert (a.argmax_index, a.argmax_value) == (b.argmax_index, b.argmax_value)
+
+
 def test_silent_captures(b2):
     grid = b2.build_candidate_grid(b2.LatLonBounds(-0.1, 0.1, -0.1, 0.1), 0.05)
     states = np.zeros((2, 2, 6))
