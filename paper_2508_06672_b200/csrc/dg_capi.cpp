@@ -513,6 +513,8 @@ struct Pipeline {
         return out;
     }
 
+    cudaStream_t lane_stream(int s) const { return lanes[s % n_lanes].st; }
+
     // phase B for slot s on lane s % n_lanes. y1_64 is the exact capture
     // (centring source).
     void correlate(int s, const double2* y1_64, const float2* y1, const float2* y2, double fs,
@@ -575,6 +577,84 @@ int64_t run_refine(Scratch& sc, const uint32_t* bits, int64_t n_elems, const Ref
     *launches += 2;
     return (int64_t)n;
 }
+
+// Refinement of batches of steps on a side stream: batch j (steps
+// [jK, (j+1)K)) starts once those steps' correlators finished (events on their
+// lanes) and runs on the FP64 pipes while the lanes correlate later steps.
+// K = 0: everything refined at the end on the main stream (profiled runs).
+struct SideRefine {
+    Scratch& sc;
+    int steps, K;
+    int64_t P, P32;
+    cudaStream_t rs = nullptr;
+    std::vector<cudaEvent_t> ev;
+    int64_t* list = nullptr;
+    unsigned long long* counts = nullptr;  // one per batch
+    int next = 0, batches = 0;
+    int64_t launches = 0;
+    SideRefine(Scratch& s, int n_steps, int64_t P_, int64_t P32_, int K_)
+        : sc(s), steps(n_steps), K(K_), P(P_), P32(P32_) {
+        const int nb = K > 0 ? (steps + K - 1) / K : 1;
+        counts = sc.alloc<unsigned long long>(nb);
+        CK(cudaMemsetAsync(counts, 0, nb * sizeof(unsigned long long), sc.st));
+        list = sc.alloc<int64_t>((size_t)(K > 0 ? std::min(K, steps) : steps) * P32);
+        if (K > 0) {
+            CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+            ev.resize(steps);
+            for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            // list/counts were allocated on the main stream
+            cudaEvent_t ready;
+            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(ready, sc.st));
+            CK(cudaStreamWaitEvent(rs, ready, 0));
+            cudaEventDestroy(ready);
+        }
+    }
+    ~SideRefine() {
+        for (auto e : ev) cudaEventDestroy(e);
+        if (rs) cudaStreamDestroy(rs);
+    }
+    void launch_batch(const uint32_t* bits, const RefineCtx& ctx, int r0, int r1,
+                      cudaStream_t st) {
+        launch_refine_rows(bits, r0, r1, P32, list, counts + batches, ctx, st);
+        ++batches;
+        launches += 2;
+    }
+    void step_done(int s, cudaStream_t lane, const uint32_t* bits, const RefineCtx& ctx) {
+        if (K <= 0) return;
+        CK(cudaEventRecord(ev[s], lane));
+        if (s + 1 - next >= K) {
+            for (int i = next; i <= s; ++i) CK(cudaStreamWaitEvent(rs, ev[i], 0));
+            launch_batch(bits, ctx, next, s + 1, rs);
+            next = s + 1;
+        }
+    }
+    void finish(const uint32_t* bits, const RefineCtx& ctx) {
+        if (K <= 0) {
+            launch_batch(bits, ctx, 0, steps, sc.st);
+            return;
+        }
+        if (next < steps) {
+            for (int i = next; i < steps; ++i) CK(cudaStreamWaitEvent(rs, ev[i], 0));
+            launch_batch(bits, ctx, next, steps, rs);
+            next = steps;
+        }
+        cudaEvent_t done;
+        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CK(cudaEventRecord(done, rs));
+        CK(cudaStreamWaitEvent(sc.st, done, 0));
+        cudaEventDestroy(done);
+    }
+    unsigned long long total() {
+        std::vector<unsigned long long> h(std::max(batches, 1));
+        CK(cudaMemcpyAsync(h.data(), counts, h.size() * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+        unsigned long long t = 0;
+        for (auto v : h) t += v;
+        return t;
+    }
+};
 
 void check_err_flag(Scratch& sc, const int* err) {
     int h = 0;
@@ -1229,12 +1309,20 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     pl.init(sc, P, sn->N, SPl, eng->sm_count, opt.profile ? 1 : 2);
     const int64_t n_elems = (int64_t)SPl * P;
     double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
-    const int64_t n_words = (n_elems + 31) / 32;
+    // refine flags: one bitmap row of whole words per step (bit p of step i at
+    // i * P32 + p), so batches of steps are refined on a side stream while the
+    // lanes correlate later steps (FP64 refinement next to FP32 correlation)
+    const int64_t P32 = (P + 31) & ~int64_t(31);
+    const int64_t n_words = SPl * (P32 / 32);
     auto* bits = sc.alloc<uint32_t>(n_words);
     CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
     const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
     const auto* y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
     const int sp0 = s0 * pairs;  // global (snapshot, pair) index of local step 0
+    RefineCtx ctx = refine_ctx(g, sn, geo, raw);  // element = local step * P + p
+    ctx.pg = geo.pg + sp0;
+    ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
+    SideRefine rf(sc, SPl, P, P32, opt.profile ? 0 : 10);
 
     for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
         const int nw = std::min(pl.slots, SPl - w0);
@@ -1254,9 +1342,10 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
             const int64_t c1 = ((int64_t)s * R + geo.prx[2 * q]) * sn->stride;
             const int64_t c2 = ((int64_t)s * R + geo.prx[2 * q + 1]) * sn->stride;
             pl.correlate(i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)lsp * P, bits,
-                         (int64_t)lsp * P, opt.profile ? evs[3 * lsp] : nullptr,
+                         (int64_t)lsp * P32, opt.profile ? evs[3 * lsp] : nullptr,
                          opt.profile ? evs[3 * lsp + 1] : nullptr,
                          opt.profile ? evs[3 * lsp + 2] : nullptr);
+            rf.step_done(lsp, pl.lane_stream(i), bits, ctx);
         }
         pl.join(sc);  // the next window reuses the d / fdoa / histogram slots
     }
@@ -1264,11 +1353,9 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     CK(cudaGetLastError());
     check_err_flag(sc, pl.err);
 
-    // exact refinement; element e = local step * P + p
-    RefineCtx ctx = refine_ctx(g, sn, geo, raw);
-    ctx.pg = geo.pg + sp0;
-    ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
-    res->n_refined = run_refine(sc, bits, n_elems, ctx, &launches);
+    rf.finish(bits, ctx);  // remaining steps; the main stream joins the side stream
+    res->n_refined = (int64_t)rf.total();
+    launches += rf.launches;
 
     if (pairs > 1) {
         launch_combine_pairs(raw, ns, pairs, P, grids, st);

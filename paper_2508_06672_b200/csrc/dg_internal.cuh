@@ -168,6 +168,10 @@ struct RefineCtx {
     double* raw;              // [S*pairs*P] (batch: [P])
 };
 void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st);
+// refine steps [row0, row1) of a bitmap with one P32-element row per step
+// (count of flagged elements left in *count); ctx.raw is dense [step][P]
+void launch_refine_rows(const uint32_t* bits, int64_t row0, int64_t row1, int64_t P32,
+                        int64_t* list, unsigned long long* count, RefineCtx ctx, cudaStream_t st);
 
 void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
                           cudaStream_t st);

@@ -598,6 +598,32 @@ __global__ void k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx 
     }
 }
 
+// Batched refinement on a side stream (overlaps the FP32 correlation of later
+// steps): `list` holds indices relative to element `base` of a bitmap laid out
+// one P32-element row per step (P32 = P rounded up to 32), `count` is on the
+// device (k_compact_flags), raw surfaces are dense [step][P].
+__global__ void k_refine_rows(const int64_t* __restrict__ list,
+                              const unsigned long long* __restrict__ count, int64_t base,
+                              int64_t P32, RefineCtx c) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n = (int64_t)*count;
+    for (int64_t i = w0; i < n; i += nw) {
+        const int64_t e = base + list[i];
+        const int64_t sp = e / P32, p = e - sp * P32;
+        const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
+        long long tdoa;
+        double fdoa;
+        offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
+        const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
+        const double v = correlate_fp64_warp(c.y64 + (s * c.R + ri) * c.stride,
+                                             c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa, fdoa,
+                                             c.fs, lane);
+        if (lane == 0) c.raw[sp * c.P + p] = v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Accumulation (correlate_snapshot_all_pairs + accumulate_grids order).
 __global__ void k_combine_pairs(const double* __restrict__ raw, int S, int pairs, int64_t P,
@@ -1043,6 +1069,14 @@ void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long lon
 void launch_compact_flags(const uint32_t* bits, int64_t n_words, int64_t* list,
                           unsigned long long* cursor, cudaStream_t st) {
     k_compact_flags<<<blocks_for(n_words, 256), 256, 0, st>>>(bits, n_words, list, cursor);
+}
+
+void launch_refine_rows(const uint32_t* bits, int64_t row0, int64_t row1, int64_t P32,
+                        int64_t* list, unsigned long long* count, RefineCtx ctx, cudaStream_t st) {
+    const int64_t w0 = row0 * (P32 / 32), nw = (row1 - row0) * (P32 / 32);
+    cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    k_compact_flags<<<blocks_for(nw, 256, 148LL * 8), 256, 0, st>>>(bits + w0, nw, list, count);
+    k_refine_rows<<<148 * 16, 256, 0, st>>>(list, count, row0 * P32, P32, ctx);
 }
 
 void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st) {
