@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 2
+#define DG_ABI_VERSION 3
 
 enum {
     DG_OK = 0,
@@ -198,6 +198,24 @@ int dg_stage_snapshots(dg_engine* engine, const dg_snapshots* snaps, dg_staged**
 int dg_geolocate_staged(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
                         const dg_options* opt, dg_result* result);
 void dg_staged_destroy(dg_staged* staged);
+
+/* DGIQ capture files, the reference's on-disk capture format (io.hpp:45-52,
+ * read_iq :140-167): 38-byte little-endian header + float32 I/Q payload. The
+ * checks and messages are read_iq's; runtime_error -> DG_ERUNTIME. */
+typedef struct {
+    double sample_rate_hz;
+    double center_freq_hz;
+    double start_time_s;
+    int64_t sample_count;
+} dg_iq_header;
+int dg_read_iq_header(const char* path, dg_iq_header* out);
+/* header + payload (2 * sample_count floats into iq_out; nullable = header only) */
+int dg_read_iq(const char* path, dg_iq_header* out, float* iq_out, int64_t capacity);
+/* load_snapshots (tools/digeo_cli.cpp:64-85) + dg_stage_snapshots for files: paths
+ * [n_snapshots][n_receivers], states likewise; each payload is read straight into a
+ * pinned buffer and copied to HBM as float2 (exact) while the next file is read. */
+int dg_stage_snapshots_iq(dg_engine* engine, const char* const* paths, int64_t n_snapshots,
+                          int64_t n_receivers, const dg_state* states, dg_staged** out);
 
 /* The two halves of geolocate_snapshots, for snapshot-sharded multi-GPU runs
  * (DESIGN.md section 7). dg_correlate_steps: snapshots [s_begin, s_end) over

@@ -79,7 +79,7 @@ class RefLib:
                      "ref_scene_state", "ref_lla_to_ecef", "ref_build_grid",
                      "ref_predict_pair_offsets", "ref_correlate_point", "ref_correlate_batch",
                      "ref_plan_batches", "ref_geolocate", "ref_correlate_snapshot_timed",
-                     "ref_detect_emitters"):
+                     "ref_detect_emitters", "ref_write_iq", "ref_read_iq"):
             getattr(L, name).restype = C.c_int
         L.ref_build_grid.argtypes = [_dp, C.c_double, C.c_double, C.c_uint64, _ip, _ip, _dp]
         L.ref_predict_pair_offsets.argtypes = [_dp, _dp, _dp, C.c_double, C.c_double, _ip, _dp]
@@ -104,10 +104,29 @@ class RefLib:
             C.c_char_p, C.c_uint, C.c_uint64, _dp, _dp]
         L.ref_detect_emitters.argtypes = [_dp, C.c_double, C.c_double, _dp, C.c_double, C.c_int,
                                           _ip, C.c_int64, _ip, _dp, _dp]
+        L.ref_write_iq.argtypes = [C.c_char_p, _dp, C.c_int64, C.c_double, C.c_double,
+                                   C.c_double]
+        L.ref_read_iq.argtypes = [C.c_char_p, _dp, _dp, C.c_int64]
 
     def _check(self, rc: int):
         if rc != 0:
             raise ReferenceError_(rc, self.lib.ref_last_error().decode())
+
+    # -- DGIQ files (io.hpp:123-167) -----------------------------------------
+    def write_iq(self, path, samples, fs, fc, t0=0.0):
+        y = np.ascontiguousarray(samples, np.complex128)
+        self._check(self.lib.ref_write_iq(str(path).encode(), y.ctypes.data_as(_dp), len(y), fs,
+                                          fc, t0))
+
+    def read_iq(self, path):
+        """-> (samples complex128, sample_rate_hz, center_freq_hz, start_time_s)"""
+        info = np.zeros(4)
+        self._check(self.lib.ref_read_iq(str(path).encode(), _d(info), None, 0))
+        n = int(info[3])
+        out = np.zeros(n, np.complex128)
+        self._check(self.lib.ref_read_iq(str(path).encode(), _d(info), out.ctypes.data_as(_dp),
+                                         n))
+        return out, info[0], info[1], info[2]
 
     # -- scenes --------------------------------------------------------------
     def simulate(self, cfg_text: str) -> RefScene:

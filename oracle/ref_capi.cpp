@@ -26,6 +26,7 @@
 #include "digeo/geodesy.hpp"
 #include "digeo/geolocate.hpp"
 #include "digeo/geometry.hpp"
+#include "digeo/io.hpp"
 #include "digeo/scene.hpp"
 
 using namespace digeo;
@@ -290,6 +291,30 @@ int ref_detect_emitters(const double* bounds4, double spacing, double alt, const
             det_score[i] = det[i].score;
             det_z[i] = det[i].score_zsigma;
         }
+    })
+}
+
+// --- DGIQ files (io.hpp:123-167) -------------------------------------------
+
+int ref_write_iq(const char* path, const double* iq, int64_t n, double fs, double fc, double t0) {
+    REF_GUARD({
+        BasebandCapture c = make_cap(iq, n, fs, fc);
+        c.start_time_s = t0;
+        write_iq(c, path);
+    })
+}
+
+// info4 = {sample_rate_hz, center_freq_hz, start_time_s, sample_count}; iq (nullable) gets
+// the widened complex<double> samples
+int ref_read_iq(const char* path, double* info4, double* iq, int64_t capacity) {
+    REF_GUARD({
+        const BasebandCapture c = read_iq(path);
+        info4[0] = c.sample_rate_hz;
+        info4[1] = c.center_freq_hz;
+        info4[2] = c.start_time_s;
+        info4[3] = static_cast<double>(c.samples.size());
+        if (iq && static_cast<int64_t>(c.samples.size()) <= capacity)
+            std::memcpy(iq, c.samples.data(), c.samples.size() * sizeof(cplx));
     })
 }
 

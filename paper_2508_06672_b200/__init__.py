@@ -13,6 +13,7 @@ from .geodesy import (CandidateGrid, GeodeticCoord, GridAxis, LatLonBounds,  # n
 from .geolocate import (CorrelationGrid, EmitterEstimate, GeolocateOptions,  # noqa: F401
                         GeolocateResult, Snapshot, StagedSnapshots, accumulate_peak,
                         correlate_snapshot, correlate_steps, geolocate_arrays,
-                        geolocate_snapshots, geolocate_staged, predict_offsets, wavelength_m)
+                        geolocate_snapshots, geolocate_staged, predict_offsets, read_iq,
+                        read_iq_header, wavelength_m)
 
 __version__ = "0.1.0"

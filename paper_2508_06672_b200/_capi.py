@@ -45,6 +45,11 @@ class dg_snapshots(C.Structure):
                 ("captures_f32", C.POINTER(C.POINTER(C.c_float)))]
 
 
+class dg_iq_header(C.Structure):
+    _fields_ = [("sample_rate_hz", C.c_double), ("center_freq_hz", C.c_double),
+                ("start_time_s", C.c_double), ("sample_count", C.c_int64)]
+
+
 class dg_options(C.Structure):
     _fields_ = [("k_sigma", C.c_double), ("exclusion_radius_cells", C.c_int),
                 ("normalize_per_snapshot", C.c_int), ("detect", C.c_int),
@@ -82,7 +87,8 @@ EXPORTS = (
     "dg_grid_info", "dg_grid_points", "dg_grid_destroy", "dg_predict_offsets",
     "dg_correlate_snapshot", "dg_options_default", "dg_geolocate_snapshots",
     "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_correlate_steps",
-    "dg_accumulate_peak", "dg_detect_emitters",
+    "dg_accumulate_peak", "dg_detect_emitters", "dg_read_iq_header", "dg_read_iq",
+    "dg_stage_snapshots_iq",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -129,6 +135,10 @@ def _load():
                                C.POINTER(dg_result)],
         "dg_detect_emitters": [_vp, _vp, _vp, C.c_int, C.c_double, C.c_int,
                                C.POINTER(dg_emitter_estimate), C.c_int64, _i64p],
+        "dg_read_iq_header": [C.c_char_p, C.POINTER(dg_iq_header)],
+        "dg_read_iq": [C.c_char_p, C.POINTER(dg_iq_header), C.POINTER(C.c_float), C.c_int64],
+        "dg_stage_snapshots_iq": [_vp, C.POINTER(C.c_char_p), C.c_int64, C.c_int64,
+                                  C.POINTER(dg_state), C.POINTER(_vp)],
         "dg_fp32_peak_tflops": [C.c_int, _dp],
         "dg_fp32x2_peak_tflops": [C.c_int, _dp],
         "dg_fp64_peak_tflops": [C.c_int, _dp],

@@ -1112,6 +1112,149 @@ void validate_snapshots(const dg_snapshots* sn) {
 
 }  // namespace
 
+// ---- DGIQ capture files (io.hpp:123-167) ------------------------------------
+namespace {
+
+// read_iq's header checks and messages (io.hpp:140-163, ByteReader io.hpp:75-84,
+// read_file_bytes :112-117); leaves `f` positioned at the payload
+struct IqReader {
+    std::FILE* f = nullptr;
+    dg_iq_header h{};
+    explicit IqReader(const char* path) {
+        if (!path) raise(DG_EINVAL, "null path");
+        const std::string p(path);
+        f = std::fopen(path, "rb");
+        if (!f) raise(DG_ERUNTIME, "cannot open " + p);
+        unsigned char hb[38];
+        const size_t got = std::fread(hb, 1, sizeof hb, f);
+        const std::string ctx = "read_iq(" + p + ")";
+        if (got < 4) raise(DG_ERUNTIME, ctx + ": truncated file");
+        if (std::memcmp(hb, "DGIQ", 4) != 0) raise(DG_ERUNTIME, "read_iq: bad magic in " + p);
+        if (got < 6) raise(DG_ERUNTIME, ctx + ": truncated file");
+        const unsigned version = hb[4] | (hb[5] << 8);
+        if (version != 1)
+            raise(DG_ERUNTIME, "read_iq: unsupported version " + std::to_string(version));
+        if (got < 38) raise(DG_ERUNTIME, ctx + ": truncated file");
+        uint64_t cnt = 0;
+        std::memcpy(&h.sample_rate_hz, hb + 6, 8);  // little-endian host (x86-64 / aarch64)
+        std::memcpy(&h.center_freq_hz, hb + 14, 8);
+        std::memcpy(&h.start_time_s, hb + 22, 8);
+        std::memcpy(&cnt, hb + 30, 8);
+        if (std::fseek(f, 0, SEEK_END) != 0) raise(DG_ERUNTIME, "cannot open " + p);
+        const long end = std::ftell(f);
+        if (end < 38 || (uint64_t)(end - 38) != cnt * 8)
+            raise(DG_ERUNTIME, "read_iq: payload length does not match sample_count in " + p);
+        std::fseek(f, 38, SEEK_SET);
+        h.sample_count = (int64_t)cnt;
+        // BasebandCapture::validate (capture.hpp:42-46)
+        if (cnt == 0) raise(DG_EINVAL, "BasebandCapture: no samples");
+        if (!(h.sample_rate_hz > 0.0)) raise(DG_EINVAL, "BasebandCapture: sample_rate_hz <= 0");
+    }
+    void read_payload(float* dst) {
+        const size_t n = (size_t)h.sample_count * 2;
+        if (std::fread(dst, sizeof(float), n, f) != n)
+            raise(DG_ERUNTIME, "read_iq: short read");
+    }
+    ~IqReader() {
+        if (f) std::fclose(f);
+    }
+};
+
+}  // namespace
+
+int dg_read_iq_header(const char* path, dg_iq_header* out) {
+    return guard([&] {
+        if (!out) raise(DG_EINVAL, "null argument");
+        IqReader r(path);
+        *out = r.h;
+    });
+}
+
+int dg_read_iq(const char* path, dg_iq_header* out, float* iq, int64_t capacity) {
+    return guard([&] {
+        if (!out) raise(DG_EINVAL, "null argument");
+        IqReader r(path);
+        *out = r.h;
+        if (iq) {
+            if (capacity < r.h.sample_count) raise(DG_EINVAL, "dg_read_iq: buffer too small");
+            r.read_payload(iq);
+        }
+    });
+}
+
+int dg_stage_snapshots_iq(dg_engine* eng, const char* const* paths, int64_t S, int64_t R,
+                          const dg_state* states, dg_staged** out) {
+    return guard([&] {
+        if (!eng || !paths || !states || !out) raise(DG_EINVAL, "null argument");
+        if (S < 1) raise(DG_EINVAL, "geolocate_snapshots: no snapshots");
+        if (R < 2) raise(DG_EINVAL, "correlate_snapshot_all_pairs: need >= 2 receivers");
+        const int64_t n_caps = S * R;
+        std::vector<dg_iq_header> hdr(n_caps);
+        for (int64_t c = 0; c < n_caps; ++c) hdr[c] = IqReader(paths[c]).h;
+        for (int64_t c = 1; c < n_caps; ++c) {  // check_pair (backend.hpp:221-228)
+            if (hdr[c].sample_rate_hz != hdr[0].sample_rate_hz)
+                raise(DG_EINVAL, "backend stage: sample rates differ");
+            if (hdr[c].sample_count != hdr[0].sample_count)
+                raise(DG_EINVAL, "backend stage: sample counts differ");
+            if (hdr[c].center_freq_hz != hdr[0].center_freq_hz)
+                raise(DG_EINVAL, "dg_stage_snapshots_iq: center frequencies differ");
+        }
+        if (!(hdr[0].center_freq_hz > 0.0)) raise(DG_EINVAL, "wavelength_m: center_freq_hz <= 0");
+        set_device(eng);
+        auto s = std::make_unique<dg_staged>();
+        s->eng = eng;
+        s->S = S;
+        s->R = R;
+        s->N = hdr[0].sample_count;
+        s->stride = capture_stride(s->N);
+        s->fs = hdr[0].sample_rate_hz;
+        s->fc = hdr[0].center_freq_hz;
+        s->states.assign(states, states + n_caps);
+        s->y32 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(float2));
+        s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
+        auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
+        auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
+        StreamGuard sg(nullptr, eng->stream);
+        CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, sg.st));
+        CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, sg.st));
+        // payloads go from disk straight into two pinned buffers (float32 I/Q is
+        // the device layout), each copy to HBM overlapping the next file's read
+        const size_t bytes = (size_t)s->N * sizeof(float2);
+        void* pin[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        struct PinFree {
+            void** p;
+            cudaEvent_t* e;
+            ~PinFree() {
+                for (int i = 0; i < 2; ++i) {
+                    if (e[i]) {
+                        cudaEventSynchronize(e[i]);
+                        cudaEventDestroy(e[i]);
+                    }
+                    if (p[i]) cudaFreeHost(p[i]);
+                }
+            }
+        } pin_free{pin, ev};
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaHostAlloc(&pin[i], bytes, cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+        for (int64_t c = 0; c < n_caps; ++c) {
+            const int b = (int)(c & 1);
+            if (c >= 2) CK(cudaEventSynchronize(ev[b]));  // its previous copy is done
+            IqReader r(paths[c]);
+            r.read_payload(static_cast<float*>(pin[b]));
+            CK(cudaMemcpyAsync(y32 + c * s->stride, pin[b], bytes, cudaMemcpyHostToDevice,
+                               sg.st));
+            CK(cudaEventRecord(ev[b], sg.st));
+            launch_f32_to_f64(y32 + c * s->stride, y64 + c * s->stride, s->N, sg.st);
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(sg.st));
+        *out = s.release();
+    });
+}
+
 int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) {
     return guard([&] {
         if (!eng) raise(DG_EINVAL, "null engine");

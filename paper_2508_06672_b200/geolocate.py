@@ -139,11 +139,49 @@ class StagedSnapshots:
     def handle(self):
         return self._h
 
+    @classmethod
+    def from_iq_files(cls, paths, states, engine: Engine | None = None) -> "StagedSnapshots":
+        """load_snapshots (tools/digeo_cli.cpp:64-85) from DGIQ files: paths[s][r],
+        states [S, R, 6]; payloads go disk -> pinned -> HBM as float32 I/Q."""
+        self = cls.__new__(cls)
+        self.engine = engine or default_engine()
+        S, R = len(paths), len(paths[0])
+        if any(len(row) != R for row in paths):
+            raise ValueError("geolocate_snapshots: receiver count differs between snapshots")
+        st = np.ascontiguousarray(states, np.float64).reshape(S * R, 6)
+        st_arr = (_capi.dg_state * (S * R))(*[_pair_states(st[k]) for k in range(S * R)])
+        cpaths = (C.c_char_p * (S * R))(*[str(p).encode() for row in paths for p in row])
+        h = C.c_void_p()
+        check(lib.dg_stage_snapshots_iq(self.engine.handle, cpaths, S, R, st_arr, C.byref(h)))
+        self._h = h
+        self._keep = None
+        hdr = read_iq_header(paths[0][0])
+        self.shape = (S, R, hdr.sample_count)
+        return self
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
             lib.dg_staged_destroy(h)
             self._h = None
+
+
+def read_iq_header(path) -> "_capi.dg_iq_header":
+    """The DGIQ header (io.hpp:45-52), validated like read_iq (io.hpp:140-167)."""
+    h = _capi.dg_iq_header()
+    check(lib.dg_read_iq_header(str(path).encode(), C.byref(h)))
+    return h
+
+
+def read_iq(path) -> BasebandCapture:
+    """read_iq (io.hpp:140-167): a DGIQ file as a BasebandCapture with complex64
+    samples (the file's float32 I/Q, exact)."""
+    h = _capi.dg_iq_header()
+    check(lib.dg_read_iq_header(str(path).encode(), C.byref(h)))
+    buf = np.empty(h.sample_count, np.complex64)
+    check(lib.dg_read_iq(str(path).encode(), C.byref(h),
+                         buf.ctypes.data_as(C.POINTER(C.c_float)), h.sample_count))
+    return BasebandCapture(buf, h.sample_rate_hz, h.start_time_s, h.center_freq_hz)
 
 
 def _snapshots_struct(states, captures, fs, fc):
