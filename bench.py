@@ -193,12 +193,17 @@ def b200_arm(args, rank, world):
     from paper_2508_06672_b200 import sharding
     from paper_2508_06672_b200._capi import lib
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; (gloo test mode: ranks may share the box's GPUs)
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:  # gloo: the multi-rank path on one GPU (tests); collectives via the host
+            dist.init_process_group("gloo")
+    coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     cfg = WORKLOADS[args.config]
     states, caps, bounds, spacing = make_inputs(cfg, args.spacing_km)
     S, R, N = caps.shape
@@ -252,7 +257,7 @@ def b200_arm(args, rank, world):
     ms = [a.elapsed_time(b) for a, b in ev]
     ms_step = sum(ms) / len(ms)
     if dist is not None:
-        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms_step], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     value = P * S / (ms_step * 1e-3)
@@ -297,7 +302,7 @@ def b200_arm(args, rank, world):
             e2e_t.append(time.perf_counter() - t0)
     e2e_s = statistics.mean(e2e_t)
     if dist is not None:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": P * S / e2e_s, "unit": UNIT,
@@ -406,6 +411,8 @@ def main():
                     help="snapshots per reference-arm step")
     ap.add_argument("--cpu-sample-snapshots", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)
     ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.ref_worker:

@@ -56,6 +56,8 @@ def exchange_argmax(value: float, index: int, device="cpu", group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if _host_collectives(group):
+        device = "cpu"
     v = torch.tensor([value], dtype=torch.float64, device=device)
     i = torch.tensor([index], dtype=torch.int64, device=device)
     vs = [torch.empty_like(v) for _ in range(world)]
@@ -65,12 +67,22 @@ def exchange_argmax(value: float, index: int, device="cpu", group=None):
     return merge_argmax((float(a.item()), int(b.item())) for a, b in zip(vs, ix))
 
 
+def _host_collectives(group=None) -> bool:
+    """gloo moves CPU tensors only: device tensors take a host round trip (the
+    multi-process tests on one GPU); NCCL works on them in place."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
 def exchange_steps(local, n_snapshots: int, n_lat: int, n_lon: int, group=None):
     """All-to-all of per-snapshot surfaces: `local` is [s1-s0][n_lat*n_lon]
     (this rank's snapshots, full grid); returns [n_snapshots][slab] for this
     rank's latitude slab, snapshots in global order."""
     import torch
     import torch.distributed as dist
+
+    if local.is_cuda and _host_collectives(group):
+        return exchange_steps(local.cpu(), n_snapshots, n_lat, n_lon, group).to(local.device)
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     s0, s1 = step_range(n_snapshots, rank, world)
@@ -94,6 +106,8 @@ def gather_vector(local, sizes, group=None):
     import torch
     import torch.distributed as dist
 
+    if local.is_cuda and _host_collectives(group):
+        return gather_vector(local.cpu(), sizes, group).to(local.device)
     world = dist.get_world_size(group)
     m = max(max(sizes), 1)
     buf = torch.zeros(m, dtype=local.dtype, device=local.device)
