@@ -49,7 +49,7 @@ __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
 }
 
 // e^{i 2 pi x} for an FP64 cycle count: exact FP64 range reduction, FP32 sincospi
-__device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
+[[maybe_unused]] __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
     sincospif((float)(2.0 * (x - rint(x))), s, c);
 }
 
@@ -354,6 +354,18 @@ __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
     }
 }
 
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    float2 d;
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
 __device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {  // elementwise
     float2 d;
     asm("{.reg .b64 ra, rb, rc, rd;\n\t"
@@ -513,13 +525,14 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                         for (int q = 0; q < R / 2; ++q) mv[q] = mg[j * (R / 2) + q];
 #pragma unroll
                         for (int c = 0; c < kEvalNC; ++c) {
-                            // one chain, smallest terms first (the c_m decay with m)
-                            float2 C = make_float2(0.f, 0.f);
+                            // two chains (odd / even m), smallest terms first
+                            float2 Co = make_float2(0.f, 0.f), Ce = make_float2(0.f, 0.f);
 #pragma unroll
                             for (int q = R / 2 - 1; q >= 0; --q) {
-                                C = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], C);
-                                C = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], C);
+                                Co = ffma2(make_float2(mv[q].z, mv[q].w), cf[c][2 * q + 1], Co);
+                                Ce = ffma2(make_float2(mv[q].x, mv[q].y), cf[c][2 * q], Ce);
                             }
+                            const float2 C = add2(Ce, Co);
                             A[c] = ffma2(C, wtr[c][j], A[c]);
                             V[c] = ffma2(C, wti[c][j], V[c]);
                             E2[c] = ffma2v(C, C, E2[c]);
