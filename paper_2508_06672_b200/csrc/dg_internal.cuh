@@ -62,6 +62,7 @@ struct RxPairF32 {
 
 constexpr int kMaxMoments = 16;  // Chebyshev table width (moments per block <= 16)
 constexpr int kEvalG = 8;  // blocks per exact-phase group in k_evaluate (moment rows padded to it)
+__host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) / kEvalG * kEvalG; }
 
 // Geometry of one (snapshot, pair): receiver states for predict_pair_offsets.
 struct PairGeom {

@@ -29,31 +29,12 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "dg_device.cuh"
 #include "dg_internal.cuh"
 
 namespace dg {
 
 namespace {
-
-__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\t"
-        "mov.b64 rb, {%4, %4};\n\t"
-        "mov.b64 rc, {%5, %6};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
-        "mov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b), "f"(c.x), "f"(c.y));
-    return d;
-}
-
-// e^{i 2 pi x} for an FP64 cycle count: exact FP64 range reduction, FP32 sincospi
-[[maybe_unused]] __device__ __forceinline__ void cis_cycles(double x, float* c, float* s) {
-    sincospif((float)(2.0 * (x - rint(x))), s, c);
-}
-
-__host__ __device__ constexpr int pad_blocks(int nb) { return (nb + kEvalG - 1) / kEvalG * kEvalG; }
 
 constexpr int kEvalStages = 3;  // bucket-moment buffers in k_evaluate's TMA ring
 inline size_t evaluate_smem(int nbmax, int R) {
@@ -79,50 +60,6 @@ __global__ void k_center(const double2* __restrict__ y, const float2* __restrict
         const float2 w = y2[k];
         y2p[padf + k] = w;
     }
-}
-
-// TMA helpers (1-D bulk copy global -> shared, mbarrier completion)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
 }
 
 // Moments of all d-buckets, blocks aligned to ABSOLUTE sample index (block b
@@ -305,78 +242,6 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[buf]);
     }
-}
-
-// J_0..J_{R-1}(x) (first kind), FP64: series for J_{R-1}, J_R (fast: m >> x),
-// then the stable backward recurrence J_{m-1} = (2m/x) J_m - J_{m+1}.
-template <int R>
-__device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
-    const double ax = fabs(x);
-    if (ax < 1e-6) {
-#pragma unroll
-        for (int m = 0; m < R; ++m) j[m] = 0.0;
-        j[0] = 1.0 - 0.25 * x * x;
-        if (R > 1) j[1] = 0.5 * x;
-        return;
-    }
-    const double h = 0.5 * x, h2 = h * h;
-    // (x/2)^(R-1) / (R-1)!
-    double t = 1.0;
-#pragma unroll
-    for (int m = 1; m < R; ++m) t *= h * (1.0 / m);
-    double jr1 = 0.0, jr = 0.0;  // J_{R-1}, J_R
-    {
-        double term = t, s = t;
-#pragma unroll
-        for (int k = 1; k <= 12; ++k) {
-            term *= -h2 * (1.0 / (k * (R - 1 + k)));
-            s += term;
-        }
-        jr1 = s;
-        term = t * h * (1.0 / R);
-        s = term;
-#pragma unroll
-        for (int k = 1; k <= 12; ++k) {
-            term *= -h2 * (1.0 / (k * (R + k)));
-            s += term;
-        }
-        jr = s;
-    }
-    const double inv = 2.0 / x;
-    j[R - 1] = jr1;
-    double jp = jr, jc = jr1;
-#pragma unroll
-    for (int m = R - 1; m >= 1; --m) {
-        const double jm = fma((double)m * inv, jc, -jp);
-        jp = jc;
-        jc = jm;
-        j[m - 1] = jm;
-    }
-}
-
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\t"
-        "mov.b64 rb, {%4, %5};\n\t"
-        "add.rn.f32x2 rd, ra, rb;\n\t"
-        "mov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-
-__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {  // elementwise
-    float2 d;
-    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\t"
-        "mov.b64 rb, {%4, %5};\n\t"
-        "mov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
-        "mov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
 }
 
 constexpr int kEvalWarps = 4;
