@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 3
+#define DG_ABI_VERSION 4
 
 enum {
     DG_OK = 0,
@@ -216,6 +216,40 @@ int dg_read_iq(const char* path, dg_iq_header* out, float* iq_out, int64_t capac
  * pinned buffer and copied to HBM as float2 (exact) while the next file is read. */
 int dg_stage_snapshots_iq(dg_engine* engine, const char* const* paths, int64_t n_snapshots,
                           int64_t n_receivers, const dg_state* states, dg_staged** out);
+
+/* Surfaces and detections on disk (io.hpp:169-280), formatted on the device.
+ * `values` = grid size doubles, lat-major, in device memory when values_on_device
+ * (e.g. dg_result.accumulated_device), else host memory. Bytes are identical to
+ * the reference writers': CSV "%.17g,%.17g,%.17g\n" rows after the
+ * "lat_deg,lon_deg,value" header (write_grid csv, :174-183), DGGR binary
+ * (:187-202), 16-bit big-endian P5 with min->0, max->65535 and north on top
+ * (render_heatmap, :245-268). Errors: "cannot open <path> for writing",
+ * "write failed: <path>" (DG_ERUNTIME), as write_file_bytes (:114-119). */
+#define DG_GRID_CSV 0
+#define DG_GRID_BINARY 1
+int dg_write_grid(dg_engine* engine, const dg_grid* grid, const double* values,
+                  int values_on_device, const char* path, int format);
+int dg_render_heatmap(dg_engine* engine, const dg_grid* grid, const double* values,
+                      int values_on_device, const char* path);
+/* write_detections_csv (:270-280) */
+int dg_write_detections_csv(const dg_emitter_estimate* detections, int64_t n, const char* path);
+/* == GridAxis pair + altitude of a DGGR file / lattice (geodesy.hpp:140-168) */
+typedef struct {
+    double lat_start_deg, lat_step_deg;
+    int64_t lat_count;
+    double lon_start_deg, lon_step_deg;
+    int64_t lon_count;
+    double altitude_m;
+} dg_grid_axes;
+/* read_grid (:205-240): header checks and messages verbatim; `values` (nullable:
+ * header only) receives lat_count*lon_count doubles if capacity allows. */
+int dg_read_grid(const char* path, dg_grid_axes* axes, double* values, int64_t capacity);
+/* the eager ECEF lattice of explicit axes (the lattice read_grid rebuilds) */
+int dg_grid_from_axes(dg_engine* engine, const dg_grid_axes* axes, dg_grid** out);
+/* "%.17g" of n host doubles by the device formatter the CSV writer uses: 32-byte
+ * slots (not terminated) and lengths; for tests against the C library. */
+int dg_format_g17(dg_engine* engine, const double* values, int64_t n, char* slots,
+                  uint8_t* lengths);
 
 /* The two halves of geolocate_snapshots, for snapshot-sharded multi-GPU runs
  * (DESIGN.md section 7). dg_correlate_steps: snapshots [s_begin, s_end) over

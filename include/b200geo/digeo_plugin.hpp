@@ -7,6 +7,7 @@
 //   b200::B200Backend gpu;                            // a digeo::CorrelationBackend
 //   auto g = digeo::correlate_snapshot(grid, snap, {0, 1}, gpu);   // reference driver
 //   auto r = b200::geolocate_snapshots(snapshots, grid, options);  // whole path on GPU
+//   b200::write_grid(r.accumulated, "acc.csv", digeo::GridFileFormat::csv);  // io.hpp writers
 //
 // B200Backend replaces digeo::CorrelationBackend (backend.hpp:211-217) and its
 // sessions replace CorrelationSession::correlate_batch (backend.hpp:196-209);
@@ -27,6 +28,7 @@
 #include "b200geo.h"
 #include "digeo/backend.hpp"
 #include "digeo/geolocate.hpp"
+#include "digeo/io.hpp"
 
 namespace b200 {
 
@@ -181,6 +183,52 @@ inline digeo::GeolocateResult geolocate_snapshots(const std::vector<digeo::Snaps
         result.detections.push_back(e);
     }
     return result;
+}
+
+namespace detail {
+inline std::unique_ptr<dg_grid, void (*)(dg_grid*)> axes_grid(dg_engine* eng,
+                                                             const digeo::CorrelationGrid& g) {
+    g.validate();
+    const dg_grid_axes a{g.grid->lat.start_deg, g.grid->lat.step_deg,
+                         static_cast<int64_t>(g.grid->lat.count), g.grid->lon.start_deg,
+                         g.grid->lon.step_deg, static_cast<int64_t>(g.grid->lon.count),
+                         g.grid->altitude_m};
+    dg_grid* h = nullptr;
+    check(dg_grid_from_axes(eng, &a, &h));
+    return {h, dg_grid_destroy};
+}
+}  // namespace detail
+
+/// io.hpp:171-203 (write_grid) and :245-268 (render_heatmap): the same files,
+/// byte for byte, with the text / pixels produced on the GPU.
+inline void write_grid(const digeo::CorrelationGrid& grid, const std::filesystem::path& path,
+                       digeo::GridFileFormat format, const B200Backend* backend = nullptr) {
+    std::unique_ptr<B200Backend> own;
+    if (!backend) backend = (own = std::make_unique<B200Backend>()).get();
+    dg_engine* eng = backend->engine()->get();
+    auto g = detail::axes_grid(eng, grid);
+    check(dg_write_grid(eng, g.get(), grid.values.data(), 0, path.string().c_str(),
+                        format == digeo::GridFileFormat::csv ? DG_GRID_CSV : DG_GRID_BINARY));
+}
+
+inline void render_heatmap(const digeo::CorrelationGrid& grid, const std::filesystem::path& path,
+                           const B200Backend* backend = nullptr) {
+    std::unique_ptr<B200Backend> own;
+    if (!backend) backend = (own = std::make_unique<B200Backend>()).get();
+    dg_engine* eng = backend->engine()->get();
+    auto g = detail::axes_grid(eng, grid);
+    check(dg_render_heatmap(eng, g.get(), grid.values.data(), 0, path.string().c_str()));
+}
+
+/// io.hpp:270-280
+inline void write_detections_csv(std::span<const digeo::EmitterEstimate> detections,
+                                 const std::filesystem::path& path) {
+    std::vector<dg_emitter_estimate> d;
+    for (const auto& e : detections)
+        d.push_back({e.location.lat_deg, e.location.lon_deg, e.location.alt_m,
+                     static_cast<int64_t>(e.grid_index), e.score, e.score_zsigma});
+    check(dg_write_detections_csv(d.data(), static_cast<int64_t>(d.size()),
+                                  path.string().c_str()));
 }
 
 }  // namespace b200

@@ -107,6 +107,10 @@ class RefLib:
         L.ref_write_iq.argtypes = [C.c_char_p, _dp, C.c_int64, C.c_double, C.c_double,
                                    C.c_double]
         L.ref_read_iq.argtypes = [C.c_char_p, _dp, _dp, C.c_int64]
+        L.ref_write_grid.argtypes = [C.c_char_p, _dp, C.c_double, _dp, C.c_int]
+        L.ref_render_heatmap.argtypes = [C.c_char_p, _dp, C.c_double, _dp]
+        L.ref_write_detections_csv.argtypes = [C.c_char_p, _dp, C.c_int64]
+        L.ref_read_grid.argtypes = [C.c_char_p, _dp, _dp, _dp, C.c_int64]
 
     def _check(self, rc: int):
         if rc != 0:
@@ -127,6 +131,33 @@ class RefLib:
         self._check(self.lib.ref_read_iq(str(path).encode(), _d(info), out.ctypes.data_as(_dp),
                                          n))
         return out, info[0], info[1], info[2]
+
+    # -- surface / detection writers (io.hpp:171-280) -------------------------
+    @staticmethod
+    def _axes(axes):
+        """axes = (lat_start, lat_step, n_lat, lon_start, lon_step, n_lon)"""
+        return np.asarray(axes, np.float64)
+
+    def write_grid(self, path, axes, alt, values, csv: bool):
+        a, v = self._axes(axes), np.ascontiguousarray(values, np.float64)
+        self._check(self.lib.ref_write_grid(str(path).encode(), _d(a), alt, _d(v), int(csv)))
+
+    def render_heatmap(self, path, axes, alt, values):
+        a, v = self._axes(axes), np.ascontiguousarray(values, np.float64)
+        self._check(self.lib.ref_render_heatmap(str(path).encode(), _d(a), alt, _d(v)))
+
+    def write_detections_csv(self, path, rows):
+        """rows: (lat, lon, alt, grid_index, score, zsigma) per detection"""
+        d = np.ascontiguousarray(np.asarray(rows, np.float64).reshape(-1, 6))
+        self._check(self.lib.ref_write_detections_csv(str(path).encode(), _d(d), len(d)))
+
+    def read_grid(self, path):
+        """-> (axes6, alt, values)"""
+        a, alt = np.zeros(6), np.zeros(1)
+        self._check(self.lib.ref_read_grid(str(path).encode(), _d(a), _d(alt), None, 0))
+        v = np.zeros(int(a[2]) * int(a[5]))
+        self._check(self.lib.ref_read_grid(str(path).encode(), _d(a), _d(alt), _d(v), len(v)))
+        return a, float(alt[0]), v
 
     # -- scenes --------------------------------------------------------------
     def simulate(self, cfg_text: str) -> RefScene:

@@ -319,3 +319,63 @@ int ref_read_iq(const char* path, double* info4, double* iq, int64_t capacity) {
 }
 
 }  // extern "C"
+
+// --- surface / detection writers (io.hpp:171-280) --------------------------
+
+namespace {
+// axes6 = {lat_start, lat_step, n_lat, lon_start, lon_step, n_lon}
+CorrelationGrid make_surface(const double* axes6, double alt, const double* values) {
+    auto g = std::make_shared<CandidateGrid>();
+    g->lat = GridAxis{axes6[0], axes6[1], static_cast<std::size_t>(axes6[2])};
+    g->lon = GridAxis{axes6[3], axes6[4], static_cast<std::size_t>(axes6[5])};
+    g->altitude_m = alt;
+    return CorrelationGrid{g, std::vector<double>(values, values + g->size())};
+}
+}  // namespace
+
+extern "C" {
+
+int ref_write_grid(const char* path, const double* axes6, double alt, const double* values,
+                   int csv) {
+    REF_GUARD({
+        write_grid(make_surface(axes6, alt, values), path,
+                   csv ? GridFileFormat::csv : GridFileFormat::binary);
+    })
+}
+
+int ref_render_heatmap(const char* path, const double* axes6, double alt, const double* values) {
+    REF_GUARD({ render_heatmap(make_surface(axes6, alt, values), path); })
+}
+
+// det7 per detection: lat, lon, alt, grid_index, score, zsigma (index as double)
+int ref_write_detections_csv(const char* path, const double* det6, int64_t n) {
+    REF_GUARD({
+        std::vector<EmitterEstimate> d(static_cast<std::size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            const double* r = det6 + 6 * i;
+            d[i].location = GeodeticCoord{r[0], r[1], r[2]};
+            d[i].grid_index = static_cast<std::size_t>(r[3]);
+            d[i].score = r[4];
+            d[i].score_zsigma = r[5];
+        }
+        write_detections_csv(d, path);
+    })
+}
+
+// read_grid: axes6/alt/count first (values nullable), then the values
+int ref_read_grid(const char* path, double* axes6, double* alt, double* values, int64_t capacity) {
+    REF_GUARD({
+        const CorrelationGrid g = read_grid(path);
+        axes6[0] = g.grid->lat.start_deg;
+        axes6[1] = g.grid->lat.step_deg;
+        axes6[2] = static_cast<double>(g.grid->lat.count);
+        axes6[3] = g.grid->lon.start_deg;
+        axes6[4] = g.grid->lon.step_deg;
+        axes6[5] = static_cast<double>(g.grid->lon.count);
+        *alt = g.grid->altitude_m;
+        if (values && static_cast<int64_t>(g.values.size()) <= capacity)
+            std::memcpy(values, g.values.data(), g.values.size() * sizeof(double));
+    })
+}
+
+}  // extern "C"

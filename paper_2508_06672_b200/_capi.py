@@ -50,6 +50,13 @@ class dg_iq_header(C.Structure):
                 ("start_time_s", C.c_double), ("sample_count", C.c_int64)]
 
 
+class dg_grid_axes(C.Structure):
+    _fields_ = [("lat_start_deg", C.c_double), ("lat_step_deg", C.c_double),
+                ("lat_count", C.c_int64), ("lon_start_deg", C.c_double),
+                ("lon_step_deg", C.c_double), ("lon_count", C.c_int64),
+                ("altitude_m", C.c_double)]
+
+
 class dg_options(C.Structure):
     _fields_ = [("k_sigma", C.c_double), ("exclusion_radius_cells", C.c_int),
                 ("normalize_per_snapshot", C.c_int), ("detect", C.c_int),
@@ -88,7 +95,8 @@ EXPORTS = (
     "dg_correlate_snapshot", "dg_options_default", "dg_geolocate_snapshots",
     "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_correlate_steps",
     "dg_accumulate_peak", "dg_detect_emitters", "dg_read_iq_header", "dg_read_iq",
-    "dg_stage_snapshots_iq",
+    "dg_stage_snapshots_iq", "dg_write_grid", "dg_render_heatmap", "dg_write_detections_csv",
+    "dg_read_grid", "dg_grid_from_axes", "dg_format_g17",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -139,6 +147,12 @@ def _load():
         "dg_read_iq": [C.c_char_p, C.POINTER(dg_iq_header), C.POINTER(C.c_float), C.c_int64],
         "dg_stage_snapshots_iq": [_vp, C.POINTER(C.c_char_p), C.c_int64, C.c_int64,
                                   C.POINTER(dg_state), C.POINTER(_vp)],
+        "dg_write_grid": [_vp, _vp, _vp, C.c_int, C.c_char_p, C.c_int],
+        "dg_render_heatmap": [_vp, _vp, _vp, C.c_int, C.c_char_p],
+        "dg_write_detections_csv": [C.POINTER(dg_emitter_estimate), C.c_int64, C.c_char_p],
+        "dg_read_grid": [C.c_char_p, C.POINTER(dg_grid_axes), _dp, C.c_int64],
+        "dg_grid_from_axes": [_vp, C.POINTER(dg_grid_axes), C.POINTER(_vp)],
+        "dg_format_g17": [_vp, _dp, C.c_int64, C.c_char_p, C.POINTER(C.c_uint8)],
         "dg_fp32_peak_tflops": [C.c_int, _dp],
         "dg_fp32x2_peak_tflops": [C.c_int, _dp],
         "dg_fp64_peak_tflops": [C.c_int, _dp],

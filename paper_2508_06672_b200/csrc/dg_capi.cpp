@@ -18,104 +18,17 @@
 #include <vector>
 
 #include "b200geo.h"
+#include "dg_host.hpp"
 #include "dg_internal.cuh"
 
 using namespace dg;
 
-namespace {
-
-thread_local std::string g_err;
-
-struct DgError {
-    int code;
-    std::string msg;
-};
-
-[[noreturn]] void raise(int code, const std::string& msg) { throw DgError{code, msg}; }
-
-#define CK(x)                                                                              \
-    do {                                                                                   \
-        cudaError_t e_ = (x);                                                              \
-        if (e_ != cudaSuccess)                                                             \
-            raise(e_ == cudaErrorMemoryAllocation ? DG_ENOMEM : DG_ERUNTIME,               \
-                  std::string(#x) + ": " + cudaGetErrorString(e_));                        \
-    } while (0)
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return DG_OK;
-    } catch (const DgError& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host out of memory";
-        return DG_ENOMEM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return DG_ERUNTIME;
-    }
+std::string& dg::last_error() {
+    thread_local std::string s;
+    return s;
 }
 
-// owning device allocation for objects that outlive a call (staged captures,
-// lattices): taken from the device's stream-ordered pool, which keeps freed
-// memory mapped (release threshold set at engine creation), so re-staging a
-// run every call costs no cudaMalloc/cudaFree device synchronisation.
-struct DevMem {
-    void* p = nullptr;
-    size_t bytes = 0;
-    explicit DevMem(size_t n) : bytes(n) {
-        if (n) {
-            CK(cudaMallocAsync(&p, n, cudaStreamPerThread));
-            CK(cudaStreamSynchronize(cudaStreamPerThread));
-        }
-    }
-    ~DevMem() {
-        if (p) cudaFreeAsync(p, cudaStreamPerThread);
-    }
-    DevMem(const DevMem&) = delete;
-    DevMem& operator=(const DevMem&) = delete;
-};
-
-// stream-ordered scratch for one call
-struct Scratch {
-    cudaStream_t st;
-    std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t s) : st(s) {}
-    template <class T>
-    T* alloc(size_t n) {
-        void* p = nullptr;
-        if (n == 0) n = 1;
-        CK(cudaMallocAsync(&p, n * sizeof(T), st));
-        ptrs.push_back(p);
-        return static_cast<T*>(p);
-    }
-    ~Scratch() {
-        for (void* p : ptrs) cudaFreeAsync(p, st);
-    }
-};
-
-// the caller's stream, else the engine's persistent stream (a fresh stream per
-// call would defeat the stream-ordered memory pool's reuse), else a private one
-struct StreamGuard {
-    cudaStream_t st = nullptr;
-    bool own = false;
-    explicit StreamGuard(void* user, cudaStream_t fallback = nullptr) {
-        if (user) {
-            st = static_cast<cudaStream_t>(user);
-        } else if (fallback) {
-            st = fallback;
-        } else {
-            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-            own = true;
-        }
-    }
-    ~StreamGuard() {
-        if (own) cudaStreamDestroy(st);
-    }
-};
-
+namespace {
 
 // geodesy.hpp:31-38
 constexpr double kA = 6378137.0;
@@ -136,31 +49,6 @@ void validate_geodetic(double lat, double lon, double alt) {
 }
 
 }  // namespace
-
-// ===========================================================================
-struct dg_engine {
-    int device = 0;
-    int sm_count = 148;
-    cudaStream_t stream = nullptr;  // default stream of calls that pass none
-    ~dg_engine() {
-        if (stream) cudaStreamDestroy(stream);
-    }
-};
-
-struct dg_grid {
-    dg_engine* eng = nullptr;
-    double lat_start = 0, lat_step = 0, lon_start = 0, lon_step = 0, alt = 0;
-    int64_t n_lat = 0, n_lon = 0, row_offset = 0;
-    std::shared_ptr<DevMem> mem;  // x | y | z of the full lattice
-    const double *x = nullptr, *y = nullptr, *z = nullptr;
-    // the FULL lattice (shared by every slab): FP32 positions relative to its
-    // centre, for partition-independent correlator planning
-    std::shared_ptr<DevMem> rel;
-    int64_t full_size = 0;
-    double cx = 0, cy = 0, cz = 0;
-    int64_t size() const { return n_lat * n_lon; }
-    const float4* rel32() const { return static_cast<const float4*>(rel->p); }
-};
 
 struct dg_session {
     dg_engine* eng = nullptr;
@@ -184,7 +72,6 @@ struct dg_staged {
 
 namespace {
 
-void set_device(const dg_engine* e) { CK(cudaSetDevice(e->device)); }
 
 // ---------------------------------------------------------------------------
 // Correlator planning. A (snapshot, pair) "step" runs either the block-moment
@@ -743,7 +630,7 @@ double fp32_fdoa_margin(const PairGeom* pg, int n, double wl) {
 // ===========================================================================
 extern "C" {
 
-const char* dg_last_error(void) { return g_err.c_str(); }
+const char* dg_last_error(void) { return last_error().c_str(); }
 int dg_abi_version(void) { return DG_ABI_VERSION; }
 
 void dg_options_default(dg_options* o) {
@@ -866,6 +753,60 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
 }
 
 // ---- grids -----------------------------------------------------------------
+}  // extern "C"
+namespace {
+// The eager ECEF lattice of GridAxis pairs (geodesy.hpp:151-168, lla_to_ecef
+// :82-92 per lattice_coord): per-row / per-column libm trig on the host, the
+// products on the device (launch_grid_ecef), then the FP32 planning copy.
+std::unique_ptr<dg_grid> make_lattice(dg_engine* eng, double lat_start, double lat_step,
+                                      int64_t n_lat, double lon_start, double lon_step,
+                                      int64_t n_lon, double alt) {
+    const int64_t n = n_lat * n_lon;
+    std::vector<double> ra(n_lat), rz(n_lat), cc(n_lon), cs(n_lon);
+    for (int64_t i = 0; i < n_lat; ++i) {
+        const double lat = deg2rad(lat_start + static_cast<double>(i) * lat_step);
+        const double slat = std::sin(lat), clat = std::cos(lat);
+        const double nn = kA / std::sqrt(1.0 - kE2 * slat * slat);
+        ra[i] = (nn + alt) * clat;
+        rz[i] = (nn * (1.0 - kE2) + alt) * slat;
+    }
+    for (int64_t j = 0; j < n_lon; ++j) {
+        const double lon = deg2rad(lon_start + static_cast<double>(j) * lon_step);
+        cc[j] = std::cos(lon);
+        cs[j] = std::sin(lon);
+    }
+    set_device(eng);
+    auto g = std::make_unique<dg_grid>();
+    g->eng = eng;
+    g->lat_start = lat_start;
+    g->lon_start = lon_start;
+    g->lat_step = lat_step;
+    g->lon_step = lon_step;
+    g->alt = alt;
+    g->n_lat = n_lat;
+    g->n_lon = n_lon;
+    g->mem = std::make_shared<DevMem>(3 * n * sizeof(double));
+    double* base = static_cast<double*>(g->mem->p);
+    g->x = base;
+    g->y = base + n;
+    g->z = base + 2 * n;
+    StreamGuard sg(nullptr, eng->stream);
+    Scratch sc(sg.st);
+    double* t = sc.alloc<double>(2 * n_lat + 2 * n_lon);
+    CK(cudaMemcpyAsync(t, ra.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
+    CK(cudaMemcpyAsync(t + n_lat, rz.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
+    CK(cudaMemcpyAsync(t + 2 * n_lat, cc.data(), n_lon * 8, cudaMemcpyHostToDevice, sg.st));
+    CK(cudaMemcpyAsync(t + 2 * n_lat + n_lon, cs.data(), n_lon * 8, cudaMemcpyHostToDevice, sg.st));
+    launch_grid_ecef(t, t + n_lat, t + 2 * n_lat, t + 2 * n_lat + n_lon, n_lat, n_lon, base,
+                     base + n, base + 2 * n, sg.st);
+    CK(cudaGetLastError());
+    finish_lattice(g.get(), sg.st);
+    return g;
+}
+
+}  // namespace
+extern "C" {
+
 int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double spacing, double alt,
                             uint64_t cap, dg_grid** out) {
     return guard([&] {
@@ -887,8 +828,7 @@ int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double sp
         if ((uint64_t)n > cap)
             raise(DG_EINVAL, "build_candidate_grid: " + std::to_string(n) +
                                  " points exceed cap of " + std::to_string(cap));
-        // per-row / per-column libm trig, validated in the reference's loop order
-        std::vector<double> ra(n_lat), rz(n_lat), cc(n_lon), cs(n_lon);
+        // validated in the reference's loop order
         for (int64_t i = 0; i < n_lat; ++i) {
             const double lat_deg = b->lat_min_deg + static_cast<double>(i) * spacing;
             if (!(lat_deg >= -90.0 && lat_deg <= 90.0))
@@ -898,44 +838,9 @@ int dg_build_candidate_grid(dg_engine* eng, const dg_latlon_bounds* b, double sp
                     const double lon_deg = b->lon_min_deg + static_cast<double>(j) * spacing;
                     validate_geodetic(lat_deg, lon_deg, alt);
                 }
-            // lla_to_ecef (geodesy.hpp:82-92), the lat-dependent factors
-            const double lat = deg2rad(lat_deg);
-            const double slat = std::sin(lat), clat = std::cos(lat);
-            const double nn = kA / std::sqrt(1.0 - kE2 * slat * slat);
-            ra[i] = (nn + alt) * clat;
-            rz[i] = (nn * (1.0 - kE2) + alt) * slat;
         }
-        for (int64_t j = 0; j < n_lon; ++j) {
-            const double lon = deg2rad(b->lon_min_deg + static_cast<double>(j) * spacing);
-            cc[j] = std::cos(lon);
-            cs[j] = std::sin(lon);
-        }
-        set_device(eng);
-        auto g = std::make_unique<dg_grid>();
-        g->eng = eng;
-        g->lat_start = b->lat_min_deg;
-        g->lon_start = b->lon_min_deg;
-        g->lat_step = g->lon_step = spacing;
-        g->alt = alt;
-        g->n_lat = n_lat;
-        g->n_lon = n_lon;
-        g->mem = std::make_shared<DevMem>(3 * n * sizeof(double));
-        double* base = static_cast<double*>(g->mem->p);
-        g->x = base;
-        g->y = base + n;
-        g->z = base + 2 * n;
-        StreamGuard sg(nullptr, eng->stream);
-        Scratch sc(sg.st);
-        double* t = sc.alloc<double>(2 * n_lat + 2 * n_lon);
-        CK(cudaMemcpyAsync(t, ra.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
-        CK(cudaMemcpyAsync(t + n_lat, rz.data(), n_lat * 8, cudaMemcpyHostToDevice, sg.st));
-        CK(cudaMemcpyAsync(t + 2 * n_lat, cc.data(), n_lon * 8, cudaMemcpyHostToDevice, sg.st));
-        CK(cudaMemcpyAsync(t + 2 * n_lat + n_lon, cs.data(), n_lon * 8, cudaMemcpyHostToDevice,
-                           sg.st));
-        launch_grid_ecef(t, t + n_lat, t + 2 * n_lat, t + 2 * n_lat + n_lon, n_lat, n_lon, base,
-                         base + n, base + 2 * n, sg.st);
-        CK(cudaGetLastError());
-        finish_lattice(g.get(), sg.st);
+        auto g = make_lattice(eng, b->lat_min_deg, spacing, n_lat, b->lon_min_deg, spacing, n_lon,
+                              alt);
         *out = g.release();
     });
 }
@@ -951,6 +856,16 @@ int dg_grid_slab(const dg_grid* g, int64_t r0, int64_t r1, dg_grid** out) {
         s->y = g->y + r0 * g->n_lon;
         s->z = g->z + r0 * g->n_lon;
         *out = s.release();
+    });
+}
+
+int dg_grid_from_axes(dg_engine* eng, const dg_grid_axes* a, dg_grid** out) {
+    return guard([&] {
+        if (!eng || !a || !out) raise(DG_EINVAL, "null argument");
+        if (a->lat_count <= 0 || a->lon_count <= 0) raise(DG_EINVAL, "dg_grid_from_axes: empty axis");
+        *out = make_lattice(eng, a->lat_start_deg, a->lat_step_deg, a->lat_count,
+                            a->lon_start_deg, a->lon_step_deg, a->lon_count, a->altitude_m)
+                   .release();
     });
 }
 
@@ -1732,7 +1647,7 @@ int dg_geolocate_snapshots(dg_engine* eng, const dg_grid* g, const dg_snapshots*
     return guard([&] {
         dg_staged* staged = nullptr;
         const int rc = dg_stage_snapshots(eng, sn, &staged);
-        if (rc != DG_OK) raise(rc, g_err);
+        if (rc != DG_OK) raise(rc, last_error());
         std::unique_ptr<dg_staged> hold(staged);
         geolocate_impl(eng, g, staged, opt, res);
     });

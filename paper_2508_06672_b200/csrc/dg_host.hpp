@@ -1,0 +1,145 @@
+// Host-side plumbing shared by the C ABI translation units (dg_capi.cpp,
+// dg_io.cpp): error codes -> thread-local message, stream-ordered device
+// memory, the engine and lattice handles. Internal; not installed.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "b200geo.h"
+
+namespace dg {
+
+std::string& last_error();  // thread-local (dg_capi.cpp)
+
+struct DgError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw DgError{code, msg}; }
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            ::dg::raise(e_ == cudaErrorMemoryAllocation ? DG_ENOMEM : DG_ERUNTIME,         \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return DG_OK;
+    } catch (const DgError& e) {
+        last_error() = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        last_error() = "host out of memory";
+        return DG_ENOMEM;
+    } catch (const std::exception& e) {
+        last_error() = e.what();
+        return DG_ERUNTIME;
+    }
+}
+
+// owning device allocation for objects that outlive a call (staged captures,
+// lattices): taken from the device's stream-ordered pool, which keeps freed
+// memory mapped (release threshold set at engine creation), so re-staging a
+// run every call costs no cudaMalloc/cudaFree device synchronisation.
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    explicit DevMem(size_t n) : bytes(n) {
+        if (n) {
+            CK(cudaMallocAsync(&p, n, cudaStreamPerThread));
+            CK(cudaStreamSynchronize(cudaStreamPerThread));
+        }
+    }
+    ~DevMem() {
+        if (p) cudaFreeAsync(p, cudaStreamPerThread);
+    }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+};
+
+// stream-ordered scratch for one call
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    template <class T>
+    T* alloc(size_t n) {
+        void* p = nullptr;
+        if (n == 0) n = 1;
+        CK(cudaMallocAsync(&p, n * sizeof(T), st));
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+// the caller's stream, else the engine's persistent stream (a fresh stream per
+// call would defeat the stream-ordered memory pool's reuse), else a private one
+struct StreamGuard {
+    cudaStream_t st = nullptr;
+    bool own = false;
+    explicit StreamGuard(void* user, cudaStream_t fallback = nullptr) {
+        if (user) {
+            st = static_cast<cudaStream_t>(user);
+        } else if (fallback) {
+            st = fallback;
+        } else {
+            CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            own = true;
+        }
+    }
+    ~StreamGuard() {
+        if (own) cudaStreamDestroy(st);
+    }
+};
+
+}  // namespace dg
+
+struct dg_engine {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;  // default stream of calls that pass none
+    // pinned double buffer of the file writers (dg_io.cpp), kept across calls
+    std::mutex stage_mu;
+    void* stage_host[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    ~dg_engine() {
+        for (void* p : stage_host)
+            if (p) cudaFreeHost(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+struct dg_grid {
+    dg_engine* eng = nullptr;
+    double lat_start = 0, lat_step = 0, lon_start = 0, lon_step = 0, alt = 0;
+    int64_t n_lat = 0, n_lon = 0, row_offset = 0;
+    std::shared_ptr<dg::DevMem> mem;  // x | y | z of the full lattice
+    const double *x = nullptr, *y = nullptr, *z = nullptr;
+    // the FULL lattice (shared by every slab): FP32 positions relative to its
+    // centre, for partition-independent correlator planning
+    std::shared_ptr<dg::DevMem> rel;
+    int64_t full_size = 0;
+    double cx = 0, cy = 0, cz = 0;
+    int64_t size() const { return n_lat * n_lon; }
+    const float4* rel32() const { return static_cast<const float4*>(rel->p); }
+};
+
+namespace dg {
+inline void set_device(const dg_engine* e) { CK(cudaSetDevice(e->device)); }
+}  // namespace dg

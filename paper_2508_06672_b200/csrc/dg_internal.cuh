@@ -148,6 +148,26 @@ void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* qu
                      uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
                      cudaStream_t st);
 
+// surface writers (dg_writers.cu): "%.17g" text in kFmtSlot-byte slots, CSV rows
+// at scanned offsets, P5 pixels
+constexpr int kFmtSlot = 32;
+// axis text of values start + (first + i) * step, i < count (GridAxis::value)
+void launch_format_axis(double start, double step, int64_t first, int64_t count, char* slots,
+                        uint8_t* len, cudaStream_t st);
+void launch_format_values(const double* v, int64_t n, char* slots, uint8_t* len, cudaStream_t st);
+size_t csv_scan_temp_bytes(int64_t n);
+// row_end = inclusive scan of the row lengths (the CSV body is row_end[n-1] bytes)
+void launch_csv_offsets(const uint8_t* lat_len, const uint8_t* lon_len, const uint8_t* val_len,
+                        int64_t n_lat, int64_t n_lon, int64_t* row_len, int64_t* row_end,
+                        void* temp, size_t temp_bytes, cudaStream_t st);
+void launch_csv_emit(const char* lat_s, const uint8_t* lat_len, const char* lon_s,
+                     const uint8_t* lon_len, const char* val_s, const uint8_t* val_len,
+                     const int64_t* row_end, int64_t n_lat, int64_t n_lon, char* out,
+                     cudaStream_t st);
+void launch_minmax(const double* v, int64_t n, double2* part, double2* out, cudaStream_t st);
+void launch_heatmap(const double* v, int64_t n_lat, int64_t n_lon, double lo, double scale,
+                    uint8_t* out, cudaStream_t st);
+
 // exact FP64 reference-order re-evaluation of flagged elements
 // elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,

@@ -151,3 +151,15 @@ def grid_from_points(points: np.ndarray, lat: GridAxis, lon: GridAxis, altitude_
         eng.handle, pts.ctypes.data_as(C.POINTER(_capi.dg_ecef)), len(pts), lat.start_deg,
         lat.step_deg, lat.count, lon.start_deg, lon.step_deg, lon.count, altitude_m, C.byref(h)))
     return CandidateGrid(h, eng)
+
+
+def grid_from_axes(lat: GridAxis, lon: GridAxis, altitude_m: float = 0.0,
+                   engine: Engine | None = None) -> CandidateGrid:
+    """The eager lattice of explicit axes (as read_grid rebuilds it, io.hpp:229-232),
+    built on the GPU like build_candidate_grid."""
+    eng = engine or default_engine()
+    a = _capi.dg_grid_axes(lat.start_deg, lat.step_deg, lat.count, lon.start_deg, lon.step_deg,
+                           lon.count, altitude_m)
+    h = C.c_void_p()
+    check(lib.dg_grid_from_axes(eng.handle, C.byref(a), C.byref(h)))
+    return CandidateGrid(h, eng)

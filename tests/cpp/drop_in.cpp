@@ -7,6 +7,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <random>
 #include <sstream>
 #include <string>
@@ -15,6 +18,7 @@
 #include "b200geo/digeo_plugin.hpp"
 #include "digeo/config.hpp"
 #include "digeo/geolocate.hpp"
+#include "digeo/io.hpp"
 #include "digeo/scene.hpp"
 
 using namespace digeo;
@@ -125,5 +129,26 @@ int main(int argc, char** argv) {
     for (std::size_t s = 0; s < ref.per_snapshot.size(); ++s)
         w = std::max(w, worst_rel(b2.per_snapshot[s].values, ref.per_snapshot[s].values));
     check(w <= 1e-4, "per-snapshot grids within 1e-4 (worst " + std::to_string(w) + ")");
+
+    // the reference's accumulated surface through both writer sets (io.hpp:171-280)
+    const auto tmp = std::filesystem::temp_directory_path();
+    const auto slurp = [](const std::filesystem::path& p) {
+        std::ifstream in(p, std::ios::binary);
+        return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    };
+    write_grid(ref.accumulated, tmp / "dg_ref.csv", GridFileFormat::csv);
+    b200::write_grid(ref.accumulated, tmp / "dg_b2.csv", GridFileFormat::csv, &gpu);
+    check(slurp(tmp / "dg_ref.csv") == slurp(tmp / "dg_b2.csv"), "write_grid csv byte-identical");
+    write_grid(ref.accumulated, tmp / "dg_ref.dggr", GridFileFormat::binary);
+    b200::write_grid(ref.accumulated, tmp / "dg_b2.dggr", GridFileFormat::binary, &gpu);
+    check(slurp(tmp / "dg_ref.dggr") == slurp(tmp / "dg_b2.dggr"),
+          "write_grid binary byte-identical");
+    render_heatmap(ref.accumulated, tmp / "dg_ref.pgm");
+    b200::render_heatmap(ref.accumulated, tmp / "dg_b2.pgm", &gpu);
+    check(slurp(tmp / "dg_ref.pgm") == slurp(tmp / "dg_b2.pgm"), "render_heatmap byte-identical");
+    write_detections_csv(ref.detections, tmp / "dg_ref_det.csv");
+    b200::write_detections_csv(ref.detections, tmp / "dg_b2_det.csv");
+    check(slurp(tmp / "dg_ref_det.csv") == slurp(tmp / "dg_b2_det.csv"),
+          "write_detections_csv byte-identical");
     return failures;
 }
