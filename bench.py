@@ -40,7 +40,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 WORKLOADS = {
-    # name: (half-span km, snapshots, samples, fs, emitters-kind, snr dB, seed)
+    # summary of each workload; the scene itself (receivers, emitters, seeds) is
+    # tests/scenes.config(name), the reference's simulate_scenario inputs
     "C1": dict(half_km=50.0, snapshots=1, samples=250_000, fs=5e6, emitters="tone", snr=-5.0,
                seed=1),
     "C2": dict(half_km=250.0, snapshots=10, samples=50_000, fs=5e6, emitters="chirp", snr=-10.0,
@@ -56,15 +57,28 @@ UNIT = "correlations/s"
 FLOP_PER_SAMPLE = 20.0  # correlate.hpp:60-68 as executed
 
 
-def make_inputs(cfg: dict, spacing_km: float = 1.0, n_snapshots: int | None = None):
-    from paper_2508_06672_b200 import scene
-    em = {"four": scene.FOUR_EMITTERS, "tone": [("tone", 0.0, 0.0, {})],
-          "chirp": [("chirp", 0.0, 0.0, {})]}[cfg["emitters"]]
-    S = n_snapshots or cfg["snapshots"]
-    states, caps = scene.synthesize(S, cfg["samples"], cfg["fs"], em, cfg["snr"], seed=cfg["seed"])
-    h = cfg["half_km"] * scene.KM_DEG
-    bounds = (-h, h, -h, h)
-    return states, caps, bounds, spacing_km * scene.KM_DEG
+def make_inputs(name: str, spacing_km: float = 1.0, n_snapshots: int | None = None,
+                reference: bool = False):
+    """The SURVEY.md §8d inputs of a workload: the reference's simulate_scenario
+    scene (paper_scenario.cfg receivers and emitters, tests/scenes.py), either
+    synthesised on the GPU by the engine's simulator (scenario values bit for
+    bit, samples within ~1e-15 of the reference's; tests/test_simulate.py) or,
+    for the reference arm, by the reference itself on the CPU.
+    -> (states [S,R,6], captures [S,R,N] complex128, bounds, spacing_deg)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import scenes
+    scene = scenes.config(name, spacing_km)
+    if n_snapshots:
+        scene["snapshots"] = n_snapshots
+    bounds = (scene["grid_lat_min_deg"], scene["grid_lat_max_deg"], scene["grid_lon_min_deg"],
+              scene["grid_lon_max_deg"])
+    if reference:
+        from oracle.bindings import RefLib
+        sc = RefLib().simulate(scenes.render(scene))
+        return sc.states, sc.captures, bounds, scene["grid_spacing_deg"]
+    import paper_2508_06672_b200.simulate as sim
+    states, caps, _, _ = sim.simulate_arrays(scenes.to_scenario(sim, scene))
+    return states, caps, bounds, scene["grid_spacing_deg"]
 
 
 class ClockSampler:
@@ -121,7 +135,8 @@ def ref_worker(args):
     from oracle.bindings import RefLib
     ref = RefLib()
     cfg = WORKLOADS[args.config]
-    states, caps, bounds, spacing = make_inputs(cfg, args.sample_km, args.sample_snapshots)
+    states, caps, bounds, spacing = make_inputs(args.config, args.sample_km,
+                                                args.sample_snapshots, reference=True)
     workers = os.cpu_count() or 1
     times = []
     for _ in range(args.warmup + args.steps):
@@ -205,7 +220,7 @@ def b200_arm(args, rank, world):
             dist.init_process_group("gloo")
     coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     cfg = WORKLOADS[args.config]
-    states, caps, bounds, spacing = make_inputs(cfg, args.spacing_km)
+    states, caps, bounds, spacing = make_inputs(args.config, args.spacing_km)
     S, R, N = caps.shape
     eng = b2.default_engine(dev)
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing, 0.0, engine=eng)
@@ -330,8 +345,9 @@ def b200_arm(args, rank, world):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (paper_2508_06672_b200.scene: 4 emitters, LEO receiver pair, "
-                    "complex Gaussian noise)",
+            "data": "synthetic: the reference's simulate_scenario scene for the workload "
+                    "(SURVEY §8d; paper_scenario.cfg receivers/emitters), synthesised on the GPU "
+                    "by paper_2508_06672_b200.simulate",
             "config": {"workload": args.config, "grid": f"{grid.lat.count}x{grid.lon.count}",
                        "points": P, "snapshots": S, "samples": N,
                        "spacing_km": args.spacing_km,

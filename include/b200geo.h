@@ -251,6 +251,53 @@ int dg_grid_from_axes(dg_engine* engine, const dg_grid_axes* axes, dg_grid** out
 int dg_format_g17(dg_engine* engine, const double* values, int64_t n, char* slots,
                   uint8_t* lengths);
 
+/* Capture synthesis on the device: the reference's simulate_scenario
+ * (scene.hpp:200-310) with its waveforms (waveform.hpp:124-204), FFT fractional
+ * delay (scene.hpp:161-191) and seeded noise (scene.hpp:124-147). Scenario
+ * arithmetic (epochs, orbits, geometry, delays, amplitudes, seeds) is the
+ * reference's, bit for bit; per-sample values agree to FP64 rounding (device
+ * cos/sin/log and FFT rounding; MT19937-64 integers exact). Captures land in HBM
+ * as a dg_staged run ready for dg_geolocate_staged. */
+#define DG_WAVE_SPOOFER 0
+#define DG_WAVE_TONE 1
+#define DG_WAVE_CHIRP 2
+#define DG_WAVE_SAWTOOTH 3
+/* == digeo::EmitterDef with its WaveformSpec (scene.hpp:46-60, waveform.hpp:58-97) */
+typedef struct {
+    double lat_deg, lon_deg, alt_m;
+    int waveform;               /* DG_WAVE_* */
+    int prn;                    /* spoofer: 1..32 */
+    uint64_t data_seed;         /* spoofer nav bits */
+    double tone_offset_hz;      /* tone */
+    double bandwidth_hz;        /* chirp / sawtooth */
+    double period_s;            /* chirp period / sawtooth chirp period */
+    double ref_snr_db, ref_range_m;
+} dg_emitter_def;
+/* == digeo::ReceiverDef: a CircularOrbit (orbit.hpp:30-35) unless `states`
+ * (snapshot_count explicit states) is non-null */
+typedef struct {
+    double alt_m, inclination_deg, raan_deg, phase_deg;
+    const dg_state* states;
+} dg_receiver_def;
+/* == digeo::Scenario (scene.hpp:72-110) without the grid */
+typedef struct {
+    const dg_receiver_def* receivers;
+    int64_t n_receivers;
+    const dg_emitter_def* emitters;
+    int64_t n_emitters;
+    int64_t snapshot_count;
+    double snapshot_spacing_s, capture_duration_s, sample_rate_hz, center_freq_hz, start_time_s;
+    uint64_t noise_seed;
+    double noise_power;
+} dg_scenario;
+/* samples per capture, llround(duration * fs) (scene.hpp:112-114) */
+int dg_scenario_samples(const dg_scenario* scenario, int64_t* n_samples);
+/* staged_out (nullable) receives the run in HBM; captures_host (nullable) the
+ * [S][R][N] complex double captures, states_host [S][R] and epochs_host [S]
+ * (nullable) the snapshot states and epochs. */
+int dg_simulate_scenario(dg_engine* engine, const dg_scenario* scenario, dg_staged** staged_out,
+                         double* captures_host, dg_state* states_host, double* epochs_host);
+
 /* The two halves of geolocate_snapshots, for snapshot-sharded multi-GPU runs
  * (DESIGN.md section 7). dg_correlate_steps: snapshots [s_begin, s_end) over
  * the whole grid — correlate_snapshot_all_pairs (geolocate.hpp:79-94) and the

@@ -57,6 +57,27 @@ class dg_grid_axes(C.Structure):
                 ("altitude_m", C.c_double)]
 
 
+class dg_emitter_def(C.Structure):
+    _fields_ = [("lat_deg", C.c_double), ("lon_deg", C.c_double), ("alt_m", C.c_double),
+                ("waveform", C.c_int), ("prn", C.c_int), ("data_seed", C.c_uint64),
+                ("tone_offset_hz", C.c_double), ("bandwidth_hz", C.c_double),
+                ("period_s", C.c_double), ("ref_snr_db", C.c_double), ("ref_range_m", C.c_double)]
+
+
+class dg_receiver_def(C.Structure):
+    _fields_ = [("alt_m", C.c_double), ("inclination_deg", C.c_double), ("raan_deg", C.c_double),
+                ("phase_deg", C.c_double), ("states", C.POINTER(dg_state))]
+
+
+class dg_scenario(C.Structure):
+    _fields_ = [("receivers", C.POINTER(dg_receiver_def)), ("n_receivers", C.c_int64),
+                ("emitters", C.POINTER(dg_emitter_def)), ("n_emitters", C.c_int64),
+                ("snapshot_count", C.c_int64), ("snapshot_spacing_s", C.c_double),
+                ("capture_duration_s", C.c_double), ("sample_rate_hz", C.c_double),
+                ("center_freq_hz", C.c_double), ("start_time_s", C.c_double),
+                ("noise_seed", C.c_uint64), ("noise_power", C.c_double)]
+
+
 class dg_options(C.Structure):
     _fields_ = [("k_sigma", C.c_double), ("exclusion_radius_cells", C.c_int),
                 ("normalize_per_snapshot", C.c_int), ("detect", C.c_int),
@@ -96,7 +117,8 @@ EXPORTS = (
     "dg_stage_snapshots", "dg_geolocate_staged", "dg_staged_destroy", "dg_correlate_steps",
     "dg_accumulate_peak", "dg_detect_emitters", "dg_read_iq_header", "dg_read_iq",
     "dg_stage_snapshots_iq", "dg_write_grid", "dg_render_heatmap", "dg_write_detections_csv",
-    "dg_read_grid", "dg_grid_from_axes", "dg_format_g17",
+    "dg_read_grid", "dg_grid_from_axes", "dg_format_g17", "dg_scenario_samples",
+    "dg_simulate_scenario",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -153,6 +175,9 @@ def _load():
         "dg_read_grid": [C.c_char_p, C.POINTER(dg_grid_axes), _dp, C.c_int64],
         "dg_grid_from_axes": [_vp, C.POINTER(dg_grid_axes), C.POINTER(_vp)],
         "dg_format_g17": [_vp, _dp, C.c_int64, C.c_char_p, C.POINTER(C.c_uint8)],
+        "dg_scenario_samples": [C.POINTER(dg_scenario), _i64p],
+        "dg_simulate_scenario": [_vp, C.POINTER(dg_scenario), C.POINTER(_vp), _dp,
+                                 C.POINTER(dg_state), _dp],
         "dg_fp32_peak_tflops": [C.c_int, _dp],
         "dg_fp32x2_peak_tflops": [C.c_int, _dp],
         "dg_fp64_peak_tflops": [C.c_int, _dp],

@@ -62,13 +62,6 @@ struct dg_session {
     }
 };
 
-struct dg_staged {
-    dg_engine* eng = nullptr;
-    int64_t S = 0, R = 0, N = 0, stride = 0;
-    double fs = 0, fc = 0;
-    std::unique_ptr<DevMem> y32, y64;
-    std::vector<dg_state> states;
-};
 
 namespace {
 

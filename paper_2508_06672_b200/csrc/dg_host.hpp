@@ -140,6 +140,17 @@ struct dg_grid {
     const float4* rel32() const { return static_cast<const float4*>(rel->p); }
 };
 
+// captures of a run resident in HBM: [S][R] rows of `stride` elements, data
+// kCapturePad elements in (dg_internal.cuh), FP32 for the correlator, FP64 for
+// centring / refinement
+struct dg_staged {
+    dg_engine* eng = nullptr;
+    int64_t S = 0, R = 0, N = 0, stride = 0;
+    double fs = 0, fc = 0;
+    std::unique_ptr<dg::DevMem> y32, y64;
+    std::vector<dg_state> states;
+};
+
 namespace dg {
 inline void set_device(const dg_engine* e) { CK(cudaSetDevice(e->device)); }
 }  // namespace dg

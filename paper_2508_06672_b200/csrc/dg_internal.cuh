@@ -168,6 +168,33 @@ void launch_minmax(const double* v, int64_t n, double2* part, double2* out, cuda
 void launch_heatmap(const double* v, int64_t n_lat, int64_t n_lon, double lo, double scale,
                     uint8_t* out, cudaStream_t st);
 
+// capture synthesis (dg_scene.cu): waveforms, the FFT fractional advance, the
+// receive channel and MT19937-64 noise (reference scene.hpp / waveform.hpp)
+constexpr int kWaveSpoofer = 0, kWaveTone = 1, kWaveChirp = 2, kWaveSawtooth = 3;
+struct WaveParams {
+    int kind;
+    uint64_t seed;  // spoofer nav-bit seed
+    double a, b;    // tone: offset; chirp: bandwidth, period; sawtooth: bandwidth, chirp period
+};
+void launch_waveform(const WaveParams& w, double start, double ts, int64_t n, const int8_t* chips,
+                     double2* out, cudaStream_t st);
+int fft_log2_max();
+// forward spectrum of the tapered record padded to 2^l (four-step layout)
+void launch_fractional_fwd(const double2* tx, int64_t n_tx, int guard, int l, double2* spec,
+                           cudaStream_t st);
+// advance by frac, inverse, and received[k] = amplitude * delayed[shift + k] * phasor[k]
+void launch_fractional_inv(const double2* spec, int l, double frac, int64_t shift, int64_t n_out,
+                           double amplitude, const double2* phasor, double2* work, double2* recv,
+                           cudaStream_t st);
+void launch_receive_direct(const double2* tx, int64_t shift, int64_t n_out, double amplitude,
+                           const double2* phasor, double2* recv, cudaStream_t st);
+void launch_phasors(const double2* rotation, int n_rec, int64_t n_out, double2* phasor,
+                    cudaStream_t st);
+// recv [S][E][R][n] -> caps (stride cap_stride per (s, r)) + sigma * noise
+void launch_noise_combine(const uint64_t* seeds, int n_snap, int n_rx, int n_em,
+                          const double2* recv, int64_t n, double sigma, int add_noise,
+                          double2* caps, int64_t cap_stride, cudaStream_t st);
+
 // exact FP64 reference-order re-evaluation of flagged elements
 // elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,

@@ -11,7 +11,7 @@ import bench  # noqa: E402
 import paper_2508_06672_b200 as b2  # noqa: E402
 
 cfg = bench.WORKLOADS["C3"]
-states, caps, bounds, spacing = bench.make_inputs(cfg)
+states, caps, bounds, spacing = bench.make_inputs("C3")
 grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
 pinned = torch.empty(caps.shape, dtype=torch.complex128, pin_memory=True).numpy()
 pinned[...] = caps

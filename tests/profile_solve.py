@@ -17,8 +17,9 @@ import paper_2508_06672_b200 as b2  # noqa: E402
 
 
 def main():
-    cfg = bench.WORKLOADS[os.environ.get("DG_PROFILE_CONFIG", "C3")]
-    states, caps, bounds, spacing = bench.make_inputs(cfg)
+    name = os.environ.get("DG_PROFILE_CONFIG", "C3")
+    cfg = bench.WORKLOADS[name]
+    states, caps, bounds, spacing = bench.make_inputs(name)
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], bench.FC)
     opts = b2.GeolocateOptions()

@@ -113,3 +113,31 @@ def config(name: str, spacing_km: float = 1.0) -> dict:
         return {**_base(steps, 1.0, 0.01, 5e6, 3 if name == "C3" else 5),
                 **_grid(-half, half, -half, half, sp), "receivers": _PAPER_RX, "emitters": _FOUR}
     raise KeyError(name)
+
+
+def to_scenario(sim, scene: dict):
+    """The same scene as a paper_2508_06672_b200.simulate.Scenario (the
+    reference's Scenario fields, config.hpp:269-324 defaults)."""
+    rx = [sim.CircularOrbit(r["orbit_alt_m"], r["orbit_inclination_deg"],
+                            r.get("orbit_raan_deg", 0.0), r.get("orbit_phase_deg", 0.0))
+          for r in scene["receivers"]]
+    em = []
+    for e in scene["emitters"]:
+        kind = e["waveform"]
+        if kind == "spoofer":
+            w = sim.SpooferSpec(int(e["prn"]), int(e.get("data_seed", 0)))
+        elif kind == "tone":
+            w = sim.ToneSpec(float(e.get("tone_offset_hz", 0.0)))
+        elif kind == "chirp":
+            w = sim.ChirpSpec(float(e["chirp_bandwidth_hz"]), float(e["chirp_period_s"]))
+        else:
+            w = sim.SawtoothSpec(float(e["sawtooth_bandwidth_hz"]),
+                                 float(e["sawtooth_chirp_period_s"]))
+        from paper_2508_06672_b200.geodesy import GeodeticCoord
+        em.append(sim.EmitterDef(GeodeticCoord(float(e["lat_deg"]), float(e["lon_deg"]),
+                                               float(e.get("alt_m", 0.0))), w,
+                                 float(e["ref_snr_db"]), float(e["ref_range_m"])))
+    return sim.Scenario(rx, em, int(scene["snapshots"]), float(scene["snapshot_spacing_s"]),
+                        float(scene["capture_duration_s"]), float(scene["sample_rate_hz"]),
+                        float(scene["center_freq_hz"]), float(scene.get("start_time_s", 0.0)),
+                        int(scene["noise_seed"]), float(scene.get("noise_power", 1.0)))
