@@ -197,6 +197,7 @@ struct Lane {
     float2 *y1c = nullptr, *y2p = nullptr;
     float2* mom = nullptr;
     size_t mom_cap = 0;
+    double* sfdoa = nullptr;  // candidates' FDOA in bucket order (moment path)
     unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
     cudaEvent_t done = nullptr;
     ~Lane() {
@@ -228,6 +229,9 @@ struct Pipeline {
         const char* v = getenv("DG_REFINE_TAU");
         return v && *v ? (float)atof(v) : kMomentRefineTau;
     }();
+    // candidate block sums on the tensor cores (dg_evaluate_tc.cu); DG_EVAL_TC=0
+    // selects the FFMA2 block loop (k_evaluate)
+    bool use_tc = env_int("DG_EVAL_TC", 1) != 0;
 
     ~Pipeline() {
         if (window_ready) cudaEventDestroy(window_ready);
@@ -273,6 +277,7 @@ struct Pipeline {
             }
             CK(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
             L.sorted = sc.alloc<int>(P);
+            L.sfdoa = sc.alloc<double>(P);
             L.tasks = sc.alloc<Task>(max_tasks);
             L.buckets = sc.alloc<Bucket>(std::min<int64_t>(P, nbins));
             L.off = sc.alloc<int>(nbins);
@@ -421,17 +426,23 @@ struct Pipeline {
         } else {
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
                           L.n_tasks, L.n_buckets, d_slot(s), P, L.sorted, L.tasks, L.buckets,
-                          L.ubin, pl.B, st);
+                          L.ubin, pl.B, st, fdoa_slot(s), L.sfdoa);
             launch_center(y1_64, y2, N, nu_c + s, L.y1c, L.y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
                            L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
             CK(cudaMemsetAsync(L.queue, 0, sizeof(int), st));
-            launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
-                            (int)std::min<int64_t>(P, pl.nbins), L.sorted, fdoa_slot(s), fs,
-                            nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
-                            sm_count, st);
+            if (use_tc && evaluate_tc_supported(pl.nbmax, pl.R))
+                launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
+                                   (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
+                                   nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
+                                   sm_count, st);
+            else
+                launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
+                                (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
+                                nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
+                                sm_count, st);
             launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, L.work, st);
             launches += 7;
         }

@@ -1,0 +1,452 @@
+// K3c: candidate evaluation of the block-moment correlator with the block sums on
+// the 5th-generation tensor cores (tcgen05, TMEM accumulators).
+//
+// For a TDOA bucket with moments M'_m[b] (b < nb, m < R; odd m stored times i) each
+// candidate needs C_b = sum_m c_m M'_m[b] for every block (k_evaluate: R FFMA2 per
+// candidate-block) and then S = |sum_b W^b C_b|. The first step is a real GEMM:
+//   D[i][2b + ri] = sum_k A[i][k] B[2b + ri][k],  A[i][k] = c_k(candidate i),
+//   B[2b][k] = Re M'_k[b],  B[2b+1][k] = Im M'_k[b],  K = R padded to 16,
+// one 128-candidate tile x 2 nb columns per bucket tile, i.e. tcgen05.mma
+// kind::f16 (BF16 operands, FP32 accumulation in TMEM) with M = 128, N = 2 nb
+// (<= 256 per instruction) and K = 16 in one instruction. BF16 keeps 8
+// significand bits, so both operands are split into three BF16 parts
+// x = h + m + l (exact for an FP32 moment; 24 bits of the FP64 coefficient) and
+// D = hl + mm + lh + hm + mh + hh (every product term down to 2^-16 relative;
+// the dropped ones are <= 2^-24): FP32-class C_b, checked by the same error
+// model as the FFMA2 path.
+//
+// One CTA (4 warps, 128 threads = the 128 TMEM lanes = one candidate each) per
+// bucket from a dynamic queue; the bucket's moments arrive by TMA bulk copy into
+// a 2-stage ring; all threads split them into the B operand (no-swizzle K-major
+// core-matrix layout); per tile each thread computes its candidate's J_m(x)
+// (FP64) into the A operand; thread 0 issues the six MMAs and commits to an
+// mbarrier; each thread then reads its TMEM lane 32 columns (16 blocks) at a time
+// (two tcgen05.ld.32x32b.x16) and runs the group sums as
+// k_evaluate does: A, V, |C_b|^2 on FFMA2 with W_j = W_1^j (FP64 recurrence,
+// rounded once), FP64 anchors across groups, refinement flag
+// S < tau max(sqrt(sum |C_b|^2), Q).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dg_device.cuh"
+#include "dg_internal.cuh"
+
+namespace dg {
+
+namespace {
+
+constexpr int kTcThreads = 128;
+constexpr int kTcStages = 1;
+constexpr int kTcK = 16;          // K (moments) padded: one kind::f16 instruction
+constexpr int kTcG = 16;          // blocks per epilogue group (32 TMEM columns)
+constexpr uint32_t kLBO = 128;    // bytes between the two 16-byte K chunks of a core matrix pair
+constexpr uint32_t kSBO = 256;    // bytes between 8-row groups (2 K chunks x 128 B)
+constexpr int kParts = 3;         // BF16 parts per operand
+constexpr int kChunkCols = 128;   // TMEM columns per MMA chunk (4 groups of 16 blocks)
+
+// byte offset of the 16-byte chunk (row r, K chunk c: k = 8c .. 8c + 7) in the
+// no-swizzle K-major core-matrix layout
+__device__ __forceinline__ uint32_t cm_off(int r, int c) {
+    return (uint32_t)(r >> 3) * kSBO + (uint32_t)c * kLBO + (uint32_t)(r & 7) * 16u;
+}
+
+// two FP32 values x = h + m + l exactly in BF16 parts (each residual is exact in
+// FP32), packed in pairs: out[0] = h, out[1] = m, out[2] = l
+__device__ __forceinline__ void split3x2(float x0, float x1, uint32_t (&out)[3]) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+    float2 f = __bfloat1622float2(h);
+    const float r0 = x0 - f.x, r1 = x1 - f.y;
+    __nv_bfloat162 m = __floats2bfloat162_rn(r0, r1);
+    f = __bfloat1622float2(m);
+    __nv_bfloat162 l = __floats2bfloat162_rn(r0 - f.x, r1 - f.y);
+    out[0] = *reinterpret_cast<uint32_t*>(&h);
+    out[1] = *reinterpret_cast<uint32_t*>(&m);
+    out[2] = *reinterpret_cast<uint32_t*>(&l);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((kLBO >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((kSBO >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;                // base offset 0, legacy LBO mode, SWIZZLE_NONE
+}
+
+// kind::f16, D f32, A/B BF16 K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t instr_desc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+struct TcLayout {
+    int NP;           // B rows: 2 blocks per group-column pair, 32 * ceil(nbmax / 16)
+    int ncols;        // TMEM columns allocated: one column chunk (<= kChunkCols)
+    size_t ring_f2;   // float2 per ring stage
+    size_t part_b;    // bytes of one BF16 part of B (NP x 16)
+    size_t off_b, off_a, bytes;
+};
+
+__host__ __device__ inline TcLayout tc_layout(int nbmax, int R) {
+    TcLayout L{};
+    L.NP = 2 * kTcG * ((nbmax + kTcG - 1) / kTcG);
+    L.ncols = 32;
+    while (L.ncols < L.NP && L.ncols < kChunkCols) L.ncols <<= 1;
+    L.ring_f2 = (size_t)nbmax * R;
+    L.part_b = (size_t)L.NP * kTcK * 2;
+    const size_t ring = (kTcStages * L.ring_f2 * 8 + 1023) / 1024 * 1024;
+    L.off_b = ring;                                  // B parts h | m | l
+    L.off_a = L.off_b + kParts * L.part_b;           // A parts h | m | l, 128 x 16 each
+    L.bytes = L.off_a + kParts * (size_t)128 * kTcK * 2;
+    return L;
+}
+
+constexpr size_t kPartA = (size_t)128 * kTcK * 2;
+
+template <int R>
+__global__ void __launch_bounds__(kTcThreads, 4)
+k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
+              int* __restrict__ queue, const int* __restrict__ sorted,
+              const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p,
+              int B, const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
+              uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
+    constexpr int G = kTcG;
+    static_assert(R <= kTcK && R % 2 == 0, "moments");
+    const TcLayout L = tc_layout(nbmax, R);
+    extern __shared__ __align__(1024) float4 smem4[];
+    char* base = reinterpret_cast<char*>(smem4);
+    const float2* ring = reinterpret_cast<const float2*>(base);
+    char* Bs = base + L.off_b;
+    char* As = base + L.off_a;
+    __shared__ uint64_t full[kTcStages], empty[kTcStages], mma_bar;
+    __shared__ int slot_u[kTcStages];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ float q2s;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nbk = *n_buckets;
+    const double nu_c = *nu_c_p;
+
+    auto produce = [&](int k, bool block) -> bool {  // thread 0 (as k_evaluate)
+        const int sl = k % kTcStages;
+        if (k >= kTcStages) {
+            const uint32_t par = ((k / kTcStages) - 1) & 1;
+            if (block)
+                mbar_wait(&empty[sl], par);
+            else if (!mbar_test(&empty[sl], par))
+                return false;
+        }
+        const int u = atomicAdd(queue, 1);
+        slot_u[sl] = u;
+        if (u < nbk) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint32_t bytes = (uint32_t)buckets[u].nb * R * sizeof(float2);
+            mbar_expect_tx(&full[sl], bytes);
+            tma_load_1d(base + sl * L.ring_f2 * 8, mom + (size_t)u * nbmax * R, bytes, &full[sl]);
+        } else {
+            mbar_arrive(&full[sl]);
+        }
+        return true;
+    };
+    if (warp == 0) {  // TMEM for this CTA's lifetime (warp-wide alloc)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "r"((uint32_t)L.ncols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < kTcStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(&mma_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    int produced = 0;
+    if (tid == 0)
+        for (; produced < kTcStages; ++produced) produce(produced, false);
+
+    const uint32_t sA = smem_u32(As), sB = smem_u32(Bs);
+    uint32_t mma_phase = 0;
+    for (int k = 0;; ++k) {
+        if (tid == 0) {
+            for (; produced <= k; ++produced) produce(produced, true);
+            while (produced < k + kTcStages && produce(produced, false)) ++produced;
+        }
+        const int sl = k % kTcStages;
+        mbar_wait(&full[sl], (k / kTcStages) & 1);
+        const int u = slot_u[sl];
+        if (u >= nbk) break;
+        const Bucket bk = buckets[u];
+        const int nb = bk.nb;
+        // the first tile's candidate, loaded now so the latency hides under the B split
+        int p = tid < bk.count ? sorted[bk.start + tid] : -1;
+        double fd = tid < bk.count ? sfdoa[bk.start + tid] : 0.0;
+        const float2* mb = ring + sl * L.ring_f2;
+        const int ng = (nb + G - 1) / G;
+        const int np = 2 * G * ng;  // B rows / TMEM columns used by this bucket
+        if (warp == 0) {  // Q = ||M_0||_2 (fixed order, as k_evaluate)
+            float q2 = 0.f;
+            for (int b = lane; b < nb; b += 32) {
+                const float2 v = mb[b * R];
+                q2 = fmaf(v.x, v.x, fmaf(v.y, v.y, q2));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+            if (lane == 0) q2s = q2;
+        }
+        // B operand: per (block b, K chunk c) the rows 2b (Re) and 2b + 1 (Im),
+        // columns 8c .. 8c + 7, three BF16 parts; zeros beyond nb / R
+        for (int e = tid; e < (np / 2) * 2; e += kTcThreads) {
+            const int b = e >> 1, c = e & 1;
+            uint32_t re[kParts][4], im[kParts][4];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int m = 8 * c + j;
+                if (b < nb && m < R)  // R even: m + 1 < R; 16-byte aligned pair
+                    v = *reinterpret_cast<const float4*>(mb + b * R + m);
+                uint32_t t[3];
+                split3x2(v.x, v.z, t);
+                re[0][j / 2] = t[0];
+                re[1][j / 2] = t[1];
+                re[2][j / 2] = t[2];
+                split3x2(v.y, v.w, t);
+                im[0][j / 2] = t[0];
+                im[1][j / 2] = t[1];
+                im[2][j / 2] = t[2];
+            }
+#pragma unroll
+            for (int q = 0; q < kParts; ++q) {
+                *reinterpret_cast<uint4*>(Bs + q * L.part_b + cm_off(2 * b, c)) =
+                    make_uint4(re[q][0], re[q][1], re[q][2], re[q][3]);
+                *reinterpret_cast<uint4*>(Bs + q * L.part_b + cm_off(2 * b + 1, c)) =
+                    make_uint4(im[q][0], im[q][1], im[q][2], im[q][3]);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) mbar_arrive(&empty[sl]);  // the ring slot is free again
+        const double qscale = sqrt((double)q2s);
+
+        for (int t0 = 0; t0 < bk.count; t0 += 128) {
+            if (t0 > 0) {
+                p = t0 + tid < bk.count ? sorted[bk.start + t0 + tid] : -1;
+                fd = t0 + tid < bk.count ? sfdoa[bk.start + t0 + tid] : 0.0;
+            }
+            const double nu = p >= 0 ? fd / fs - nu_c : 0.0;
+            // warps without a candidate in this tile skip the Bessel terms and the
+            // epilogue (their A rows are zero); tcgen05.ld stays warp-uniform
+            const bool warp_live = __any_sync(0xffffffffu, p >= 0);
+            // ---- A operand: this thread's candidate, c_m rounded to FP32 (as the
+            // FFMA2 path) and split exactly into three BF16 parts ----
+            {
+                float cf[kTcK];
+#pragma unroll
+                for (int m = 0; m < kTcK; ++m) cf[m] = 0.f;
+                if (p >= 0) {
+                    double jv[R];
+                    bessel_j<R>(3.141592653589793 * nu * (double)B, jv);
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        cf[m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t w[kParts][4];
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        uint32_t t[3];
+                        split3x2(cf[8 * c + j], cf[8 * c + j + 1], t);
+                        w[0][j / 2] = t[0];
+                        w[1][j / 2] = t[1];
+                        w[2][j / 2] = t[2];
+                    }
+#pragma unroll
+                    for (int q = 0; q < kParts; ++q)
+                        *reinterpret_cast<uint4*>(As + q * kPartA + cm_off(tid, c)) =
+                            make_uint4(w[q][0], w[q][1], w[q][2], w[q][3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
+            tc_fence_before();
+            __syncthreads();
+            // the bucket's columns in chunks of kChunkCols TMEM columns: MMA a chunk,
+            // then every thread reads its lane of it (4 groups of 16 blocks)
+            float wtr[G], wti[G];
+            double sr = 1.0, si = 0.0;
+            double acc_re = 0.0, acc_im = 0.0, en = 0.0, ar = 1.0, ai = 0.0;
+            for (int c0 = 0; c0 < np; c0 += kChunkCols) {
+                const int nn = np - c0 < kChunkCols ? np - c0 : kChunkCols;
+                if (tid == 0) {
+                    tc_fence_after();
+                    const uint32_t idesc = instr_desc(nn);
+                    const uint32_t boff = (uint32_t)(c0 >> 3) * kSBO;
+                    // smallest terms first: hl, mm, lh, hm, mh, hh
+                    constexpr int pa[6] = {0, 1, 2, 0, 1, 0};
+                    constexpr int pb[6] = {2, 1, 0, 1, 0, 0};
+#pragma unroll
+                    for (int t = 0; t < 6; ++t)
+                        mma_bf16(tmem, smem_desc(sA + pa[t] * (uint32_t)kPartA),
+                                 smem_desc(sB + pb[t] * (uint32_t)L.part_b + boff), idesc,
+                                 t ? 1u : 0u);
+                    mma_commit(&mma_bar);
+                }
+                if (c0 == 0 && warp_live) {
+                    // W_j = W_1^j (FP64 recurrence, one FP32 rounding each) while the MMAs run
+                    const double x1 = nu * (double)B;
+                    double w1r, w1i;
+                    sincospi(2.0 * (x1 - rint(x1)), &w1i, &w1r);
+                    double pr = 1.0, pi_ = 0.0;
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        wtr[j] = (float)pr;
+                        wti[j] = (float)pi_;
+                        const double nr = fma(pr, w1r, -pi_ * w1i);
+                        pi_ = fma(pr, w1i, pi_ * w1r);
+                        pr = nr;
+                    }
+                    sr = pr;
+                    si = pi_;
+                }
+                mbar_wait(&mma_bar, mma_phase);
+                mma_phase ^= 1;
+                tc_fence_after();
+                for (int gc = 0; warp_live && gc < nn; gc += 2 * G) {
+                    float v[2][16];
+                    tmem_ld16(lane_addr + (uint32_t)gc, v[0]);
+                    tmem_ld16(lane_addr + (uint32_t)(gc + 16), v[1]);
+                    float2 A = make_float2(0.f, 0.f), V = A, E2 = A;
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        const float2 C =
+                            make_float2(v[j >> 3][2 * (j & 7)], v[j >> 3][2 * (j & 7) + 1]);
+                        A = ffma2(C, wtr[j], A);
+                        V = ffma2(C, wti[j], V);
+                        E2 = ffma2v(C, C, E2);
+                    }
+                    const double hr = (double)(A.x - V.y), hi = (double)(A.y + V.x);
+                    acc_re = fma(ar, hr, fma(-ai, hi, acc_re));
+                    acc_im = fma(ar, hi, fma(ai, hr, acc_im));
+                    en += (double)(E2.x + E2.y);
+                    const double nr = fma(ar, sr, -ai * si);
+                    ai = fma(ar, si, ai * sr);
+                    ar = nr;
+                }
+                tc_fence_before();  // this chunk's TMEM reads done before the next MMAs
+                __syncthreads();
+            }
+            if (p >= 0) {
+                const double sv = sqrt(acc_re * acc_re + acc_im * acc_im);
+                s_out[p] = sv;
+                if (sv < (double)tau * fmax(sqrt(en), qscale)) {
+                    const int64_t e = flag_base + p;
+                    atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
+                }
+            }
+        }
+        __syncthreads();  // B / A / q2s reuse by the next bucket
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((uint32_t)L.ncols));
+}
+
+template <int R>
+void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
+                         const int* sorted, const double* fdoa, double fs, const double* nu_c,
+                         int B, const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
+                         int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
+    auto kern = k_evaluate_tc<R>;
+    const TcLayout L = tc_layout(nbmax, R);
+    // CTAs per SM bounded by TMEM (512 columns per SM): request enough shared
+    // memory that no more CTAs than fit in TMEM are resident on one SM
+    const int per_sm = 512 / L.ncols;
+    size_t smem = L.bytes;
+    const size_t floor_bytes = (size_t)(228 * 1024) / (per_sm + 1) + 1024;
+    if (smem < floor_bytes) smem = floor_bytes;
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    // resident CTAs: TMEM-bound, or shared-memory-bound (228 KB per SM, 1 KB
+    // reserved per CTA, ~1 KB of static shared memory)
+    int resident = (int)((228 * 1024) / (smem + 2048));
+    if (resident > per_sm) resident = per_sm;
+    if (resident < 1) resident = 1;
+    int grid = sm_count * resident;
+    if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
+    kern<<<grid, kTcThreads, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c, B, mom,
+                                         nbmax, s_out, flag_bits, flag_base, tau);
+}
+
+}  // namespace
+
+bool evaluate_tc_supported(int nbmax, int R) {
+    const TcLayout L = tc_layout(nbmax, R);
+    return L.ncols <= 512 && L.bytes <= 200 * 1024 && R <= kTcK;
+}
+
+void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+                        int max_buckets, const int* sorted, const double* fdoa, double fs,
+                        const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
+                        uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
+                        cudaStream_t st) {
+#define DG_TC_CASE(RR)                                                                          \
+    evaluate_tc_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
+                            mom, nbmax, s_out, flag_bits, flag_base, tau, sm_count, st)
+    switch (R) {
+        case 8: DG_TC_CASE(8); break;
+        case 10: DG_TC_CASE(10); break;
+        case 12: DG_TC_CASE(12); break;
+        case 14: DG_TC_CASE(14); break;
+        default: DG_TC_CASE(16); break;
+    }
+#undef DG_TC_CASE
+}
+
+}  // namespace dg

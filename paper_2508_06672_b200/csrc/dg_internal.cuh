@@ -123,7 +123,8 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 // Bucket per non-empty bin (blocks of length B; B = 0 skips buckets)
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
                    int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st);
+                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st,
+                   const double* fdoa = nullptr, double* sfdoa = nullptr);
 // candidates per warp task of the active correlator variant (32 x candidates/lane)
 int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
@@ -140,7 +141,8 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
 void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
                     int N, const float* tcheb, const float2* y1c, const float2* y2p, int padf,
                     float2* mom, int nbmax, int sm_count, cudaStream_t st);
-// per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue)
+// per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue);
+// sfdoa = the candidates' FDOA in bucket order (launch_bucket's sfdoa)
 size_t evaluate_smem_bytes(int nbmax, int R);
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                      int max_buckets, const int* sorted, const double* fdoa, double fs,
@@ -194,6 +196,15 @@ void launch_phasors(const double2* rotation, int n_rec, int64_t n_out, double2* 
 void launch_noise_combine(const uint64_t* seeds, int n_snap, int n_rx, int n_em,
                           const double2* recv, int64_t n, double sigma, int add_noise,
                           double2* caps, int64_t cap_stride, cudaStream_t st);
+
+// the same evaluation with the block sums C_b on the tensor cores (dg_evaluate_tc.cu,
+// tcgen05 kind::tf32, split hi/lo operands); needs 2 nbmax <= 512 TMEM columns
+bool evaluate_tc_supported(int nbmax, int R);
+void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+                        int max_buckets, const int* sorted, const double* fdoa, double fs,
+                        const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
+                        uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
+                        cudaStream_t st);
 
 // exact FP64 reference-order re-evaluation of flagged elements
 // elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)

@@ -439,8 +439,11 @@ k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
     }
 }
 
+// sfdoa (nullable): the candidates' FDOA in the same bucket order, so the
+// candidate evaluators read contiguous values instead of gathering fdoa[p]
 __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __restrict__ cursor,
-                          int* __restrict__ sorted) {
+                          int* __restrict__ sorted, const double* __restrict__ fdoa,
+                          double* __restrict__ sfdoa) {
     // four independent cursor atomics in flight per thread (latency-bound)
     constexpr int U = 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -456,7 +459,10 @@ __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __re
             pos[u] = dd[u] != kNoOverlap ? atomicAdd(&cursor[dd[u] + N - 1], 1) : -1;
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (pos[u] >= 0) sorted[pos[u]] = (int)(p0 + u * stride);
+            if (pos[u] >= 0) {
+                sorted[pos[u]] = (int)(p0 + u * stride);
+                if (sfdoa) sfdoa[pos[u]] = fdoa[p0 + u * stride];
+            }
     }
 }
 
@@ -1052,11 +1058,12 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
                    int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st) {
+                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st,
+                   const double* fdoa, double* sfdoa) {
     const int ts = correlate_task_size();
     k_scan<<<1, kScanThreads, 0, st>>>(hist + bin0, nb, ts, off + bin0, toff + bin0, boff + bin0,
                                        cursor + bin0, n_tasks, n_buckets);
-    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted);
+    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted, fdoa, sfdoa);
     k_build_tasks<<<blocks_for(nb, 256), 256, 0, st>>>(hist + bin0, nb, bin0, N, ts, off + bin0,
                                                       toff + bin0, boff + bin0, tasks, buckets, ubin, B);
 }

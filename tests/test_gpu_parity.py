@@ -158,13 +158,18 @@ def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, m
 
 
 @pytest.mark.parametrize("block", [64, 128, 256, 512])
-@pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200)])
-def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, monkeypatch):
+@pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200),
+                                            (3e3, 12)])  # ~250 per bucket: 2 tiles
+@pytest.mark.parametrize("tc", ["1", "0"])  # block sums on tcgen05 / FFMA2 block loop
+def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, tc, monkeypatch):
     """The block-moment correlator at every block length against the reference,
     on buckets dense enough that it is the planner's choice (many candidates
-    per TDOA), including FDOA == 0 (x = 0) and the full TDOA range."""
+    per TDOA), including FDOA == 0 (x = 0) and the full TDOA range; candidate
+    evaluation on the tensor cores (k_evaluate_tc, B = 256 and 512 at 50k
+    samples: 2 nb <= 512 TMEM columns) and on the FFMA2 block loop."""
     monkeypatch.setenv("DG_CORRELATOR_MOMENTS", "2")
     monkeypatch.setenv("DG_MOMENT_B", str(block))
+    monkeypatch.setenv("DG_EVAL_TC", tc)
     n, fs, count = 50_000, 5e6, 6_000
     rng = np.random.default_rng(block + int(span))
     y1, y2 = gauss(rng, n), gauss(rng, n)
