@@ -13,9 +13,12 @@ accumulation, exact argmax and detect_emitters, all on the GPU.
 * e2e       — the same solve through the public API with host (pinned) captures:
               H2D of every capture and D2H of the accumulated surface inside the
               timed region.
-* roofline  — the correlator kernel: 20 FLOP per overlapping sample (the
-              reference kernel as executed) x sum N_ov / its
-              event time, against the FP32 CUDA-core peak measured in-process.
+* roofline  — the dominant correlator kernel (k_moments at C3): its FMA-pipe
+              work counted on the device (k_work_count) over its event time,
+              against the FP32 CUDA-core peak measured in-process; the
+              tensor-core part of k_evaluate_tc against MEASURED_PEAKS.json's
+              BF16 figure; the reference-equivalent rate (20 FLOP per
+              overlapping sample) beside it.
 * cpu_baseline / --impl reference — the reference's own CPU path (oracle/_ref,
               compiled from the unmodified reference headers) on this host's
               cores, on a bounded sample of the same workload.
@@ -287,11 +290,16 @@ def b200_arm(args, rank, world):
     mom_ms = last["moments_ms"]
     ev_ms = last["evaluate_ms"]
     corr_ms = mom_ms + ev_ms
+    # FMA-pipe work in FP32x2 operations x 4 FLOP-equivalents (k_work_count)
     mom_tf = 4.0 * last["moment_ffma2"] / (mom_ms * 1e-3) / 1e12 if mom_ms else None
     ev_tf = 4.0 * last["evaluate_ffma2"] / (ev_ms * 1e-3) / 1e12 if ev_ms else None
+    tc_flop = last.get("evaluate_tc_flop") or 0.0
+    ev_name = "k_evaluate_tc" if tc_flop > 0 else "k_evaluate"
+    tc_tf = tc_flop / (ev_ms * 1e-3) / 1e12 if ev_ms and tc_flop else None
+    bf16_peak = measured_peaks().get("bf16_tflops")
     ovl = last["sum_overlap_samples"]
-    dominant = "k_evaluate" if ev_ms >= mom_ms else "k_moments"
-    achieved = ev_tf if dominant == "k_evaluate" else mom_tf
+    dominant = ev_name if ev_ms >= mom_ms else "k_moments"
+    achieved = ev_tf if dominant == ev_name else mom_tf
     launches = last["kernel_launches"]
 
     # e2e: host (pinned) captures in, accumulated surface out, through the public API
@@ -363,13 +371,24 @@ def b200_arm(args, rank, world):
                 "traffic_source": f"dram__bytes_read.sum + dram__bytes_write.sum per {dominant} "
                                   "launch, profiles/r01_ncu_kernels.txt",
                 "peak_source": "dg_fp32_peak_tflops FFMA probe in this process",
-                "flop_definition": "4 x FP32x2 MACs the kernel performs, counted on the device "
-                                   "(k_moments: nb*B/2*R per bucket, folded; k_evaluate: "
-                                   "count*nb*(R+3) per bucket)",
-                "kernels": {"k_moments": {"ms": mom_ms, "tflops": mom_tf,
+                "flop_definition": "FMA-pipe work: 4 x the FP32x2 operations the kernel's "
+                                   "algorithm performs, counted on the device by k_work_count "
+                                   "(k_moments: B/2*(R+6) per bucket-block = R moment MACs per "
+                                   "folded sample pair + 2 complex products + 1 fold; "
+                                   "k_evaluate_tc: 3 per candidate-block on CUDA cores, the "
+                                   "block sums on tensor cores reported separately)",
+                "kernels": {"k_moments": {"ms": mom_ms, "tflops": mom_tf, "bound": "fp32 fma pipe",
                                           "frac": mom_tf / peak if mom_tf and peak else None},
-                            "k_evaluate": {"ms": ev_ms, "tflops": ev_tf,
-                                           "frac": ev_tf / peak if ev_tf and peak else None}},
+                            ev_name: {"ms": ev_ms, "tflops": ev_tf,
+                                      "frac": ev_tf / peak if ev_tf and peak else None,
+                                      "tensor_tflops": tc_tf,
+                                      "tensor_frac": (tc_tf / bf16_peak
+                                                      if tc_tf and bf16_peak else None),
+                                      "tensor_peak": bf16_peak,
+                                      "tensor_peak_source": "MEASURED_PEAKS.json bf16_tflops",
+                                      "tensor_flop_definition":
+                                          "BF16 MMA FLOPs issued: 6 split products x "
+                                          "2*128*np*16 per 128-candidate tile"}},
                 "reference_equivalent": {
                     "flop_per_sample": FLOP_PER_SAMPLE, "sum_overlap_samples": ovl,
                     "tflops": FLOP_PER_SAMPLE * ovl / (corr_ms * 1e-3) / 1e12,
@@ -385,6 +404,14 @@ def b200_arm(args, rank, world):
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 def ncu_traffic(kernel):

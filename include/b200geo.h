@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 4
+#define DG_ABI_VERSION 5
 
 enum {
     DG_OK = 0,
@@ -181,9 +181,13 @@ typedef struct {
     /* block-moment correlator accounting */
     double moments_ms;          /* profile: event time of k_moments (+ k_center) */
     double evaluate_ms;         /* profile: event time of k_evaluate */
-    double moment_ffma2;        /* packed FP32x2 MACs k_moments performs (sum nb*B*R) */
-    double evaluate_ffma2;      /* packed FP32x2 MACs k_evaluate performs (sum count*nb*R) */
+    double moment_ffma2;        /* k_moments FMA-pipe work in FP32x2 operations: per bucket-
+                                   block B/2 (R + 6) (R moment MACs per folded sample pair,
+                                   two complex products, one fold) */
+    double evaluate_ffma2;      /* candidate-side FP32x2 operations: block loop count*nb*(R+3);
+                                   tensor-core path count*nb*3 (group sums on CUDA cores) */
     int64_t direct_steps;       /* (snapshot, pair) steps run on the direct correlator */
+    double evaluate_tc_flop;    /* tensor-core FLOPs k_evaluate_tc issued (BF16 MMAs, 0 if none) */
 } dg_result;
 
 void dg_options_default(dg_options* opt);

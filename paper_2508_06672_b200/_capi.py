@@ -104,7 +104,8 @@ class dg_result(C.Structure):
                 ("evaluate_ms", C.c_double),
                 ("moment_ffma2", C.c_double),
                 ("evaluate_ffma2", C.c_double),
-                ("direct_steps", C.c_int64)]
+                ("direct_steps", C.c_int64),
+                ("evaluate_tc_flop", C.c_double)]
 
 
 # every symbol include/b200geo.h declares (tests check the .so exports them)

@@ -288,11 +288,11 @@ struct Pipeline {
             L.n_tasks = sc.alloc<int>(1);
             L.n_buckets = sc.alloc<int>(1);
             L.queue = sc.alloc<int>(1);
-            L.work = sc.alloc<unsigned long long>(2);
+            L.work = sc.alloc<unsigned long long>(3);
             L.y1c = sc.alloc<float2>(N + 576);
             L.y2p = sc.alloc<float2>(ylen);
             CK(cudaMemsetAsync(L.y2p, 0, ylen * sizeof(float2), sc.st));
-            CK(cudaMemsetAsync(L.work, 0, 2 * sizeof(unsigned long long), sc.st));
+            CK(cudaMemsetAsync(L.work, 0, 3 * sizeof(unsigned long long), sc.st));
         }
         CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
         static const int kB[4] = {64, 128, 256, 512};
@@ -373,7 +373,7 @@ struct Pipeline {
     unsigned long long work_total(Scratch& sc, int which) {
         unsigned long long t = 0;
         for (int l = 0; l < n_lanes; ++l) {
-            unsigned long long w[2] = {0, 0};
+            unsigned long long w[3] = {0, 0, 0};
             CK(cudaMemcpyAsync(w, lanes[l].work, sizeof w, cudaMemcpyDeviceToHost, sc.st));
             CK(cudaStreamSynchronize(sc.st));
             t += w[which];
@@ -433,7 +433,8 @@ struct Pipeline {
                            L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
             if (ev1) CK(cudaEventRecord(ev1, st));
             CK(cudaMemsetAsync(L.queue, 0, sizeof(int), st));
-            if (use_tc && evaluate_tc_supported(pl.nbmax, pl.R))
+            const bool tc = use_tc && evaluate_tc_supported(pl.nbmax, pl.R);
+            if (tc)
                 launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
                                    (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
                                    nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
@@ -443,7 +444,7 @@ struct Pipeline {
                                 (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
                                 nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
                                 sm_count, st);
-            launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, L.work, st);
+            launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, tc ? 1 : 0, L.work, st);
             launches += 7;
         }
         if (ev2) CK(cudaEventRecord(ev2, st));
@@ -1442,7 +1443,8 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         CK(cudaStreamSynchronize(st));  // `init` is host memory of this frame
     }
 
-    unsigned long long ovl = 0, work[2] = {pl.work_total(sc, 0), pl.work_total(sc, 1)};
+    unsigned long long ovl = 0,
+                       work[3] = {pl.work_total(sc, 0), pl.work_total(sc, 1), pl.work_total(sc, 2)};
     CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     res->sum_overlap_samples = (double)ovl;
@@ -1450,6 +1452,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     res->correlate_launches = SPl;
     res->moment_ffma2 = (double)work[0];
     res->evaluate_ffma2 = (double)work[1];
+    res->evaluate_tc_flop = (double)work[2];
     res->direct_steps = pl.direct_steps;
     if (opt.profile) {
         double tm = 0.0, te = 0.0;

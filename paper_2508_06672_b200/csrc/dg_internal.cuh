@@ -134,7 +134,7 @@ void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, cons
 // block-moment correlator (dg_moments.cu)
 void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
                    float2* y2p, int padf, cudaStream_t st);
-void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
+void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R, int tc,
                        unsigned long long* work, cudaStream_t st);
 // moments of every bucket of a step (blocks aligned to absolute sample index);
 // ubin[bin - bin0] = bucket of a TDOA bin or -1

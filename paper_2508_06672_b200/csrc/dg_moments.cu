@@ -434,25 +434,37 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
     }
 }
 
-// algorithmic work of one step (FP32x2 MACs): moments sum nb*(B/2)*R (folded
-// pairs), evaluation sum count*nb*(R+3) — the numerators of bench.py's roofline
+// algorithmic work of one step in FP32x2 operations (the numerators of bench.py's
+// rooflines): moments per bucket-block B/2 (R + 6): R moment MACs per folded
+// sample pair, two complex products (2 each) and the fold (2); candidates
+// count*nb*(R+3) on the block loop, count*nb*3 plus the MMA FLOPs (work[2]) on
+// the tensor-core path (six BF16 MMAs of 128 x np x 16 per 128-candidate tile)
 __global__ void k_work_count(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
-                             int B, int R, unsigned long long* __restrict__ work) {
-    unsigned long long a = 0, b = 0;
+                             int B, int R, int tc, unsigned long long* __restrict__ work) {
+    unsigned long long a = 0, b = 0, c = 0;
     for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < *n_buckets;
          u += gridDim.x * blockDim.x) {
         const Bucket bk = buckets[u];
-        a += (unsigned long long)bk.nb * (B / 2) * R;             // folded pair MACs
-        b += (unsigned long long)bk.count * bk.nb * (R + 3);      // C_b, A, V, |C_b|^2
+        a += (unsigned long long)bk.nb * (B / 2) * (R + 6);
+        if (tc) {
+            b += (unsigned long long)bk.count * bk.nb * 3;
+            const unsigned long long tiles = (bk.count + 127) / 128;
+            const unsigned long long np = 32ull * ((bk.nb + 15) / 16);
+            c += tiles * 6ull * 2ull * 128ull * np * 16ull;
+        } else {
+            b += (unsigned long long)bk.count * bk.nb * (R + 3);
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
     }
-    if ((threadIdx.x & 31) == 0 && (a || b)) {
+    if ((threadIdx.x & 31) == 0 && (a || b || c)) {
         atomicAdd(&work[0], a);
         atomicAdd(&work[1], b);
+        atomicAdd(&work[2], c);
     }
 }
 
@@ -526,9 +538,9 @@ void launch_center(const double2* y, const float2* y2, int N, const double* nu_c
     k_center<<<blocks, 256, 0, st>>>(y, y2, N, nu_c, y1c, y2p, padf);
 }
 
-void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R,
+void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R, int tc,
                        unsigned long long* work, cudaStream_t st) {
-    k_work_count<<<64, 256, 0, st>>>(buckets, n_buckets, B, R, work);
+    k_work_count<<<64, 256, 0, st>>>(buckets, n_buckets, B, R, tc, work);
 }
 
 

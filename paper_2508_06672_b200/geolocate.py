@@ -251,7 +251,7 @@ def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, w
                  kernel_launches=res.kernel_launches, n_detections=res.n_detections,
                  moments_ms=res.moments_ms, evaluate_ms=res.evaluate_ms,
                  moment_ffma2=res.moment_ffma2, evaluate_ffma2=res.evaluate_ffma2,
-                 direct_steps=res.direct_steps)
+                 direct_steps=res.direct_steps, evaluate_tc_flop=res.evaluate_tc_flop)
     per_list = [CorrelationGrid(grid, per[s]) for s in range(n_snap)] if per is not None else []
     return GeolocateResult(grid, per_list, CorrelationGrid(grid, acc), detections,
                            int(res.argmax_index), float(res.argmax_value), stats)
@@ -298,6 +298,7 @@ def correlate_steps(grid: CandidateGrid, staged: StagedSnapshots, s_begin: int, 
                 correlate_ms=res.correlate_ms, moments_ms=res.moments_ms,
                 evaluate_ms=res.evaluate_ms, moment_ffma2=res.moment_ffma2,
                 evaluate_ffma2=res.evaluate_ffma2, direct_steps=res.direct_steps,
+                evaluate_tc_flop=res.evaluate_tc_flop,
                 kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
 
 

@@ -149,6 +149,7 @@ def geolocate_sharded(grid, staged, options=None, gather=True, group=None, strea
     norm = bool(options.normalize_per_snapshot)
     stats = dict(n_refined=0, sum_overlap_samples=0.0, correlate_ms=0.0, moments_ms=0.0,
                  evaluate_ms=0.0, moment_ffma2=0.0, evaluate_ffma2=0.0, direct_steps=0,
+                 evaluate_tc_flop=0.0,
                  kernel_launches=0, correlate_launches=0)
     if s1 > s0:
         stats = correlate_steps(grid, staged, s0, s1, local.data_ptr(),
