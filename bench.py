@@ -314,7 +314,7 @@ def b200_arm(args, rank, world):
         t0 = time.perf_counter()
         if dist is None:
             b2.geolocate_arrays(grid, states, pinned, cfg["fs"], FC, opts, want_surface=True,
-                                want_per_snapshot=False)
+                                want_per_snapshot=False, out=surf.numpy())
         else:
             stg = b2.StagedSnapshots(states, pinned, cfg["fs"], FC, engine=eng)
             _, _, full, _, _ = sharding.geolocate_sharded(grid, stg, opts, gather=True,

@@ -362,6 +362,10 @@ struct Pipeline {
         for (int l = 1; l < n_lanes; ++l) CK(cudaStreamWaitEvent(lanes[l].st, window_ready, 0));
     }
 
+    void wait_event(cudaEvent_t e) {
+        for (int l = 0; l < n_lanes; ++l) CK(cudaStreamWaitEvent(lanes[l].st, e, 0));
+    }
+
     // the main stream waits for every lane (end of a window / of the call)
     void join(Scratch& sc) {
         for (int l = 1; l < n_lanes; ++l) {
@@ -668,6 +672,7 @@ int dg_engine_create(int device, dg_engine** out) {
         e->device = device;
         e->sm_count = prop.multiProcessorCount;
         CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&e->upload, cudaStreamNonBlocking));
         *out = e.release();
     });
 }
@@ -1175,45 +1180,77 @@ int dg_stage_snapshots_iq(dg_engine* eng, const char* const* paths, int64_t S, i
     });
 }
 
-int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) {
-    return guard([&] {
-        if (!eng) raise(DG_EINVAL, "null engine");
-        validate_snapshots(sn);
-        set_device(eng);
-        auto s = std::make_unique<dg_staged>();
-        s->eng = eng;
-        s->S = sn->n_snapshots;
-        s->R = sn->n_receivers;
-        s->N = sn->n_samples;
-        s->stride = capture_stride(s->N);
-        s->fs = sn->sample_rate_hz;
-        s->fc = sn->center_freq_hz;
-        s->states.assign(sn->states, sn->states + s->S * s->R);
-        const int64_t n_caps = s->S * s->R;
-        s->y32 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(float2));
-        s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
-        auto* y32 = static_cast<float2*>(s->y32->p) + kCapturePad;
-        auto* y64 = static_cast<double2*>(s->y64->p) + kCapturePad;
-        StreamGuard sg(nullptr, eng->stream);
-        CK(cudaMemsetAsync(s->y32->p, 0, s->y32->bytes, sg.st));
-        CK(cudaMemsetAsync(s->y64->p, 0, s->y64->bytes, sg.st));
+}  // extern "C"
+
+namespace {
+
+// H2D staging of a run's captures (complex double or float I/Q). Contiguous
+// [S][R][N] host captures go up in one 2-D copy and one conversion kernel.
+// async: on the engine's upload stream, completion recorded in s->ready and
+// not waited for here (dg_geolocate_snapshots overlaps it with the geometry
+// and planning phase; the correlator lanes wait for the event).
+std::unique_ptr<dg_staged> stage_impl(dg_engine* eng, const dg_snapshots* sn, bool async) {
+    if (!eng) raise(DG_EINVAL, "null engine");
+    validate_snapshots(sn);
+    set_device(eng);
+    auto s = std::make_unique<dg_staged>();
+    s->eng = eng;
+    s->S = sn->n_snapshots;
+    s->R = sn->n_receivers;
+    s->N = sn->n_samples;
+    s->stride = capture_stride(s->N);
+    s->fs = sn->sample_rate_hz;
+    s->fc = sn->center_freq_hz;
+    s->states.assign(sn->states, sn->states + s->S * s->R);
+    const int64_t n_caps = s->S * s->R;
+    s->y32 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(float2));
+    s->y64 = std::make_unique<DevMem>(n_caps * s->stride * sizeof(double2));
+    auto* y32 = static_cast<float2*>(s->y32->p);
+    auto* y64 = static_cast<double2*>(s->y64->p);
+    cudaStream_t st = async ? eng->upload : eng->stream;
+    const bool f64 = sn->captures_iq != nullptr;
+    bool contiguous = true;
+    for (int64_t c = 0; c < n_caps; ++c) {
+        const void* p = f64 ? (const void*)sn->captures_iq[c] : (const void*)sn->captures_f32[c];
+        if (!p) raise(DG_EINVAL, "null capture pointer");
+        const char* base = f64 ? (const char*)sn->captures_iq[0] : (const char*)sn->captures_f32[0];
+        const size_t el = f64 ? sizeof(double2) : sizeof(float2);
+        contiguous = contiguous && (const char*)p == base + c * s->N * el;
+    }
+    const size_t el = f64 ? sizeof(double2) : sizeof(float2);
+    char* dst = f64 ? (char*)(y64 + kCapturePad) : (char*)(y32 + kCapturePad);
+    CK(cudaMemsetAsync(f64 ? s->y64->p : s->y32->p, 0, f64 ? s->y64->bytes : s->y32->bytes, st));
+    if (contiguous) {
+        const void* src = f64 ? (const void*)sn->captures_iq[0] : (const void*)sn->captures_f32[0];
+        CK(cudaMemcpy2DAsync(dst, s->stride * el, src, s->N * el, s->N * el, n_caps,
+                             cudaMemcpyHostToDevice, st));
+    } else {
         for (int64_t c = 0; c < n_caps; ++c) {
-            if (sn->captures_iq) {
-                if (!sn->captures_iq[c]) raise(DG_EINVAL, "null capture pointer");
-                CK(cudaMemcpyAsync(y64 + c * s->stride, sn->captures_iq[c], s->N * sizeof(double2),
-                                   cudaMemcpyHostToDevice, sg.st));
-                launch_f64_to_f32(y64 + c * s->stride, y32 + c * s->stride, s->N, sg.st);
-            } else {
-                if (!sn->captures_f32[c]) raise(DG_EINVAL, "null capture pointer");
-                CK(cudaMemcpyAsync(y32 + c * s->stride, sn->captures_f32[c], s->N * sizeof(float2),
-                                   cudaMemcpyHostToDevice, sg.st));
-                launch_f32_to_f64(y32 + c * s->stride, y64 + c * s->stride, s->N, sg.st);
-            }
+            const void* src = f64 ? (const void*)sn->captures_iq[c] : (const void*)sn->captures_f32[c];
+            CK(cudaMemcpyAsync(dst + c * s->stride * el, src, s->N * el, cudaMemcpyHostToDevice, st));
         }
-        CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(sg.st));
-        *out = s.release();
-    });
+    }
+    // the whole padded buffer (pads are zero in the source)
+    if (f64)
+        launch_f64_to_f32(y64, y32, n_caps * s->stride, st);
+    else
+        launch_f32_to_f64(y32, y64, n_caps * s->stride, st);
+    CK(cudaGetLastError());
+    if (async) {
+        CK(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(s->ready, st));
+    } else {
+        CK(cudaStreamSynchronize(st));
+    }
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) {
+    return guard([&] { *out = stage_impl(eng, sn, false).release(); });
 }
 
 void dg_staged_destroy(dg_staged* s) { delete s; }
@@ -1399,6 +1436,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         const StepRange* approx = pl.lattice_ranges(sc, g, hw, nw, fs, wl);
         pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size,
                        /*exact_ranges=*/false);
+        if (w0 == 0 && sn->ready) pl.wait_event(sn->ready);  // captures still uploading
         for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each step
             const int lsp = w0 + i, sp = sp0 + lsp;
             const int s = sp / pairs, q = sp - s * pairs;
@@ -1652,11 +1690,10 @@ int dg_geolocate_staged(dg_engine* eng, const dg_grid* g, const dg_staged* sn, c
 int dg_geolocate_snapshots(dg_engine* eng, const dg_grid* g, const dg_snapshots* sn,
                            const dg_options* opt, dg_result* res) {
     return guard([&] {
-        dg_staged* staged = nullptr;
-        const int rc = dg_stage_snapshots(eng, sn, &staged);
-        if (rc != DG_OK) raise(rc, last_error());
-        std::unique_ptr<dg_staged> hold(staged);
-        geolocate_impl(eng, g, staged, opt, res);
+        // the capture upload overlaps the geometry / planning phase
+        std::unique_ptr<dg_staged> staged = stage_impl(eng, sn, true);
+        geolocate_impl(eng, g, staged.get(), opt, res);
+        CK(cudaStreamSynchronize(eng->upload));  // before the host captures may change
     });
 }
 

@@ -114,6 +114,7 @@ struct dg_engine {
     int device = 0;
     int sm_count = 148;
     cudaStream_t stream = nullptr;  // default stream of calls that pass none
+    cudaStream_t upload = nullptr;  // capture uploads overlapped with the geometry phase
     // pinned double buffer of the file writers (dg_io.cpp), kept across calls
     std::mutex stage_mu;
     void* stage_host[2] = {nullptr, nullptr};
@@ -122,6 +123,7 @@ struct dg_engine {
         for (void* p : stage_host)
             if (p) cudaFreeHost(p);
         if (stream) cudaStreamDestroy(stream);
+        if (upload) cudaStreamDestroy(upload);
     }
 };
 
@@ -149,6 +151,10 @@ struct dg_staged {
     double fs = 0, fc = 0;
     std::unique_ptr<dg::DevMem> y32, y64;
     std::vector<dg_state> states;
+    cudaEvent_t ready = nullptr;  // async staging: the upload's completion
+    ~dg_staged() {
+        if (ready) cudaEventDestroy(ready);
+    }
 };
 
 namespace dg {

@@ -226,11 +226,16 @@ def _options(options: GeolocateOptions, stream=None, profile=False) -> _capi.dg_
 
 def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, want_surface=True,
          want_per_snapshot=False, accumulated_device=None, stream=None, profile=False,
-         det_cap=4096):
+         det_cap=4096, out=None):
     P = grid.size()
     res = _capi.dg_result()
-    acc = np.zeros(P, np.float64) if want_surface else None
-    per = np.zeros((n_snap, P), np.float64) if want_per_snapshot else None
+    acc = None
+    if want_surface:  # `out`: a caller-owned (e.g. pinned) float64 [P] host buffer
+        if out is not None and (out.dtype != np.float64 or out.size != P or
+                                not out.flags["C_CONTIGUOUS"]):
+            raise ValueError("out: need a contiguous float64 array of grid.size() values")
+        acc = out if out is not None else np.empty(P, np.float64)
+    per = np.empty((n_snap, P), np.float64) if want_per_snapshot else None
     dets = (_capi.dg_emitter_estimate * det_cap)()
     if acc is not None:
         res.accumulated = acc.ctypes.data_as(C.POINTER(C.c_double))
