@@ -51,6 +51,8 @@ WORKLOADS = {
                seed=2),
     "C3": dict(half_km=1000.0, snapshots=50, samples=50_000, fs=5e6, emitters="four", snr=-20.0,
                seed=3),
+    "C4": dict(half_km=None, snapshots=10, samples=50_000, fs=5e6, emitters="four", snr=-15.0,
+               seed=4),  # coarse pass: the globe at 10 km (--spacing-km scales it)
     "C5": dict(half_km=2000.0, snapshots=100, samples=50_000, fs=5e6, emitters="four", snr=-20.0,
                seed=5),
 }

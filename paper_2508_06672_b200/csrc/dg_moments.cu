@@ -110,7 +110,7 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
           float2* __restrict__ mom, int nbmax) {
     static_assert(B % 64 == 0 && B <= 512, "block length");
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
-    static_assert(kMomThreads == 512, "mapping");
+    static_assert(kMomThreads % 32 == 0, "mapping");
     using L = MomLayout<B, R>;
     constexpr int CB = L::CB, BPW = L::BPW, G = L::G;
     constexpr int RP = L::RP, RS1 = L::RS1, RS2 = L::RS2, W2 = L::W2;

@@ -107,6 +107,11 @@ def config(name: str, spacing_km: float = 1.0) -> dict:
         half = 250 * KM_DEG
         return {**_base(10, 1.0, 0.01, 5e6, 2), **_grid(-half, half, -half, half, sp),
                 "receivers": _PAPER_RX, "emitters": [_chirp(0.0, 0.0, -10)]}
+    if name == "C4":  # coarse global lattice at 10 km (the fine 100 m grids are built
+        # around the coarse detections by the test)
+        return {**_base(10, 1.0, 0.01, 5e6, 4), **_grid(-90.0, 90.0, -180.0, 179.9, 10 * sp),
+                "receivers": _PAPER_RX,
+                "emitters": [{**e, "ref_snr_db": -15} for e in _FOUR]}
     if name in ("C3", "C5"):
         half = (1000 if name == "C3" else 2000) * KM_DEG
         steps = 50 if name == "C3" else 100

@@ -2,7 +2,8 @@
 
 * C1 (101x101, one 250,000-sample snapshot) runs in full on the reference CPU
   path and is compared element by element.
-* C3 (4,004,001 candidates x 50 snapshots x 50,000 samples) is far beyond the
+* C3 (4,004,001 candidates x 50 snapshots x 50,000 samples) and C4 (the globe at
+  10 km, 8,012,004 candidates x 10 snapshots, then four 100 m fine grids) are far beyond the
   reference's CPU budget (~hours), so it is checked through size-independent
   properties: randomly sampled cells, the argmax cell and its neighbours are
   recomputed exactly by the oracle restatement (correlate.hpp:44-71 order,
@@ -32,12 +33,32 @@ def test_c1_full_vs_reference(b2, ref):
     assert [d.grid_index for d in res.detections] == [d["grid_index"] for d in want["detections"]]
 
 
+def _simulated(b2, name):
+    """The workload's reference-simulator scene, synthesised on the GPU (within
+    1e-15 of oracle/_ref's own simulate_scenario, tests/test_simulate.py)."""
+    import scenes
+    import paper_2508_06672_b200.simulate as sim
+    scene = scenes.config(name)
+    states, caps, _, _ = sim.simulate_arrays(scenes.to_scenario(sim, scene))
+    bounds = (scene["grid_lat_min_deg"], scene["grid_lat_max_deg"], scene["grid_lon_min_deg"],
+              scene["grid_lon_max_deg"])
+    return states, caps, bounds, scene["grid_spacing_deg"], scene
+
+
+def _oracle_acc(orc, states, caps, fs, fc, point):
+    v = 0.0
+    for s in range(caps.shape[0]):
+        d, f = orc.predict_pair_offsets(point, states[s, 0], states[s, 1], fs, orc.wavelength(fc))
+        x = orc.correlate(caps[s, 0], caps[s, 1], d, f, fs)
+        v = x if s == 0 else v + x
+    return v
+
+
 def test_c3_sampled_cells_vs_oracle(b2, orc):
-    from paper_2508_06672_b200 import scene
+    states, caps, bounds, spacing, _ = _simulated(b2, "C3")
     S, N, fs, fc = 50, 50_000, 5e6, 1575.42e6
-    states, caps = scene.synthesize(S, N, fs, scene.FOUR_EMITTERS, -20.0, seed=3)
-    h = 1000 * scene.KM_DEG
-    grid = b2.build_candidate_grid(b2.LatLonBounds(-h, h, -h, h), scene.KM_DEG)
+    assert caps.shape == (S, 2, N)
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
     assert grid.size() == 4_004_001
     res = b2.geolocate_arrays(grid, states, caps, fs, fc, b2.GeolocateOptions(detect=False),
                               want_per_snapshot=False)
@@ -45,13 +66,7 @@ def test_c3_sampled_cells_vs_oracle(b2, orc):
     pts = grid.points
 
     def oracle_acc(p):
-        v = 0.0
-        for s in range(S):
-            d, f = orc.predict_pair_offsets(pts[p], states[s, 0], states[s, 1], fs,
-                                            orc.wavelength(fc))
-            x = orc.correlate(caps[s, 0], caps[s, 1], d, f, fs)
-            v = x if s == 0 else v + x
-        return v
+        return _oracle_acc(orc, states, caps, fs, fc, pts[p])
 
     rng = np.random.default_rng(0)
     cells = list(rng.integers(0, grid.size(), 96))
@@ -65,3 +80,39 @@ def test_c3_sampled_cells_vs_oracle(b2, orc):
     assert best[0] == res.argmax_index
     # FP32 surface error stays far below the gap to the runner-up
     assert np.abs(acc[top] - np.array([exact[int(p)] for p in top])).max() / acc.max() <= NORM_TOL
+
+
+def test_c4_coarse_then_fine_vs_oracle(b2, orc):
+    """C4: the whole globe at 10 km (2002 x 4002 = 8,012,004 cells,
+    TDOA +-4,938 samples, FDOA spread of the far side of the Earth), 10 snapshots
+    of four emitters at -15 dB; then a 101 x 101 grid at 100 m around each of the
+    four coarse detections. Sampled coarse cells and every fine peak are checked
+    against the oracle's FP64 reference-order correlation."""
+    states, caps, bounds, spacing, _ = _simulated(b2, "C4")
+    fs, fc = 5e6, 1575.42e6
+    coarse = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
+    assert (coarse.lat.count, coarse.lon.count) == (2002, 4002)
+    opts = b2.GeolocateOptions(k_sigma=5.0, exclusion_radius_cells=5)
+    res = b2.geolocate_arrays(coarse, states, caps, fs, fc, opts, want_per_snapshot=False)
+    acc = res.accumulated.values
+    pts = coarse.points
+    rng = np.random.default_rng(4)
+    cells = list(rng.integers(0, coarse.size(), 48)) + [res.argmax_index]
+    want = np.array([_oracle_acc(orc, states, caps, fs, fc, pts[p]) for p in cells])
+    assert rel_err(acc[cells], want).max() <= REL_TOL
+    assert res.argmax_value == pytest.approx(want[-1], rel=1e-12)
+    assert len(res.detections) >= 4
+    m100 = 0.1 / 111.195  # 100 m of arc in degrees
+    for det in res.detections[:4]:
+        c = det.location
+        fine = b2.build_candidate_grid(
+            b2.LatLonBounds(c.lat_deg - 50 * m100, c.lat_deg + 50 * m100,
+                            c.lon_deg - 50 * m100, c.lon_deg + 50 * m100), m100)
+        assert (fine.lat.count, fine.lon.count) == (101, 101)
+        r = b2.geolocate_arrays(fine, states, caps, fs, fc, b2.GeolocateOptions(detect=False),
+                                want_per_snapshot=False)
+        exact = _oracle_acc(orc, states, caps, fs, fc, fine.points[r.argmax_index])
+        assert r.argmax_value == pytest.approx(exact, rel=1e-12)
+        sample = list(rng.integers(0, fine.size(), 8))
+        w = np.array([_oracle_acc(orc, states, caps, fs, fc, fine.points[p]) for p in sample])
+        assert rel_err(r.accumulated.values[sample], w).max() <= REL_TOL
