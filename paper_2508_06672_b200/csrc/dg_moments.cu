@@ -175,13 +175,16 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
         const int bf = kb / B, bl = (ke - 1) / B;      // the bucket's absolute block range
         const int babs = c * CB + blk;
         const bool active = u >= 0 && babs >= bf && babs <= bl;
+        const int lo = kb - babs * B, hi = ke - babs * B;  // valid j in [lo, hi)
+        // warps whose blocks all lie inside their buckets' overlaps skip the
+        // per-sample masks (all but the first / last block of each bucket)
+        const bool interior = __all_sync(0xffffffffu, !active || (lo <= 0 && hi >= B));
         mbar_wait(&full[buf], (k >> 1) & 1);
         if (active) {
             const float2* st = stage + (size_t)buf * L::stage_f2;
             const float2* r1 = st + blk * RS1;
             // y2 samples [bB + d ..) start at offset t of the window row
             const float2* r2 = st + CB * RS1 + blk * RS2 + t;
-            const int lo = kb - babs * B, hi = ke - babs * B;  // valid j in [lo, hi)
             // two-level accumulation: sums of 16 pairs, then their sum, so the
             // FP32 rounding of coherent partial sums stays ~16x below one
             // sequential 256-pair run
@@ -200,10 +203,14 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
                     const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
                     const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
                     const float2 zero = make_float2(0.f, 0.f);
-                    const float2 z0 = (j >= lo && j < hi) ? cmulc(f1, f2, 0) : zero;
-                    const float2 z1 = (j + 1 >= lo && j + 1 < hi) ? cmulc(f1, f2, 1) : zero;
-                    const float2 w1 = (B - 2 - j >= lo && B - 2 - j < hi) ? cmulc(g1, g2, 0) : zero;
-                    const float2 w0 = (B - 1 - j >= lo && B - 1 - j < hi) ? cmulc(g1, g2, 1) : zero;
+                    float2 z0 = cmulc(f1, f2, 0), z1 = cmulc(f1, f2, 1);
+                    float2 w1 = cmulc(g1, g2, 0), w0 = cmulc(g1, g2, 1);
+                    if (!interior) {
+                        if (!(j >= lo && j < hi)) z0 = zero;
+                        if (!(j + 1 >= lo && j + 1 < hi)) z1 = zero;
+                        if (!(B - 2 - j >= lo && B - 2 - j < hi)) w1 = zero;
+                        if (!(B - 1 - j >= lo && B - 1 - j < hi)) w0 = zero;
+                    }
                     // pair j: (z0, w0); pair j+1: (z1, w1)
                     const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
                     const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
