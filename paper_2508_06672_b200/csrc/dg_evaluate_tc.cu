@@ -357,15 +357,20 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                     float v[2][16];
                     tmem_ld16(lane_addr + (uint32_t)gc, v[0]);
                     tmem_ld16(lane_addr + (uint32_t)(gc + 16), v[1]);
-                    float2 A = make_float2(0.f, 0.f), V = A, E2 = A;
+                    // two interleaved chains per sum (blocks 0-7 / 8-15 of the group)
+                    float2 A0 = make_float2(0.f, 0.f), V0 = A0, E0 = A0, A1 = A0, V1 = A0, E1 = A0;
 #pragma unroll
-                    for (int j = 0; j < G; ++j) {
-                        const float2 C =
-                            make_float2(v[j >> 3][2 * (j & 7)], v[j >> 3][2 * (j & 7) + 1]);
-                        A = ffma2(C, wtr[j], A);
-                        V = ffma2(C, wti[j], V);
-                        E2 = ffma2v(C, C, E2);
+                    for (int j = 0; j < 8; ++j) {
+                        const float2 C0 = make_float2(v[0][2 * j], v[0][2 * j + 1]);
+                        const float2 C1 = make_float2(v[1][2 * j], v[1][2 * j + 1]);
+                        A0 = ffma2(C0, wtr[j], A0);
+                        A1 = ffma2(C1, wtr[j + 8], A1);
+                        V0 = ffma2(C0, wti[j], V0);
+                        V1 = ffma2(C1, wti[j + 8], V1);
+                        E0 = ffma2v(C0, C0, E0);
+                        E1 = ffma2v(C1, C1, E1);
                     }
+                    const float2 A = add2(A0, A1), V = add2(V0, V1), E2 = add2(E0, E1);
                     const double hr = (double)(A.x - V.y), hi = (double)(A.y + V.x);
                     acc_re = fma(ar, hr, fma(-ai, hi, acc_re));
                     acc_im = fma(ar, hi, fma(ai, hr, acc_im));
