@@ -271,21 +271,23 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         const double qscale = sqrt((double)q2s);
 
         for (int t0 = 0; t0 < bk.count; t0 += 128) {
-            if (t0 > 0) {
-                p = t0 + tid < bk.count ? sorted[bk.start + t0 + tid] : -1;
-                fd = t0 + tid < bk.count ? sfdoa[bk.start + t0 + tid] : 0.0;
-            }
             const double nu = p >= 0 ? fd / fs - nu_c : 0.0;
+            const int pc = p;  // this tile's candidate; p / fd now prefetch the next tile's
+            {
+                const int nx = t0 + 128 + tid;
+                p = nx < bk.count ? sorted[bk.start + nx] : -1;
+                fd = nx < bk.count ? sfdoa[bk.start + nx] : 0.0;
+            }
             // warps without a candidate in this tile skip the Bessel terms and the
             // epilogue (their A rows are zero); tcgen05.ld stays warp-uniform
-            const bool warp_live = __any_sync(0xffffffffu, p >= 0);
+            const bool warp_live = __any_sync(0xffffffffu, pc >= 0);
             // ---- A operand: this thread's candidate, c_m rounded to FP32 (as the
             // FFMA2 path) and split exactly into three BF16 parts ----
             {
                 float cf[kTcK];
 #pragma unroll
                 for (int m = 0; m < kTcK; ++m) cf[m] = 0.f;
-                if (p >= 0) {
+                if (pc >= 0) {
                     double jv[R];
                     bessel_j<R>(3.141592653589793 * nu * (double)B, jv);
 #pragma unroll
@@ -382,11 +384,11 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                 tc_fence_before();  // this chunk's TMEM reads done before the next MMAs
                 __syncthreads();
             }
-            if (p >= 0) {
+            if (pc >= 0) {
                 const double sv = sqrt(acc_re * acc_re + acc_im * acc_im);
-                s_out[p] = sv;
+                s_out[pc] = sv;
                 if (sv < (double)tau * fmax(sqrt(en), qscale)) {
-                    const int64_t e = flag_base + p;
+                    const int64_t e = flag_base + pc;
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
             }
