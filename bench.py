@@ -63,7 +63,7 @@ FLOP_PER_SAMPLE = 20.0  # correlate.hpp:60-68 as executed
 
 
 def make_inputs(name: str, spacing_km: float = 1.0, n_snapshots: int | None = None,
-                reference: bool = False):
+                reference: bool = False, engine=None):
     """The SURVEY.md §8d inputs of a workload: the reference's simulate_scenario
     scene (paper_scenario.cfg receivers and emitters, tests/scenes.py), either
     synthesised on the GPU by the engine's simulator (scenario values bit for
@@ -82,7 +82,7 @@ def make_inputs(name: str, spacing_km: float = 1.0, n_snapshots: int | None = No
         sc = RefLib().simulate(scenes.render(scene))
         return sc.states, sc.captures, bounds, scene["grid_spacing_deg"]
     import paper_2508_06672_b200.simulate as sim
-    states, caps, _, _ = sim.simulate_arrays(scenes.to_scenario(sim, scene))
+    states, caps, _, _ = sim.simulate_arrays(scenes.to_scenario(sim, scene), engine=engine)
     return states, caps, bounds, scene["grid_spacing_deg"]
 
 
@@ -225,9 +225,9 @@ def b200_arm(args, rank, world):
             dist.init_process_group("gloo")
     coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     cfg = WORKLOADS[args.config]
-    states, caps, bounds, spacing = make_inputs(args.config, args.spacing_km)
-    S, R, N = caps.shape
     eng = b2.default_engine(dev)
+    states, caps, bounds, spacing = make_inputs(args.config, args.spacing_km, engine=eng)
+    S, R, N = caps.shape
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing, 0.0, engine=eng)
     P = grid.size()
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], FC, engine=eng)
