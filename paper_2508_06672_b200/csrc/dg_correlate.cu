@@ -263,11 +263,8 @@ void launch_variant(int n_tasks_max, cudaStream_t st, const Task* tasks, const i
                     int N, double fs, double* s_out, uint32_t* flag_bits, int64_t flag_base) {
     auto kern = k_correlate<NC, LB, CH, WPC, MINB>;
     const size_t smem = sizeof(WarpSmemT<CH>) * WPC;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    static size_t attr[64] = {};
+    ensure_smem(kern, smem, attr);
     const int blocks = (n_tasks_max + WPC - 1) / WPC;
     kern<<<blocks, 32 * WPC, smem, st>>>(tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
                                          flag_bits, flag_base);

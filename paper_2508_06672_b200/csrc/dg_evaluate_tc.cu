@@ -415,11 +415,8 @@ void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue
     size_t smem = L.bytes;
     const size_t floor_bytes = (size_t)(228 * 1024) / (per_sm + 1) + 1024;
     if (smem < floor_bytes) smem = floor_bytes;
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    static size_t attr[64] = {};
+    ensure_smem(kern, smem, attr);
     // resident CTAs: TMEM-bound, or shared-memory-bound (228 KB per SM, 1 KB
     // reserved per CTA, ~1 KB of static shared memory)
     int resident = (int)((228 * 1024) / (smem + 2048));

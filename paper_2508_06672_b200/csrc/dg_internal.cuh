@@ -206,6 +206,19 @@ void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int*
                         uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
                         cudaStream_t st);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the current device, once
+// per (call site, device, larger size): function attributes are per device and one
+// process may drive engines on several GPUs
+template <class K>
+inline void ensure_smem(K kern, size_t smem, size_t (&done)[64]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || smem > done[dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (dev < 64) done[dev] = smem;
+    }
+}
+
 // exact FP64 reference-order re-evaluation of flagged elements
 // elem = s*pairs*P + pair*P + p ; (geolocate path recomputes geometry)
 void launch_count_flags(const uint32_t* bits, int64_t n_words, unsigned long long* count,

@@ -495,11 +495,8 @@ void moments_variant(MomArgs a, int sm_count, cudaStream_t st) {
     a.cpb = ((a.N + B - 1) / B + L::CB - 1) / L::CB;
     auto kern = k_moments<B, R>;
     const size_t smem = MomLayout<B, R>::smem;
-    static const bool attr = [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return true;
-    }();
-    (void)attr;
+    static size_t attr[64] = {};
+    ensure_smem(kern, smem, attr);
     const int items = a.ngroups * a.cpb;
     const int grid = items < sm_count ? (items > 0 ? items : 1) : sm_count;
     kern<<<grid, kMomThreads, smem, st>>>(a.buckets, a.ubin, a.bin0, a.nbins, a.bin_lo, a.ngroups,
@@ -525,11 +522,8 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
                       int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
     auto kern = k_evaluate<R, kEvalG>;
     const size_t smem = evaluate_smem(nbmax, R);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
+    static size_t attr[64] = {};
+    ensure_smem(kern, smem, attr);
     int grid = sm_count * 4;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
     kern<<<grid, 32 * kEvalWarps, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c,

@@ -363,14 +363,11 @@ void launch_fractional_fwd(const double2* tx, int64_t n_tx, int guard, int l, do
     const int l1 = l / 2, l2 = l - l1;
     const size_t col_smem = ((size_t)(kColTile << l1) + (1 << (l1 - 1))) * sizeof(double2);
     const size_t row_smem = ((size_t)(1 << l2) + (1 << (l2 - 1))) * sizeof(double2);
-    static bool attr = [] {
-        cudaFuncSetAttribute(k_fft_cols_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-        cudaFuncSetAttribute(k_fft_rows_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-        cudaFuncSetAttribute(k_fft_rows_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-        cudaFuncSetAttribute(k_fft_cols_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
-        return true;
-    }();
-    (void)attr;
+    static size_t a0[64] = {}, a1[64] = {}, a2[64] = {}, a3[64] = {};
+    ensure_smem(k_fft_cols_fwd, 200 << 10, a0);
+    ensure_smem(k_fft_rows_fwd, 200 << 10, a1);
+    ensure_smem(k_fft_rows_inv, 200 << 10, a2);
+    ensure_smem(k_fft_cols_inv, 200 << 10, a3);
     k_fft_cols_fwd<<<(1 << l2) / kColTile, kFftThreads, col_smem, st>>>(tx, n_tx, guard, l1, l2,
                                                                           spec);
     k_fft_rows_fwd<<<1 << l1, kFftThreads, row_smem, st>>>(l1, l2, spec);
