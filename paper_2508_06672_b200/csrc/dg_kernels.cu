@@ -731,6 +731,101 @@ __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ 
     }
 }
 
+// The same exact chains with the work of one chain spread over three warps of a
+// CTA (bit-identical: every FP64 operation and its order are the reference's,
+// only the thread that executes it changes). Per tile of kRrT samples, double
+// buffered: warp 1 forms the products p_k = y1[k] conj(y2[k+d]) (independent per
+// sample, all lanes), warp 2 lane 0 runs the phasor recurrence, warp 0 lane 0 the
+// accumulation acc += p_k ph_k; the single-lane chains issue 6-8 FP64 operations
+// per sample instead of 22, and the two chains overlap.
+constexpr int kRrT = 256;
+
+__device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* __restrict__ y2,
+                                int N, long long d, double fdoa, double fs, double* out) {
+    __shared__ double2 pbuf[2][kRrT], hbuf[2][kRrT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long kb = d < 0 ? -d : 0;
+    const long long ke = (N - d) < N ? (N - d) : N;
+    if (kb >= ke) {
+        if (tid == 0) *out = 0.0;
+        return;
+    }
+    const double step = __ddiv_rn(__dmul_rn(kTwoPi, fdoa), fs);
+    double rot_im, rot_re, ph_im, ph_re;
+    sincos(step, &rot_im, &rot_re);
+    sincos(__dmul_rn(step, (double)kb), &ph_im, &ph_re);
+    double acc_re = 0.0, acc_im = 0.0;
+    const double2* b = y2 + d;
+    const long long n = ke - kb;
+    const int ntile = (int)((n + kRrT - 1) / kRrT);
+    auto produce = [&](int t) {  // warps 1 and 2: tile t into buffer t & 1
+        const long long k0 = kb + (long long)t * kRrT;
+        const int len = (int)min((long long)kRrT, ke - k0);
+        const int bf = t & 1;
+        if (warp == 1) {
+            for (int i = lane; i < len; i += 32) {
+                const double2 a = __ldg(y1 + k0 + i), bb = __ldg(b + k0 + i);
+                const double b_re = bb.x, b_im = -bb.y;
+                pbuf[bf][i] = make_double2(__dsub_rn(__dmul_rn(a.x, b_re), __dmul_rn(a.y, b_im)),
+                                           __dadd_rn(__dmul_rn(a.x, b_im), __dmul_rn(a.y, b_re)));
+            }
+        } else if (warp == 2 && lane == 0) {
+#pragma unroll 4
+            for (int i = 0; i < len; ++i) {
+                hbuf[bf][i] = make_double2(ph_re, ph_im);
+                const double nr = __dsub_rn(__dmul_rn(ph_re, rot_re), __dmul_rn(ph_im, rot_im));
+                ph_im = __dadd_rn(__dmul_rn(ph_re, rot_im), __dmul_rn(ph_im, rot_re));
+                ph_re = nr;
+            }
+        }
+    };
+    produce(0);
+    __syncthreads();
+    for (int t = 0; t < ntile; ++t) {
+        if (t + 1 < ntile) produce(t + 1);
+        if (warp == 0 && lane == 0) {
+            const int bf = t & 1;
+            const int len = (int)min((long long)kRrT, n - (long long)t * kRrT);
+#pragma unroll 8
+            for (int i = 0; i < len; ++i) {
+                const double2 pk = pbuf[bf][i], hk = hbuf[bf][i];
+                acc_re = __dadd_rn(acc_re, __dsub_rn(__dmul_rn(pk.x, hk.x), __dmul_rn(pk.y, hk.y)));
+                acc_im = __dadd_rn(acc_im, __dadd_rn(__dmul_rn(pk.x, hk.y), __dmul_rn(pk.y, hk.x)));
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0)
+        *out = __dsqrt_rn(__dadd_rn(__dmul_rn(acc_re, acc_re), __dmul_rn(acc_im, acc_im)));
+}
+
+__global__ void __launch_bounds__(96)
+k_rerank_cta(const int* __restrict__ cells, const int* __restrict__ n_cells, int cap, int SP,
+             RefineCtx c, double* __restrict__ ex) {
+    const int n = min(*n_cells, cap);
+    const int64_t total = (int64_t)n * SP;
+    for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+        const int64_t ci = i / SP, sp = i - ci * SP;
+        const int64_t p = cells[ci];
+        const double2 *y1, *y2;
+        long long tdoa;
+        double fdoa;
+        if (c.offsets) {
+            tdoa = c.offsets[p].tdoa_samples;
+            fdoa = c.offsets[p].fdoa_hz;
+            y1 = c.y64;
+            y2 = c.y64 + c.stride;
+        } else {
+            const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
+            offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
+            y1 = c.y64 + (s * c.R + c.pair_rx[2 * pr]) * c.stride;
+            y2 = c.y64 + (s * c.R + c.pair_rx[2 * pr + 1]) * c.stride;
+        }
+        exact_chain_cta(y1, y2, c.N, tdoa, fdoa, c.fs, ex + i);
+        __syncthreads();
+    }
+}
+
 // per candidate: pair sums (correlate_snapshot_all_pairs), optional median
 // scaling, accumulation over snapshots in order (accumulate_grids)
 __global__ void k_recombine_cells(const int* __restrict__ n_cells, int cap,
@@ -1118,9 +1213,13 @@ void launch_select_near(const double* v, int64_t P, const double* vmax, double r
 void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
                    RefineCtx ctx, double* ex, cudaStream_t st) {
     const int64_t items = (int64_t)std::min(n_items_hint, cap) * SP;
-    const int stride = items <= 148 * 16 ? 32 : 1;  // one chain per warp when they fit
-    k_rerank<<<blocks_for((int64_t)cap * SP * stride, 64, 148LL * 64), 64, 0, st>>>(
-        cells, n_cells, cap, SP, ctx, ex, stride);
+    if (items <= 148 * 16) {  // one three-warp CTA per chain
+        k_rerank_cta<<<(int)std::max<int64_t>(items, 1), 96, 0, st>>>(cells, n_cells, cap, SP,
+                                                                      ctx, ex);
+        return;
+    }
+    k_rerank<<<blocks_for((int64_t)cap * SP, 64, 148LL * 64), 64, 0, st>>>(cells, n_cells, cap,
+                                                                           SP, ctx, ex, 1);
 }
 
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
