@@ -542,26 +542,33 @@ __device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, 
     return correlate_exact(y1, y2, c.N, tdoa, fdoa, c.fs);
 }
 
-// Eq. 11 in FP64 for one element, split across the 32 lanes of a warp: lane l
-// takes samples kb + l + 32 t with its own phasor (FP64 sincos of the exact
-// FP64-reduced start phase, FP64 recurrence by e^{i 32 step}), fixed-order
-// butterfly sum. Agrees with the reference's single recurrence to ~1e-12
-// relative — far inside the 1e-4 contract the refinement exists to meet.
-__device__ double correlate_fp64_warp(const double2* __restrict__ y1, const double2* __restrict__ y2,
-                                      int N, long long d, double fdoa, double fs, int lane) {
+// Eq. 11 in FP64 for one element, split across a group of T threads (a warp, or
+// a whole 256-thread CTA for long captures): thread t takes samples kb + t + T j
+// with its own phasor (FP64 sincos of the exact FP64-reduced start phase, FP64
+// recurrence by e^{i 2 pi T nu}); warp butterflies, then the warp sums in order.
+// Agrees with the reference's single recurrence to ~1e-12 relative — far inside
+// the 1e-4 contract the refinement exists to meet. T is chosen from N alone
+// (refine_group), so every partition of a run computes the same bits.
+constexpr int kRefThreads = 256;
+
+template <int T>
+__device__ double correlate_fp64_group(const double2* __restrict__ y1,
+                                       const double2* __restrict__ y2, int N, long long d,
+                                       double fdoa, double fs) {
+    const int t = threadIdx.x % T, lane = threadIdx.x & 31;
     const long long kb = d < 0 ? -d : 0;
     const long long ke = (N - d) < N ? (N - d) : N;
     double acc_re = 0.0, acc_im = 0.0;
     if (kb < ke) {
-        const double nu = fdoa / fs;  // cycles per sample
-        const long long k0 = kb + lane;
+        const double nu = fdoa / fs;
+        const long long k0 = kb + t;
         const double ph0 = nu * (double)k0;
         double pr, pi_, rr, ri;
         sincospi(2.0 * (ph0 - rint(ph0)), &pi_, &pr);
-        const double st = nu * 32.0;
+        const double st = nu * (double)T;
         sincospi(2.0 * (st - rint(st)), &ri, &rr);
         const double2* b = y2 + d;
-        for (long long k = k0; k < ke; k += 32) {
+        for (long long k = k0; k < ke; k += T) {
             const double2 a = __ldg(y1 + k), bb = __ldg(b + k);
             const double zr = a.x * bb.x + a.y * bb.y, zi = a.y * bb.x - a.x * bb.y;
             acc_re += zr * pr - zi * pi_;
@@ -576,31 +583,52 @@ __device__ double correlate_fp64_warp(const double2* __restrict__ y1, const doub
         acc_re += __shfl_xor_sync(0xffffffffu, acc_re, o);
         acc_im += __shfl_xor_sync(0xffffffffu, acc_im, o);
     }
+    if constexpr (T > 32) {
+        __shared__ double part[2][T / 32];
+        const int warp = threadIdx.x >> 5;
+        if (lane == 0) {
+            part[0][warp] = acc_re;
+            part[1][warp] = acc_im;
+        }
+        __syncthreads();
+        acc_re = acc_im = 0.0;
+#pragma unroll
+        for (int w = 0; w < T / 32; ++w) {
+            acc_re += part[0][w];
+            acc_im += part[1][w];
+        }
+        __syncthreads();  // `part` is reused by the next element
+    }
     return sqrt(acc_re * acc_re + acc_im * acc_im);
 }
 
-__global__ void k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx c) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = w0; i < n; i += nw) {
+// threads per element: the whole CTA for long captures (few, long chains), a warp
+// otherwise; a function of N only
+inline bool refine_cta(int N) { return N >= 131072; }
+
+template <int T>
+__global__ void __launch_bounds__(kRefThreads)
+k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx c) {
+    const int per = kRefThreads / T;
+    for (int64_t i = (int64_t)blockIdx.x * per + threadIdx.x / T; i < n;
+         i += (int64_t)gridDim.x * per) {
         const int64_t e = list[i];
         const int64_t sp = e / c.P, p = e - sp * c.P;
         double v;
         if (c.offsets) {
             const dg_pair_offsets o = c.offsets[p];
-            v = correlate_fp64_warp(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz, c.fs,
-                                    lane);
+            v = correlate_fp64_group<T>(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz,
+                                        c.fs);
         } else {
             const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
             long long tdoa;
             double fdoa;
             offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
             const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
-            v = correlate_fp64_warp(c.y64 + (s * c.R + ri) * c.stride,
-                                    c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa, fdoa, c.fs, lane);
+            v = correlate_fp64_group<T>(c.y64 + (s * c.R + ri) * c.stride,
+                                        c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa, fdoa, c.fs);
         }
-        if (lane == 0) c.raw[e] = v;
+        if (threadIdx.x % T == 0) c.raw[e] = v;
     }
 }
 
@@ -608,14 +636,14 @@ __global__ void k_refine(const int64_t* __restrict__ list, int64_t n, RefineCtx 
 // steps): `list` holds indices relative to element `base` of a bitmap laid out
 // one P32-element row per step (P32 = P rounded up to 32), `count` is on the
 // device (k_compact_flags), raw surfaces are dense [step][P].
-__global__ void k_refine_rows(const int64_t* __restrict__ list,
-                              const unsigned long long* __restrict__ count, int64_t base,
-                              int64_t P32, RefineCtx c) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+template <int T>
+__global__ void __launch_bounds__(kRefThreads)
+k_refine_rows(const int64_t* __restrict__ list, const unsigned long long* __restrict__ count,
+              int64_t base, int64_t P32, RefineCtx c) {
     const int64_t n = (int64_t)*count;
-    for (int64_t i = w0; i < n; i += nw) {
+    const int per = kRefThreads / T;
+    for (int64_t i = (int64_t)blockIdx.x * per + threadIdx.x / T; i < n;
+         i += (int64_t)gridDim.x * per) {
         const int64_t e = base + list[i];
         const int64_t sp = e / P32, p = e - sp * P32;
         const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
@@ -623,10 +651,10 @@ __global__ void k_refine_rows(const int64_t* __restrict__ list,
         double fdoa;
         offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &fdoa);
         const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
-        const double v = correlate_fp64_warp(c.y64 + (s * c.R + ri) * c.stride,
-                                             c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa, fdoa,
-                                             c.fs, lane);
-        if (lane == 0) c.raw[sp * c.P + p] = v;
+        const double v = correlate_fp64_group<T>(c.y64 + (s * c.R + ri) * c.stride,
+                                                 c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa,
+                                                 fdoa, c.fs);
+        if (threadIdx.x % T == 0) c.raw[sp * c.P + p] = v;
     }
 }
 
@@ -1178,12 +1206,21 @@ void launch_refine_rows(const uint32_t* bits, int64_t row0, int64_t row1, int64_
     const int64_t w0 = row0 * (P32 / 32), nw = (row1 - row0) * (P32 / 32);
     cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
     k_compact_flags<<<blocks_for(nw, 256, 148LL * 8), 256, 0, st>>>(bits + w0, nw, list, count);
-    k_refine_rows<<<148 * 16, 256, 0, st>>>(list, count, row0 * P32, P32, ctx);
+    if (refine_cta(ctx.N))
+        k_refine_rows<kRefThreads><<<148 * 8, kRefThreads, 0, st>>>(list, count, row0 * P32, P32,
+                                                                    ctx);
+    else
+        k_refine_rows<32><<<148 * 16, kRefThreads, 0, st>>>(list, count, row0 * P32, P32, ctx);
 }
 
 void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st) {
     if (n <= 0) return;
-    k_refine<<<blocks_for(n * 32, 256, 148LL * 16), 256, 0, st>>>(list, n, ctx);
+    if (refine_cta(ctx.N))
+        k_refine<kRefThreads><<<(int)std::min<int64_t>(n, 148 * 8), kRefThreads, 0, st>>>(list, n,
+                                                                                         ctx);
+    else
+        k_refine<32><<<blocks_for(n * 32, kRefThreads, 148LL * 16), kRefThreads, 0, st>>>(list, n,
+                                                                                         ctx);
 }
 
 void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
