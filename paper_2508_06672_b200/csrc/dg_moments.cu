@@ -85,11 +85,11 @@ struct MomLayout {
     static constexpr int CB = B >= 512 ? 8 : 16;       // blocks per item
     static constexpr int BPW = 32 / CB;                // TDOA values per warp
     static constexpr int G = BPW * kMomWarps;           // TDOA values per item
-    static constexpr int RP = (R + 3) / 4 * 4;          // table row (floats)
+    static constexpr int RP = (2 * R + 3) / 4 * 4;      // table row: T_m(t_j), T_m(t_j+1) pairs
     static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
     static constexpr int W2 = B + G + 2;                // y2 window samples copied
     static constexpr int RS2 = (W2 + 13) / 16 * 16 + 2; // y2 row: 2 float2 mod 16
-    static constexpr size_t table_floats = (size_t)B / 2 * RP;
+    static constexpr size_t table_floats = (size_t)B / 4 * RP;  // one row per two folded pairs
     static constexpr size_t stage_f2 = (size_t)CB * (RS1 + RS2);  // one buffer
     static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
                                    2 * stage_f2 * sizeof(float2);
@@ -147,8 +147,10 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
         }
     };
 
-    for (int i = tid; i < B / 2 * RP; i += kMomThreads)
-        ts[i] = tcheb[(i / RP) * kMaxMoments + (i % RP)];
+    for (int i = tid; i < B / 4 * RP; i += kMomThreads) {  // row r: pairs 2r, 2r + 1
+        const int r = i / RP, q = i % RP;
+        ts[i] = q < 2 * R ? tcheb[(2 * r + (q & 1)) * kMaxMoments + (q >> 1)] : 0.f;
+    }
     if (tid == 0) {
         mbar_init(&full[0], 1);
         mbar_init(&full[1], 1);
@@ -216,15 +218,13 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
                     const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
                     const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
                     const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
-                    const float4* t0 = reinterpret_cast<const float4*>(ts + j * RP);
-                    const float4* t1 = reinterpret_cast<const float4*>(ts + (j + 1) * RP);
+                    // (T_m(t_j), T_m(t_j+1)) for m = 2qq, 2qq + 1 in one LDS.128
+                    const float4* tr = reinterpret_cast<const float4*>(ts + (j >> 1) * RP);
 #pragma unroll
-                    for (int qq = 0; qq < RP / 4; ++qq) {
-                        const float4 a = t0[qq], bq = t1[qq];
-                        if (4 * qq + 0 < R) part[4 * qq + 0] = ffma2(u1, bq.x, ffma2(u0, a.x, part[4 * qq + 0]));
-                        if (4 * qq + 1 < R) part[4 * qq + 1] = ffma2(v1, bq.y, ffma2(v0, a.y, part[4 * qq + 1]));
-                        if (4 * qq + 2 < R) part[4 * qq + 2] = ffma2(u1, bq.z, ffma2(u0, a.z, part[4 * qq + 2]));
-                        if (4 * qq + 3 < R) part[4 * qq + 3] = ffma2(v1, bq.w, ffma2(v0, a.w, part[4 * qq + 3]));
+                    for (int qq = 0; qq < R / 2; ++qq) {
+                        const float4 t = tr[qq];
+                        part[2 * qq] = ffma2(u1, t.y, ffma2(u0, t.x, part[2 * qq]));
+                        part[2 * qq + 1] = ffma2(v1, t.w, ffma2(v0, t.z, part[2 * qq + 1]));
                     }
                 }
 #pragma unroll
