@@ -336,21 +336,36 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                     mma_commit(&mma_bar);
                 }
                 if (c0 == 0 && warp_live) {
-                    // W_j = W_1^j (FP64 recurrence, one FP32 rounding each) while the MMAs run
+                    // W_j = W_1^j while the MMAs run: W_0..W_4 by an FP64 recurrence,
+                    // W_8 = W_4^2, W_12 = W_8 W_4, W_16 = W_8^2 in FP64, each rounded
+                    // once to FP32; W_{4a+b} = W_{4a} W_b as one FP32 complex product
                     const double x1 = nu * (double)B;
                     double w1r, w1i;
                     sincospi(2.0 * (x1 - rint(x1)), &w1i, &w1r);
-                    double pr = 1.0, pi_ = 0.0;
+                    double br[5], bi[5];
+                    br[0] = 1.0;
+                    bi[0] = 0.0;
 #pragma unroll
-                    for (int j = 0; j < G; ++j) {
-                        wtr[j] = (float)pr;
-                        wti[j] = (float)pi_;
-                        const double nr = fma(pr, w1r, -pi_ * w1i);
-                        pi_ = fma(pr, w1i, pi_ * w1r);
-                        pr = nr;
+                    for (int j = 1; j <= 4; ++j) {
+                        br[j] = fma(br[j - 1], w1r, -bi[j - 1] * w1i);
+                        bi[j] = fma(br[j - 1], w1i, bi[j - 1] * w1r);
                     }
-                    sr = pr;
-                    si = pi_;
+                    const double w8r = fma(br[4], br[4], -bi[4] * bi[4]), w8i = 2.0 * br[4] * bi[4];
+                    const double w12r = fma(w8r, br[4], -w8i * bi[4]);
+                    const double w12i = fma(w8r, bi[4], w8i * br[4]);
+                    sr = fma(w8r, w8r, -w8i * w8i);
+                    si = 2.0 * w8r * w8i;
+                    const float hr[4] = {1.f, (float)br[4], (float)w8r, (float)w12r};
+                    const float hi4[4] = {0.f, (float)bi[4], (float)w8i, (float)w12i};
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const float lr = (float)br[b], li = (float)bi[b];
+#pragma unroll
+                        for (int a = 0; a < 4; ++a) {
+                            wtr[4 * a + b] = fmaf(hr[a], lr, -hi4[a] * li);
+                            wti[4 * a + b] = fmaf(hr[a], li, hi4[a] * lr);
+                        }
+                    }
                 }
                 mbar_wait(&mma_bar, mma_phase);
                 mma_phase ^= 1;
