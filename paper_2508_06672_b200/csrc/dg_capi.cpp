@@ -239,7 +239,8 @@ struct Pipeline {
 
     // lanes: 2 overlap consecutive steps; 1 serialises them (profiled runs, so
     // each kernel's CUDA-event time is its own)
-    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms, int max_lanes = 2) {
+    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms, int max_lanes = 2,
+              cudaStream_t lane1 = nullptr) {
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
@@ -271,6 +272,8 @@ struct Pipeline {
             Lane& L = lanes[l];
             if (l == 0) {
                 L.st = sc.st;
+            } else if (lane1) {
+                L.st = lane1;
             } else {
                 CK(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
                 L.own_stream = true;
@@ -374,30 +377,23 @@ struct Pipeline {
         }
     }
 
-    unsigned long long work_total(Scratch& sc, int which) {
-        unsigned long long t = 0;
-        for (int l = 0; l < n_lanes; ++l) {
-            unsigned long long w[3] = {0, 0, 0};
-            CK(cudaMemcpyAsync(w, lanes[l].work, sizeof w, cudaMemcpyDeviceToHost, sc.st));
-            CK(cudaStreamSynchronize(sc.st));
-            t += w[which];
-        }
-        return t;
-    }
-
     // FP32 planning ranges over the full lattice of `g` for steps pg[0..n)
+    // (run after the geometry pass: beside it, at one CTA per SM, this pass was
+    // slower than the two in sequence)
+    std::vector<RxPairF32> h_rx;  // members: alive until plan_window synchronises
+    std::vector<StepRange> h_init;
     StepRange* lattice_ranges(Scratch& sc, const dg_grid* g, const PairGeom* pg_host,
                               int n, double fs, double wl) {
-        auto rx = rx_pairs_f32(g, pg_host, n);
+        h_rx = rx_pairs_f32(g, pg_host, n);
+        h_init.assign(n, StepRange{});
+        for (auto& r : h_init) step_range_init(&r);
         auto* rx_dev = sc.alloc<RxPairF32>(n);
         auto* out = sc.alloc<StepRange>(n);
-        std::vector<StepRange> init(n);
-        for (auto& r : init) step_range_init(&r);
-        CK(cudaMemcpyAsync(rx_dev, rx.data(), n * sizeof(RxPairF32), cudaMemcpyHostToDevice,
+        CK(cudaMemcpyAsync(rx_dev, h_rx.data(), n * sizeof(RxPairF32), cudaMemcpyHostToDevice,
                            sc.st));
-        CK(cudaMemcpyAsync(out, init.data(), n * sizeof(StepRange), cudaMemcpyHostToDevice, sc.st));
+        CK(cudaMemcpyAsync(out, h_init.data(), n * sizeof(StepRange), cudaMemcpyHostToDevice,
+                           sc.st));
         launch_range_fp32(g->rel32(), g->full_size, rx_dev, n, fs, wl, out, sc.st);
-        CK(cudaStreamSynchronize(sc.st));  // host vectors of this frame
         launches += 1;
         return out;
     }
@@ -474,9 +470,9 @@ int64_t run_refine(Scratch& sc, const uint32_t* bits, int64_t n_elems, const Ref
     return (int64_t)n;
 }
 
-// Refinement of batches of steps on a side stream: batch j (steps
-// [jK, (j+1)K)) starts once those steps' correlators finished (events on their
-// lanes) and runs on the FP64 pipes while the lanes correlate later steps.
+// Refinement of batches of steps on a side stream: a batch (up to K steps)
+// starts once those steps' correlators finished (events on their lanes) and
+// runs on the FP64 pipes while the lanes correlate later steps.
 // K = 0: everything refined at the end on the main stream (profiled runs).
 struct SideRefine {
     Scratch& sc;
@@ -488,14 +484,19 @@ struct SideRefine {
     unsigned long long* counts = nullptr;  // one per batch
     int next = 0, batches = 0;
     int64_t launches = 0;
-    SideRefine(Scratch& s, int n_steps, int64_t P_, int64_t P32_, int K_)
+    bool own_rs = false;
+    SideRefine(Scratch& s, int n_steps, int64_t P_, int64_t P32_, int K_, cudaStream_t side)
         : sc(s), steps(n_steps), K(K_), P(P_), P32(P32_) {
-        const int nb = K > 0 ? (steps + K - 1) / K : 1;
+        const int nb = K > 0 ? steps : 1;  // at most one batch per step
         counts = sc.alloc<unsigned long long>(nb);
         CK(cudaMemsetAsync(counts, 0, nb * sizeof(unsigned long long), sc.st));
         list = sc.alloc<int64_t>((size_t)(K > 0 ? std::min(K, steps) : steps) * P32);
         if (K > 0) {
-            CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+            rs = side;
+            if (!rs) {
+                CK(cudaStreamCreateWithFlags(&rs, cudaStreamNonBlocking));
+                own_rs = true;
+            }
             ev.resize(steps);
             for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             // list/counts were allocated on the main stream
@@ -508,7 +509,7 @@ struct SideRefine {
     }
     ~SideRefine() {
         for (auto e : ev) cudaEventDestroy(e);
-        if (rs) cudaStreamDestroy(rs);
+        if (own_rs && rs) cudaStreamDestroy(rs);
     }
     void launch_batch(const uint32_t* bits, const RefineCtx& ctx, int r0, int r1,
                       cudaStream_t st) {
@@ -519,7 +520,10 @@ struct SideRefine {
     void step_done(int s, cudaStream_t lane, const uint32_t* bits, const RefineCtx& ctx) {
         if (K <= 0) return;
         CK(cudaEventRecord(ev[s], lane));
-        if (s + 1 - next >= K) {
+        // batches of K steps, shrinking towards the end (a batch is due once it
+        // holds as many steps as remain after it), so the refinement left after
+        // the last correlation is about one step's
+        if (s + 1 - next >= std::min(K, steps - 1 - s)) {
             for (int i = next; i <= s; ++i) CK(cudaStreamWaitEvent(rs, ev[i], 0));
             launch_batch(bits, ctx, next, s + 1, rs);
             next = s + 1;
@@ -540,15 +544,6 @@ struct SideRefine {
         CK(cudaEventRecord(done, rs));
         CK(cudaStreamWaitEvent(sc.st, done, 0));
         cudaEventDestroy(done);
-    }
-    unsigned long long total() {
-        std::vector<unsigned long long> h(std::max(batches, 1));
-        CK(cudaMemcpyAsync(h.data(), counts, h.size() * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, sc.st));
-        CK(cudaStreamSynchronize(sc.st));
-        unsigned long long t = 0;
-        for (auto v : h) t += v;
-        return t;
     }
 };
 
@@ -673,6 +668,8 @@ int dg_engine_create(int device, dg_engine** out) {
         e->sm_count = prop.multiProcessorCount;
         CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&e->upload, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&e->lane, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&e->refine, cudaStreamNonBlocking));
         *out = e.release();
     });
 }
@@ -1406,7 +1403,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     } ev_free{&evs};
 
     Pipeline pl;
-    pl.init(sc, P, sn->N, SPl, eng->sm_count, opt.profile ? 1 : 2);
+    pl.init(sc, P, sn->N, SPl, eng->sm_count, opt.profile ? 1 : 2, eng->lane);
     const int64_t n_elems = (int64_t)SPl * P;
     double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
     // refine flags: one bitmap row of whole words per step (bit p of step i at
@@ -1422,7 +1419,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     RefineCtx ctx = refine_ctx(g, sn, geo, raw);  // element = local step * P + p
     ctx.pg = geo.pg + sp0;
     ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
-    SideRefine rf(sc, SPl, P, P32, opt.profile ? 0 : 10);
+    SideRefine rf(sc, SPl, P, P32, opt.profile ? 0 : 10, eng->refine);
 
     for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
         const int nw = std::min(pl.slots, SPl - w0);
@@ -1452,10 +1449,8 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     }
     launches += pl.launches;
     CK(cudaGetLastError());
-    check_err_flag(sc, pl.err);
 
     rf.finish(bits, ctx);  // remaining steps; the main stream joins the side stream
-    res->n_refined = (int64_t)rf.total();
     launches += rf.launches;
 
     if (pairs > 1) {
@@ -1481,11 +1476,28 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         CK(cudaStreamSynchronize(st));  // `init` is host memory of this frame
     }
 
-    unsigned long long ovl = 0,
-                       work[3] = {pl.work_total(sc, 0), pl.work_total(sc, 1), pl.work_total(sc, 2)};
-    CK(cudaMemcpyAsync(&ovl, pl.overlap, sizeof ovl, cudaMemcpyDeviceToHost, st));
+    // the run's counters in one read-back (no host round trip before the last
+    // refinement batch is queued): error flag, overlap, work per lane, refined
+    // elements per batch
+    std::vector<unsigned long long> hc(2 + 3 * pl.n_lanes + std::max(rf.batches, 1), 0ull);
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, pl.err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), pl.overlap, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
+    for (int l = 0; l < pl.n_lanes; ++l)
+        CK(cudaMemcpyAsync(hc.data() + 2 + 3 * l, pl.lanes[l].work, 3 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+    const size_t c0 = 2 + 3 * (size_t)pl.n_lanes;
+    CK(cudaMemcpyAsync(hc.data() + c0, rf.counts, (hc.size() - c0) * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    res->sum_overlap_samples = (double)ovl;
+    if (herr) raise(DG_EINVAL, "predict_geometry: candidate coincides with receiver");
+    unsigned long long work[3] = {0, 0, 0}, refined = 0;
+    for (int l = 0; l < pl.n_lanes; ++l)
+        for (int k = 0; k < 3; ++k) work[k] += hc[2 + 3 * l + k];
+    for (size_t i = c0; i < hc.size(); ++i) refined += hc[i];
+    res->n_refined = (int64_t)refined;
+    res->sum_overlap_samples = (double)hc[0];
     res->kernel_launches += launches;
     res->correlate_launches = SPl;
     res->moment_ffma2 = (double)work[0];
