@@ -1523,10 +1523,42 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
 // from per-snapshot grids [S][P] (device), then the exact peak (near-peak
 // cells re-evaluated in FP64 for every (snapshot, pair)), detection and the
 // host copies — the other half of geolocate_snapshots.
+
+// stream `st` waits for the work queued so far on two side streams
+struct SideJoin {
+    cudaStream_t st, side[2];
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    SideJoin(cudaStream_t s, cudaStream_t a, cudaStream_t b) : st(s), side{a, b} {
+        for (auto& x : e) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    void join() {
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventRecord(e[i], side[i]));
+            CK(cudaStreamWaitEvent(st, e[i], 0));
+        }
+    }
+    ~SideJoin() {
+        for (int i = 0; i < 2; ++i) {
+            if (cudaEventRecord(e[i], side[i]) == cudaSuccess) cudaStreamWaitEvent(st, e[i], 0);
+            cudaEventDestroy(e[i]);
+        }
+    }
+};
+
+// detect_emitters on the surface `acc` on stream `det` (own scratch; its host
+// synchronisations wait for that stream only)
+void detect_beside(cudaStream_t det, const dg_grid* g, const double* acc, const dg_options& opt,
+                   dg_result* res, int64_t* launches) {
+    res->n_detections = 0;
+    if (!opt.detect) return;
+    Scratch sd(det);
+    run_detect(g, acc, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
+               res->detections_capacity, &res->n_detections, sd, launches);
+}
+
 void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunGeo& geo,
                const double* grids, const double* medians, const dg_options& opt,
                bool acc_dev_allowed, dg_result* res, Scratch& sc) {
-    (void)eng;
     const int64_t P = g->size();
     const int S = geo.S, SP = geo.SP, pairs = geo.pairs;
     cudaStream_t st = sc.st;
@@ -1535,6 +1567,30 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
                                                              : sc.alloc<double>(P);
     launch_accumulate(grids, S, P, acc, st);
     launches += 1;
+    // the surfaces are final here: their device->host copies (engine refine
+    // stream) and the detection (engine lane stream) run beside the
+    // latency-bound exact re-rank; the re-ranked values are patched into the
+    // host copies afterwards (the device surface, which detection reads, is
+    // not patched)
+    cudaEvent_t acc_done;
+    CK(cudaEventCreateWithFlags(&acc_done, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t e;
+        ~EvGuard() { cudaEventDestroy(e); }
+    } acc_guard{acc_done};
+    CK(cudaEventRecord(acc_done, st));
+    cudaStream_t d2h = eng->refine, det = eng->lane;
+    CK(cudaStreamWaitEvent(d2h, acc_done, 0));
+    CK(cudaStreamWaitEvent(det, acc_done, 0));
+    if (res->accumulated)
+        CK(cudaMemcpyAsync(res->accumulated, acc, P * sizeof(double), cudaMemcpyDeviceToHost,
+                           d2h));
+    if (res->per_snapshot)
+        CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
+                           cudaMemcpyDeviceToHost, d2h));
+    // `acc` / `grids` are freed on st when the caller's scratch goes: st waits
+    // for these readers before returning (also when an error unwinds)
+    SideJoin sj(st, d2h, det);
 
     // peak: FP64 max over the surface, then exact re-rank of every cell within
     // a relative band of it (covers the FP32 error), lowest index on ties.
@@ -1569,6 +1625,7 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
         launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, grid_ex, st);
         launch_argmax_cells(cells, n_cells, kRerankCap, acc_ex, best_i, best_v, st);
         launches += 3;
+        detect_beside(det, g, acc, opt, res, &launches);
         long long bi = 0;
         double bv = 0.0;
         CK(cudaMemcpyAsync(&bi, best_i, sizeof bi, cudaMemcpyDeviceToHost, st));
@@ -1582,17 +1639,9 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
         res->argmax_value = hmax;
     }
     res->n_reranked = std::min(hn, kRerankCap);
+    if (!(hmax > 0.0)) detect_beside(det, g, acc, opt, res, &launches);
 
-    res->n_detections = 0;
-    if (opt.detect)
-        run_detect(g, acc, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
-                   res->detections_capacity, &res->n_detections, sc, &launches);
-
-    if (res->accumulated)
-        CK(cudaMemcpyAsync(res->accumulated, acc, P * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (res->per_snapshot)
-        CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
-                           cudaMemcpyDeviceToHost, st));
+    sj.join();
     CK(cudaStreamSynchronize(st));
     if (opt.patch_peak && acc_ex && res->n_reranked > 0 && (res->accumulated || res->per_snapshot)) {
         // exact FP64 values of the re-ranked cells into the host copies
