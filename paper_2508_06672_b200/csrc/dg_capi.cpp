@@ -311,7 +311,7 @@ struct Pipeline {
         tcheb[1] = tdev + 64 * kMaxMoments;
         tcheb[2] = tdev + (64 + 128) * kMaxMoments;
         tcheb[3] = tdev + (64 + 128 + 256) * kMaxMoments;
-        CK(cudaStreamSynchronize(sc.st));  // `all` is host memory of this frame
+        // `all` is pageable: staged by cudaMemcpyAsync before it returns
     }
 
     int* d_slot(int s) const { return d + (size_t)s * P; }
@@ -1214,24 +1214,23 @@ std::unique_ptr<dg_staged> stage_impl(dg_engine* eng, const dg_snapshots* sn, bo
         const size_t el = f64 ? sizeof(double2) : sizeof(float2);
         contiguous = contiguous && (const char*)p == base + c * s->N * el;
     }
+    // one contiguous upload (a pitched 2-D copy of ~100 rows stalled the host
+    // for ~0.3 ms in the driver), then one kernel fills both padded copies
     const size_t el = f64 ? sizeof(double2) : sizeof(float2);
-    char* dst = f64 ? (char*)(y64 + kCapturePad) : (char*)(y32 + kCapturePad);
-    CK(cudaMemsetAsync(f64 ? s->y64->p : s->y32->p, 0, f64 ? s->y64->bytes : s->y32->bytes, st));
+    void* tmp = nullptr;
+    CK(cudaMallocAsync(&tmp, (size_t)n_caps * s->N * el, st));
     if (contiguous) {
         const void* src = f64 ? (const void*)sn->captures_iq[0] : (const void*)sn->captures_f32[0];
-        CK(cudaMemcpy2DAsync(dst, s->stride * el, src, s->N * el, s->N * el, n_caps,
-                             cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(tmp, src, (size_t)n_caps * s->N * el, cudaMemcpyHostToDevice, st));
     } else {
         for (int64_t c = 0; c < n_caps; ++c) {
             const void* src = f64 ? (const void*)sn->captures_iq[c] : (const void*)sn->captures_f32[c];
-            CK(cudaMemcpyAsync(dst + c * s->stride * el, src, s->N * el, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync((char*)tmp + c * s->N * el, src, s->N * el, cudaMemcpyHostToDevice,
+                               st));
         }
     }
-    // the whole padded buffer (pads are zero in the source)
-    if (f64)
-        launch_f64_to_f32(y64, y32, n_caps * s->stride, st);
-    else
-        launch_f32_to_f64(y32, y64, n_caps * s->stride, st);
+    launch_stage_captures(tmp, f64, n_caps, s->N, s->stride, kCapturePad, y64, y32, st);
+    CK(cudaFreeAsync(tmp, st));
     CK(cudaGetLastError());
     if (async) {
         CK(cudaEventCreateWithFlags(&s->ready, cudaEventDisableTiming));
@@ -1342,7 +1341,7 @@ RunGeo make_geo(Scratch& sc, const dg_staged* sn) {
     CK(cudaMemcpyAsync(r.pg, r.hpg.data(), r.SP * sizeof(PairGeom), cudaMemcpyHostToDevice, sc.st));
     CK(cudaMemcpyAsync(r.d_prx, r.prx.data(), r.prx.size() * sizeof(int), cudaMemcpyHostToDevice,
                        sc.st));
-    CK(cudaStreamSynchronize(sc.st));  // host vectors may move with the struct
+    // pageable sources: cudaMemcpyAsync has staged them when it returns
     return r;
 }
 

@@ -281,5 +281,9 @@ void launch_greedy(const DetCand* cands, const int* n_cands, int cap, int radius
 
 void launch_f64_to_f32(const double2* in, float2* out, int64_t n, cudaStream_t st);
 void launch_f32_to_f64(const float2* in, double2* out, int64_t n, cudaStream_t st);
+// contiguous uploaded captures [n_caps][N] (double2 if f64, else float2) ->
+// padded resident slots of stride elements (data at `pad`), FP64 and FP32
+void launch_stage_captures(const void* in, bool f64, int64_t n_caps, int64_t N, int64_t stride,
+                           int64_t pad, double2* y64, float2* y32, cudaStream_t st);
 
 }  // namespace dg

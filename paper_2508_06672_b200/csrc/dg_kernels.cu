@@ -1115,6 +1115,26 @@ __global__ void k_f64_to_f32(const double2* __restrict__ in, float2* __restrict_
     }
 }
 
+// captures [n_caps][N] (contiguous, as uploaded) -> the padded slots of both
+// resident copies, pads zeroed: slot c element i holds sample i - pad
+template <typename T>
+__global__ void k_stage_captures(const T* __restrict__ in, int64_t n_caps, int64_t N,
+                                 int64_t stride, int64_t pad, double2* __restrict__ y64,
+                                 float2* __restrict__ y32) {
+    const int64_t n = n_caps * stride;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / stride, k = i - c * stride - pad;
+        double2 v = make_double2(0.0, 0.0);
+        if (k >= 0 && k < N) {
+            const T w = in[c * N + k];
+            v = make_double2((double)w.x, (double)w.y);
+        }
+        y64[i] = v;
+        y32[i] = make_float2((float)v.x, (float)v.y);
+    }
+}
+
 __global__ void k_f32_to_f64(const float2* __restrict__ in, double2* __restrict__ out, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -1306,6 +1326,17 @@ void launch_greedy(const DetCand* cands, const int* n_cands, int cap, int radius
 
 void launch_f64_to_f32(const double2* in, float2* out, int64_t n, cudaStream_t st) {
     k_f64_to_f32<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+}
+
+void launch_stage_captures(const void* in, bool f64, int64_t n_caps, int64_t N, int64_t stride,
+                           int64_t pad, double2* y64, float2* y32, cudaStream_t st) {
+    const int64_t n = n_caps * stride;
+    if (f64)
+        k_stage_captures<double2><<<blocks_for(n, 256), 256, 0, st>>>(
+            static_cast<const double2*>(in), n_caps, N, stride, pad, y64, y32);
+    else
+        k_stage_captures<float2><<<blocks_for(n, 256), 256, 0, st>>>(
+            static_cast<const float2*>(in), n_caps, N, stride, pad, y64, y32);
 }
 
 void launch_f32_to_f64(const float2* in, double2* out, int64_t n, cudaStream_t st) {

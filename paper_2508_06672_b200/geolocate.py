@@ -190,9 +190,10 @@ def _snapshots_struct(states, captures, fs, fc):
     if caps.ndim != 3:
         raise ValueError("captures must be [n_snapshots, n_receivers, n_samples]")
     S, R, N = caps.shape
-    st = np.ascontiguousarray(states, np.float64).reshape(S * R, 6)
-    st_arr = (_capi.dg_state * (S * R))(*[_pair_states(st[k]) for k in range(S * R)])
-    keep = [st_arr]
+    # dg_state is 6 packed doubles (position, velocity): view the states array
+    st = np.array(states, np.float64, order="C", copy=True).reshape(S * R, 6)
+    st_arr = (_capi.dg_state * (S * R)).from_buffer(st)
+    keep = [st, st_arr]
     snaps = _capi.dg_snapshots()
     snaps.n_snapshots, snaps.n_receivers, snaps.n_samples = S, R, N
     snaps.sample_rate_hz, snaps.center_freq_hz = float(fs), float(fc)
@@ -200,12 +201,17 @@ def _snapshots_struct(states, captures, fs, fc):
     if caps.dtype == np.complex64:
         caps = np.ascontiguousarray(caps)
         fp = C.POINTER(C.c_float)
-        ptrs = (fp * (S * R))(*[caps[s, r].ctypes.data_as(fp) for s in range(S) for r in range(R)])
-        snaps.captures_f32 = ptrs
     else:
         caps = np.ascontiguousarray(caps, np.complex128)
-        dp = C.POINTER(C.c_double)
-        ptrs = (dp * (S * R))(*[caps[s, r].ctypes.data_as(dp) for s in range(S) for r in range(R)])
+        fp = C.POINTER(C.c_double)
+    # one pointer per (snapshot, receiver) row, computed as addresses
+    addr = np.asarray(caps.ctypes.data + np.arange(S * R, dtype=np.uint64) * (N * caps.itemsize),
+                      dtype=np.uintp)
+    ptrs = (fp * (S * R)).from_buffer(addr)
+    keep.append(addr)
+    if caps.dtype == np.complex64:
+        snaps.captures_f32 = ptrs
+    else:
         snaps.captures_iq = ptrs
     keep += [caps, ptrs]
     return snaps, keep

@@ -1,7 +1,7 @@
 """GPU timeline of one solve from CUPTI (torch.profiler): span, busy union, idle gaps,
 and per-kernel concurrency -- where a solve's time goes beyond its two big kernels.
 
-    python tests/gpu_timeline.py [C3]   -> gpurun_out/timeline.json + printed summary
+    python tests/gpu_timeline.py [C3] [e2e]  -> gpurun_out/timeline.json + printed summary
 Not collected by pytest.
 """
 import json
@@ -25,11 +25,23 @@ def main():
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], bench.FC)
     opts = b2.GeolocateOptions()
-    for _ in range(2):
-        b2.geolocate_staged(grid, staged, opts)
+    e2e = len(sys.argv) > 2 and sys.argv[2] == "e2e"
+    if e2e:  # the bench's e2e call: pinned host captures in, pinned surface out
+        pinned = torch.empty(caps.shape, dtype=torch.complex128, pin_memory=True).numpy()
+        pinned[...] = caps
+        surf = torch.empty(grid.size(), dtype=torch.float64, pin_memory=True).numpy()
+
+        def solve():
+            b2.geolocate_arrays(grid, states, pinned, cfg["fs"], bench.FC, opts,
+                                want_surface=True, want_per_snapshot=False, out=surf)
+    else:
+        def solve():
+            b2.geolocate_staged(grid, staged, opts)
+    for _ in range(5):  # steady state (stream-ordered pool grown)
+        solve()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        b2.geolocate_staged(grid, staged, opts)
+        solve()
         torch.cuda.synchronize()
     os.makedirs("gpurun_out", exist_ok=True)
     trace = "gpurun_out/timeline_trace.json"
