@@ -92,7 +92,7 @@ double jacobi_anger_tail(double x, int R) {
 constexpr double kMomentTail = 1e-8;
 constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of moments
 constexpr int kMomentR[] = {8, 10, 12, 14, 16};
-constexpr int kMomentB[] = {512, 256, 128, 64};
+constexpr int kMomentB[] = {768, 640, 512, 256, 128, 64};
 
 int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -217,9 +217,9 @@ struct Pipeline {
     Lane lanes[2];
     cudaEvent_t window_ready = nullptr;
     unsigned long long* overlap = nullptr;
-    const float* tcheb[4] = {nullptr, nullptr, nullptr, nullptr};  // B = 64, 128, 256, 512
+    const float* tcheb[6] = {};  // B = 64, 128, 256, 512, 640, 768
     const float* tcheb_for(int B) const {
-        return tcheb[B == 64 ? 0 : B == 128 ? 1 : B == 256 ? 2 : 3];
+        return tcheb[B == 64 ? 0 : B == 128 ? 1 : B == 256 ? 2 : B == 512 ? 3 : B == 640 ? 4 : 5];
     }
     std::vector<StepPlan> plans;
     int64_t launches = 0, direct_steps = 0;
@@ -292,25 +292,24 @@ struct Pipeline {
             L.n_buckets = sc.alloc<int>(1);
             L.queue = sc.alloc<int>(1);
             L.work = sc.alloc<unsigned long long>(3);
-            L.y1c = sc.alloc<float2>(N + 576);
+            L.y1c = sc.alloc<float2>(N + 768 + 64);  // + one block (B <= 768)
             L.y2p = sc.alloc<float2>(ylen);
             CK(cudaMemsetAsync(L.y2p, 0, ylen * sizeof(float2), sc.st));
             CK(cudaMemsetAsync(L.work, 0, 3 * sizeof(unsigned long long), sc.st));
         }
         CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
-        static const int kB[4] = {64, 128, 256, 512};
+        static const int kB[6] = {64, 128, 256, 512, 640, 768};
         std::vector<float> all;
-        for (int B : kB) {
-            auto t = chebyshev_table(B);
+        size_t off[6];
+        for (int i = 0; i < 6; ++i) {
+            off[i] = all.size();
+            auto t = chebyshev_table(kB[i]);
             all.insert(all.end(), t.begin(), t.end());
         }
         auto* tdev = sc.alloc<float>(all.size());
         CK(cudaMemcpyAsync(tdev, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice,
                            sc.st));
-        tcheb[0] = tdev;
-        tcheb[1] = tdev + 64 * kMaxMoments;
-        tcheb[2] = tdev + (64 + 128) * kMaxMoments;
-        tcheb[3] = tdev + (64 + 128 + 256) * kMaxMoments;
+        for (int i = 0; i < 6; ++i) tcheb[i] = tdev + off[i];
         // `all` is pageable: staged by cudaMemcpyAsync before it returns
     }
 

@@ -82,18 +82,21 @@ __global__ void k_center(const double2* __restrict__ y, const float2* __restrict
 // 2B per bucket.
 template <int B, int R>
 struct MomLayout {
-    static constexpr int CB = B >= 512 ? 8 : 16;       // blocks per item
+    static constexpr int CB = B > 640 ? 4 : B >= 512 ? 8 : 16;  // blocks per item
     static constexpr int BPW = 32 / CB;                // TDOA values per warp
     static constexpr int G = BPW * kMomWarps;           // TDOA values per item
     static constexpr int RP = (2 * R + 3) / 4 * 4;      // table row: T_m(t_j), T_m(t_j+1) pairs
     static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
     static constexpr int W2 = B + G + 2;                // y2 window samples copied
-    static constexpr int RS2 = (W2 + 13) / 16 * 16 + 2; // y2 row: 2 float2 mod 16
+    // y2 row: 16 / CB float2 mod 16 (2 at CB = 8, 16), so a 16-lane half-warp's
+    // (block, TDOA) LDS.64 at any shift covers 16 distinct bank pairs
+    static constexpr int RM2 = CB == 4 ? 4 : 2;
+    static constexpr int RS2 = (W2 + 15 - RM2) / 16 * 16 + RM2;
     static constexpr size_t table_floats = (size_t)B / 4 * RP;  // one row per two folded pairs
     static constexpr size_t stage_f2 = (size_t)CB * (RS1 + RS2);  // one buffer
     static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
                                    2 * stage_f2 * sizeof(float2);
-    static_assert(RS2 % 16 == 2 && RS2 >= W2 && W2 % 2 == 0, "y2 row padding");
+    static_assert(RS2 % 16 == RM2 && RS2 >= W2 && W2 % 2 == 0, "y2 row padding");
 };
 
 __device__ __forceinline__ float2 cmulc(float4 a, float4 b, int hi) {  // a * conj(b), one sample
@@ -108,7 +111,7 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
           int nbins, int bin_lo, int ngroups, int cpb, const float* __restrict__ tcheb,
           const float2* __restrict__ y1c, const float2* __restrict__ y2p, int padf, int N,
           float2* __restrict__ mom, int nbmax) {
-    static_assert(B % 64 == 0 && B <= 512, "block length");
+    static_assert(B % 64 == 0 && B <= 768, "block length");
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
     static_assert(kMomThreads % 32 == 0, "mapping");
     using L = MomLayout<B, R>;
@@ -121,10 +124,10 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
     __shared__ uint64_t full[2], empty[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // a 16-lane half-warp = 8 blocks x 2 TDOA values, so the y2 LDS.64 at shifts
-    // t, t+1 fill each other's bank gaps (row stride 4 banks mod 32)
-    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & 7);
-    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane >> 3);
+    // a 16-lane half-warp = 8 blocks x 2 TDOA values (CB = 8; 4 x 4 at CB = 4),
+    // so the y2 LDS.64 at shifts t, t+1, .. fill each other's bank gaps
+    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & (CB - 1));
+    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane / CB);
     const int nitems = ngroups * cpb;
     const int nblk_abs = (N + B - 1) / B;
 
@@ -564,6 +567,8 @@ void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bi
         case 64: moments_b<64>(R, a, sm_count, st); break;
         case 128: moments_b<128>(R, a, sm_count, st); break;
         case 256: moments_b<256>(R, a, sm_count, st); break;
+        case 640: moments_b<640>(R, a, sm_count, st); break;
+        case 768: moments_b<768>(R, a, sm_count, st); break;
         default: moments_b<512>(R, a, sm_count, st); break;
     }
 }

@@ -157,7 +157,7 @@ def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, m
     assert np.array_equal(got, again)  # bit-identical rerun (test_backend.cpp:97-108)
 
 
-@pytest.mark.parametrize("block", [64, 128, 256, 512])
+@pytest.mark.parametrize("block", [64, 128, 256, 512, 640, 768])
 @pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200),
                                             (3e3, 12)])  # ~250 per bucket: 2 tiles
 @pytest.mark.parametrize("tc", ["1", "0"])  # block sums on tcgen05 / FFMA2 block loop
