@@ -217,9 +217,12 @@ struct Pipeline {
     Lane lanes[2];
     cudaEvent_t window_ready = nullptr;
     unsigned long long* overlap = nullptr;
-    const float* tcheb[6] = {};  // B = 64, 128, 256, 512, 640, 768
+    static constexpr int kTables = 6;  // the block lengths of kMomentB
+    const float* tcheb[kTables] = {};
     const float* tcheb_for(int B) const {
-        return tcheb[B == 64 ? 0 : B == 128 ? 1 : B == 256 ? 2 : B == 512 ? 3 : B == 640 ? 4 : 5];
+        for (int i = 0; i < kTables; ++i)
+            if (kMomentB[i] == B) return tcheb[i];
+        raise(DG_ERUNTIME, "b200: no Chebyshev table for this block length");
     }
     std::vector<StepPlan> plans;
     int64_t launches = 0, direct_steps = 0;
@@ -298,18 +301,18 @@ struct Pipeline {
             CK(cudaMemsetAsync(L.work, 0, 3 * sizeof(unsigned long long), sc.st));
         }
         CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
-        static const int kB[6] = {64, 128, 256, 512, 640, 768};
+        static_assert(sizeof(kMomentB) / sizeof(kMomentB[0]) == kTables, "tables");
         std::vector<float> all;
-        size_t off[6];
-        for (int i = 0; i < 6; ++i) {
+        size_t off[kTables];
+        for (int i = 0; i < kTables; ++i) {
             off[i] = all.size();
-            auto t = chebyshev_table(kB[i]);
+            auto t = chebyshev_table(kMomentB[i]);
             all.insert(all.end(), t.begin(), t.end());
         }
         auto* tdev = sc.alloc<float>(all.size());
         CK(cudaMemcpyAsync(tdev, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice,
                            sc.st));
-        for (int i = 0; i < 6; ++i) tcheb[i] = tdev + off[i];
+        for (int i = 0; i < kTables; ++i) tcheb[i] = tdev + off[i];
         // `all` is pageable: staged by cudaMemcpyAsync before it returns
     }
 

@@ -82,7 +82,7 @@ __global__ void k_center(const double2* __restrict__ y, const float2* __restrict
 // 2B per bucket.
 template <int B, int R>
 struct MomLayout {
-    static constexpr int CB = B > 640 ? 4 : B >= 512 ? 8 : 16;  // blocks per item
+    static constexpr int CB = B >= 512 ? 8 : 16;       // blocks per item
     static constexpr int BPW = 32 / CB;                // TDOA values per warp
     static constexpr int G = BPW * kMomWarps;           // TDOA values per item
     static constexpr int RP = (2 * R + 3) / 4 * 4;      // table row: T_m(t_j), T_m(t_j+1) pairs
@@ -97,6 +97,7 @@ struct MomLayout {
     static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
                                    2 * stage_f2 * sizeof(float2);
     static_assert(RS2 % 16 == RM2 && RS2 >= W2 && W2 % 2 == 0, "y2 row padding");
+    static_assert(smem <= 227 * 1024 - 64, "k_moments stage exceeds shared memory");
 };
 
 __device__ __forceinline__ float2 cmulc(float4 a, float4 b, int hi) {  // a * conj(b), one sample
