@@ -242,8 +242,9 @@ struct Pipeline {
 
     // lanes: 2 overlap consecutive steps; 1 serialises them (profiled runs, so
     // each kernel's CUDA-event time is its own)
-    void init(Scratch& sc, int64_t P_, int64_t N_, int n_steps, int sms, int max_lanes = 2,
+    void init(Scratch& sc, dg_engine* eng, int64_t P_, int64_t N_, int n_steps, int max_lanes = 2,
               cudaStream_t lane1 = nullptr) {
+        const int sms = eng->sm_count;
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
@@ -302,18 +303,27 @@ struct Pipeline {
         }
         CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
         static_assert(sizeof(kMomentB) / sizeof(kMomentB[0]) == kTables, "tables");
-        std::vector<float> all;
-        size_t off[kTables];
+        size_t off[kTables], total = 0;
         for (int i = 0; i < kTables; ++i) {
-            off[i] = all.size();
-            auto t = chebyshev_table(kMomentB[i]);
-            all.insert(all.end(), t.begin(), t.end());
+            off[i] = total;
+            total += (size_t)kMomentB[i] * kMaxMoments;
         }
-        auto* tdev = sc.alloc<float>(all.size());
-        CK(cudaMemcpyAsync(tdev, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice,
-                           sc.st));
-        for (int i = 0; i < kTables; ++i) tcheb[i] = tdev + off[i];
-        // `all` is pageable: staged by cudaMemcpyAsync before it returns
+        {
+            std::lock_guard<std::mutex> lk(eng->tables_mu);
+            if (!eng->tables) {
+                std::vector<float> all;
+                for (int i = 0; i < kTables; ++i) {
+                    auto t = chebyshev_table(kMomentB[i]);
+                    all.insert(all.end(), t.begin(), t.end());
+                }
+                auto mem = std::make_unique<DevMem>(all.size() * sizeof(float));
+                CK(cudaMemcpy(mem->p, all.data(), all.size() * sizeof(float),
+                              cudaMemcpyHostToDevice));
+                eng->tables = std::move(mem);
+            }
+        }
+        for (int i = 0; i < kTables; ++i)
+            tcheb[i] = static_cast<const float*>(eng->tables->p) + off[i];
     }
 
     int* d_slot(int s) const { return d + (size_t)s * P; }
@@ -731,7 +741,7 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         set_device(s->eng);
         Scratch sc(s->st);
         Pipeline pl;
-        pl.init(sc, n, s->N, 1, s->eng->sm_count);
+        pl.init(sc, s->eng, n, s->N, 1);
         auto* off = sc.alloc<dg_pair_offsets>(n);
         auto* vals = sc.alloc<double>(n);
         const int64_t n_words = (n + 31) / 32;
@@ -976,7 +986,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         Scratch sc(s->st);
         const int64_t P = g->size();
         Pipeline pl;
-        pl.init(sc, P, s->N, 1, s->eng->sm_count);
+        pl.init(sc, s->eng, P, s->N, 1);
         auto* pg = sc.alloc<PairGeom>(1);
         auto* vals = sc.alloc<double>(P);
         const int64_t n_words = (P + 31) / 32;
@@ -1404,7 +1414,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     } ev_free{&evs};
 
     Pipeline pl;
-    pl.init(sc, P, sn->N, SPl, eng->sm_count, opt.profile ? 1 : 2, eng->lane);
+    pl.init(sc, eng, P, sn->N, SPl, opt.profile ? 1 : 2, eng->lane);
     const int64_t n_elems = (int64_t)SPl * P;
     double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
     // refine flags: one bitmap row of whole words per step (bit p of step i at

@@ -118,6 +118,10 @@ struct dg_engine {
     // the second correlation lane and the side refinement of a run, created once
     // (stream creation costs ~0.1-0.3 ms of host time per call)
     cudaStream_t lane = nullptr, refine = nullptr;
+    // the correlator's Chebyshev tables, uploaded once (a per-call upload over
+    // 64 KB queued behind capture uploads on the copy engine)
+    std::mutex tables_mu;
+    std::unique_ptr<dg::DevMem> tables;
     // pinned double buffer of the file writers (dg_io.cpp), kept across calls
     std::mutex stage_mu;
     void* stage_host[2] = {nullptr, nullptr};
