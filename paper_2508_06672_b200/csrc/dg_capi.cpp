@@ -266,12 +266,23 @@ struct Pipeline {
         CK(cudaMemsetAsync(hist, 0, sizeof(int) * nbins * slots, sc.st));
         CK(cudaMemsetAsync(err, 0, sizeof(int), sc.st));
         CK(cudaMemsetAsync(overlap, 0, sizeof(unsigned long long), sc.st));
+        n_lanes = n_steps > 1 ? std::max(1, std::min(2, max_lanes)) : 1;
+        lane1_ = lane1;
+        eng_ = eng;
+    }
+
+    // the correlation lanes' working sets (after the first geometry launch, so
+    // the geometry pass does not wait for this host work)
+    cudaStream_t lane1_ = nullptr;
+    dg_engine* eng_ = nullptr;
+    void init_lanes(Scratch& sc) {
+        dg_engine* eng = eng_;
+        cudaStream_t lane1 = lane1_;
         // centred y1 (k_moments' row copies may run one block past N) and y2 in a
         // zero-padded array: its window copies reach from N samples before to
         // N + 1200 samples after the data
         padf = (N + 65) & ~1;  // even: window copies start 16-byte aligned
         const size_t ylen = (size_t)padf + 2 * (size_t)N + 1280;
-        n_lanes = n_steps > 1 ? std::max(1, std::min(2, max_lanes)) : 1;
         for (int l = 0; l < n_lanes; ++l) {
             Lane& L = lanes[l];
             if (l == 0) {
@@ -742,6 +753,7 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         Scratch sc(s->st);
         Pipeline pl;
         pl.init(sc, s->eng, n, s->N, 1);
+        pl.init_lanes(sc);
         auto* off = sc.alloc<dg_pair_offsets>(n);
         auto* vals = sc.alloc<double>(n);
         const int64_t n_words = (n + 31) / 32;
@@ -987,6 +999,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         const int64_t P = g->size();
         Pipeline pl;
         pl.init(sc, s->eng, P, s->N, 1);
+        pl.init_lanes(sc);
         auto* pg = sc.alloc<PairGeom>(1);
         auto* vals = sc.alloc<double>(P);
         const int64_t n_words = (P + 31) / 32;
@@ -1422,15 +1435,14 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     // lanes correlate later steps (FP64 refinement next to FP32 correlation)
     const int64_t P32 = (P + 31) & ~int64_t(31);
     const int64_t n_words = SPl * (P32 / 32);
-    auto* bits = sc.alloc<uint32_t>(n_words);
-    CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
     const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
     const auto* y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
     const int sp0 = s0 * pairs;  // global (snapshot, pair) index of local step 0
     RefineCtx ctx = refine_ctx(g, sn, geo, raw);  // element = local step * P + p
     ctx.pg = geo.pg + sp0;
     ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
-    SideRefine rf(sc, SPl, P, P32, opt.profile ? 0 : 10, eng->refine);
+    uint32_t* bits = nullptr;
+    std::unique_ptr<SideRefine> rfp;
 
     for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
         const int nw = std::min(pl.slots, SPl - w0);
@@ -1440,6 +1452,13 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
                               pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins,
                               raw + (int64_t)w0 * P, pl.overlap, pl.err, st);
         launches += (nw + 63) / 64;
+        if (w0 == 0) {  // the rest of the run's state, while the first geometry pass runs
+            pl.init_lanes(sc);
+            bits = sc.alloc<uint32_t>(n_words);
+            CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), st));
+            rfp = std::make_unique<SideRefine>(sc, SPl, P, P32, opt.profile ? 0 : 10, eng->refine);
+        }
+        SideRefine& rf = *rfp;
         const PairGeom* hw = geo.hpg.data() + sp0 + w0;
         const StepRange* approx = pl.lattice_ranges(sc, g, hw, nw, fs, wl);
         pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size,
@@ -1461,6 +1480,7 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     launches += pl.launches;
     CK(cudaGetLastError());
 
+    SideRefine& rf = *rfp;
     rf.finish(bits, ctx);  // remaining steps; the main stream joins the side stream
     launches += rf.launches;
 
