@@ -316,10 +316,13 @@ k_range_fp32(const float4* __restrict__ rel, int64_t P, const RxPairF32* __restr
             const float4 c = rel[p];
             const float ax = g.pi[0] - c.x, ay = g.pi[1] - c.y, az = g.pi[2] - c.z;
             const float bx = g.pj[0] - c.x, by = g.pj[1] - c.y, bz = g.pj[2] - c.z;
-            const float ri = sqrtf(ax * ax + ay * ay + az * az);
-            const float rj = sqrtf(bx * bx + by * by + bz * bz);
-            const float di = -(ax * g.vi[0] + ay * g.vi[1] + az * g.vi[2]) / ri;
-            const float dj = -(bx * g.vj[0] + by * g.vj[1] + bz * g.vj[2]) / rj;
+            // MUFU reciprocal square roots (~2 ulp): the planning margin is 1e-5
+            // relative (fp32_fdoa_margin), the TDOA margin 2 samples
+            const float si = ax * ax + ay * ay + az * az, sj = bx * bx + by * by + bz * bz;
+            const float qi = rsqrtf(si), qj = rsqrtf(sj);
+            const float ri = si * qi, rj = sj * qj;
+            const float di = -(ax * g.vi[0] + ay * g.vi[1] + az * g.vi[2]) * qi;
+            const float dj = -(bx * g.vj[0] + by * g.vj[1] + bz * g.vj[2]) * qj;
             const float f = (dj - di) * inv_wl;
             const float t = (rj - ri) * fs_over_c;
             fmn = fminf(fmn, f);
