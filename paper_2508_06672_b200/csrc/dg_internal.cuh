@@ -86,7 +86,10 @@ constexpr int kL = 16;       // phasor table length (samples per inner block)
 // Threshold on S / sqrt(sum |z|^2) below which an FP32 value is re-evaluated
 // exactly; see DESIGN.md "Parity" for the error model behind it.
 constexpr float kRefineTau = 0.02f;         // direct correlator (dg_correlate.cu)
-constexpr float kMomentRefineTau = 0.02f;   // block-moment correlator
+// block-moment correlator: S < tau * max(sqrt(A), Q). Measured
+// worst unrefined relative error over noise / 0 dB / +20 dB tone scenes at C3 scale
+// (tests/gpu_error_model.py): tau 0.02 -> 3.6e-5, 0.015 -> 4.5e-5, 0.01 -> 6.1e-5
+constexpr float kMomentRefineTau = 0.015f;
 
 // --------------------------------------------------------------------------
 // launchers (dg_kernels.cu). All asynchronous on `st`.

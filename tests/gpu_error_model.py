@@ -37,6 +37,8 @@ def run(snr, kind_seed, tau_env=None):
     snap = b2.Snapshot(0.0, states[0], [b2.BasebandCapture(caps[0, r], fs, 0.0, fc) for r in range(2)])
     be = b2.make_backend("b200")
     os.environ.pop("DG_REFINE_TAU", None)
+    if tau_env is not None:  # a candidate refinement threshold instead of the default
+        os.environ["DG_REFINE_TAU"] = str(tau_env)
     fast = b2.correlate_snapshot(grid, snap, (0, 1), be).values
     os.environ["DG_REFINE_TAU"] = "1e30"
     exact = b2.correlate_snapshot(grid, snap, (0, 1), be).values
@@ -47,7 +49,8 @@ def run(snr, kind_seed, tau_env=None):
     rel = np.abs(fast - exact) / np.maximum(np.abs(exact), 1e-300)
     absn = np.abs(fast - exact) / norm
     edges = [0, 1e-3, 2e-3, 5e-3, 1e-2, 2e-2, 5e-2, 0.1, 0.3, 1, 3, 1e9]
-    out = {"snr_db": snr, "points": int(grid.size()), "max_rel": float(rel.max()),
+    out = {"snr_db": snr, "tau": tau_env, "n_refined_like": int(np.sum(fast == exact)),
+           "points": int(grid.size()), "max_rel": float(rel.max()),
            "max_abs_over_norm": float(absn.max()),
            "p999_abs_over_norm": float(np.quantile(absn, 0.999)),
            "std_abs_over_norm": float(np.std((fast - exact) / norm)), "bins": []}
@@ -60,8 +63,10 @@ def run(snr, kind_seed, tau_env=None):
 
 
 if __name__ == "__main__":
-    res = [run(-20.0, 3), run(0.0, 11)]
+    tau = float(sys.argv[1]) if len(sys.argv) > 1 else None  # default: the engine's
+    res = [run(-20.0, 3, tau), run(0.0, 11, tau), run(20.0, 5, tau)]
     print(json.dumps(res, indent=1))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "error_model.json"), "w") as f:
+    name = "error_model.json" if tau is None else f"error_model_tau{tau:g}.json"
+    with open(os.path.join(ROOT, "gpurun_out", name), "w") as f:
         json.dump(res, f, indent=1)
