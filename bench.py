@@ -426,6 +426,7 @@ def b200_arm(args, rank, world):
             "gpu_launches": launches * args.steps,
             "argmax": {"index": best[1], "value": best[0]},
             "refined_elements": last["n_refined"],
+            "step_ms": [round(x, 3) for x in ms],  # this rank's timed solves
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
