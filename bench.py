@@ -106,6 +106,10 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+            # one untimed query first: on a fresh box the first clock / reason
+            # queries were seen to stall a concurrent solve for ~0.5 s
+            for _ in range(3):
+                self._sample_nvml()
         except Exception:
             self._nvml = None
 

@@ -40,8 +40,10 @@ def main():
     for _ in range(5):  # steady state (stream-ordered pool grown)
         solve()
     torch.cuda.synchronize()
+    n_prof = int(os.environ.get("DG_TL_SOLVES", "1"))  # >1: look for sporadic stalls
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        solve()
+        for _ in range(n_prof):
+            solve()
         torch.cuda.synchronize()
     os.makedirs("gpurun_out", exist_ok=True)
     trace = "gpurun_out/timeline_trace.json"
