@@ -88,9 +88,9 @@ struct MomLayout {
     static constexpr int RP = (2 * R + 3) / 4 * 4;      // table row: T_m(t_j), T_m(t_j+1) pairs
     static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
     static constexpr int W2 = B + G + 2;                // y2 window samples copied
-    // y2 row: 16 / CB float2 mod 16 (2 at CB = 8, 16), so a 16-lane half-warp's
-    // (block, TDOA) LDS.64 at any shift covers 16 distinct bank pairs
-    static constexpr int RM2 = CB == 4 ? 4 : 2;
+    // y2 row: 2 float2 mod 16, so a 16-lane half-warp's (8 blocks x 2 TDOA values)
+    // LDS.64 at any shift covers 16 distinct bank pairs
+    static constexpr int RM2 = 2;
     static constexpr int RS2 = (W2 + 15 - RM2) / 16 * 16 + RM2;
     static constexpr size_t table_floats = (size_t)B / 4 * RP;  // one row per two folded pairs
     static constexpr size_t stage_f2 = (size_t)CB * (RS1 + RS2);  // one buffer
@@ -125,10 +125,10 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
     __shared__ uint64_t full[2], empty[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // a 16-lane half-warp = 8 blocks x 2 TDOA values (CB = 8; 4 x 4 at CB = 4),
-    // so the y2 LDS.64 at shifts t, t+1, .. fill each other's bank gaps
-    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & (CB - 1));
-    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane / CB);
+    // a 16-lane half-warp = 8 blocks x 2 TDOA values, so the y2 LDS.64 at shifts
+    // t, t+1 fill each other's bank gaps (row stride 4 banks mod 32)
+    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & 7);
+    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane >> 3);
     const int nitems = ngroups * cpb;
     const int nblk_abs = (N + B - 1) / B;
 
