@@ -88,7 +88,7 @@ def make_inputs(name: str, spacing_km: float = 1.0, n_snapshots: int | None = No
 
 class ClockSampler:
     """SM clocks and throttle reasons sampled during the timed region: NVML every
-    10 ms (nvidia-smi every 0.2 s if NVML is unavailable)."""
+    50 ms (nvidia-smi every 0.2 s if NVML is unavailable)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -116,7 +116,9 @@ class ClockSampler:
     def _sample_nvml(self):
         nv, h = self._nvml
         sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        if getattr(self, "_max_sm", None) is None:  # constant: queried once
+            self._max_sm = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = self._max_sm
         try:
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
@@ -136,16 +138,20 @@ class ClockSampler:
                         self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.01 if self._nvml else 0.2)
+            # 50 ms: NVML queries contend with the solve's CUDA calls in the driver
+            # (at 10 ms a 16M-point solve occasionally stalled by tens of ms)
+            self._stop.wait(0.05 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._loop, daemon=True)
-        self._t.start()
+        if os.environ.get("DG_BENCH_NO_CLOCKS") != "1":  # diagnostics only
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t.is_alive():
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:

@@ -95,8 +95,9 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
+// two x16 loads, one wait (the group's 32 columns in one TMEM round trip)
+__device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v0)[16], float (&v1)[16]) {
+    uint32_t r[32];
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
         "%11, %12, %13, %14, %15}, [%16];"
@@ -104,9 +105,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
           "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr + 16u));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 16; ++i) {
+        v0[i] = __uint_as_float(r[i]);
+        v1[i] = __uint_as_float(r[16 + i]);
+    }
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -372,8 +383,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                 tc_fence_after();
                 for (int gc = 0; warp_live && gc < nn; gc += 2 * G) {
                     float v[2][16];
-                    tmem_ld16(lane_addr + (uint32_t)gc, v[0]);
-                    tmem_ld16(lane_addr + (uint32_t)(gc + 16), v[1]);
+                    tmem_ld16x2(lane_addr + (uint32_t)gc, v[0], v[1]);
                     // two interleaved chains per sum (blocks 0-7 / 8-15 of the group)
                     float2 A0 = make_float2(0.f, 0.f), V0 = A0, E0 = A0, A1 = A0, V1 = A0, E1 = A0;
 #pragma unroll
