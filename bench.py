@@ -266,7 +266,9 @@ def b200_arm(args, rank, world):
     P = grid.size()
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], FC, engine=eng)
     opts = b2.GeolocateOptions(k_sigma=5.0, exclusion_radius_cells=5, detect=True)
-    stream = torch.cuda.current_stream()
+    # the solve's launching stream: the engine runs on it (side streams joined
+    # back into it) and the events and the L2 flush are recorded on it
+    stream = torch.cuda.Stream()
     acc_dev = torch.empty(P, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -296,14 +298,16 @@ def b200_arm(args, rank, world):
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
         for k in range(args.steps):
-            flush.zero_()  # outside the events: L2 starts cold every step
+            with torch.cuda.stream(stream):
+                flush.zero_()  # outside the events: L2 starts cold every step
             ev[k][0].record(stream)
             st, best = solve(staged)
             ev[k][1].record(stream)
         torch.cuda.synchronize()
     # one more solve with per-kernel events (steps serialised on one stream so
     # each kernel's time is its own) for the rooflines; not part of `value`
-    flush.zero_()
+    with torch.cuda.stream(stream):
+        flush.zero_()
     stats.append(solve(staged, profile=True)[0])
     torch.cuda.synchronize()
     if dist is not None:
