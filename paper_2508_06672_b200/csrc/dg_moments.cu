@@ -201,7 +201,7 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
                 float2 part[R];
 #pragma unroll
                 for (int m = 0; m < R; ++m) part[m] = make_float2(0.f, 0.f);
-#pragma unroll 2
+#pragma unroll 4
                 for (int j = j0; j < j0 + kMomRun; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
                     const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
                     const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
