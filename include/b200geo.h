@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 5
+#define DG_ABI_VERSION 6
 
 enum {
     DG_OK = 0,
@@ -82,6 +82,29 @@ int dg_engine_create(int device, dg_engine** out);
 void dg_engine_destroy(dg_engine* engine);
 int dg_engine_descriptor(const dg_engine* engine, char* name, size_t name_len, char* kind,
                          size_t kind_len, unsigned* workers);
+
+/* ---- correlator tuning (tests / benchmarks; defaults are the product path) --
+ * Replaces no reference interface: the reference's CPU kernel has no
+ * variants. The settings live on the engine and are validated here, so no
+ * caller environment can silently change a result: a forced moment count is
+ * still used only where it meets the truncation bound (otherwise the planner
+ * picks the next admissible choice), and a refinement threshold below the
+ * default (which would weaken the 1e-4 relative contract) is rejected unless
+ * allow_weaker_refine is set explicitly. */
+#define DG_CORRELATOR_AUTO 0    /* block moments where cheaper, else the direct correlator */
+#define DG_CORRELATOR_DIRECT 1  /* direct FP32 correlator only */
+#define DG_CORRELATOR_MOMENTS 2 /* block moments wherever the truncation bound admits them */
+typedef struct {
+    int correlator;          /* DG_CORRELATOR_* */
+    int moment_block;        /* 0 = planner's choice, else 64/128/256/512/640/768 */
+    int moment_count;        /* 0 = planner's choice, else 8/10/12/14/16 */
+    int evaluate_tensor;     /* 1: block sums on tcgen05 where they fit; 0: FFMA2 block loop */
+    double refine_tau;       /* FP64 re-evaluation threshold of the moment path (0 = default) */
+    int allow_weaker_refine; /* permit refine_tau below the default (error-model studies only) */
+} dg_tuning;
+void dg_tuning_default(dg_tuning* t);
+int dg_engine_set_tuning(dg_engine* engine, const dg_tuning* t);
+int dg_engine_get_tuning(const dg_engine* engine, dg_tuning* t);
 
 /* ---- session == CorrelationBackend::stage + CorrelationSession ---------
  * dg_stage replaces backend.hpp:214-215 (+ check_pair :221-228): copies both
@@ -155,9 +178,22 @@ typedef struct {
                                    (steps then run serialised on one stream, so each
                                    kernel's event time is its own) */
     int patch_peak;             /* write the exact FP64 values of the re-ranked near-peak
-                                   cells into the HOST surfaces (default 1) so max_element on
-                                   them is the exact argmax; 0 keeps every cell the FP32-path
-                                   value, bit-identical under any grid partition */
+                                   cells into the returned surfaces, host and device, before
+                                   detection (default 1), so max_element on them is the exact
+                                   argmax and detection scores equal the surface; 0 keeps every
+                                   cell the FP32-path value */
+    /* Exact peak: every cell whose fast accumulated value
+     * is >= M (1 - 1e-4) / (1 + 1e-4), M the fast maximum, is re-evaluated in the
+     * reference's FP64 order (the 1e-4 per-element contract bounds where the true
+     * argmax can lie); past 4096 such cells they are re-ranked in rounds by
+     * descending fast value until no remaining cell can reach the best exact one. */
+    int peak_stage;             /* 0: accumulate + exact peak (default); 1: accumulate only
+                                   (argmax_* = the fast maximum, lowest index); 2: exact peak of
+                                   the surface given in accumulated_device (no accumulation) */
+    double peak_max;            /* > 0: M for the band instead of this call's own maximum (the
+                                   maximum over all slabs of a sharded run, so every partition
+                                   re-ranks the same cells); a slab with no cell in the band
+                                   returns argmax_index -1 */
 } dg_options;
 
 typedef struct {
@@ -165,7 +201,10 @@ typedef struct {
     double* accumulated;        /* host [P] */
     double* accumulated_device; /* device [P] (caller-owned, e.g. a torch tensor) */
     double* per_snapshot;       /* host [n_snapshots][P] */
-    dg_emitter_estimate* detections;
+    dg_emitter_estimate* detections; /* the first detections_capacity of n_detections are
+                                        written; the whole list (never truncated by the
+                                        engine) comes from dg_detect_emitters on the returned
+                                        surface with a buffer of n_detections entries */
     int64_t detections_capacity;
     /* filled by the call */
     int64_t n_detections;

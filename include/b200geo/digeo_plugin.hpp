@@ -126,6 +126,10 @@ inline digeo::GeolocateResult geolocate_snapshots(const std::vector<digeo::Snaps
                 throw std::invalid_argument("backend stage: sample rates differ");
             if (c.size() != c0.size())
                 throw std::invalid_argument("backend stage: sample counts differ");
+            // the reference takes each pair's wavelength from its first capture
+            // (geolocate.hpp:55); the engine runs one carrier per run
+            if (c.center_freq_hz != c0.center_freq_hz)
+                throw std::invalid_argument("geolocate_snapshots: center frequencies differ");
             states.push_back(*reinterpret_cast<const dg_state*>(&snap.states[r]));
             caps.push_back(reinterpret_cast<const double*>(c.samples.data()));
         }
@@ -173,6 +177,15 @@ inline digeo::GeolocateResult geolocate_snapshots(const std::vector<digeo::Snaps
     for (std::size_t s = 0; s < snapshots.size(); ++s)
         result.per_snapshot.push_back(digeo::CorrelationGrid{
             grid, std::vector<double>(per.begin() + s * P, per.begin() + (s + 1) * P)});
+    if (res.n_detections > res.detections_capacity) {  // the whole list, same surface
+        dets.resize(static_cast<std::size_t>(res.n_detections));
+        int64_t n = 0;
+        check(dg_detect_emitters(eng, g, result.accumulated.values.data(), 0, options.k_sigma,
+                                 options.exclusion_radius_cells, dets.data(),
+                                 static_cast<int64_t>(dets.size()), &n));
+        res.n_detections = n;
+        res.detections_capacity = static_cast<int64_t>(dets.size());
+    }
     const auto n_det = std::min<int64_t>(res.n_detections, res.detections_capacity);
     for (int64_t i = 0; i < n_det; ++i) {
         digeo::EmitterEstimate e;

@@ -81,7 +81,17 @@ class dg_scenario(C.Structure):
 class dg_options(C.Structure):
     _fields_ = [("k_sigma", C.c_double), ("exclusion_radius_cells", C.c_int),
                 ("normalize_per_snapshot", C.c_int), ("detect", C.c_int),
-                ("stream", C.c_void_p), ("profile", C.c_int), ("patch_peak", C.c_int)]
+                ("stream", C.c_void_p), ("profile", C.c_int), ("patch_peak", C.c_int),
+                ("peak_stage", C.c_int), ("peak_max", C.c_double)]
+
+
+class dg_tuning(C.Structure):
+    _fields_ = [("correlator", C.c_int), ("moment_block", C.c_int), ("moment_count", C.c_int),
+                ("evaluate_tensor", C.c_int), ("refine_tau", C.c_double),
+                ("allow_weaker_refine", C.c_int)]
+
+
+DG_CORRELATOR_AUTO, DG_CORRELATOR_DIRECT, DG_CORRELATOR_MOMENTS = 0, 1, 2
 
 
 class dg_result(C.Structure):
@@ -120,6 +130,7 @@ EXPORTS = (
     "dg_stage_snapshots_iq", "dg_write_grid", "dg_render_heatmap", "dg_write_detections_csv",
     "dg_read_grid", "dg_grid_from_axes", "dg_format_g17", "dg_scenario_samples",
     "dg_simulate_scenario",
+    "dg_tuning_default", "dg_engine_set_tuning", "dg_engine_get_tuning",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -179,6 +190,8 @@ def _load():
         "dg_scenario_samples": [C.POINTER(dg_scenario), _i64p],
         "dg_simulate_scenario": [_vp, C.POINTER(dg_scenario), C.POINTER(_vp), _dp,
                                  C.POINTER(dg_state), _dp],
+        "dg_engine_set_tuning": [_vp, C.POINTER(dg_tuning)],
+        "dg_engine_get_tuning": [_vp, C.POINTER(dg_tuning)],
         "dg_fp32_peak_tflops": [C.c_int, _dp],
         "dg_fp32x2_peak_tflops": [C.c_int, _dp],
         "dg_fp64_peak_tflops": [C.c_int, _dp],
@@ -194,6 +207,8 @@ def _load():
         fn = getattr(L, name)
         fn.restype = None
         fn.argtypes = [_vp]
+    L.dg_tuning_default.restype = None
+    L.dg_tuning_default.argtypes = [C.POINTER(dg_tuning)]
     L.dg_options_default.restype = None
     L.dg_options_default.argtypes = [C.POINTER(dg_options)]
     return L

@@ -15,6 +15,7 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "b200geo.h"
@@ -94,17 +95,12 @@ constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of
 constexpr int kMomentR[] = {8, 10, 12, 14, 16};
 constexpr int kMomentB[] = {768, 640, 512, 256, 128, 64};
 
-int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
-
 // `r`: the exact range of the candidates being correlated (bins, emptiness).
 // `a` (nullable): the FP32 planning range of the whole lattice with its FDOA
 // margin; when given, B / R / nu_c depend only on it, so every slab of a
 // lattice computes every cell bit-identically.
 StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, int64_t P_plan,
-                   int N, double fs) {
+                   int N, double fs, const dg_tuning& tn) {
     StepPlan pl;
     if (r.dmin > r.dmax) return pl;
     pl.empty = false;
@@ -127,17 +123,17 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
     // costs in FP32x2-MAC units per bucket: direct ~2.3 per candidate-sample;
     // moments R per sample (x1.5 for smem traffic) + (R + 5) per candidate-block
     double best = 2.3 * avg * N;
-    const int mode = env_int("DG_CORRELATOR_MOMENTS", 1);  // 0: force direct, 2: force moments
-    const int forceB = env_int("DG_MOMENT_B", 0), forceR = env_int("DG_MOMENT_R", 0);
+    const int forceB = tn.moment_block, forceR = tn.moment_count;
     pl.direct = true;
-    if (mode == 0) return pl;
-    if (mode == 2) best = INFINITY;
+    if (tn.correlator == DG_CORRELATOR_DIRECT) return pl;
+    if (tn.correlator == DG_CORRELATOR_MOMENTS) best = INFINITY;
     for (int B : kMomentB) {
         if (forceB && B != forceB) continue;
         const double x = M_PI * half * B;
         for (int R : kMomentR) {
             if (forceR && R != forceR) continue;
-            if (!forceR && jacobi_anger_tail(x, R) > kMomentTail) continue;
+            // a forced R is used only where it meets the truncation bound too
+            if (jacobi_anger_tail(x, R) > kMomentTail) continue;
             if (evaluate_smem_bytes(((N + B - 1) / B + kEvalG - 1) / kEvalG * kEvalG, R) >
                 kEvalSmemMax)
                 break;
@@ -226,15 +222,14 @@ struct Pipeline {
     }
     std::vector<StepPlan> plans;
     int64_t launches = 0, direct_steps = 0;
-    // refinement threshold of the block-moment path; DG_REFINE_TAU overrides
-    // (tests use a huge value to re-evaluate every element exactly)
-    float tau = [] {
-        const char* v = getenv("DG_REFINE_TAU");
-        return v && *v ? (float)atof(v) : kMomentRefineTau;
-    }();
-    // candidate block sums on the tensor cores (dg_evaluate_tc.cu); DG_EVAL_TC=0
-    // selects the FFMA2 block loop (k_evaluate)
-    bool use_tc = env_int("DG_EVAL_TC", 1) != 0;
+    // the engine's tuning (dg_engine_set_tuning), copied once per call:
+    // refinement threshold of the block-moment path (error-model studies use a
+    // huge value to re-evaluate every element exactly) and whether the
+    // candidate block sums run on the tensor cores (dg_evaluate_tc.cu) or the
+    // FFMA2 block loop (k_evaluate)
+    dg_tuning tn{};
+    float tau = kMomentRefineTau;
+    bool use_tc = true;
 
     ~Pipeline() {
         if (window_ready) cudaEventDestroy(window_ready);
@@ -245,6 +240,12 @@ struct Pipeline {
     void init(Scratch& sc, dg_engine* eng, int64_t P_, int64_t N_, int n_steps, int max_lanes = 2,
               cudaStream_t lane1 = nullptr) {
         const int sms = eng->sm_count;
+        {
+            std::lock_guard<std::mutex> lk(eng->tables_mu);
+            tn = eng->tuning;
+        }
+        tau = tn.refine_tau > 0.0 ? (float)tn.refine_tau : kMomentRefineTau;
+        use_tc = tn.evaluate_tensor != 0;
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
@@ -351,12 +352,14 @@ struct Pipeline {
     // one synchronisation: read the window's ranges (and the lattice planning
     // ranges `approx`, nullable), plan each step, upload nu_c, size the moment
     // buffers; the lanes then wait for `window_ready` (main stream)
+    // exact_ranges: `range` holds the exact FDOA and TDOA ranges of each step;
+    // otherwise (the windowed geometry pass) only its TDOA range, reduced from
+    // the step's histogram (k_hist_range), and the FDOA range is the planning one
     void plan_window(Scratch& sc, int n, double fs, const StepRange* approx = nullptr,
                      double margin_hz = 0.0, int64_t P_plan = 0, bool exact_ranges = true) {
         std::vector<StepRange> h(n), ha(approx ? n : 0);
-        if (exact_ranges)
-            CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost,
-                               sc.st));
+        if (!exact_ranges && !approx) raise(DG_ERUNTIME, "b200: plan without FDOA range");
+        CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost, sc.st));
         if (approx)
             CK(cudaMemcpyAsync(ha.data(), approx, n * sizeof(StepRange), cudaMemcpyDeviceToHost,
                                sc.st));
@@ -365,13 +368,12 @@ struct Pipeline {
         std::vector<double> nc(n);
         size_t need = 0;
         for (int i = 0; i < n; ++i) {
-            if (!exact_ranges) {  // the planning range bounds the bins (TDOA +-2 samples)
-                h[i] = ha[i];
-                h[i].dmin = std::max(h[i].dmin, 1 - N);
-                h[i].dmax = std::min(h[i].dmax, N - 1);
+            if (!exact_ranges) {  // exact bins, planning FDOA range
+                h[i].fmin = ha[i].fmin;
+                h[i].fmax = ha[i].fmax;
             }
             plans[i] = plan_step(h[i], approx ? &ha[i] : nullptr, margin_hz, approx ? P_plan : P, N,
-                                 fs);
+                                 fs, tn);
             nc[i] = plans[i].nu_c;
             const StepPlan& pl = plans[i];
             if (!pl.empty && !pl.direct)
@@ -668,6 +670,41 @@ void dg_options_default(dg_options* o) {
     o->patch_peak = 1;
 }
 
+void dg_tuning_default(dg_tuning* t) {
+    std::memset(t, 0, sizeof *t);
+    t->correlator = DG_CORRELATOR_AUTO;
+    t->evaluate_tensor = 1;
+}
+
+int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
+    return guard([&] {
+        if (!e || !t) raise(DG_EINVAL, "null argument");
+        if (t->correlator < DG_CORRELATOR_AUTO || t->correlator > DG_CORRELATOR_MOMENTS)
+            raise(DG_EINVAL, "dg_tuning: unknown correlator mode " + std::to_string(t->correlator));
+        if (t->moment_block &&
+            std::find(std::begin(kMomentB), std::end(kMomentB), t->moment_block) == std::end(kMomentB))
+            raise(DG_EINVAL, "dg_tuning: unsupported moment block " + std::to_string(t->moment_block));
+        if (t->moment_count &&
+            std::find(std::begin(kMomentR), std::end(kMomentR), t->moment_count) == std::end(kMomentR))
+            raise(DG_EINVAL, "dg_tuning: unsupported moment count " + std::to_string(t->moment_count));
+        if (!(t->refine_tau >= 0.0) || !std::isfinite(t->refine_tau))
+            raise(DG_EINVAL, "dg_tuning: refine_tau must be finite and >= 0");
+        if (t->refine_tau > 0.0 && t->refine_tau < kMomentRefineTau && !t->allow_weaker_refine)
+            raise(DG_EINVAL, "dg_tuning: refine_tau below the default " +
+                                 std::to_string(kMomentRefineTau) +
+                                 " weakens the 1e-4 contract (set allow_weaker_refine)");
+        std::lock_guard<std::mutex> lk(e->tables_mu);
+        e->tuning = *t;
+    });
+}
+
+int dg_engine_get_tuning(const dg_engine* e, dg_tuning* t) {
+    return guard([&] {
+        if (!e || !t) raise(DG_EINVAL, "null argument");
+        *t = e->tuning;
+    });
+}
+
 int dg_engine_create(int device, dg_engine** out) {
     return guard([&] {
         int n = 0;
@@ -689,6 +726,7 @@ int dg_engine_create(int device, dg_engine** out) {
         auto e = std::make_unique<dg_engine>();
         e->device = device;
         e->sm_count = prop.multiProcessorCount;
+        dg_tuning_default(&e->tuning);
         CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&e->upload, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&e->lane, cudaStreamNonBlocking));
@@ -1280,12 +1318,66 @@ void dg_staged_destroy(dg_staged* s) { delete s; }
 namespace {
 
 constexpr int kDetCap = 8192;
-constexpr int kRerankCap = 1024;
+
+// detect_emitters (correlate.hpp:127-201). Mean / sigma, the threshold and the
+// 3x3 local-maximum test run on the device; up to kDetCap local maxima are
+// sorted and greedily excluded by one CTA (k_greedy). Past that (low k_sigma
+// on large grids) every local maximum is listed on the device and the sort +
+// Chebyshev exclusion run on the host over a bucket grid of side radius + 1
+// (at most 4 accepted peaks per bucket), so the list is never truncated.
+void lattice_fill(const dg_grid* g, dg_emitter_estimate* out, int64_t m) {
+    for (int64_t i = 0; i < m; ++i) {
+        // lattice_coord (geodesy.hpp:160-162) with GridAxis::value (:145)
+        const int64_t ilat = (int64_t)out[i].lat_deg + g->row_offset;
+        const int64_t ilon = (int64_t)out[i].lon_deg;
+        out[i].lat_deg = g->lat_start + static_cast<double>(ilat) * g->lat_step;
+        out[i].lon_deg = g->lon_start + static_cast<double>(ilon) * g->lon_step;
+        out[i].alt_m = g->alt;
+        out[i].grid_index = ilat * g->n_lon + ilon;
+    }
+}
+
+void greedy_host(std::vector<DetCand>& c, int radius, double mean, double sigma, int64_t n_lon,
+                 std::vector<dg_emitter_estimate>& out) {
+    std::sort(c.begin(), c.end(), [](const DetCand& a, const DetCand& b) {
+        if (a.score != b.score) return a.score > b.score;
+        return a.key < b.key;  // correlate.hpp:172-175
+    });
+    const int64_t side = (int64_t)radius + 1;
+    std::unordered_map<uint64_t, std::vector<int>> buckets;  // accepted (ilat, ilon) by bucket
+    std::vector<DetCand> acc;
+    auto bkey = [](int64_t a, int64_t b) { return ((uint64_t)(uint32_t)a << 32) | (uint32_t)b; };
+    for (const DetCand& d : c) {
+        const int64_t bi = d.ilat / side, bj = d.ilon / side;
+        bool excluded = false;
+        for (int64_t a = bi - 1; a <= bi + 1 && !excluded; ++a)
+            for (int64_t b = bj - 1; b <= bj + 1 && !excluded; ++b) {
+                auto it = buckets.find(bkey(a, b));
+                if (it == buckets.end()) continue;
+                for (int k : it->second)
+                    if (std::max(std::abs(d.ilat - acc[k].ilat), std::abs(d.ilon - acc[k].ilon)) <=
+                        radius) {
+                        excluded = true;
+                        break;
+                    }
+            }
+        if (excluded) continue;
+        buckets[bkey(bi, bj)].push_back((int)acc.size());
+        acc.push_back(d);
+        dg_emitter_estimate e;
+        e.lat_deg = (double)d.ilat;  // lattice coordinates filled in by lattice_fill
+        e.lon_deg = (double)d.ilon;
+        e.alt_m = 0.0;
+        e.grid_index = (int64_t)d.ilat * n_lon + d.ilon;
+        e.score = d.score;
+        e.score_zsigma = (d.score - mean) / sigma;
+        out.push_back(e);
+    }
+}
 
 void run_detect(const dg_grid* g, const double* v_dev, double k_sigma, int radius,
                 dg_emitter_estimate* out, int64_t capacity, int64_t* n_out, Scratch& sc,
                 int64_t* launches) {
-    // detect_emitters (correlate.hpp:127-201)
     if (radius < 0) raise(DG_EINVAL, "detect_emitters: negative exclusion radius");
     const int64_t P = g->size();
     const int n_part = 148 * 4;
@@ -1301,12 +1393,26 @@ void run_detect(const dg_grid* g, const double* v_dev, double k_sigma, int radiu
     CK(cudaMemcpyAsync(&hc, n_c, sizeof hc, cudaMemcpyDeviceToHost, sc.st));
     CK(cudaStreamSynchronize(sc.st));
     *launches += 6;
-    if (hc > kDetCap)
-        raise(DG_ERUNTIME, "detect_emitters: " + std::to_string(hc) +
-                               " local maxima above threshold exceed the device list of " +
-                               std::to_string(kDetCap));
-    if (hc == 0) {
-        *n_out = 0;
+    *n_out = 0;
+    if (hc == 0) return;
+    if (hc > kDetCap) {  // every local maximum, host sort + exclusion
+        auto* all = sc.alloc<DetCand>(hc);
+        CK(cudaMemsetAsync(n_c, 0, sizeof(int), sc.st));
+        launch_local_max(v_dev, g->n_lat, g->n_lon, stats, k_sigma, all, n_c, hc, sc.st);
+        *launches += 1;
+        std::vector<DetCand> h(hc);
+        double hs[3];
+        CK(cudaMemcpyAsync(h.data(), all, hc * sizeof(DetCand), cudaMemcpyDeviceToHost, sc.st));
+        CK(cudaMemcpyAsync(hs, stats, sizeof hs, cudaMemcpyDeviceToHost, sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+        std::vector<dg_emitter_estimate> d;
+        greedy_host(h, radius, hs[0], hs[2], g->n_lon, d);
+        *n_out = (int64_t)d.size();
+        if (out && capacity > 0) {
+            const int64_t m = std::min<int64_t>((int64_t)d.size(), capacity);
+            std::copy(d.begin(), d.begin() + m, out);
+            lattice_fill(g, out, m);
+        }
         return;
     }
     launch_greedy(cands, n_c, kDetCap, radius, stats, g->n_lon, dets, n_c + 1, sc.st);
@@ -1321,15 +1427,7 @@ void run_detect(const dg_grid* g, const double* v_dev, double k_sigma, int radiu
         CK(cudaMemcpyAsync(out, dets, m * sizeof(dg_emitter_estimate), cudaMemcpyDeviceToHost,
                            sc.st));
         CK(cudaStreamSynchronize(sc.st));
-        for (int64_t i = 0; i < m; ++i) {
-            // lattice_coord (geodesy.hpp:160-162) with GridAxis::value (:145)
-            const int64_t ilat = (int64_t)out[i].lat_deg + g->row_offset;
-            const int64_t ilon = (int64_t)out[i].lon_deg;
-            out[i].lat_deg = g->lat_start + static_cast<double>(ilat) * g->lat_step;
-            out[i].lon_deg = g->lon_start + static_cast<double>(ilon) * g->lon_step;
-            out[i].alt_m = g->alt;
-            out[i].grid_index = ilat * g->n_lon + ilon;
-        }
+        lattice_fill(g, out, m);
     }
 }
 
@@ -1451,7 +1549,8 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         launch_geometry_steps(g->x, g->y, g->z, P, geo.pg + sp0 + w0, nw, fs, wl, pl.N,
                               pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins,
                               raw + (int64_t)w0 * P, pl.overlap, pl.err, st);
-        launches += (nw + 63) / 64;
+        launch_hist_range(pl.hist_slot(0), pl.nbins, nw, pl.N, pl.range, st);
+        launches += (nw + 63) / 64 + 1;
         if (w0 == 0) {  // the rest of the run's state, while the first geometry pass runs
             pl.init_lanes(sc);
             bits = sc.alloc<uint32_t>(n_words);
@@ -1576,117 +1675,205 @@ struct SideJoin {
     }
 };
 
-// detect_emitters on the surface `acc` on stream `det` (own scratch; its host
-// synchronisations wait for that stream only)
-void detect_beside(cudaStream_t det, const dg_grid* g, const double* acc, const dg_options& opt,
-                   dg_result* res, int64_t* launches) {
-    res->n_detections = 0;
-    if (!opt.detect) return;
-    Scratch sd(det);
-    run_detect(g, acc, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
-               res->detections_capacity, &res->n_detections, sd, launches);
+// The exact peak. Every unrefined element meets |fast - exact| <= eps exact
+// (eps = 1e-4, the per-element contract; refined elements are FP64), so with
+// all terms non-negative every accumulated value does too, and the true argmax
+// c* satisfies fast(c*) >= exact(c*)(1 - eps) >= M (1 - eps) / (1 + eps), M the
+// fast maximum. Every cell at or above that threshold is re-evaluated with the
+// reference's FP64 recurrence for all (snapshot, pair) steps and recombined in
+// the reference's order; the exact maximum (lowest flat index on ties, as
+// std::max_element) over them is the reference's argmax. Past kRerankRound
+// cells they are re-ranked in rounds in descending fast order, stopping once
+// the best exact value exceeds fast(next) / (1 - eps) >= exact(any later cell).
+constexpr double kPeakEps = 1e-4;
+constexpr int kRerankRound = 4096;
+
+struct PeakCells {
+    int n = 0;                   // re-ranked cells
+    int* cells = nullptr;        // [n] device, in re-rank order
+    double* acc_ex = nullptr;    // [n] exact accumulated values
+    double* grid_ex = nullptr;   // [n][S] exact per-snapshot values
+    long long best_i = -1;
+    double best_v = 0.0;
+};
+
+PeakCells exact_peak(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, const double* acc,
+                     const double* medians, double M, Scratch& sc, int64_t* launches) {
+    const int64_t P = g->size();
+    const int S = geo.S, SP = geo.SP, pairs = geo.pairs;
+    cudaStream_t st = sc.st;
+    PeakCells pk;
+    const double thr = M * (1.0 - kPeakEps) / (1.0 + kPeakEps);
+    auto* cnt = sc.alloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    launch_count_ge(acc, P, thr, cnt, st);
+    unsigned long long hc = 0;
+    CK(cudaMemcpyAsync(&hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *launches += 1;
+    if (hc == 0) return pk;
+    const int n = (int)hc;
+    const size_t tb = select_ge_temp_bytes(P, n);
+    void* temp = sc.alloc<unsigned char>(tb);
+    int* sel = sc.alloc<int>(n);
+    auto* n_sel = sc.alloc<int>(1);
+    launch_select_ge(acc, P, thr, sel, n_sel, temp, tb, st);
+    *launches += 1;
+    int* order = sel;
+    if (n > kRerankRound) {  // rounds in descending fast value
+        auto* keys = sc.alloc<unsigned long long>(2 * (size_t)n);
+        order = sc.alloc<int>(n);
+        launch_sort_by_value(acc, sel, n, keys, keys + n, order, temp, tb, st);
+        *launches += 2;
+    }
+    RefineCtx ctx = refine_ctx(g, sn, geo, nullptr);
+    auto* ex = sc.alloc<double>((int64_t)std::min(n, kRerankRound) * SP);
+    pk.acc_ex = sc.alloc<double>(n);
+    pk.grid_ex = sc.alloc<double>((int64_t)n * S);
+    auto* n_batch = sc.alloc<int>(1);
+    auto* best_i = sc.alloc<long long>(1);
+    auto* best_v = sc.alloc<double>(1);
+    std::vector<double> next_fast(1);
+    for (int r0 = 0; r0 < n; r0 += kRerankRound) {
+        const int m = std::min(kRerankRound, n - r0);
+        CK(cudaMemcpyAsync(n_batch, &m, sizeof m, cudaMemcpyHostToDevice, st));
+        launch_rerank(order + r0, n_batch, m, m, SP, ctx, ex, st);
+        launch_recombine_cells(n_batch, m, ex, S, pairs, medians, pk.acc_ex + r0,
+                               pk.grid_ex + (int64_t)r0 * S, st);
+        launch_argmax_cells(order + r0, n_batch, m, pk.acc_ex + r0, best_i, best_v, st);
+        *launches += 3;
+        long long bi = 0;
+        double bv = 0.0;
+        CK(cudaMemcpyAsync(&bi, best_i, sizeof bi, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&bv, best_v, sizeof bv, cudaMemcpyDeviceToHost, st));
+        const bool more = r0 + m < n;
+        int next_cell = 0;
+        if (more)
+            CK(cudaMemcpyAsync(&next_cell, order + r0 + m, sizeof next_cell,
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));  // m is host memory of this frame
+        if (pk.best_i < 0 || bv > pk.best_v || (bv == pk.best_v && bi < pk.best_i)) {
+            pk.best_i = bi;
+            pk.best_v = bv;
+        }
+        pk.n = r0 + m;
+        if (!more) break;
+        CK(cudaMemcpyAsync(next_fast.data(), acc + next_cell, sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (pk.best_v > next_fast[0] / (1.0 - kPeakEps)) break;  // no later cell can reach it
+    }
+    pk.cells = order;
+    return pk;
 }
 
 void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunGeo& geo,
                const double* grids, const double* medians, const dg_options& opt,
                bool acc_dev_allowed, dg_result* res, Scratch& sc) {
     const int64_t P = g->size();
-    const int S = geo.S, SP = geo.SP, pairs = geo.pairs;
+    const int S = geo.S;
     cudaStream_t st = sc.st;
     int64_t launches = 0;
+    if (opt.peak_stage < 0 || opt.peak_stage > 2) raise(DG_EINVAL, "dg_options: bad peak_stage");
+    if (opt.peak_stage == 2 && !res->accumulated_device)
+        raise(DG_EINVAL, "dg_options: peak_stage 2 needs the surface in accumulated_device");
+    if (!(opt.peak_max >= 0.0)) raise(DG_EINVAL, "dg_options: peak_max < 0");
     double* acc = acc_dev_allowed && res->accumulated_device ? res->accumulated_device
                                                              : sc.alloc<double>(P);
-    launch_accumulate(grids, S, P, acc, st);
-    launches += 1;
-    // the surfaces are final here: their device->host copies (engine refine
-    // stream) and the detection (engine lane stream) run beside the
-    // latency-bound exact re-rank; the re-ranked values are patched into the
-    // host copies afterwards (the device surface, which detection reads, is
-    // not patched)
-    cudaEvent_t acc_done;
+    if (opt.peak_stage != 2) {
+        launch_accumulate(grids, S, P, acc, st);
+        launches += 1;
+    }
+    const int64_t base = g->row_offset * g->n_lon;  // flat index of this grid's first cell
+    const bool patch = opt.patch_peak && opt.peak_stage != 1;
+    // the fast surfaces' device->host copies (engine refine stream) run beside
+    // the latency-bound exact re-rank; the re-ranked values are patched into
+    // the host copies afterwards and into the device surface before detection
+    cudaEvent_t acc_done, patched;
     CK(cudaEventCreateWithFlags(&acc_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&patched, cudaEventDisableTiming));
     struct EvGuard {
-        cudaEvent_t e;
-        ~EvGuard() { cudaEventDestroy(e); }
-    } acc_guard{acc_done};
+        cudaEvent_t a, b;
+        ~EvGuard() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } ev_guard{acc_done, patched};
     CK(cudaEventRecord(acc_done, st));
     cudaStream_t d2h = eng->refine, det = eng->lane;
     CK(cudaStreamWaitEvent(d2h, acc_done, 0));
-    CK(cudaStreamWaitEvent(det, acc_done, 0));
     if (res->accumulated)
         CK(cudaMemcpyAsync(res->accumulated, acc, P * sizeof(double), cudaMemcpyDeviceToHost,
                            d2h));
-    if (res->per_snapshot)
+    if (res->per_snapshot && grids)
         CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
                            cudaMemcpyDeviceToHost, d2h));
     // `acc` / `grids` are freed on st when the caller's scratch goes: st waits
     // for these readers before returning (also when an error unwinds)
     SideJoin sj(st, d2h, det);
 
-    // peak: FP64 max over the surface, then exact re-rank of every cell within
-    // a relative band of it (covers the FP32 error), lowest index on ties.
     const int n_part = 148 * 4;
     auto* part = sc.alloc<double>(n_part);
     auto* vmax = sc.alloc<double>(1);
-    auto* cells = sc.alloc<int>(kRerankCap);
-    auto* n_cells = sc.alloc<int>(1);
-    auto* best_i = sc.alloc<long long>(1);
-    auto* best_v = sc.alloc<double>(1);
     launch_max(acc, P, part, n_part, vmax, st);
     launches += 2;
     double hmax = 0.0;
     CK(cudaMemcpyAsync(&hmax, vmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    int hn = 0;
-    double *acc_ex = nullptr, *grid_ex = nullptr;
-    if (hmax > 0.0) {
-        for (double rel = 1e-5;; rel *= 0.1) {
-            CK(cudaMemsetAsync(n_cells, 0, sizeof(int), st));
-            launch_select_near(acc, P, vmax, rel, cells, n_cells, kRerankCap, st);
-            launches += 1;
-            CK(cudaMemcpyAsync(&hn, n_cells, sizeof hn, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (hn <= kRerankCap || rel < 1e-12) break;
-        }
-        RefineCtx ctx = refine_ctx(g, sn, geo, nullptr);
-        auto* ex = sc.alloc<double>((int64_t)kRerankCap * SP);
-        acc_ex = sc.alloc<double>(kRerankCap);
-        grid_ex = sc.alloc<double>((int64_t)kRerankCap * S);
-        launch_rerank(cells, n_cells, kRerankCap, hn, SP, ctx, ex, st);
-        launch_recombine_cells(n_cells, kRerankCap, ex, S, pairs, medians, acc_ex, grid_ex, st);
-        launch_argmax_cells(cells, n_cells, kRerankCap, acc_ex, best_i, best_v, st);
-        launches += 3;
-        detect_beside(det, g, acc, opt, res, &launches);
-        long long bi = 0;
-        double bv = 0.0;
-        CK(cudaMemcpyAsync(&bi, best_i, sizeof bi, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(&bv, best_v, sizeof bv, cudaMemcpyDeviceToHost, st));
+    PeakCells pk;
+    if (opt.peak_stage == 1) {  // fast maximum only (sharded runs, before peak_max is known)
+        auto* fi = sc.alloc<unsigned long long>(1);
+        CK(cudaMemsetAsync(fi, 0xff, sizeof(unsigned long long), st));
+        launch_first_max(acc, P, vmax, fi, st);
+        launches += 1;
+        unsigned long long hi = 0;
+        CK(cudaMemcpyAsync(&hi, fi, sizeof hi, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        res->argmax_index = bi + g->row_offset * g->n_lon;
-        res->argmax_value = bv;
-    } else {
-        // all-zero surface (no overlap / silent captures): first index wins
-        res->argmax_index = g->row_offset * g->n_lon;
+        res->argmax_index = (int64_t)hi + base;
         res->argmax_value = hmax;
+    } else {
+        const double M = opt.peak_max > 0.0 ? opt.peak_max : hmax;
+        if (opt.peak_max > 0.0 && hmax > opt.peak_max)
+            raise(DG_EINVAL, "dg_options: peak_max below this surface's maximum");
+        if (M > 0.0) {
+            pk = exact_peak(g, sn, geo, acc, medians, M, sc, &launches);
+            res->argmax_index = pk.best_i >= 0 ? pk.best_i + base : -1;
+            res->argmax_value = pk.best_i >= 0 ? pk.best_v : 0.0;
+        } else {
+            // all-zero surface (no overlap / silent captures): first index wins
+            res->argmax_index = base;
+            res->argmax_value = hmax;
+        }
+        if (patch && pk.n > 0) {
+            launch_patch_cells(pk.cells, pk.n, pk.acc_ex, acc, st);
+            launches += 1;
+        }
     }
-    res->n_reranked = std::min(hn, kRerankCap);
-    if (!(hmax > 0.0)) detect_beside(det, g, acc, opt, res, &launches);
+    res->n_reranked = pk.n;
+    CK(cudaEventRecord(patched, st));
+    CK(cudaStreamWaitEvent(det, patched, 0));
+    res->n_detections = 0;
+    if (opt.detect && opt.peak_stage != 1) {
+        Scratch sd(det);
+        run_detect(g, acc, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
+                   res->detections_capacity, &res->n_detections, sd, &launches);
+    }
 
     sj.join();
     CK(cudaStreamSynchronize(st));
-    if (opt.patch_peak && acc_ex && res->n_reranked > 0 && (res->accumulated || res->per_snapshot)) {
+    if (patch && pk.n > 0 && (res->accumulated || res->per_snapshot)) {
         // exact FP64 values of the re-ranked cells into the host copies
-        const int n = (int)res->n_reranked;
+        const int n = pk.n;
         std::vector<int> hc(n);
         std::vector<double> ha(n), hg((size_t)n * S);
-        CK(cudaMemcpyAsync(hc.data(), cells, n * sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(ha.data(), acc_ex, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hg.data(), grid_ex, (size_t)n * S * sizeof(double),
+        CK(cudaMemcpyAsync(hc.data(), pk.cells, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ha.data(), pk.acc_ex, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hg.data(), pk.grid_ex, (size_t)n * S * sizeof(double),
                            cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         for (int i = 0; i < n; ++i) {
             if (res->accumulated) res->accumulated[hc[i]] = ha[i];
-            if (res->per_snapshot)
+            if (res->per_snapshot && grids)
                 for (int s = 0; s < S; ++s)
                     res->per_snapshot[(int64_t)s * P + hc[i]] = hg[(size_t)i * S + s];
         }
@@ -1762,7 +1949,8 @@ int dg_accumulate_peak(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     return guard([&] {
         const dg_options opt = options_or_default(opt_in);
         check_run(eng, g, sn, opt, res);
-        if (!grids_device) raise(DG_EINVAL, "dg_accumulate_peak: null grids");
+        if (!grids_device && opt.peak_stage != 2)
+            raise(DG_EINVAL, "dg_accumulate_peak: null grids");
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
         Scratch sc(sg.st);

@@ -24,8 +24,8 @@
 // the block rotation + ~0.2 shared (z production, anchor) instructions.
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdlib.h>
 
+#include "dg_device.cuh"
 #include "dg_internal.cuh"
 
 namespace dg {
@@ -33,53 +33,6 @@ namespace dg {
 namespace {
 
 constexpr int kYPad = 8;  // extra samples per y2 staging buffer (parity shift + slack)
-
-__device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) {
-    float2 d;
-    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\t"
-        "mov.b64 rb, {%4, %4};\n\t"
-        "mov.b64 rc, {%5, %6};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
-        "mov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b), "f"(c.x), "f"(c.y));
-    return d;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
-// 1-D bulk copy global -> shared (TMA engine), completion on `bar`
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 template <int kCh>
 struct alignas(16) WarpSmemT {
@@ -270,52 +223,18 @@ void launch_variant(int n_tasks_max, cudaStream_t st, const Task* tasks, const i
                                          flag_bits, flag_base);
 }
 
-int variant_from_env() {
-    const char* v = getenv("DG_CORRELATE_VARIANT");
-    return v ? atoi(v) : 0;
-}
-
 }  // namespace
 
-int correlate_task_size() {
-    static const int v = variant_from_env();
-    return v == 1 || v == 2 ? 32 : 64;
-}
+// two candidates per lane (a 64-candidate warp task), 3 CTAs x 4 warps per SM
+// (148 registers): the variant kept from the r01 sweep of (NC, LB, CH, WPC, MINB)
+int correlate_task_size() { return 64; }
 
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
                       double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st) {
     if (max_tasks <= 0) return;
-    static const int variant = variant_from_env();
-    switch (variant) {
-        case 1:  // one candidate per lane (r01b)
-            launch_variant<1, 16, 256, 8, 2>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-            break;
-        case 2:
-            launch_variant<1, 16, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-            break;
-        case 4:
-            launch_variant<2, 8, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                            fs, s_out, flag_bits, flag_base);
-            break;
-        case 5:
-            launch_variant<2, 16, 256, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-            break;
-        case 6:
-            launch_variant<2, 12, 192, 4, 4>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-            break;
-        case 7:
-            launch_variant<2, 12, 192, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-            break;
-        default:  // two candidates per lane, 3 CTAs x 4 warps per SM, 148 registers
-            launch_variant<2, 16, 256, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N,
-                                             fs, s_out, flag_bits, flag_base);
-    }
+    launch_variant<2, 16, 256, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N, fs,
+                                     s_out, flag_bits, flag_base);
 }
 
 }  // namespace dg

@@ -113,6 +113,7 @@ struct StreamGuard {
 struct dg_engine {
     int device = 0;
     int sm_count = 148;
+    dg_tuning tuning{};  // validated by dg_engine_set_tuning; read once per call
     cudaStream_t stream = nullptr;  // default stream of calls that pass none
     cudaStream_t upload = nullptr;  // capture uploads overlapped with the geometry phase
     // the second correlation lane and the side refinement of a run, created once

@@ -109,6 +109,9 @@ void launch_geometry_steps(const double* x, const double* y, const double* z, in
                            const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
                            double* fdoa_out, int* hist, int nbins, double* s_out,
                            unsigned long long* overlap, int* err, cudaStream_t st);
+// exact TDOA range (first / last non-empty bin) of each of n_steps histograms
+void launch_hist_range(const int* hist, int nbins, int n_steps, int N, StepRange* out,
+                       cudaStream_t st);
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
                             const PairGeom* pg_dev, double fs, double wl, dg_pair_offsets* out,
                             int* err, cudaStream_t st);
@@ -254,8 +257,21 @@ void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st);
 void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st);
 void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,
                 cudaStream_t st);
-void launch_select_near(const double* v, int64_t P, const double* vmax, double rel,
-                        int* list, int* count, int cap, cudaStream_t st);
+// near-peak selection for the exact re-rank: count of cells >= thr; the cells
+// >= thr in ascending index (CUB select; temp sized by select_ge_temp_bytes for
+// P cells and n_sel selected); a stable descending sort of selected cells by
+// value (ties keep ascending index); exact values written into a surface
+void launch_count_ge(const double* v, int64_t P, double thr, unsigned long long* count,
+                     cudaStream_t st);
+size_t select_ge_temp_bytes(int64_t P, int n_sel);
+void launch_select_ge(const double* v, int64_t P, double thr, int* cells, int* n_out, void* temp,
+                      size_t temp_bytes, cudaStream_t st);
+void launch_sort_by_value(const double* v, const int* cells, int n, unsigned long long* keys,
+                          unsigned long long* keys_out, int* cells_out, void* temp,
+                          size_t temp_bytes, cudaStream_t st);
+void launch_patch_cells(const int* cells, int n, const double* val, double* surf, cudaStream_t st);
+void launch_first_max(const double* v, int64_t P, const double* vmax, unsigned long long* idx,
+                      cudaStream_t st);
 // n_items_hint: host-side count of near-peak cells (sizes the launch)
 void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
                    RefineCtx ctx, double* ex, cudaStream_t st);

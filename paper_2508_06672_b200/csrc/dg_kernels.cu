@@ -11,6 +11,9 @@
 //   warp tasks, raw surface double [S*pairs][P], refine bitmap 1 bit/element.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include <algorithm>
 #include <float.h>
 #include <limits.h>
@@ -222,9 +225,9 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
 // Phase A of a window of steps in one pass: each thread loads its candidate
 // once and predicts the offsets of every step of the window (receiver states
 // staged in shared memory), writing d[s][P], fdoa[s][P], the per-step TDOA
-// histograms and S = 0 for candidates without overlap. The exact ranges are
-// not reduced here: the window is planned from the FP32 lattice ranges
-// (k_range_fp32), whose TDOA range (+-2 samples) bounds the bins.
+// histograms and S = 0 for candidates without overlap. The ranges are not
+// reduced here: the bins come from the histograms (k_hist_range), B / R / the
+// centre frequency from the FP32 lattice ranges (k_range_fp32).
 constexpr int kGeoStepsMax = 64;  // steps per launch (shared-memory receiver table)
 
 __global__ void __launch_bounds__(256)
@@ -239,7 +242,7 @@ k_geometry_steps(const double* __restrict__ x, const double* __restrict__ y,
         reinterpret_cast<double*>(sg)[i] = reinterpret_cast<const double*>(pg)[i];
     __syncthreads();
     unsigned long long ovl = 0;
-    RangeAcc ra;  // unused: planning ranges come from the FP32 pass
+    RangeAcc ra;  // not flushed: ranges come from k_hist_range / k_range_fp32
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         const double cx = x[p], cy = y[p], cz = z[p];
@@ -359,6 +362,47 @@ k_range_fp32(const float4* __restrict__ rel, int64_t P, const RxPairF32* __restr
             }
         }
         __syncthreads();
+    }
+}
+
+// Exact TDOA range of each step of a window: the first and last non-empty
+// bin of its histogram (one CTA per step). The buckets are planned over these
+// bins, so every candidate lands in a planned bin whatever the error of the
+// FP32 planning pass (which now only sets B, R and the centre frequency).
+constexpr int kHistRangeThreads = 512;
+
+__global__ void __launch_bounds__(kHistRangeThreads)
+k_hist_range(const int* __restrict__ hist, int nbins, int N, StepRange* __restrict__ out) {
+    __shared__ int red[2][kHistRangeThreads / 32];
+    const int* h = hist + (int64_t)blockIdx.x * nbins;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+        if (h[b]) {
+            lo = min(lo, b);
+            hi = max(hi, b);
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][warp] = lo;
+        red[1][warp] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kHistRangeThreads / 32; ++w) {
+            lo = min(lo, red[0][w]);
+            hi = max(hi, red[1][w]);
+        }
+        StepRange r;
+        r.fmin = ~0ull;
+        r.fmax = 0ull;
+        r.dmin = lo <= hi ? lo - (N - 1) : INT_MAX;
+        r.dmax = lo <= hi ? hi - (N - 1) : INT_MIN;
+        out[blockIdx.x] = r;
     }
 }
 
@@ -729,18 +773,48 @@ __global__ void k_max_final(const double* __restrict__ part, int n, double* __re
     }
 }
 
-__global__ void k_select_near(const double* __restrict__ v, int64_t P,
-                              const double* __restrict__ vmax, double rel, int* __restrict__ list,
-                              int* __restrict__ count, int cap) {
-    const double m = *vmax;
-    const double thr = m - fabs(m) * rel;
+// Near-peak cells for the exact re-rank: every cell whose fast value is >= thr,
+// counted, then listed in ascending flat index (CUB select, stable) so the
+// candidate set never depends on atomic order.
+__global__ void k_count_ge(const double* __restrict__ v, int64_t P, double thr,
+                           unsigned long long* __restrict__ count) {
+    unsigned long long c = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        if (v[i] >= thr) {
-            const int pos = atomicAdd(count, 1);
-            if (pos < cap) list[pos] = (int)i;
-        }
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        c += v[i] >= thr ? 1ull : 0ull;
+    c = warp_sum_u64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+struct GeThreshold {
+    const double* v;
+    double thr;
+    __device__ __forceinline__ bool operator()(const int& i) const { return v[i] >= thr; }
+};
+
+// cells[i] = the i-th selected cell; keys[i] = its fast value's bit pattern
+// (order-preserving for v >= 0) for the descending sort of large selections
+__global__ void k_gather_keys(const double* __restrict__ v, const int* __restrict__ cells, int n,
+                              unsigned long long* __restrict__ keys) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        keys[i] = (unsigned long long)__double_as_longlong(v[cells[i]]);
+}
+
+// the exact values of the re-ranked cells written into a surface
+__global__ void k_patch_cells(const int* __restrict__ cells, int n, const double* __restrict__ val,
+                              double* __restrict__ surf) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        surf[cells[i]] = val[i];
+}
+
+// lowest flat index whose value equals the maximum (std::max_element on the
+// fast surface; accumulate-only calls of sharded runs)
+__global__ void k_first_max(const double* __restrict__ v, int64_t P, const double* __restrict__ vmax,
+                            unsigned long long* __restrict__ idx) {
+    const double m = *vmax;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (v[i] == m) atomicMin(idx, (unsigned long long)i);
 }
 
 // Exact re-evaluation of the near-peak candidates into a private buffer
@@ -1177,6 +1251,11 @@ void launch_geometry_steps(const double* x, const double* y, const double* z, in
     }
 }
 
+void launch_hist_range(const int* hist, int nbins, int n_steps, int N, StepRange* out,
+                       cudaStream_t st) {
+    k_hist_range<<<n_steps, kHistRangeThreads, 0, st>>>(hist, nbins, N, out);
+}
+
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
                             const PairGeom* pg, double fs, double wl, dg_pair_offsets* out, int* err,
                             cudaStream_t st) {
@@ -1265,9 +1344,43 @@ void launch_max(const double* v, int64_t P, double* partial, int n_partial, doub
     k_max_final<<<1, 1024, 0, st>>>(partial, n_partial, out);
 }
 
-void launch_select_near(const double* v, int64_t P, const double* vmax, double rel, int* list,
-                        int* count, int cap, cudaStream_t st) {
-    k_select_near<<<blocks_for(P, 256), 256, 0, st>>>(v, P, vmax, rel, list, count, cap);
+void launch_count_ge(const double* v, int64_t P, double thr, unsigned long long* count,
+                     cudaStream_t st) {
+    k_count_ge<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(v, P, thr, count);
+}
+
+size_t select_ge_temp_bytes(int64_t P, int n_sel) {
+    size_t a = 0, b = 0;
+    cub::DeviceSelect::If(nullptr, a, thrust::counting_iterator<int>(0), (int*)nullptr,
+                          (int*)nullptr, (int)P, GeThreshold{nullptr, 0.0});
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (const unsigned long long*)nullptr,
+                                              (unsigned long long*)nullptr, (const int*)nullptr,
+                                              (int*)nullptr, n_sel);
+    return std::max(a, b);
+}
+
+void launch_select_ge(const double* v, int64_t P, double thr, int* cells, int* n_out, void* temp,
+                      size_t temp_bytes, cudaStream_t st) {
+    cub::DeviceSelect::If(temp, temp_bytes, thrust::counting_iterator<int>(0), cells, n_out,
+                          (int)P, GeThreshold{v, thr}, st);
+}
+
+void launch_sort_by_value(const double* v, const int* cells, int n, unsigned long long* keys,
+                          unsigned long long* keys_out, int* cells_out, void* temp,
+                          size_t temp_bytes, cudaStream_t st) {
+    k_gather_keys<<<blocks_for(n, 256), 256, 0, st>>>(v, cells, n, keys);
+    // radix sort is stable: equal values keep ascending flat index
+    cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, keys, keys_out, cells, cells_out, n,
+                                              0, 64, st);
+}
+
+void launch_patch_cells(const int* cells, int n, const double* val, double* surf, cudaStream_t st) {
+    if (n > 0) k_patch_cells<<<blocks_for(n, 256), 256, 0, st>>>(cells, n, val, surf);
+}
+
+void launch_first_max(const double* v, int64_t P, const double* vmax, unsigned long long* idx,
+                      cudaStream_t st) {
+    k_first_max<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(v, P, vmax, idx);
 }
 
 void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,

@@ -4,6 +4,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
+from . import _capi
 from ._capi import check, lib
 
 
@@ -26,6 +27,33 @@ class Engine:
         workers = C.c_uint()
         check(lib.dg_engine_descriptor(self._h, name, 32, kind, 32, C.byref(workers)))
         return name.value.decode(), kind.value.decode(), workers.value
+
+    def tuning(self) -> dict:
+        t = _capi.dg_tuning()
+        check(lib.dg_engine_get_tuning(self._h, C.byref(t)))
+        return {name: getattr(t, name) for name, _ in t._fields_}
+
+    def set_tuning(self, **kw) -> None:
+        """Correlator tuning for tests / benchmarks (dg_engine_set_tuning, validated
+        by the library): correlator ("auto" | "direct" | "moments"), moment_block,
+        moment_count, evaluate_tensor, refine_tau, allow_weaker_refine. Keys not
+        given keep the library default."""
+        t = _capi.dg_tuning()
+        lib.dg_tuning_default(C.byref(t))
+        modes = {"auto": _capi.DG_CORRELATOR_AUTO, "direct": _capi.DG_CORRELATOR_DIRECT,
+                 "moments": _capi.DG_CORRELATOR_MOMENTS}
+        for k, v in kw.items():
+            if k == "correlator" and isinstance(v, str):
+                v = modes[v]
+            if not hasattr(t, k):
+                raise ValueError(f"set_tuning: unknown key {k}")
+            setattr(t, k, v)
+        check(lib.dg_engine_set_tuning(self._h, C.byref(t)))
+
+    def reset_tuning(self) -> None:
+        t = _capi.dg_tuning()
+        lib.dg_tuning_default(C.byref(t))
+        check(lib.dg_engine_set_tuning(self._h, C.byref(t)))
 
     def __del__(self):
         h = getattr(self, "_h", None)

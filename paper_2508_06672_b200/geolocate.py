@@ -217,7 +217,8 @@ def _snapshots_struct(states, captures, fs, fc):
     return snaps, keep
 
 
-def _options(options: GeolocateOptions, stream=None, profile=False) -> _capi.dg_options:
+def _options(options: GeolocateOptions, stream=None, profile=False, peak_stage=0,
+             peak_max=0.0) -> _capi.dg_options:
     o = _capi.dg_options()
     lib.dg_options_default(C.byref(o))
     o.k_sigma = float(options.k_sigma)
@@ -227,12 +228,14 @@ def _options(options: GeolocateOptions, stream=None, profile=False) -> _capi.dg_
     o.stream = stream
     o.profile = int(bool(profile))
     o.patch_peak = int(bool(options.patch_peak))
+    o.peak_stage = int(peak_stage)
+    o.peak_max = float(peak_max)
     return o
 
 
 def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, want_surface=True,
          want_per_snapshot=False, accumulated_device=None, stream=None, profile=False,
-         det_cap=4096, out=None):
+         det_cap=4096, out=None, peak_stage=0, peak_max=0.0):
     P = grid.size()
     res = _capi.dg_result()
     acc = None
@@ -251,8 +254,21 @@ def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, w
         res.accumulated_device = int(accumulated_device)
     res.detections = dets
     res.detections_capacity = det_cap
-    opt = _options(options, stream, profile)
+    opt = _options(options, stream, profile, peak_stage, peak_max)
     check(call(C.byref(opt), C.byref(res)))
+    if options.detect and res.n_detections > det_cap:
+        # the engine never truncates: the whole list from the returned surface
+        surf, on_dev = (acc.ctypes.data, 0) if acc is not None else (accumulated_device, 1)
+        if surf is None:
+            raise RuntimeError(f"{res.n_detections} detections exceed the {det_cap}-entry buffer "
+                               "and no surface was returned to re-run detect_emitters on")
+        det_cap = int(res.n_detections)
+        dets = (_capi.dg_emitter_estimate * det_cap)()
+        n = C.c_int64()
+        check(lib.dg_detect_emitters(grid.engine.handle, grid.handle, C.c_void_p(int(surf)), on_dev,
+                                     float(options.k_sigma), int(options.exclusion_radius_cells),
+                                     dets, det_cap, C.byref(n)))
+        res.n_detections = n.value
     detections = [EmitterEstimate(GeodeticCoord(d.lat_deg, d.lon_deg, d.alt_m), int(d.grid_index),
                                   d.score, d.score_zsigma)
                   for d in dets[:min(res.n_detections, det_cap)]]
@@ -266,6 +282,33 @@ def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, w
     per_list = [CorrelationGrid(grid, per[s]) for s in range(n_snap)] if per is not None else []
     return GeolocateResult(grid, per_list, CorrelationGrid(grid, acc), detections,
                            int(res.argmax_index), float(res.argmax_value), stats)
+
+
+def detect_emitters(grid: CorrelationGrid, k_sigma: float = 5.0,
+                    exclusion_radius_cells: int = 5, values_device: int | None = None) -> list:
+    """detect_emitters (correlate.hpp:127-201) on the GPU: every detection, in the
+    reference's order. `grid.values` (host float64) or, if given, a device
+    pointer to the surface (values_device) over grid.grid."""
+    g = grid.grid
+    if values_device is None:
+        v = np.ascontiguousarray(grid.values, np.float64)
+        if v.size != g.size():
+            raise ValueError("CorrelationGrid: value count != grid size")
+        surf, on_dev = v.ctypes.data, 0
+    else:
+        surf, on_dev = int(values_device), 1
+    cap = 256
+    while True:
+        out = (_capi.dg_emitter_estimate * cap)()
+        n = C.c_int64()
+        check(lib.dg_detect_emitters(g.engine.handle, g.handle, C.c_void_p(surf), on_dev,
+                                     float(k_sigma), int(exclusion_radius_cells), out, cap,
+                                     C.byref(n)))
+        if n.value <= cap:
+            return [EmitterEstimate(GeodeticCoord(d.lat_deg, d.lon_deg, d.alt_m),
+                                    int(d.grid_index), d.score, d.score_zsigma)
+                    for d in out[:n.value]]
+        cap = int(n.value)
 
 
 def geolocate_arrays(grid: CandidateGrid, states: np.ndarray, captures: np.ndarray,
@@ -349,6 +392,10 @@ def geolocate_snapshots(snapshots: list, grid: CandidateGrid,
                 raise ValueError("backend stage: sample rates differ")
             if len(c.samples) != len(c0.samples):
                 raise ValueError("backend stage: sample counts differ")
+            # the reference takes each pair's wavelength from its first capture
+            # (geolocate.hpp:55); the engine runs one carrier per run
+            if c.center_freq_hz != c0.center_freq_hz:
+                raise ValueError("geolocate_snapshots: center frequencies differ")
     f32 = all(np.asarray(c.samples).dtype == np.complex64 for s in snapshots for c in s.captures)
     caps = np.stack([np.stack([np.asarray(c.samples) for c in s.captures]) for s in snapshots])
     caps = caps.astype(np.complex64 if f32 else np.complex128, copy=False)

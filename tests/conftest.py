@@ -37,3 +37,12 @@ def b2():
     import paper_2508_06672_b200 as b2
     b2.default_engine(0)
     return b2
+
+
+@pytest.fixture
+def tune(b2):
+    """Set the default engine's correlator tuning for one test (dg_engine_set_tuning);
+    restored to the product defaults afterwards."""
+    eng = b2.default_engine(0)
+    yield eng.set_tuning
+    eng.reset_tuning()

@@ -116,3 +116,57 @@ def test_c4_coarse_then_fine_vs_oracle(b2, orc):
         sample = list(rng.integers(0, fine.size(), 8))
         w = np.array([_oracle_acc(orc, states, caps, fs, fc, fine.points[p]) for p in sample])
         assert rel_err(r.accumulated.values[sample], w).max() <= REL_TOL
+
+
+def test_c2_full_vs_reference(b2, ref):
+    """C2 in full: 501 x 501 cells x 10 snapshots of a chirp at -10 dB,
+    the reference's own geolocate_snapshots (ParallelBatchedBackend, ~30 s on the
+    box's host cores) against the engine: every per-snapshot element within
+    1e-4, the argmax index and value bit-exact, the detection list equal."""
+    import scenes
+    sc = ref.simulate(scenes.render(scenes.config("C2")))
+    assert sc.captures.shape == (10, 2, 50_000)
+    want = ref.geolocate(sc.states, sc.captures, sc.fs, sc.fc, sc.bounds, sc.spacing, sc.alt,
+                         backend="parallel", batch_size=4096, per_snapshot=True)
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    assert (grid.lat.count, grid.lon.count) == (501, 501)
+    res = b2.geolocate_arrays(grid, sc.states, sc.captures, sc.fs, sc.fc)
+    per = np.stack([g.values for g in res.per_snapshot])
+    assert rel_err(per, want["per_snapshot"]).max() <= REL_TOL
+    acc = res.accumulated.values
+    assert np.abs(acc - want["accumulated"]).max() / want["accumulated"].max() <= NORM_TOL
+    assert res.argmax_index == int(np.argmax(want["accumulated"]))
+    assert res.argmax_value == want["accumulated"][res.argmax_index]
+    assert [d.grid_index for d in res.detections] == [d["grid_index"] for d in want["detections"]]
+
+
+def test_c5_sampled_cells_vs_oracle(b2, orc):
+    """C5 (the scaling configuration): 4001 x 4001 = 16,008,001 cells x
+    100 snapshots. Sampled cells and the eight largest cells against the oracle's
+    FP64 reference-order correlation; the peak is the exact maximum over every
+    cell the fast surface cannot rule out."""
+    states, caps, bounds, spacing, _ = _simulated(b2, "C5")
+    S, N, fs, fc = 100, 50_000, 5e6, 1575.42e6
+    assert caps.shape == (S, 2, N)
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
+    assert grid.size() == 16_008_001
+    res = b2.geolocate_arrays(grid, states, caps, fs, fc, b2.GeolocateOptions(detect=True),
+                              want_per_snapshot=False)
+    acc = res.accumulated.values
+    pts = grid.points
+
+    def oracle_acc(p):
+        return _oracle_acc(orc, states, caps, fs, fc, pts[p])
+
+    rng = np.random.default_rng(5)
+    cells = list(rng.integers(0, grid.size(), 96))
+    want = np.array([oracle_acc(p) for p in cells])
+    assert rel_err(acc[cells], want).max() <= REL_TOL
+    assert res.argmax_value == pytest.approx(oracle_acc(res.argmax_index), rel=1e-12)
+    top = np.argsort(acc)[::-1][:8]
+    exact = {int(p): oracle_acc(int(p)) for p in top}
+    best = max(exact.items(), key=lambda kv: (kv[1], -kv[0]))
+    assert best[0] == res.argmax_index
+    assert len(res.detections) >= 4
+    for d in res.detections:
+        assert d.score == acc[d.grid_index]

@@ -140,9 +140,9 @@ def test_golden_correlate_batch(b2):
     (4096, 20_000, 5e6, 1.25e6, 1),      # BenchWorkload distribution (bench.hpp:65-88)
     (50_000, 4_000, 5e6, 2e4, 3),        # C2..C5 capture length
 ])
-@pytest.mark.parametrize("mode", ["1", "0", "2"])  # auto / direct only / moments when admissible
-def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, monkeypatch):
-    monkeypatch.setenv("DG_CORRELATOR_MOMENTS", mode)
+@pytest.mark.parametrize("mode", ["auto", "direct", "moments"])  # moments: when admissible
+def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, tune):
+    tune(correlator=mode)
     rng = np.random.default_rng(seed)
     y1, y2 = gauss(rng, n), gauss(rng, n)
     if seed == 1:  # BenchWorkload: uniform [-1, 1] I/Q, |tdoa| <= N/2
@@ -160,16 +160,14 @@ def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, m
 @pytest.mark.parametrize("block", [64, 128, 256, 512, 640, 768])
 @pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200),
                                             (3e3, 12)])  # ~250 per bucket: 2 tiles
-@pytest.mark.parametrize("tc", ["1", "0"])  # block sums on tcgen05 / FFMA2 block loop
-def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, tc, monkeypatch):
+@pytest.mark.parametrize("tc", [1, 0])  # block sums on tcgen05 / FFMA2 block loop
+def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, tc, tune):
     """The block-moment correlator at every block length against the reference,
     on buckets dense enough that it is the planner's choice (many candidates
     per TDOA), including FDOA == 0 (x = 0) and the full TDOA range; candidate
     evaluation on the tensor cores (k_evaluate_tc, B = 256 and 512 at 50k
     samples: 2 nb <= 512 TMEM columns) and on the FFMA2 block loop."""
-    monkeypatch.setenv("DG_CORRELATOR_MOMENTS", "2")
-    monkeypatch.setenv("DG_MOMENT_B", str(block))
-    monkeypatch.setenv("DG_EVAL_TC", tc)
+    tune(correlator="moments", moment_block=block, evaluate_tensor=tc)
     n, fs, count = 50_000, 5e6, 6_000
     rng = np.random.default_rng(block + int(span))
     y1, y2 = gauss(rng, n), gauss(rng, n)

@@ -1,0 +1,169 @@
+"""GPU parity of the exact peak and of detect_emitters at the edges.
+
+* The re-rank band is derived from the 1e-4 per-element contract (DESIGN.md
+  section 6): the exact argmax must equal std::max_element over the oracle's
+  surface (tests/test_geolocate.cpp:30-33) even when thousands of cells tie,
+  which forces the round-by-round re-rank in descending fast order.
+* With patch_peak the returned surfaces (host and device) hold the exact values
+  of the re-ranked cells before detection, so detection scores equal the
+  surface and max_element on it is the argmax.
+* detect_emitters (correlate.hpp:127-201) returns every detection: past the
+  8,192 local maxima of the one-CTA path the sort and exclusion run on the
+  host, identical to the reference's list.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import load_scene
+
+pytestmark = pytest.mark.gpu
+
+
+def _plateau_points(ref, sc, n_copies, n_other, seed):
+    """Lattice-shaped point set: n_copies copies of the emitter's node (identical
+    offsets, so identical fast and exact values) spread among other nodes."""
+    nl, nn, pts = ref.build_grid(sc.bounds, sc.spacing, sc.alt)
+    rng = np.random.default_rng(seed)
+    peak = ref.lla_to_ecef(0.0, 0.0, 0.0)
+    other = pts[rng.integers(0, len(pts), n_other)]
+    out = np.concatenate([np.tile(peak, (n_copies, 1)), other])
+    return out[rng.permutation(len(out))]
+
+
+@pytest.mark.parametrize("n_copies", [3000, 9000])  # one round / three rounds of 4,096
+def test_plateau_argmax_is_first_max(b2, ref, orc, n_copies):
+    sc = load_scene(ref, "DESK_SAWTOOTH")  # one sawtooth emitter on node (0, 0)
+    pts = _plateau_points(ref, sc, n_copies, 1000, n_copies)
+    P = len(pts)
+    lat = b2.GridAxis(0.0, 1.0, 1)
+    lon = b2.GridAxis(0.0, 1.0, P)
+    grid = b2.grid_from_points(pts, lat, lon)
+    S = 4
+    res = b2.geolocate_arrays(grid, sc.states[:S], sc.captures[:S], sc.fs, sc.fc,
+                              b2.GeolocateOptions(detect=False))
+    per = np.stack([orc.correlate_snapshot(pts, sc.states[s, 0], sc.states[s, 1],
+                                           sc.captures[s, 0], sc.captures[s, 1], sc.fs, sc.fc)
+                    for s in range(S)])
+    want = orc.accumulate(per)
+    first = orc.argmax(want)
+    assert res.argmax_index == first
+    assert res.argmax_value == want[first]
+    assert res.stats["n_reranked"] >= n_copies
+    acc = res.accumulated.values
+    assert int(np.argmax(acc)) == first  # patched surface: max_element is the exact argmax
+
+
+def test_patched_surface_consistent(b2, ref):
+    """Host surface, device surface and detection scores agree after patching."""
+    import torch
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    dev = torch.empty(grid.size(), dtype=torch.float64, device="cuda")
+    staged = b2.StagedSnapshots(sc.states, sc.captures, sc.fs, sc.fc)
+    opts = b2.GeolocateOptions(k_sigma=sc.k_sigma, exclusion_radius_cells=sc.radius)
+    res = b2.geolocate_staged(grid, staged, opts, want_surface=True,
+                              accumulated_device=dev.data_ptr())
+    torch.cuda.synchronize()
+    host = res.accumulated.values
+    assert np.array_equal(dev.cpu().numpy(), host)
+    assert host[res.argmax_index] == res.argmax_value
+    for d in res.detections:
+        assert d.score == host[d.grid_index]
+    unpatched = b2.geolocate_staged(grid, staged, b2.GeolocateOptions(
+        k_sigma=sc.k_sigma, exclusion_radius_cells=sc.radius, patch_peak=False))
+    assert unpatched.argmax_index == res.argmax_index
+    assert unpatched.argmax_value == res.argmax_value
+    diff = np.nonzero(unpatched.accumulated.values != host)[0]
+    assert len(diff) <= res.stats["n_reranked"]
+
+
+def test_two_stage_peak_matches_single_call(b2, ref):
+    """peak_stage 1 (accumulate only) + peak_stage 2 with the global maximum
+    (sharded runs) re-rank the same cells as the one-call peak."""
+    import torch
+
+    from paper_2508_06672_b200.sharding import slab_rows
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    staged = b2.StagedSnapshots(sc.states, sc.captures, sc.fs, sc.fc)
+    opts = b2.GeolocateOptions(detect=False)
+    full = b2.geolocate_staged(grid, staged, opts, want_surface=True)
+    S, P, n_lon = sc.states.shape[0], grid.size(), grid.lon.count
+    grids = torch.empty((S, P), dtype=torch.float64, device="cuda")
+    b2.correlate_steps(grid, staged, 0, S, grids.data_ptr(), None, opts)
+    world = 3
+    accs, fast_max = [], 0.0
+    for j in range(world):
+        r0, r1 = slab_rows(grid.lat.count, j, world)
+        a = torch.empty((r1 - r0) * n_lon, dtype=torch.float64, device="cuda")
+        slab = grids[:, r0 * n_lon:r1 * n_lon].contiguous()
+        r = b2.accumulate_peak(grid.slab(r0, r1), staged, slab.data_ptr(), None, opts,
+                               want_surface=False, accumulated_device=a.data_ptr(), peak_stage=1)
+        fast_max = max(fast_max, r.argmax_value)
+        accs.append((a, slab, r0, r1))
+    peaks, parts = [], []
+    for a, slab, r0, r1 in accs:
+        r = b2.accumulate_peak(grid.slab(r0, r1), staged, slab.data_ptr(), None, opts,
+                               want_surface=True, accumulated_device=a.data_ptr(), peak_stage=2,
+                               peak_max=fast_max)
+        peaks.append((r.argmax_value, r.argmax_index))
+        parts.append(r.accumulated.values)
+    from paper_2508_06672_b200.sharding import merge_argmax
+    assert merge_argmax(peaks) == (full.argmax_value, full.argmax_index)
+    assert np.array_equal(np.concatenate(parts), full.accumulated.values)
+
+
+def test_detect_beyond_device_list_vs_reference(b2, ref):
+    """A 1001 x 1001 surface with ~10^5 local maxima above mean + 1 sigma: the
+    engine's list equals the reference's detect_emitters element for element."""
+    bounds, spacing = (0.0, 10.0, 0.0, 10.0), 0.01
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
+    rng = np.random.default_rng(5)
+    v = rng.random(grid.size()) ** 2
+    for k_sigma, radius in ((1.0, 0), (1.0, 2), (0.5, 5)):
+        want = ref.detect_emitters(bounds, spacing, 0.0, v, k_sigma, radius, cap=grid.size())
+        got = b2.detect_emitters(b2.CorrelationGrid(grid, v), k_sigma, radius)
+        assert len(got) > 8192 or radius > 0
+        assert [d.grid_index for d in got] == [w[0] for w in want]
+        assert [d.score for d in got] == [w[1] for w in want]
+        np.testing.assert_allclose([d.score_zsigma for d in got], [w[2] for w in want],
+                                   rtol=1e-12)
+
+
+def test_detect_capacity_recall(b2, ref):
+    """n_detections reports the whole list; the Python driver fetches it all."""
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    opts = b2.GeolocateOptions(k_sigma=0.5, exclusion_radius_cells=0)
+    res = b2.geolocate_arrays(grid, sc.states, sc.captures, sc.fs, sc.fc, opts, det_cap=4)
+    want = ref.detect_emitters(sc.bounds, sc.spacing, sc.alt, res.accumulated.values, 0.5, 0,
+                               cap=grid.size())
+    assert len(res.detections) == len(want) > 4
+    assert [d.grid_index for d in res.detections] == [w[0] for w in want]
+
+
+def test_center_frequency_mismatch_rejected(b2, ref):
+    sc = load_scene(ref, "DESK_SAWTOOTH")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    snaps = [b2.Snapshot(0.0, sc.states[0], [b2.BasebandCapture(sc.captures[0, 0], sc.fs, 0.0,
+                                                                sc.fc),
+                                             b2.BasebandCapture(sc.captures[0, 1], sc.fs, 0.0,
+                                                                sc.fc + 1.0)])]
+    with pytest.raises(ValueError, match="center frequencies differ"):
+        b2.geolocate_snapshots(snaps, grid)
+
+
+def test_tuning_api(b2, tune):
+    eng = b2.default_engine(0)
+    with pytest.raises(ValueError, match="unsupported moment block"):
+        tune(moment_block=100)
+    with pytest.raises(ValueError, match="unsupported moment count"):
+        tune(moment_count=9)
+    with pytest.raises(ValueError, match="weakens the 1e-4 contract"):
+        tune(refine_tau=0.001)
+    tune(refine_tau=0.001, allow_weaker_refine=1)
+    assert eng.tuning()["refine_tau"] == pytest.approx(0.001)
+    eng.reset_tuning()
+    assert eng.tuning()["refine_tau"] == 0.0
