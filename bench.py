@@ -23,8 +23,22 @@ accumulation, exact argmax and detect_emitters, all on the GPU.
               compiled from the unmodified reference headers) on this host's
               cores, on a bounded sample of the same workload.
 
-Multi-GPU (torchrun): the grid is split into contiguous latitude slabs, one per
-rank; the only exchange is the final argmax all-gather over NCCL.
+* plugin_path — the reference's own plugin benchmark (compare_backends on
+              BenchWorkload, bench.hpp:65-88, 280-330): stage + correlate_batch
+              of 500,000 random offsets over 4,096-sample captures through the
+              CorrelationSession boundary (the direct k_correlate kernel), at
+              several batch sizes, overlapping samples/s, beside the reference's
+              ParallelBatchedBackend on this host's cores.
+
+Multi-GPU (--gpus N): one process per GPU. Without torchrun's WORLD_SIZE the
+bench re-executes itself under torch.distributed.run with N ranks (or, with
+--in-process, drives all N GPUs from one process through the multi-GPU engine,
+dg_engine_create_multi). The run is sharded into work units (whole
+(snapshot, pair) steps plus bucket-range parts of the remainder steps,
+dg_shard_plan); one all-to-all moves every unit's columns to the owner of each
+latitude slab, which accumulates its slab in the reference's order; the peak is
+a fast-maximum all-reduce plus an exact re-rank per slab and an all-gather of
+(value, index); rank 0 detects on the gathered surface.
 """
 from __future__ import annotations
 
@@ -84,6 +98,72 @@ def make_inputs(name: str, spacing_km: float = 1.0, n_snapshots: int | None = No
     import paper_2508_06672_b200.simulate as sim
     states, caps, _, _ = sim.simulate_arrays(scenes.to_scenario(sim, scene), engine=engine)
     return states, caps, bounds, scene["grid_spacing_deg"]
+
+
+# ---------------------------------------------------------------------------
+# The reference's plugin-path workload (BenchWorkload, bench.hpp:41-88): seeded
+# uniform captures and candidate offsets, regenerated here bit for bit
+# (std::mt19937_64; tests/test_bench.py checks the arrays and the reference's
+# workload_checksum against oracle/_ref).
+_MT_N, _MT_M = 312, 156
+_MT_A = np.uint64(0xB5026F5AA96619E9)
+_MT_UM, _MT_LM = np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
+
+
+def mt19937_64(seed: int, n: int) -> np.ndarray:
+    """The first n outputs of std::mt19937_64(seed) (twist vectorised in the
+    three dependency-free ranges of the recurrence)."""
+    mt = np.zeros(_MT_N, np.uint64)
+    mt[0] = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for i in range(1, _MT_N):
+            prev = int(mt[i - 1])
+            mt[i] = np.uint64((6364136223846793005 * (prev ^ (prev >> 62)) + i)
+                              & 0xFFFFFFFFFFFFFFFF)
+    one, sh1 = np.uint64(1), np.uint64(1)
+
+    def mix(hi, lo, far):
+        x = (hi & _MT_UM) | (lo & _MT_LM)
+        return far ^ (x >> sh1) ^ ((x & one) * _MT_A)
+
+    out = np.empty(((n + _MT_N - 1) // _MT_N) * _MT_N, np.uint64)
+    with np.errstate(over="ignore"):
+        for blk in range(len(out) // _MT_N):
+            k = _MT_N - _MT_M
+            mt[:k] = mix(mt[:k], mt[1:k + 1], mt[_MT_M:])
+            mt[k:_MT_N - 1] = mix(mt[k:_MT_N - 1], mt[k + 1:], mt[:_MT_N - 1 - k])
+            mt[_MT_N - 1] = mix(mt[_MT_N - 1:], mt[:1], mt[_MT_M - 1:_MT_M])[0]
+            y = mt.copy()
+            y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+            y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+            y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+            y ^= y >> np.uint64(43)
+            out[blk * _MT_N:(blk + 1) * _MT_N] = y
+    return out[:n]
+
+
+def build_workload(n_points: int = 500_000, n_samples: int = 4096, fs: float = 5e6,
+                   seed: int = 1):
+    """bench.hpp:65-88 -> (y1, y2, offsets [tdoa int64, fdoa f64])."""
+    r = mt19937_64(seed, 4 * n_samples + 2 * n_points)
+    u = (r >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+    def uniform(x, lo, hi):
+        return lo + (hi - lo) * x
+
+    caps = []
+    for c in range(2):  # emplace_back(re, im): g++ evaluates the im draw first
+        w = u[2 * c * n_samples:2 * (c + 1) * n_samples].reshape(n_samples, 2)
+        caps.append(uniform(w[:, 1], -1.0, 1.0) + 1j * uniform(w[:, 0], -1.0, 1.0))
+    w = u[4 * n_samples:].reshape(n_points, 2)
+    ms = float(n_samples // 2)
+    t = uniform(w[:, 0], -ms, ms)
+    tr = np.trunc(t)
+    tdoa = tr + np.where(np.abs(t - tr) >= 0.5, np.sign(t), 0.0)  # std::llround
+    off = np.zeros(n_points, np.dtype([("tdoa_samples", "<i8"), ("fdoa_hz", "<f8")]))
+    off["tdoa_samples"] = tdoa.astype(np.int64)
+    off["fdoa_hz"] = uniform(w[:, 1], -fs / 4.0, fs / 4.0)
+    return caps[0], caps[1], off
 
 
 class ClockSampler:
@@ -259,15 +339,25 @@ def b200_arm(args, rank, world):
             dist.init_process_group("gloo")
     coll_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     cfg = WORKLOADS[args.config]
-    eng = b2.default_engine(dev)
-    states, caps, bounds, spacing = make_inputs(args.config, args.spacing_km, engine=eng)
+    # --in-process: one engine over every GPU of this process (dg_engine_create_multi)
+    devices = [dev]
+    if world == 1 and args.gpus > 1:
+        devices = ([int(d) for d in args.device_list.split(",")] if args.device_list else
+                   list(range(args.gpus)))
+        if len(devices) != args.gpus or max(devices) >= torch.cuda.device_count():
+            raise SystemExit(f"bench: --gpus {args.gpus} needs {args.gpus} visible GPUs")
+    n_gpus = world if world > 1 else len(devices)
+    eng = b2.default_engine(dev) if len(devices) == 1 else b2.Engine(devices=devices)
+    states, caps, bounds, spacing = make_inputs(args.config, args.spacing_km,
+                                                engine=b2.default_engine(dev))
     S, R, N = caps.shape
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing, 0.0, engine=eng)
     P = grid.size()
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], FC, engine=eng)
     opts = b2.GeolocateOptions(k_sigma=5.0, exclusion_radius_cells=5, detect=True)
     # the solve's launching stream: the engine runs on it (side streams joined
-    # back into it) and the events and the L2 flush are recorded on it
+    # back into it) and the events and the L2 flush are recorded on it; the
+    # multi-GPU engine's call returns when every device is done
     stream = torch.cuda.Stream()
     acc_dev = torch.empty(P, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -279,10 +369,10 @@ def b200_arm(args, rank, world):
                                       accumulated_device=acc_dev.data_ptr(),
                                       stream=stream.cuda_stream, profile=profile)
             return res.stats, (res.argmax_value, res.argmax_index)
-        # snapshot-sharded (paper_2508_06672_b200.sharding): each rank correlates
-        # S/world snapshots over the whole grid, one all-to-all to latitude
-        # slabs, per-slab accumulation + exact peak, peak all-gather, surface
-        # gather for detect_emitters
+        # work-unit sharded (paper_2508_06672_b200.sharding): each rank correlates
+        # its units over the whole grid, one all-to-all to latitude slabs,
+        # per-slab accumulation + two-stage exact peak, surface gather,
+        # detection on rank 0
         value, index, _, _, st = sharding.geolocate_sharded(
             grid, stg, opts, gather=True, stream=stream.cuda_stream, profile=profile)
         return st, (value, index)
@@ -292,7 +382,6 @@ def b200_arm(args, rank, world):
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    stats = []
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -306,9 +395,19 @@ def b200_arm(args, rank, world):
         torch.cuda.synchronize()
     # one more solve with per-kernel events (steps serialised on one stream so
     # each kernel's time is its own) for the rooflines; not part of `value`
+    # (the multi-GPU engine is profiled through one device's engine)
     with torch.cuda.stream(stream):
         flush.zero_()
-    stats.append(solve(staged, profile=True)[0])
+    if len(devices) > 1:
+        g1 = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing, 0.0,
+                                     engine=b2.default_engine(dev))
+        s1 = b2.StagedSnapshots(states, caps, cfg["fs"], FC, engine=b2.default_engine(dev))
+        last = b2.geolocate_staged(g1, s1, opts, want_surface=False,
+                                   accumulated_device=acc_dev.data_ptr(),
+                                   stream=stream.cuda_stream, profile=True).stats
+        del g1, s1
+    else:
+        last = solve(staged, profile=True)[0]
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -322,7 +421,6 @@ def b200_arm(args, rank, world):
 
     # rooflines of the two correlator kernels, this rank's launches (FP32x2 MACs
     # counted on the device by k_work_count: 4 FLOP each)
-    last = stats[-1]
     print("[bench] per-solve stats: " + json.dumps({k: last.get(k) for k in (
         "correlate_ms", "moments_ms", "evaluate_ms", "moment_ffma2", "evaluate_ffma2",
         "direct_steps", "n_refined", "total_ms", "kernel_launches")}), file=sys.stderr)
@@ -340,7 +438,7 @@ def b200_arm(args, rank, world):
     ovl = last["sum_overlap_samples"]
     dominant = ev_name if ev_ms >= mom_ms else "k_moments"
     achieved = ev_tf if dominant == ev_name else mom_tf
-    launches = last["kernel_launches"]
+    launches = st.get("kernel_launches", last["kernel_launches"])
 
     # e2e: host (pinned) captures in, accumulated surface out, through the public API
     pinned = torch.empty(caps.shape, dtype=torch.complex128, pin_memory=True).numpy()
@@ -373,6 +471,10 @@ def b200_arm(args, rank, world):
            "d2h_bytes_per_step": int(P * 8 + 4096 * 48),
            "ms_per_step": e2e_s * 1e3}
 
+    plugin = None
+    if rank == 0 and not args.no_plugin:
+        plugin = plugin_leg(args, b2, peak, world == 1)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -389,18 +491,19 @@ def b200_arm(args, rank, world):
                    "sample": f"failed: {e}"[:300]}
 
     if rank == 0:
+        par = ("1 GPU" if n_gpus == 1 else
+               f"{n_gpus} GPUs, work-unit sharded ({'one process' if dist is None else 'one rank'}"
+               " per GPU; all-to-all to latitude slabs)")
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: the reference's simulate_scenario scene for the workload "
                     "(SURVEY §8d; paper_scenario.cfg receivers/emitters), synthesised on the GPU "
                     "by paper_2508_06672_b200.simulate",
             "config": {"workload": args.config, "grid": f"{grid.lat.count}x{grid.lon.count}",
                        "points": P, "snapshots": S, "samples": N,
-                       "spacing_km": args.spacing_km,
-                       "parallelism": (f"snapshot-sharded x{world} (all-to-all to lat slabs)"
-                                       if world > 1 else "1 GPU"),
+                       "spacing_km": args.spacing_km, "parallelism": par,
                        "l2": "flushed between timed steps (256 MB write)",
                        "precision": "FP32 correlator, FP64 geometry/accumulation/refine"},
             "e2e": e2e,
@@ -409,7 +512,7 @@ def b200_arm(args, rank, world):
                 "unit": "TFLOP/s", "frac": achieved / peak if achieved and peak else None,
                 "traffic": ncu_traffic(dominant),
                 "traffic_source": f"dram__bytes_read.sum + dram__bytes_write.sum per {dominant} "
-                                  "launch, profiles/r01_ncu_kernels.txt",
+                                  f"launch, {NCU_SUMMARY}",
                 "peak_source": "dg_fp32_peak_tflops FFMA probe in this process",
                 "flop_definition": "FMA-pipe work: 4 x the FP32x2 operations the kernel's "
                                    "algorithm performs, counted on the device by k_work_count "
@@ -431,10 +534,11 @@ def b200_arm(args, rank, world):
                                           "2*128*np*16 per 128-candidate tile"}},
                 "reference_equivalent": {
                     "flop_per_sample": FLOP_PER_SAMPLE, "sum_overlap_samples": ovl,
-                    "tflops": FLOP_PER_SAMPLE * ovl / (corr_ms * 1e-3) / 1e12,
+                    "tflops": FLOP_PER_SAMPLE * ovl / (corr_ms * 1e-3) / 1e12 if corr_ms else None,
                     "note": "the reference kernel's 20 FLOP per overlapping sample over the "
                             "correlator time: work the block-moment factorisation avoids"},
                 "correlate_ms_per_step": corr_ms},
+            "plugin_path": plugin,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": launches * args.steps,
@@ -447,6 +551,82 @@ def b200_arm(args, rank, world):
         dist.destroy_process_group()
 
 
+PLUGIN_POINTS = 500_000    # BenchWorkload defaults (bench.hpp:41-45)
+PLUGIN_SAMPLES = 4096
+PLUGIN_BATCHES = (8, 4096, PLUGIN_POINTS)
+
+
+def plugin_leg(args, b2, fp32_peak, with_cpu):
+    """The reference's plugin benchmark on this engine: BenchWorkload (500k random
+    offsets, |tdoa| <= 2048, |fdoa| <= fs/4, uniform I/Q) through
+    stage + correlate_batch (bench.hpp:113-118 time_run), at the paper's batch
+    of 8, the bench's 4096 and one batch of everything; the direct correlator
+    (the FDOA range admits no block moments). Overlapping samples/s counts
+    sum_i (N - |tdoa_i|), the reference kernel's work (20 FLOP each)."""
+    y1, y2, off = build_workload(PLUGIN_POINTS, PLUGIN_SAMPLES, 5e6, 1)
+    ovl = float(np.maximum(0, PLUGIN_SAMPLES - np.abs(off["tdoa_samples"])).sum())
+    be = b2.make_backend("b200", 1)
+    c1, c2 = b2.BasebandCapture(y1, 5e6), b2.BasebandCapture(y2, 5e6)
+    out = np.zeros(PLUGIN_POINTS)
+    rows = {}
+    for bs in PLUGIN_BATCHES:
+        reps = 1 if bs < 64 else 5
+        times = []
+        for r in range(reps + 1):
+            t0 = time.perf_counter()
+            s = be.stage(c1, c2)
+            for a in range(0, PLUGIN_POINTS, bs):
+                s.correlate_batch(off[a:a + bs], out[a:a + bs])
+            dt = time.perf_counter() - t0
+            if r:
+                times.append(dt)
+        sec = statistics.mean(times)
+        rows[str(bs)] = {"s_per_run": sec, "overlap_samples_per_s": ovl / sec,
+                         "points_per_s": PLUGIN_POINTS / sec}
+    best = rows[str(PLUGIN_POINTS)]
+    # k_correlate FMA-pipe work: 2 FFMA2 per candidate-sample (A, B) = 8 FLOP
+    fma_tf = 8.0 * ovl / best["s_per_run"] / 1e12
+    res = {"workload": f"BenchWorkload {PLUGIN_POINTS} points x {PLUGIN_SAMPLES} samples, seed 1 "
+                       "(bench.hpp:65-88, regenerated bit for bit)",
+           "overlap_samples": ovl, "batches": rows,
+           "k_correlate": {"bound": "fp32 fma pipe", "achieved": fma_tf, "peak": fp32_peak,
+                           "unit": "TFLOP/s", "frac": fma_tf / fp32_peak if fp32_peak else None,
+                           "flop_definition": "8 per overlapping candidate-sample (2 FFMA2: the "
+                                              "A / B phasor-table MACs), whole call incl. "
+                                              "staging and copies"},
+           "reference_equivalent_tflops": 20.0 * ovl / best["s_per_run"] / 1e12}
+    if with_cpu and not args.no_cpu_baseline:
+        try:
+            cmd = [sys.executable, os.path.abspath(__file__), "--ref-plugin-worker"]
+            o = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+            d = json.loads(o.stdout.strip().splitlines()[-1])
+            res["cpu_baseline"] = {"overlap_samples_per_s": d["ovl"] / d["s"], "unit":
+                                   "overlapping samples/s", "cores": d["workers"],
+                                   "kind": "reference",
+                                   "sample": f"first {d['points']} offsets of the workload, "
+                                             "reference ParallelBatchedBackend "
+                                             f"({d['workers']}) correlate_batch, batch 4096, "
+                                             f"{d['s']:.1f} s; {cpu_model()}"}
+        except Exception as e:
+            res["cpu_baseline"] = {"overlap_samples_per_s": None, "sample": f"failed: {e}"[:300]}
+    return res
+
+
+def ref_plugin_worker(args):
+    from oracle.bindings import RefLib
+    ref = RefLib()
+    n = 60_000
+    y1, y2, off = build_workload(PLUGIN_POINTS, PLUGIN_SAMPLES, 5e6, 1)
+    off = off[:n]
+    workers = os.cpu_count() or 1
+    ref.correlate_batch(y1, y2, 5e6, off[:4096], "parallel", workers, 4096)  # warm-up
+    t0 = time.perf_counter()
+    ref.correlate_batch(y1, y2, 5e6, off, "parallel", workers, 4096)
+    s = time.perf_counter() - t0
+    ovl = float(np.maximum(0, PLUGIN_SAMPLES - np.abs(off["tdoa_samples"])).sum())
+    print(json.dumps({"s": s, "ovl": ovl, "points": n, "workers": workers}))
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -455,9 +635,12 @@ def measured_peaks():
         return {}
 
 
+NCU_SUMMARY = "profiles/r01_ncu_kernels.txt"
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_kernels.txt")
+    path = os.path.join(ROOT, NCU_SUMMARY)
     try:
         vals, cur = {}, None
         for line in open(path):
@@ -495,19 +678,43 @@ def main():
                     help="snapshots per reference-arm step")
     ap.add_argument("--cpu-sample-snapshots", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--in-process", action="store_true",
+                    help="--gpus N > 1 without torchrun: one process drives every GPU through "
+                         "the multi-GPU engine instead of spawning N ranks")
+    ap.add_argument("--no-plugin", action="store_true", help="skip the plugin-path leg")
+    ap.add_argument("--device-list", default="", help=argparse.SUPPRESS)  # tests: 0,0
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help=argparse.SUPPRESS)
     ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-plugin-worker", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.ref_worker:
         return ref_worker(args)
+    if args.ref_plugin_worker:
+        return ref_plugin_worker(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and not args.in_process:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
-    if world != args.gpus and rank == 0:
-        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
     return b200_arm(args, rank, world)
+
+
+def spawn_ranks(args):
+    """--gpus N without torchrun: re-run this command as N ranks (one per GPU)
+    under torch.distributed.run on this node; rank 0 prints the line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node",
+           str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.run(cmd, cwd=ROOT).returncode)
 
 
 if __name__ == "__main__":

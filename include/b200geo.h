@@ -75,10 +75,19 @@ const char* dg_last_error(void);
 int dg_abi_version(void);
 
 /* ---- engine == digeo::CorrelationBackend (backend.hpp:211-217) ----------
- * Bound to one CUDA device. Descriptor is {"b200", "parallel-batched",
- * workers = 1 GPU} — never "gpu", which the reference's tests require to be
- * rejected by its own registry (test_backend.cpp:181). */
+ * Bound to one CUDA device (or several: dg_engine_create_multi). Descriptor is
+ * {"b200", "parallel-batched", workers = number of GPUs} — never "gpu", which
+ * the reference's tests require to be rejected by its own registry
+ * (test_backend.cpp:181). */
+int dg_device_count(int* n); /* visible CUDA devices */
 int dg_engine_create(int device, dg_engine** out);
+/* One engine over several GPUs of this process (devices[0] drives the calls
+ * that use one device: sessions, grids, detection): dg_geolocate_snapshots /
+ * dg_geolocate_staged on it shard the run across all of them (DESIGN.md
+ * section 7), with peer copies over NVLink for the exchange. The descriptor's
+ * workers = n_devices, as ParallelBatchedBackend(workers) (backend.hpp:292-317).
+ * A device may repeat (tests run the sharded path on one GPU). */
+int dg_engine_create_multi(const int* devices, int n_devices, dg_engine** out);
 void dg_engine_destroy(dg_engine* engine);
 int dg_engine_descriptor(const dg_engine* engine, char* name, size_t name_len, char* kind,
                          size_t kind_len, unsigned* workers);
@@ -357,6 +366,29 @@ int dg_correlate_steps(dg_engine* engine, const dg_grid* grid, const dg_staged* 
 int dg_accumulate_peak(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
                        const double* grids_device, const double* medians_device,
                        const dg_options* opt, dg_result* result);
+
+/* Work units of a sharded run. A unit is one
+ * (snapshot, pair) step s * pairs + q over the whole grid, or part `part` of
+ * `parts` of it: the candidates of a contiguous, cost-balanced range of the
+ * step's TDOA buckets, the other candidates 0, so the parts of a step sum to
+ * the whole step exactly. dg_shard_plan gives rank r the whole steps
+ * [r q, (r + 1) q), q = floor(steps / world), and part r of each of the last
+ * steps mod world steps, so every rank holds q + (steps mod world) / world
+ * steps of work (whole_snapshots: snapshot units [r S / world, (r + 1) S /
+ * world) for median normalisation, which needs a whole snapshot surface). */
+typedef struct {
+    int64_t step;  /* s * pairs + q (whole_snapshots: the snapshot s) */
+    int32_t part, parts;
+    int32_t rank;  /* owner */
+    int32_t reserved;
+} dg_work_unit;
+int dg_shard_plan(int64_t n_snapshots, int64_t n_receivers, int world, int whole_snapshots,
+                  dg_work_unit* out, int64_t capacity, int64_t* n_out);
+/* raw per-unit surfaces [n_units][P] (device, caller-owned) of the grid's
+ * cells: correlation + exact refinement, no pair sums or normalisation. */
+int dg_correlate_units(dg_engine* engine, const dg_grid* grid, const dg_staged* staged,
+                       const dg_work_unit* units, int64_t n_units, const dg_options* opt,
+                       double* raw_device, dg_result* result);
 
 /* detect_emitters (correlate.hpp:127-201) on a caller-provided surface over a
  * grid lattice (host or device pointer; is_device selects). */

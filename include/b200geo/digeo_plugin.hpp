@@ -17,6 +17,7 @@
 // codes are rethrown as the reference's exception types.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <new>
@@ -48,6 +49,9 @@ static_assert(sizeof(digeo::cplx) == 2 * sizeof(double), "complex<double> layout
 class Engine {
 public:
     explicit Engine(int device = 0) { check(dg_engine_create(device, &h_)); }
+    explicit Engine(const std::vector<int>& devices) {
+        check(dg_engine_create_multi(devices.data(), static_cast<int>(devices.size()), &h_));
+    }
     ~Engine() { dg_engine_destroy(h_); }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -78,6 +82,22 @@ class B200Backend final : public digeo::CorrelationBackend {
 public:
     explicit B200Backend(int device = 0)
         : engine_(std::make_shared<Engine>(device)), descriptor_{"b200", "parallel-batched", 1} {}
+    /// One engine over several GPUs: geolocate_snapshots shards each run across
+    /// them (dg_engine_create_multi); sessions run on devices.front().
+    explicit B200Backend(const std::vector<int>& devices)
+        : engine_(std::make_shared<Engine>(devices)),
+          descriptor_{"b200", "parallel-batched", static_cast<unsigned>(devices.size())} {}
+
+    /// The GPUs for a worker count as GeolocateOptions::workers reads it
+    /// (geolocate.hpp:98): 0 = every visible GPU, else min(workers, visible).
+    static std::vector<int> devices_for(unsigned workers) {
+        int n = 0;
+        check(dg_device_count(&n));
+        const int m = workers ? std::min<int>(static_cast<int>(workers), n) : n;
+        std::vector<int> d(static_cast<std::size_t>(std::max(m, 1)));
+        for (std::size_t i = 0; i < d.size(); ++i) d[i] = static_cast<int>(i);
+        return d;
+    }
 
     const digeo::BackendDescriptor& descriptor() const override { return descriptor_; }
 
@@ -98,6 +118,14 @@ private:
     digeo::BackendDescriptor descriptor_;
 };
 
+/// The reference's registry (backend.hpp:311-317) for this engine: "b200"
+/// with `workers` GPUs (0 = all visible).
+inline std::unique_ptr<digeo::CorrelationBackend> make_backend(const std::string& name,
+                                                               unsigned workers = 0) {
+    if (name == "b200") return std::make_unique<B200Backend>(B200Backend::devices_for(workers));
+    throw std::invalid_argument("make_backend: unknown backend '" + name + "' (expected b200)");
+}
+
 /// geolocate.hpp:127-146 with the same inputs and result. `options.backend_name`
 /// is ignored (the engine is the backend); everything after the captures is on
 /// the GPU. The grid's eager ECEF points are uploaded as-is.
@@ -108,7 +136,9 @@ inline digeo::GeolocateResult geolocate_snapshots(const std::vector<digeo::Snaps
     if (snapshots.empty()) throw std::invalid_argument("geolocate_snapshots: no snapshots");
     if (!grid || grid->size() == 0) throw std::invalid_argument("correlate_snapshot: empty grid");
     std::unique_ptr<B200Backend> own;
-    if (!backend) backend = (own = std::make_unique<B200Backend>()).get();
+    if (!backend)
+        backend =
+            (own = std::make_unique<B200Backend>(B200Backend::devices_for(options.workers))).get();
     dg_engine* eng = backend->engine()->get();
 
     const std::size_t R = snapshots.front().captures.size();

@@ -286,6 +286,18 @@ class RefLib:
             _d(vals) if vals is not None else None, C.byref(sec)))
         return sec.value, vals
 
+    def build_workload(self, n_points, n_samples=4096, fs=5e6, seed=1):
+        """bench.hpp:65-88 -> (y1, y2, offsets, workload_checksum)."""
+        y1 = np.zeros(n_samples, np.complex128)
+        y2 = np.zeros(n_samples, np.complex128)
+        off = np.zeros(n_points, PAIR_OFFSETS_DTYPE)
+        h = C.c_uint64()
+        self._check(self.lib.ref_build_workload(
+            C.c_uint64(n_points), C.c_uint64(n_samples), C.c_double(fs), C.c_uint64(seed),
+            y1.ctypes.data_as(_dp), y2.ctypes.data_as(_dp), off.ctypes.data_as(C.c_void_p),
+            C.byref(h)))
+        return y1, y2, off, h.value
+
     def detect_emitters(self, bounds, spacing, alt, values, k_sigma=5.0, radius=5, cap=4096):
         v = np.ascontiguousarray(values, np.float64)
         b = np.asarray(bounds, np.float64)

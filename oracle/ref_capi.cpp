@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "digeo/backend.hpp"
+#include "digeo/bench.hpp"
 #include "digeo/config.hpp"
 #include "digeo/correlate.hpp"
 #include "digeo/geodesy.hpp"
@@ -291,6 +292,24 @@ int ref_detect_emitters(const double* bounds4, double spacing, double alt, const
             det_score[i] = det[i].score;
             det_z[i] = det[i].score_zsigma;
         }
+    })
+}
+
+// --- BenchWorkload (bench.hpp:41-88): the reference's plugin-path workload ---
+// y1, y2: n_samples complex doubles each; offsets: n_points {int64, double}
+int ref_build_workload(uint64_t n_points, uint64_t n_samples, double fs, uint64_t seed,
+                       double* y1, double* y2, void* offsets, uint64_t* checksum) {
+    REF_GUARD({
+        BenchWorkload w;
+        w.n_points = n_points;
+        w.capture_samples = n_samples;
+        w.sample_rate_hz = fs;
+        w.seed = seed;
+        const auto d = detail::build_workload(w);
+        std::memcpy(y1, d.y1.samples.data(), n_samples * sizeof(cplx));
+        std::memcpy(y2, d.y2.samples.data(), n_samples * sizeof(cplx));
+        std::memcpy(offsets, d.offsets.data(), n_points * sizeof(PairOffsets));
+        *checksum = detail::workload_checksum(d);
     })
 }
 

@@ -12,7 +12,8 @@ from .geodesy import (CandidateGrid, GeodeticCoord, GridAxis, LatLonBounds,  # n
                       build_candidate_grid, grid_from_axes, grid_from_points)
 from .geolocate import (CorrelationGrid, EmitterEstimate, GeolocateOptions,  # noqa: F401
                         GeolocateResult, Snapshot, StagedSnapshots, accumulate_peak,
-                        correlate_snapshot, correlate_steps, detect_emitters, geolocate_arrays,
+                        correlate_snapshot, correlate_steps, correlate_units, detect_emitters,
+                        geolocate_arrays,
                         geolocate_snapshots, geolocate_staged, predict_offsets, read_iq,
                         read_iq_header, wavelength_m)
 

@@ -85,6 +85,11 @@ class dg_options(C.Structure):
                 ("peak_stage", C.c_int), ("peak_max", C.c_double)]
 
 
+class dg_work_unit(C.Structure):
+    _fields_ = [("step", C.c_int64), ("part", C.c_int32), ("parts", C.c_int32),
+                ("rank", C.c_int32), ("reserved", C.c_int32)]
+
+
 class dg_tuning(C.Structure):
     _fields_ = [("correlator", C.c_int), ("moment_block", C.c_int), ("moment_count", C.c_int),
                 ("evaluate_tensor", C.c_int), ("refine_tau", C.c_double),
@@ -121,6 +126,7 @@ class dg_result(C.Structure):
 # every symbol include/b200geo.h declares (tests check the .so exports them)
 EXPORTS = (
     "dg_last_error", "dg_abi_version", "dg_engine_create", "dg_engine_destroy",
+    "dg_device_count", "dg_engine_create_multi",
     "dg_engine_descriptor", "dg_stage", "dg_stage_f32", "dg_session_destroy",
     "dg_correlate_batch", "dg_build_candidate_grid", "dg_grid_slab", "dg_grid_from_points",
     "dg_grid_info", "dg_grid_points", "dg_grid_destroy", "dg_predict_offsets",
@@ -130,7 +136,8 @@ EXPORTS = (
     "dg_stage_snapshots_iq", "dg_write_grid", "dg_render_heatmap", "dg_write_detections_csv",
     "dg_read_grid", "dg_grid_from_axes", "dg_format_g17", "dg_scenario_samples",
     "dg_simulate_scenario",
-    "dg_tuning_default", "dg_engine_set_tuning", "dg_engine_get_tuning",
+    "dg_tuning_default", "dg_engine_set_tuning", "dg_engine_get_tuning", "dg_shard_plan",
+    "dg_correlate_units",
     "dg_plan_batches", "dg_fp32_peak_tflops", "dg_fp32x2_peak_tflops", "dg_fp64_peak_tflops",
 )
 
@@ -149,6 +156,8 @@ def _load():
     L.dg_abi_version.restype = C.c_int
     sigs = {
         "dg_engine_create": [C.c_int, C.POINTER(_vp)],
+        "dg_engine_create_multi": [C.POINTER(C.c_int), C.c_int, C.POINTER(_vp)],
+        "dg_device_count": [C.POINTER(C.c_int)],
         "dg_engine_descriptor": [_vp, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t,
                                  C.POINTER(C.c_uint)],
         "dg_stage": [_vp, _dp, C.c_int64, C.c_double, _dp, C.c_int64, C.c_double, C.POINTER(_vp)],
@@ -190,6 +199,10 @@ def _load():
         "dg_scenario_samples": [C.POINTER(dg_scenario), _i64p],
         "dg_simulate_scenario": [_vp, C.POINTER(dg_scenario), C.POINTER(_vp), _dp,
                                  C.POINTER(dg_state), _dp],
+        "dg_shard_plan": [C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(dg_work_unit),
+                          C.c_int64, _i64p],
+        "dg_correlate_units": [_vp, _vp, _vp, C.POINTER(dg_work_unit), C.c_int64,
+                               C.POINTER(dg_options), _vp, C.POINTER(dg_result)],
         "dg_engine_set_tuning": [_vp, C.POINTER(dg_tuning)],
         "dg_engine_get_tuning": [_vp, C.POINTER(dg_tuning)],
         "dg_fp32_peak_tflops": [C.c_int, _dp],

@@ -136,7 +136,14 @@ class B200Backend:
     """backend.hpp:211-217 — the engine registered as "b200" (never "gpu")."""
 
     def __init__(self, workers: int = 0, engine: Engine | None = None):
-        self.engine = engine or default_engine()
+        """workers = GPUs (the reference's worker count, backend.hpp:292-309):
+        0 every visible GPU, else min(workers, visible); one engine drives them."""
+        if engine is None:
+            from .engine import device_count
+            n = device_count()
+            m = min(workers, n) if workers else n
+            engine = default_engine() if m <= 1 else Engine(devices=list(range(m)))
+        self.engine = engine
         name, kind, w = self.engine.descriptor()
         self._descriptor = BackendDescriptor(name, kind, w)
 

@@ -1,6 +1,6 @@
 """Build recipe for libb200geo.so (in-tree, sm_100a only).
 
-    python -m paper_2508_06672_b200.build
+    python paper_2508_06672_b200/build.py   (a file path: importing the package needs the .so)
 
 Kernels: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo.
 C ABI layer: g++ -std=c++20 -ffp-contract=off (host math must not contract,

@@ -15,6 +15,7 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -73,6 +74,14 @@ namespace {
 // FFMA2 correlator (dg_correlate.cu) when no (B, R) meets the truncation bound
 // (very wide FDOA ranges) or when the direct form is cheaper (few candidates
 // per TDOA bucket). See DESIGN.md section 4.
+// One work unit of a run: the (snapshot, pair) step sp over the whole grid, or
+// part `part` of `parts` of it (the candidates of a contiguous range of its
+// TDOA buckets, cost-balanced on the step's histogram; the other candidates
+// are left 0 so the parts of a step sum to the whole step exactly).
+struct StepUnit {
+    int sp = 0, part = 0, parts = 1;
+};
+
 struct StepPlan {
     bool empty = true;    // no candidate overlaps: every S is 0 (already written)
     bool direct = false;
@@ -91,6 +100,13 @@ double jacobi_anger_tail(double x, int R) {
 }
 
 constexpr double kMomentTail = 1e-8;
+// Largest Jacobi-Anger argument x = pi h B the planner admits. Past it the
+// coefficients a_m(x) grow and the block sums cancel more, so the FP32
+// evaluation error of sidelobe candidates in coherent buckets rises faster
+// than the refinement test tracks (measured on +40 dB tone / chirp scenes:
+// B = 768 at x = 3.5 reached 1.4e-4, B = 640 at x = 2.9 stayed at 3e-5;
+// tests/test_gpu_error_model.py). Below it R <= 14 always meets kMomentTail.
+constexpr double kMomentXMax = 3.0;
 constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of moments
 constexpr int kMomentR[] = {8, 10, 12, 14, 16};
 constexpr int kMomentB[] = {768, 640, 512, 256, 128, 64};
@@ -130,6 +146,7 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
     for (int B : kMomentB) {
         if (forceB && B != forceB) continue;
         const double x = M_PI * half * B;
+        if (x > kMomentXMax) continue;
         for (int R : kMomentR) {
             if (forceR && R != forceR) continue;
             // a forced R is used only where it meets the truncation bound too
@@ -355,8 +372,13 @@ struct Pipeline {
     // exact_ranges: `range` holds the exact FDOA and TDOA ranges of each step;
     // otherwise (the windowed geometry pass) only its TDOA range, reduced from
     // the step's histogram (k_hist_range), and the FDOA range is the planning one
+    // units (nullable): a unit with parts > 1 keeps only its share of the
+    // step's bins, split where the cumulative planner cost of the histogram's
+    // buckets crosses part / parts of the total (the same split on every rank:
+    // the histograms are bit-exact)
     void plan_window(Scratch& sc, int n, double fs, const StepRange* approx = nullptr,
-                     double margin_hz = 0.0, int64_t P_plan = 0, bool exact_ranges = true) {
+                     double margin_hz = 0.0, int64_t P_plan = 0, bool exact_ranges = true,
+                     const std::vector<StepUnit>* units = nullptr) {
         std::vector<StepRange> h(n), ha(approx ? n : 0);
         if (!exact_ranges && !approx) raise(DG_ERUNTIME, "b200: plan without FDOA range");
         CK(cudaMemcpyAsync(h.data(), range, n * sizeof(StepRange), cudaMemcpyDeviceToHost, sc.st));
@@ -374,6 +396,8 @@ struct Pipeline {
             }
             plans[i] = plan_step(h[i], approx ? &ha[i] : nullptr, margin_hz, approx ? P_plan : P, N,
                                  fs, tn);
+            if (units && (*units)[i].parts > 1 && !plans[i].empty)
+                split_bins(sc, i, (*units)[i].part, (*units)[i].parts, plans[i]);
             nc[i] = plans[i].nu_c;
             const StepPlan& pl = plans[i];
             if (!pl.empty && !pl.direct)
@@ -388,6 +412,33 @@ struct Pipeline {
         CK(cudaStreamSynchronize(sc.st));
         CK(cudaEventRecord(window_ready, sc.st));
         for (int l = 1; l < n_lanes; ++l) CK(cudaStreamWaitEvent(lanes[l].st, window_ready, 0));
+    }
+
+    void split_bins(Scratch& sc, int slot, int part, int parts, StepPlan& pl) const {
+        std::vector<int> h(pl.nbins);
+        CK(cudaMemcpyAsync(h.data(), hist_slot(slot) + pl.bin0, pl.nbins * sizeof(int),
+                           cudaMemcpyDeviceToHost, sc.st));
+        CK(cudaStreamSynchronize(sc.st));
+        // planner cost of each non-empty bin (plan_step's model)
+        std::vector<double> cum(pl.nbins + 1, 0.0);
+        for (int b = 0; b < pl.nbins; ++b) {
+            double c = 0.0;
+            if (h[b] > 0)
+                c = pl.direct ? 2.3 * h[b] * (double)N
+                              : 1.5 * pl.R * (double)N + h[b] * ((double)N / pl.B) * (pl.R + 3);
+            cum[b + 1] = cum[b] + c;
+        }
+        const double total = cum[pl.nbins];
+        auto cut = [&](int k) {  // first bin whose cumulative cost reaches k / parts
+            if (k <= 0) return 0;
+            if (k >= parts) return pl.nbins;
+            const double t = total * k / parts;
+            return (int)(std::lower_bound(cum.begin() + 1, cum.end(), t) - cum.begin());
+        };
+        const int lo = cut(part), hi = std::max(lo, cut(part + 1));
+        pl.bin0 += lo;
+        pl.nbins = hi - lo;
+        if (pl.nbins <= 0) pl.empty = true;
     }
 
     void wait_event(cudaEvent_t e) {
@@ -695,6 +746,10 @@ int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
                                  " weakens the 1e-4 contract (set allow_weaker_refine)");
         std::lock_guard<std::mutex> lk(e->tables_mu);
         e->tuning = *t;
+        for (dg_engine* p : e->peers) {
+            std::lock_guard<std::mutex> lp(p->tables_mu);
+            p->tuning = *t;
+        }
     });
 }
 
@@ -735,6 +790,44 @@ int dg_engine_create(int device, dg_engine** out) {
     });
 }
 
+int dg_device_count(int* n) {
+    return guard([&] {
+        if (!n) raise(DG_EINVAL, "null argument");
+        CK(cudaGetDeviceCount(n));
+    });
+}
+
+int dg_engine_create_multi(const int* devices, int n, dg_engine** out) {
+    return guard([&] {
+        if (!devices || n < 1 || !out) raise(DG_EINVAL, "dg_engine_create_multi: no devices");
+        dg_engine* first = nullptr;
+        if (int rc = dg_engine_create(devices[0], &first)) raise(rc, last_error());
+        std::unique_ptr<dg_engine> e(first);
+        for (int k = 1; k < n; ++k) {
+            dg_engine* p = nullptr;
+            if (int rc = dg_engine_create(devices[k], &p)) raise(rc, last_error());
+            e->peers.push_back(p);
+            p->tuning = e->tuning;
+        }
+        // peer access between distinct devices (NVLink / NVSwitch P2P)
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) {
+                if (devices[a] == devices[b]) continue;
+                int can = 0;
+                CK(cudaDeviceCanAccessPeer(&can, devices[a], devices[b]));
+                if (!can) continue;
+                CK(cudaSetDevice(devices[a]));
+                const cudaError_t rc = cudaDeviceEnablePeerAccess(devices[b], 0);
+                if (rc == cudaErrorPeerAccessAlreadyEnabled)
+                    cudaGetLastError();
+                else
+                    CK(rc);
+            }
+        CK(cudaSetDevice(devices[0]));
+        *out = e.release();
+    });
+}
+
 void dg_engine_destroy(dg_engine* e) { delete e; }
 
 int dg_engine_descriptor(const dg_engine* e, char* name, size_t nl, char* kind, size_t kl,
@@ -743,7 +836,7 @@ int dg_engine_descriptor(const dg_engine* e, char* name, size_t nl, char* kind, 
         if (!e) raise(DG_EINVAL, "null engine");
         if (name && nl) std::snprintf(name, nl, "%s", "b200");
         if (kind && kl) std::snprintf(kind, kl, "%s", "parallel-batched");
-        if (workers) *workers = 1;
+        if (workers) *workers = (unsigned)e->n_devices();
     });
 }
 
@@ -919,6 +1012,7 @@ int dg_grid_slab(const dg_grid* g, int64_t r0, int64_t r1, dg_grid** out) {
         if (!g) raise(DG_EINVAL, "null grid");
         if (r0 < 0 || r1 > g->n_lat || r0 > r1) raise(DG_EINVAL, "dg_grid_slab: bad row range");
         auto s = std::make_unique<dg_grid>(*g);
+        s->replicas = std::make_shared<Replicas<dg_grid>>();
         s->n_lat = r1 - r0;
         s->row_offset = g->row_offset + r0;
         s->x = g->x + r0 * g->n_lon;
@@ -1314,6 +1408,8 @@ int dg_stage_snapshots(dg_engine* eng, const dg_snapshots* sn, dg_staged** out) 
 
 void dg_staged_destroy(dg_staged* s) { delete s; }
 
+}  // extern "C"
+
 // ---- the driver --------------------------------------------------------------
 namespace {
 
@@ -1487,6 +1583,23 @@ RefineCtx refine_ctx(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, d
     return ctx;
 }
 
+// the per-call counters of a dg_result (the correlate phases add to them)
+void reset_stats(dg_result* r) {
+    r->n_refined = 0;
+    r->n_reranked = 0;
+    r->sum_overlap_samples = 0.0;
+    r->correlate_ms = 0.0;
+    r->correlate_launches = 0;
+    r->total_ms = 0.0;
+    r->kernel_launches = 0;
+    r->moments_ms = 0.0;
+    r->evaluate_ms = 0.0;
+    r->moment_ffma2 = 0.0;
+    r->evaluate_ffma2 = 0.0;
+    r->direct_steps = 0;
+    r->evaluate_tc_flop = 0.0;
+}
+
 dg_options options_or_default(const dg_options* o) {
     dg_options opt;
     if (o) {
@@ -1497,20 +1610,20 @@ dg_options options_or_default(const dg_options* o) {
     return opt;
 }
 
-// Snapshots [s0, s1) over the whole grid g: geometry, correlation of every
-// pair, exact refinement, pair sums (correlate_snapshot_all_pairs) and the
-// optional median scaling -> grids [(s1-s0)][P] (device), medians [s1-s0].
-// This is the step-sharded half of geolocate_snapshots.
-void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
-                          const RunGeo& geo, int s0, int s1, const dg_options& opt, double* grids,
-                          double* medians, Scratch& sc, dg_result* res) {
+// Units over the whole grid g: geometry, correlation, exact refinement -> raw
+// surfaces [n_units][P] (device). The step-sharded half of geolocate_snapshots
+// and, with every step of a snapshot range, the
+// single-GPU path.
+void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                          const RunGeo& geo, const std::vector<StepUnit>& units,
+                          const dg_options& opt, double* raw, Scratch& sc, dg_result* res) {
     const int64_t P = g->size();
     const int pairs = geo.pairs, R = geo.R;
-    const int ns = s1 - s0, SPl = ns * pairs;
+    const int SPl = (int)units.size();
     const double fs = geo.fs, wl = geo.wl;
     cudaStream_t st = sc.st;
     int64_t launches = 0;
-    if (ns <= 0) return;
+    if (SPl <= 0) return;
 
     std::vector<cudaEvent_t> evs;
     if (opt.profile) {
@@ -1524,31 +1637,47 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         }
     } ev_free{&evs};
 
+    // the units' receiver pairs and global step indices (refinement maps a
+    // unit row back to its snapshot / pair)
+    std::vector<PairGeom> hpg(SPl);
+    std::vector<int> hstep(SPl);
+    for (int u = 0; u < SPl; ++u) {
+        if (units[u].sp < 0 || units[u].sp >= geo.SP || units[u].parts < 1 ||
+            units[u].part < 0 || units[u].part >= units[u].parts)
+            raise(DG_EINVAL, "dg_correlate_units: bad work unit");
+        hpg[u] = geo.hpg[units[u].sp];
+        hstep[u] = units[u].sp;
+    }
+    auto* upg = sc.alloc<PairGeom>(SPl);
+    auto* ustep = sc.alloc<int>(SPl);
+    CK(cudaMemcpyAsync(upg, hpg.data(), SPl * sizeof(PairGeom), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ustep, hstep.data(), SPl * sizeof(int), cudaMemcpyHostToDevice, st));
+
     Pipeline pl;
     pl.init(sc, eng, P, sn->N, SPl, opt.profile ? 1 : 2, eng->lane);
-    const int64_t n_elems = (int64_t)SPl * P;
-    double* raw = pairs == 1 ? grids : sc.alloc<double>(n_elems);
-    // refine flags: one bitmap row of whole words per step (bit p of step i at
-    // i * P32 + p), so batches of steps are refined on a side stream while the
-    // lanes correlate later steps (FP64 refinement next to FP32 correlation)
+    // refine flags: one bitmap row of whole words per unit (bit p of unit i at
+    // i * P32 + p), so batches of units are refined on a side stream while the
+    // lanes correlate later units (FP64 refinement next to FP32 correlation)
     const int64_t P32 = (P + 31) & ~int64_t(31);
     const int64_t n_words = SPl * (P32 / 32);
     const auto* y32 = static_cast<const float2*>(sn->y32->p) + kCapturePad;
     const auto* y64 = static_cast<const double2*>(sn->y64->p) + kCapturePad;
-    const int sp0 = s0 * pairs;  // global (snapshot, pair) index of local step 0
-    RefineCtx ctx = refine_ctx(g, sn, geo, raw);  // element = local step * P + p
-    ctx.pg = geo.pg + sp0;
-    ctx.y64 = y64 + (int64_t)s0 * R * sn->stride;  // local snapshot 0
+    RefineCtx ctx = refine_ctx(g, sn, geo, raw);  // element = unit row * P + p
+    ctx.unit_step = ustep;
+    for (int u = 0; u < SPl; ++u)  // parts: candidates of the other parts stay 0
+        if (units[u].parts > 1)
+            CK(cudaMemsetAsync(raw + (int64_t)u * P, 0, P * sizeof(double), st));
     uint32_t* bits = nullptr;
     std::unique_ptr<SideRefine> rfp;
 
     for (int w0 = 0; w0 < SPl; w0 += pl.slots) {
         const int nw = std::min(pl.slots, SPl - w0);
-        // phase A: geometry of the whole window in one pass (planned from the
-        // FP32 lattice ranges, which bound the exact TDOA bins)
-        launch_geometry_steps(g->x, g->y, g->z, P, geo.pg + sp0 + w0, nw, fs, wl, pl.N,
-                              pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins,
-                              raw + (int64_t)w0 * P, pl.overlap, pl.err, st);
+        // phase A: geometry of the whole window in one pass; bins from the
+        // histograms, B / R / centre frequency from the FP32 lattice ranges
+        if (w0 > 0) CK(cudaMemsetAsync(pl.hist, 0, sizeof(int) * pl.nbins * nw, st));
+        launch_geometry_steps(g->x, g->y, g->z, P, upg + w0, nw, fs, wl, pl.N, pl.d_slot(0),
+                              pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins, raw + (int64_t)w0 * P,
+                              pl.overlap, pl.err, st);
         launch_hist_range(pl.hist_slot(0), pl.nbins, nw, pl.N, pl.range, st);
         launches += (nw + 63) / 64 + 1;
         if (w0 == 0) {  // the rest of the run's state, while the first geometry pass runs
@@ -1558,13 +1687,14 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
             rfp = std::make_unique<SideRefine>(sc, SPl, P, P32, opt.profile ? 0 : 10, eng->refine);
         }
         SideRefine& rf = *rfp;
-        const PairGeom* hw = geo.hpg.data() + sp0 + w0;
+        const PairGeom* hw = hpg.data() + w0;
         const StepRange* approx = pl.lattice_ranges(sc, g, hw, nw, fs, wl);
+        std::vector<StepUnit> wunits(units.begin() + w0, units.begin() + w0 + nw);
         pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size,
-                       /*exact_ranges=*/false);
+                       /*exact_ranges=*/false, &wunits);
         if (w0 == 0 && sn->ready) pl.wait_event(sn->ready);  // captures still uploading
-        for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each step
-            const int lsp = w0 + i, sp = sp0 + lsp;
+        for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each unit
+            const int lsp = w0 + i, sp = units[lsp].sp;
             const int s = sp / pairs, q = sp - s * pairs;
             const int64_t c1 = ((int64_t)s * R + geo.prx[2 * q]) * sn->stride;
             const int64_t c2 = ((int64_t)s * R + geo.prx[2 * q + 1]) * sn->stride;
@@ -1580,9 +1710,68 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     CK(cudaGetLastError());
 
     SideRefine& rf = *rfp;
-    rf.finish(bits, ctx);  // remaining steps; the main stream joins the side stream
+    rf.finish(bits, ctx);  // remaining units; the main stream joins the side stream
     launches += rf.launches;
 
+    // the run's counters in one read-back (no host round trip before the last
+    // refinement batch is queued): error flag, overlap, work per lane, refined
+    // elements per batch
+    std::vector<unsigned long long> hc(2 + 3 * pl.n_lanes + std::max(rf.batches, 1), 0ull);
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, pl.err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), pl.overlap, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
+    for (int l = 0; l < pl.n_lanes; ++l)
+        CK(cudaMemcpyAsync(hc.data() + 2 + 3 * l, pl.lanes[l].work, 3 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+    const size_t c0 = 2 + 3 * (size_t)pl.n_lanes;
+    CK(cudaMemcpyAsync(hc.data() + c0, rf.counts, (hc.size() - c0) * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (herr) raise(DG_EINVAL, "predict_geometry: candidate coincides with receiver");
+    unsigned long long work[3] = {0, 0, 0}, refined = 0;
+    for (int l = 0; l < pl.n_lanes; ++l)
+        for (int k = 0; k < 3; ++k) work[k] += hc[2 + 3 * l + k];
+    for (size_t i = c0; i < hc.size(); ++i) refined += hc[i];
+    res->n_refined += (int64_t)refined;
+    res->sum_overlap_samples += (double)hc[0];
+    res->kernel_launches += launches;
+    res->correlate_launches += SPl;
+    res->moment_ffma2 += (double)work[0];
+    res->evaluate_ffma2 += (double)work[1];
+    res->evaluate_tc_flop += (double)work[2];
+    res->direct_steps += pl.direct_steps;
+    if (opt.profile) {
+        double tm = 0.0, te = 0.0;
+        for (int i = 0; i < SPl; ++i) {
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, evs[3 * i], evs[3 * i + 1]));
+            CK(cudaEventElapsedTime(&b, evs[3 * i + 1], evs[3 * i + 2]));
+            tm += a;
+            te += b;
+        }
+        res->moments_ms += tm;
+        res->evaluate_ms += te;
+        res->correlate_ms += tm + te;
+    }
+}
+
+// Snapshots [s0, s1) over the whole grid g: every pair of each (the units of
+// the snapshot range), pair sums (correlate_snapshot_all_pairs) and the
+// optional median scaling -> grids [(s1-s0)][P] (device), medians [s1-s0].
+void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                          const RunGeo& geo, int s0, int s1, const dg_options& opt, double* grids,
+                          double* medians, Scratch& sc, dg_result* res) {
+    const int64_t P = g->size();
+    const int pairs = geo.pairs;
+    const int ns = s1 - s0;
+    cudaStream_t st = sc.st;
+    if (ns <= 0) return;
+    std::vector<StepUnit> units(ns * pairs);
+    for (int i = 0; i < ns * pairs; ++i) units[i].sp = s0 * pairs + i;
+    double* raw = pairs == 1 ? grids : sc.alloc<double>((int64_t)ns * pairs * P);
+    correlate_units_impl(eng, g, sn, geo, units, opt, raw, sc, res);
+    int64_t launches = 0;
     if (pairs > 1) {
         launch_combine_pairs(raw, ns, pairs, P, grids, st);
         launches += 1;
@@ -1605,48 +1794,26 @@ void correlate_steps_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         }
         CK(cudaStreamSynchronize(st));  // `init` is host memory of this frame
     }
-
-    // the run's counters in one read-back (no host round trip before the last
-    // refinement batch is queued): error flag, overlap, work per lane, refined
-    // elements per batch
-    std::vector<unsigned long long> hc(2 + 3 * pl.n_lanes + std::max(rf.batches, 1), 0ull);
-    int herr = 0;
-    CK(cudaMemcpyAsync(&herr, pl.err, sizeof herr, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hc.data(), pl.overlap, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       st));
-    for (int l = 0; l < pl.n_lanes; ++l)
-        CK(cudaMemcpyAsync(hc.data() + 2 + 3 * l, pl.lanes[l].work, 3 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
-    const size_t c0 = 2 + 3 * (size_t)pl.n_lanes;
-    CK(cudaMemcpyAsync(hc.data() + c0, rf.counts, (hc.size() - c0) * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (herr) raise(DG_EINVAL, "predict_geometry: candidate coincides with receiver");
-    unsigned long long work[3] = {0, 0, 0}, refined = 0;
-    for (int l = 0; l < pl.n_lanes; ++l)
-        for (int k = 0; k < 3; ++k) work[k] += hc[2 + 3 * l + k];
-    for (size_t i = c0; i < hc.size(); ++i) refined += hc[i];
-    res->n_refined = (int64_t)refined;
-    res->sum_overlap_samples = (double)hc[0];
     res->kernel_launches += launches;
-    res->correlate_launches = SPl;
-    res->moment_ffma2 = (double)work[0];
-    res->evaluate_ffma2 = (double)work[1];
-    res->evaluate_tc_flop = (double)work[2];
-    res->direct_steps = pl.direct_steps;
-    if (opt.profile) {
-        double tm = 0.0, te = 0.0;
-        for (int i = 0; i < SPl; ++i) {
-            float a = 0.f, b = 0.f;
-            CK(cudaEventElapsedTime(&a, evs[3 * i], evs[3 * i + 1]));
-            CK(cudaEventElapsedTime(&b, evs[3 * i + 1], evs[3 * i + 2]));
-            tm += a;
-            te += b;
-        }
-        res->moments_ms = tm;
-        res->evaluate_ms = te;
-        res->correlate_ms = tm + te;
+}
+
+// dg_shard_plan (b200geo.h): whole steps in contiguous blocks, the remainder
+// steps split into `world` bucket-range parts, one per rank.
+std::vector<dg_work_unit> shard_plan(int64_t S, int64_t pairs, int world, bool whole) {
+    std::vector<dg_work_unit> u;
+    if (whole) {
+        for (int r = 0; r < world; ++r)
+            for (int64_t s = r * S / world; s < (r + 1) * S / world; ++s)
+                u.push_back(dg_work_unit{s, 0, 1, r, 0});
+        return u;
     }
+    const int64_t steps = S * pairs, q = steps / world;
+    for (int r = 0; r < world; ++r) {
+        for (int64_t sp = r * q; sp < (r + 1) * q; ++sp) u.push_back(dg_work_unit{sp, 0, 1, r, 0});
+        for (int64_t sp = world * q; sp < steps; ++sp)
+            u.push_back(dg_work_unit{sp, r, world, r, 0});
+    }
+    return u;
 }
 
 // Accumulation over ALL S snapshots of grid g (a slab or the full lattice)
@@ -1734,8 +1901,33 @@ PeakCells exact_peak(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, c
     auto* best_i = sc.alloc<long long>(1);
     auto* best_v = sc.alloc<double>(1);
     std::vector<double> next_fast(1);
+    // each chain's phasor start and step from the host's libm, as the reference
+    // computes them (correlate.hpp:51-54), so the FP64 chains are bit-identical
+    const int chains_max = std::min(n, kRerankRound) * SP;
+    auto* offs = sc.alloc<dg_pair_offsets>(chains_max);
+    auto* trig = sc.alloc<double>(4 * (size_t)chains_max);
+    std::vector<dg_pair_offsets> h_offs(chains_max);
+    std::vector<double> h_trig(4 * (size_t)chains_max);
+    ctx.trig = trig;
     for (int r0 = 0; r0 < n; r0 += kRerankRound) {
         const int m = std::min(kRerankRound, n - r0);
+        launch_chain_offsets(order + r0, m, SP, ctx, offs, st);
+        CK(cudaMemcpyAsync(h_offs.data(), offs, (size_t)m * SP * sizeof(dg_pair_offsets),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < (int64_t)m * SP; ++i) {
+            const int64_t d = h_offs[i].tdoa_samples;
+            const int64_t kb = std::max<int64_t>(0, -d);
+            const double step = 2.0 * std::numbers::pi * h_offs[i].fdoa_hz / geo.fs;
+            const double phase0 = step * static_cast<double>(kb);
+            double* t = h_trig.data() + 4 * i;
+            t[0] = std::cos(step);
+            t[1] = std::sin(step);
+            t[2] = std::cos(phase0);
+            t[3] = std::sin(phase0);
+        }
+        CK(cudaMemcpyAsync(trig, h_trig.data(), 4 * (size_t)m * SP * sizeof(double),
+                           cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(n_batch, &m, sizeof m, cudaMemcpyHostToDevice, st));
         launch_rerank(order + r0, n_batch, m, m, SP, ctx, ex, st);
         launch_recombine_cells(n_batch, m, ex, S, pairs, medians, pk.acc_ex + r0,
@@ -1767,10 +1959,13 @@ PeakCells exact_peak(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, c
     return pk;
 }
 
+// per_pitch: elements between snapshot rows of the host per_snapshot buffer
+// (0: P; a slab of a multi-GPU run writes its columns of the full rows)
 void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunGeo& geo,
                const double* grids, const double* medians, const dg_options& opt,
-               bool acc_dev_allowed, dg_result* res, Scratch& sc) {
+               bool acc_dev_allowed, dg_result* res, Scratch& sc, int64_t per_pitch = 0) {
     const int64_t P = g->size();
+    if (per_pitch == 0) per_pitch = P;
     const int S = geo.S;
     cudaStream_t st = sc.st;
     int64_t launches = 0;
@@ -1806,8 +2001,9 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
         CK(cudaMemcpyAsync(res->accumulated, acc, P * sizeof(double), cudaMemcpyDeviceToHost,
                            d2h));
     if (res->per_snapshot && grids)
-        CK(cudaMemcpyAsync(res->per_snapshot, grids, (int64_t)S * P * sizeof(double),
-                           cudaMemcpyDeviceToHost, d2h));
+        CK(cudaMemcpy2DAsync(res->per_snapshot, per_pitch * sizeof(double), grids,
+                             P * sizeof(double), P * sizeof(double), S, cudaMemcpyDeviceToHost,
+                             d2h));
     // `acc` / `grids` are freed on st when the caller's scratch goes: st waits
     // for these readers before returning (also when an error unwinds)
     SideJoin sj(st, d2h, det);
@@ -1875,7 +2071,7 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
             if (res->accumulated) res->accumulated[hc[i]] = ha[i];
             if (res->per_snapshot && grids)
                 for (int s = 0; s < S; ++s)
-                    res->per_snapshot[(int64_t)s * P + hc[i]] = hg[(size_t)i * S + s];
+                    res->per_snapshot[(int64_t)s * per_pitch + hc[i]] = hg[(size_t)i * S + s];
         }
     }
     res->kernel_launches += launches;
@@ -1896,7 +2092,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     set_device(eng);
     StreamGuard sg(opt.stream, eng->stream);
     Scratch sc(sg.st);
-    res->kernel_launches = 0;
+    reset_stats(res);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (opt.profile) {
         CK(cudaEventCreate(&e0));
@@ -1920,7 +2116,294 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     }
 }
 
+// ---- multi-GPU engine (dg_engine_create_multi) --------------------------------
+// The rows [r0, r1) of a grid as a grid of its own (flat indices stay global).
+dg_grid slab_view(const dg_grid& g, int64_t r0, int64_t r1) {
+    dg_grid s = g;
+    s.replicas = std::make_shared<Replicas<dg_grid>>();
+    s.n_lat = r1 - r0;
+    s.row_offset = g.row_offset + r0;
+    s.x = g.x + r0 * g.n_lon;
+    s.y = g.y + r0 * g.n_lon;
+    s.z = g.z + r0 * g.n_lon;
+    return s;
+}
+
+// g's cells (and its full FP32 planning lattice) on engine e's device
+const dg_grid* grid_on(const dg_grid* g, const dg_engine* e) {
+    if (g->eng == e) return g;
+    std::lock_guard<std::mutex> lk(g->replicas->mu);
+    for (auto& [k, v] : g->replicas->v)
+        if (k == e) return v.get();
+    set_device(e);
+    auto r = std::make_unique<dg_grid>(slab_view(*g, 0, g->n_lat));
+    r->eng = const_cast<dg_engine*>(e);
+    r->row_offset = g->row_offset;
+    const int64_t P = g->size();
+    r->mem = std::make_shared<DevMem>(3 * P * sizeof(double));
+    double* base = static_cast<double*>(r->mem->p);
+    CK(cudaMemcpyPeer(base, e->device, g->x, g->eng->device, P * sizeof(double)));
+    CK(cudaMemcpyPeer(base + P, e->device, g->y, g->eng->device, P * sizeof(double)));
+    CK(cudaMemcpyPeer(base + 2 * P, e->device, g->z, g->eng->device, P * sizeof(double)));
+    r->x = base;
+    r->y = base + P;
+    r->z = base + 2 * P;
+    r->rel = std::make_shared<DevMem>(g->rel->bytes);
+    CK(cudaMemcpyPeer(r->rel->p, e->device, g->rel->p, g->eng->device, g->rel->bytes));
+    const dg_grid* out = r.get();
+    g->replicas->v.emplace_back(e, std::move(r));
+    return out;
+}
+
+const dg_staged* staged_on(const dg_staged* s, const dg_engine* e) {
+    if (s->eng == e) return s;
+    std::lock_guard<std::mutex> lk(s->replicas->mu);
+    for (auto& [k, v] : s->replicas->v)
+        if (k == e) return v.get();
+    if (s->ready) CK(cudaEventSynchronize(s->ready));
+    set_device(e);
+    auto r = std::make_unique<dg_staged>();
+    r->eng = const_cast<dg_engine*>(e);
+    r->S = s->S;
+    r->R = s->R;
+    r->N = s->N;
+    r->stride = s->stride;
+    r->fs = s->fs;
+    r->fc = s->fc;
+    r->states = s->states;
+    r->y32 = std::make_unique<DevMem>(s->y32->bytes);
+    r->y64 = std::make_unique<DevMem>(s->y64->bytes);
+    CK(cudaMemcpyPeer(r->y32->p, e->device, s->y32->p, s->eng->device, s->y32->bytes));
+    CK(cudaMemcpyPeer(r->y64->p, e->device, s->y64->p, s->eng->device, s->y64->bytes));
+    const dg_staged* out = r.get();
+    s->replicas->v.emplace_back(e, std::move(r));
+    return out;
+}
+
+// run f(k) on one host thread per device; the first exception is rethrown
+template <class F>
+void on_devices(int G, F&& f) {
+    std::vector<std::exception_ptr> err(G);
+    std::vector<std::thread> th;
+    for (int k = 0; k < G; ++k)
+        th.emplace_back([&, k] {
+            try {
+                f(k);
+            } catch (...) {
+                err[k] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+// geolocate_snapshots over every device of a multi-GPU engine (DESIGN.md
+// section 7): the run's work units (dg_shard_plan) are correlated on their
+// devices (no communication), every unit's slab columns go by peer copy
+// (NVLink) to the device owning that latitude slab, which sums the parts of a
+// step (exact: disjoint candidates), adds the pairs and accumulates its slab
+// over all snapshots in the reference's order — every accumulated value is
+// bit-identical to the one-GPU solve. The exact peak re-ranks the cells above
+// the band of the global fast maximum on every slab (two-stage peak), and
+// detection runs on device 0 over the gathered surface.
+void geolocate_multi(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                     const dg_options* opt_in, dg_result* res) {
+    const dg_options opt = options_or_default(opt_in);
+    check_run(eng, g, sn, opt, res);
+    if (opt.profile) raise(DG_EINVAL, "b200: profiled runs use one device");
+    reset_stats(res);
+    const int G = eng->n_devices();
+    const int64_t P = g->size(), n_lon = g->n_lon, n_lat = g->n_lat;
+    const int S = (int)sn->S, R = (int)sn->R, pairs = R * (R - 1) / 2;
+    const bool whole = opt.normalize_per_snapshot != 0;
+    const auto plan = shard_plan(S, pairs, G, whole);
+    const int U = (int)plan.size();
+    std::vector<std::vector<int>> mine(G);  // plan indices of each device's units
+    for (int u = 0; u < U; ++u) mine[plan[u].rank].push_back(u);
+    std::vector<int64_t> r0(G), r1(G);
+    for (int k = 0; k < G; ++k) {
+        r0[k] = k * n_lat / G;
+        r1[k] = (k + 1) * n_lat / G;
+    }
+    std::vector<std::unique_ptr<Scratch>> scr(G);
+    std::vector<RunGeo> geo(G);
+    std::vector<const dg_grid*> gk(G);
+    std::vector<const dg_staged*> sk(G);
+    std::vector<double*> out(G, nullptr), med(G, nullptr);
+    std::vector<dg_result> part(G);
+    // phase 1: each device correlates its units over the whole grid
+    on_devices(G, [&](int k) {
+        dg_engine* e = eng->dev(k);
+        set_device(e);
+        gk[k] = grid_on(g, e);
+        sk[k] = staged_on(sn, e);
+        scr[k] = std::make_unique<Scratch>(e->stream);
+        Scratch& sc = *scr[k];
+        geo[k] = make_geo(sc, sk[k]);
+        std::memset(&part[k], 0, sizeof(dg_result));
+        const int n = (int)mine[k].size();
+        out[k] = sc.alloc<double>((int64_t)std::max(n, 1) * P);
+        if (whole) {  // contiguous snapshots, pair sums and median scaling on the device
+            med[k] = sc.alloc<double>(std::max(n, 1));
+            if (n > 0)
+                correlate_steps_impl(e, gk[k], sk[k], geo[k], (int)plan[mine[k][0]].step,
+                                     (int)plan[mine[k][0]].step + n, opt, out[k], med[k], sc,
+                                     &part[k]);
+        } else if (n > 0) {
+            std::vector<StepUnit> u(n);
+            for (int i = 0; i < n; ++i) {
+                const dg_work_unit& w = plan[mine[k][i]];
+                u[i] = StepUnit{(int)w.step, w.part, w.parts};
+            }
+            correlate_units_impl(e, gk[k], sk[k], geo[k], u, opt, out[k], sc, &part[k]);
+        }
+        CK(cudaStreamSynchronize(sc.st));
+    });
+    // phase 2: slab j gathers its columns of every unit (peer copies), then the
+    // per-snapshot slab surfaces [S][slab] in the reference's pair / step order
+    std::vector<double*> grids(G, nullptr), meds(G, nullptr);
+    std::vector<int> local_idx(U);
+    for (int k = 0; k < G; ++k)
+        for (int i = 0; i < (int)mine[k].size(); ++i) local_idx[mine[k][i]] = i;
+    on_devices(G, [&](int j) {
+        dg_engine* e = eng->dev(j);
+        set_device(e);
+        Scratch& sc = *scr[j];
+        const int64_t slab = (r1[j] - r0[j]) * n_lon, c0 = r0[j] * n_lon;
+        if (slab == 0) return;
+        const int rows = whole ? S : U;
+        double* recv = sc.alloc<double>((int64_t)rows * slab);
+        for (int u = 0; u < U; ++u) {
+            const int k = plan[u].rank;
+            const int dst_row = whole ? (int)plan[u].step : u;
+            CK(cudaMemcpyPeerAsync(recv + (int64_t)dst_row * slab, e->device,
+                                   out[k] + (int64_t)local_idx[u] * P + c0, eng->dev(k)->device,
+                                   slab * sizeof(double), sc.st));
+        }
+        if (whole) {
+            grids[j] = recv;
+            meds[j] = sc.alloc<double>(S);
+            for (int u = 0; u < U; ++u)
+                CK(cudaMemcpyPeerAsync(meds[j] + plan[u].step, e->device,
+                                       med[plan[u].rank] + local_idx[u],
+                                       eng->dev(plan[u].rank)->device, sizeof(double), sc.st));
+            return;
+        }
+        // the parts of a step hold disjoint candidates: their sum is exact in
+        // any order; then the pairs in the reference's order
+        std::vector<int> hstep(U);
+        for (int u = 0; u < U; ++u) hstep[u] = (int)plan[u].step;
+        int* ustep = sc.alloc<int>(U);
+        CK(cudaMemcpyAsync(ustep, hstep.data(), U * sizeof(int), cudaMemcpyHostToDevice, sc.st));
+        double* steps = sc.alloc<double>((int64_t)S * pairs * slab);
+        CK(cudaMemsetAsync(steps, 0, (int64_t)S * pairs * slab * sizeof(double), sc.st));
+        launch_sum_units(recv, U, slab, ustep, steps, sc.st);
+        if (pairs == 1) {
+            grids[j] = steps;
+        } else {
+            grids[j] = sc.alloc<double>((int64_t)S * slab);
+            launch_combine_pairs(steps, S, pairs, slab, grids[j], sc.st);
+        }
+        CK(cudaStreamSynchronize(sc.st));  // hstep is host memory of this frame
+    });
+    // phase 3: accumulation and the fast maximum of every slab
+    std::vector<dg_grid> slabs;
+    for (int k = 0; k < G; ++k) slabs.push_back(slab_view(*gk[k], r0[k], r1[k]));
+    std::vector<double*> acc(G, nullptr);
+    std::vector<dg_result> pr(G);
+    dg_options o1 = opt;
+    o1.stream = nullptr;
+    o1.detect = 0;
+    o1.peak_stage = 1;
+    on_devices(G, [&](int j) {
+        if (slabs[j].size() == 0) return;
+        dg_engine* e = eng->dev(j);
+        set_device(e);
+        Scratch& sc = *scr[j];
+        acc[j] = sc.alloc<double>(slabs[j].size());
+        std::memset(&pr[j], 0, sizeof(dg_result));
+        pr[j].accumulated_device = acc[j];
+        peak_impl(e, &slabs[j], sk[j], geo[j], grids[j], whole ? meds[j] : nullptr, o1, true,
+                  &pr[j], sc);
+    });
+    double M = 0.0;
+    for (int j = 0; j < G; ++j)
+        if (slabs[j].size() > 0) M = std::max(M, pr[j].argmax_value);
+    // phase 4: exact peak of every slab against the global band, host copies
+    dg_options o2 = o1;
+    o2.peak_stage = 2;
+    o2.peak_max = M;
+    on_devices(G, [&](int j) {
+        if (slabs[j].size() == 0) return;
+        dg_engine* e = eng->dev(j);
+        set_device(e);
+        Scratch& sc = *scr[j];
+        dg_result& r = pr[j];
+        const int64_t c0 = r0[j] * n_lon;
+        r.accumulated = res->accumulated ? res->accumulated + c0 : nullptr;
+        r.per_snapshot = res->per_snapshot ? res->per_snapshot + c0 : nullptr;
+        peak_impl(e, &slabs[j], sk[j], geo[j], grids[j], whole ? meds[j] : nullptr, o2, true, &r,
+                  sc, P);
+    });
+    if (M > 0.0) {
+        res->argmax_index = -1;
+        for (int j = 0; j < G; ++j) {
+            const dg_result& r = pr[j];
+            if (slabs[j].size() == 0 || r.argmax_index < 0) continue;
+            if (res->argmax_index < 0 || r.argmax_value > res->argmax_value ||
+                (r.argmax_value == res->argmax_value && r.argmax_index < res->argmax_index)) {
+                res->argmax_index = r.argmax_index;
+                res->argmax_value = r.argmax_value;
+            }
+        }
+    } else {  // all-zero surface: first index wins
+        res->argmax_index = g->row_offset * n_lon;
+        res->argmax_value = 0.0;
+    }
+    // the full surface on device 0 (caller's buffer or scratch) and detection
+    set_device(eng);
+    Scratch& s0 = *scr[0];
+    double* full = res->accumulated_device ? res->accumulated_device : nullptr;
+    if (!full && opt.detect) full = s0.alloc<double>(P);
+    if (full) {
+        for (int j = 0; j < G; ++j)
+            if (slabs[j].size() > 0)
+                CK(cudaMemcpyPeerAsync(full + r0[j] * n_lon, eng->device, acc[j],
+                                       eng->dev(j)->device, slabs[j].size() * sizeof(double),
+                                       s0.st));
+    }
+    res->n_detections = 0;
+    int64_t launches = 0;
+    if (opt.detect)
+        run_detect(g, full, opt.k_sigma, opt.exclusion_radius_cells, res->detections,
+                   res->detections_capacity, &res->n_detections, s0, &launches);
+    CK(cudaStreamSynchronize(s0.st));
+    for (int k = 0; k < G; ++k) {
+        const dg_result& a = part[k];
+        res->n_refined += a.n_refined;
+        res->sum_overlap_samples += a.sum_overlap_samples;
+        res->correlate_launches += a.correlate_launches;
+        res->moment_ffma2 += a.moment_ffma2;
+        res->evaluate_ffma2 += a.evaluate_ffma2;
+        res->evaluate_tc_flop += a.evaluate_tc_flop;
+        res->direct_steps += a.direct_steps;
+        res->kernel_launches += a.kernel_launches + pr[k].kernel_launches;
+        res->n_reranked += pr[k].n_reranked;
+    }
+    res->kernel_launches += launches;
+    // scratch of each device freed on its own device
+    for (int k = G - 1; k >= 0; --k) {
+        set_device(eng->dev(k));
+        CK(cudaStreamSynchronize(scr[k]->st));
+        scr[k].reset();
+    }
+    set_device(eng);
+}
+
 }  // namespace
+
+extern "C" {
 
 int dg_correlate_steps(dg_engine* eng, const dg_grid* g, const dg_staged* sn, int64_t s_begin,
                        int64_t s_end, const dg_options* opt_in, double* grids_device,
@@ -1936,10 +2419,44 @@ int dg_correlate_steps(dg_engine* eng, const dg_grid* g, const dg_staged* sn, in
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
         Scratch sc(sg.st);
-        res->kernel_launches = 0;
+        reset_stats(res);
         const RunGeo geo = make_geo(sc, sn);
         correlate_steps_impl(eng, g, sn, geo, (int)s_begin, (int)s_end, opt, grids_device,
                              medians_device, sc, res);
+    });
+}
+
+int dg_shard_plan(int64_t S, int64_t R, int world, int whole, dg_work_unit* out, int64_t cap,
+                  int64_t* n_out) {
+    return guard([&] {
+        if (S < 1) raise(DG_EINVAL, "geolocate_snapshots: no snapshots");
+        if (R < 2) raise(DG_EINVAL, "correlate_snapshot_all_pairs: need >= 2 receivers");
+        if (world < 1) raise(DG_EINVAL, "dg_shard_plan: world < 1");
+        const auto units = shard_plan(S, R * (R - 1) / 2, world, whole != 0);
+        if (n_out) *n_out = (int64_t)units.size();
+        if (out)
+            for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)units.size()); ++i)
+                out[i] = units[i];
+    });
+}
+
+int dg_correlate_units(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
+                       const dg_work_unit* units, int64_t n_units, const dg_options* opt_in,
+                       double* raw, dg_result* res) {
+    return guard([&] {
+        const dg_options opt = options_or_default(opt_in);
+        check_run(eng, g, sn, opt, res);
+        if (n_units < 0 || (n_units > 0 && (!units || !raw)))
+            raise(DG_EINVAL, "dg_correlate_units: null units / surfaces");
+        set_device(eng);
+        StreamGuard sg(opt.stream, eng->stream);
+        Scratch sc(sg.st);
+        reset_stats(res);
+        const RunGeo geo = make_geo(sc, sn);
+        std::vector<StepUnit> u(n_units);
+        for (int64_t i = 0; i < n_units; ++i)
+            u[i] = StepUnit{(int)units[i].step, units[i].part, units[i].parts};
+        correlate_units_impl(eng, g, sn, geo, u, opt, raw, sc, res);
     });
 }
 
@@ -1954,7 +2471,7 @@ int dg_accumulate_peak(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
         Scratch sc(sg.st);
-        res->kernel_launches = 0;
+        reset_stats(res);
         const RunGeo geo = make_geo(sc, sn);
         peak_impl(eng, g, sn, geo, grids_device,
                   opt.normalize_per_snapshot ? medians_device : nullptr, opt, opt_in != nullptr,
@@ -1964,7 +2481,12 @@ int dg_accumulate_peak(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
 
 int dg_geolocate_staged(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const dg_options* opt,
                         dg_result* res) {
-    return guard([&] { geolocate_impl(eng, g, sn, opt, res); });
+    return guard([&] {
+        if (eng && eng->n_devices() > 1)
+            geolocate_multi(eng, g, sn, opt, res);
+        else
+            geolocate_impl(eng, g, sn, opt, res);
+    });
 }
 
 int dg_geolocate_snapshots(dg_engine* eng, const dg_grid* g, const dg_snapshots* sn,
@@ -1972,7 +2494,10 @@ int dg_geolocate_snapshots(dg_engine* eng, const dg_grid* g, const dg_snapshots*
     return guard([&] {
         // the capture upload overlaps the geometry / planning phase
         std::unique_ptr<dg_staged> staged = stage_impl(eng, sn, true);
-        geolocate_impl(eng, g, staged.get(), opt, res);
+        if (eng->n_devices() > 1)
+            geolocate_multi(eng, g, staged.get(), opt, res);
+        else
+            geolocate_impl(eng, g, staged.get(), opt, res);
         CK(cudaStreamSynchronize(eng->upload));  // before the host captures may change
     });
 }

@@ -34,6 +34,17 @@ namespace {
 
 constexpr int kYPad = 8;  // extra samples per y2 staging buffer (parity shift + slack)
 
+// e^{i 2 pi x} for an FP64 cycle count: FP64 range reduction and sincospi,
+// one rounding to FP32 (<= 0.5 ulp): the phasor tables, block steps and chunk
+// anchors carry no FP32 argument rounding, whose systematic phase error
+// aliased into the block sums of strong off-TDOA chirp products
+__device__ __forceinline__ void cis_f64(double x, float* c, float* s) {
+    double sd, cd;
+    sincospi(2.0 * (x - rint(x)), &sd, &cd);
+    *c = (float)cd;
+    *s = (float)sd;
+}
+
 template <int kCh>
 struct alignas(16) WarpSmemT {
     float2 y1[2][kCh];          // staged y1[c0 .. c0+kCh); z overwrites it in place
@@ -100,16 +111,20 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
 #pragma unroll
         for (int j = 0; j < LB; ++j) {
             const double x = f[c] * (double)j;
-            sincospif((float)(2.0 * (x - rint(x))), &ei[c][j], &er[c][j]);
+            cis_f64(x, &er[c][j], &ei[c][j]);
         }
         const double x = f[c] * (double)LB;
-        sincospif((float)(2.0 * (x - rint(x))), &w1i[c], &w1r[c]);
+        cis_f64(x, &w1r[c], &w1i[c]);
     }
 
-    double acc_re[NC], acc_im[NC];
+    // this candidate's FP32 error scale: the block sums round relative to the
+    // blocks (eb = sum_b |C_b|^2), the Horner chunk sums relative to the chunks
+    // (e2 = sum_c |chunk sum|^2). For noise both are ||z||_2^2; a tone at the
+    // candidate's frequency makes the chunk term CH/LB x larger, a chirp off its
+    // TDOA (coherent within blocks, not within chunks) the block term.
+    double acc_re[NC], acc_im[NC], e2[NC], eb[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc_re[c] = acc_im[c] = 0.0;
-    float z2 = 0.f;
+    for (int c = 0; c < NC; ++c) acc_re[c] = acc_im[c] = e2[c] = eb[c] = 0.0;
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int buf = ch & 1;
         const int c0 = kb0 + ch * CH;
@@ -134,16 +149,15 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
             zz.y = v0 ? fmaf(a.y, b0.x, -(a.x * b0.y)) : 0.f;
             zz.z = v1 ? fmaf(a.z, b1.x, a.w * b1.y) : 0.f;
             zz.w = v1 ? fmaf(a.w, b1.x, -(a.z * b1.y)) : 0.f;
-            z2 = fmaf(zz.x, zz.x, fmaf(zz.y, zz.y, fmaf(zz.z, zz.z, fmaf(zz.w, zz.w, z2))));
             zq[q] = zz;
         }
         __syncwarp();
 
         // ---- blocks in reverse, Horner: H = (((C_last) W1 + C_last-1) W1 + ...) ----
         //      chunk sum = W(c0) * H,  C_b = sum_j z[c0 + LB b + j] E[j]
-        float hr[NC], hi[NC];
+        float hr[NC], hi[NC], bq[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) hr[c] = hi[c] = 0.f;
+        for (int c = 0; c < NC; ++c) hr[c] = hi[c] = bq[c] = 0.f;
         constexpr int QB = LB / 2;        // z quads (2 samples each) per block
         constexpr int NB = CH / LB;       // blocks per chunk
         float4 znext = zq[(NB - 1) * QB];  // rolling one-quad-ahead prefetch
@@ -176,6 +190,7 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const float cr = A[c].x - B[c].y, ci = A[c].y + B[c].x;  // C = A + jB
+                bq[c] = fmaf(cr, cr, fmaf(ci, ci, bq[c]));
                 const float nr = fmaf(hr[c], w1r[c], fmaf(-hi[c], w1i[c], cr));
                 hi[c] = fmaf(hr[c], w1i[c], fmaf(hi[c], w1r[c], ci));
                 hr[c] = nr;
@@ -186,22 +201,21 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
         for (int c = 0; c < NC; ++c) {
             float wr, wi;
             const double x = f[c] * (double)c0;
-            sincospif((float)(2.0 * (x - rint(x))), &wi, &wr);
+            cis_f64(x, &wr, &wi);
             acc_re[c] += (double)fmaf(wr, hr[c], -(wi * hi[c]));
             acc_im[c] += (double)fmaf(wr, hi[c], wi * hr[c]);
+            e2[c] += (double)fmaf(hr[c], hr[c], hi[c] * hi[c]);
+            eb[c] += (double)bq[c];
         }
         __syncwarp();  // this stage's buffers are free for the next bulk copy
     }
 
 #pragma unroll
-    for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
-    const double thr = (double)kRefineTau * sqrt((double)z2);
-#pragma unroll
     for (int c = 0; c < NC; ++c) {
         if (p[c] < 0) continue;
         const double s = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
         s_out[p[c]] = s;
-        if (s < thr) {
+        if (s < (double)kRefineTau * sqrt(fmax(e2[c], eb[c]))) {
             const int64_t e = flag_base + p[c];
             atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
         }

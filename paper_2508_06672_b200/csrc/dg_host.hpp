@@ -114,6 +114,11 @@ struct dg_engine {
     int device = 0;
     int sm_count = 148;
     dg_tuning tuning{};  // validated by dg_engine_set_tuning; read once per call
+    // multi-GPU engine (dg_engine_create_multi): this engine drives devices[0],
+    // `peers` the others; whole-run calls shard the run across all of them
+    std::vector<dg_engine*> peers;
+    int n_devices() const { return 1 + (int)peers.size(); }
+    dg_engine* dev(int k) { return k == 0 ? this : peers[k - 1]; }
     cudaStream_t stream = nullptr;  // default stream of calls that pass none
     cudaStream_t upload = nullptr;  // capture uploads overlapped with the geometry phase
     // the second correlation lane and the side refinement of a run, created once
@@ -128,6 +133,7 @@ struct dg_engine {
     void* stage_host[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     ~dg_engine() {
+        for (dg_engine* e : peers) delete e;
         for (void* p : stage_host)
             if (p) cudaFreeHost(p);
         if (stream) cudaStreamDestroy(stream);
@@ -137,8 +143,21 @@ struct dg_engine {
     }
 };
 
+struct dg_grid;
+struct dg_staged;
+namespace dg {
+// copies of a grid / staged run on the other devices of a multi-GPU engine,
+// made by peer copies on first use and kept with the object
+template <class T>
+struct Replicas {
+    std::mutex mu;
+    std::vector<std::pair<const dg_engine*, std::unique_ptr<T>>> v;
+};
+}  // namespace dg
+
 struct dg_grid {
     dg_engine* eng = nullptr;
+    std::shared_ptr<dg::Replicas<dg_grid>> replicas = std::make_shared<dg::Replicas<dg_grid>>();
     double lat_start = 0, lat_step = 0, lon_start = 0, lon_step = 0, alt = 0;
     int64_t n_lat = 0, n_lon = 0, row_offset = 0;
     std::shared_ptr<dg::DevMem> mem;  // x | y | z of the full lattice
@@ -157,6 +176,7 @@ struct dg_grid {
 // centring / refinement
 struct dg_staged {
     dg_engine* eng = nullptr;
+    std::shared_ptr<dg::Replicas<dg_staged>> replicas = std::make_shared<dg::Replicas<dg_staged>>();
     int64_t S = 0, R = 0, N = 0, stride = 0;
     double fs = 0, fc = 0;
     std::unique_ptr<dg::DevMem> y32, y64;

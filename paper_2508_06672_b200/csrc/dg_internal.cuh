@@ -83,13 +83,17 @@ inline int64_t capture_stride(int64_t n) {
 }
 constexpr int kL = 16;       // phasor table length (samples per inner block)
 
-// Threshold on S / sqrt(sum |z|^2) below which an FP32 value is re-evaluated
-// exactly; see DESIGN.md "Parity" for the error model behind it.
-constexpr float kRefineTau = 0.02f;         // direct correlator (dg_correlate.cu)
-// block-moment correlator: S < tau * max(sqrt(A), Q). Measured
-// worst unrefined relative error over noise / 0 dB / +20 dB tone scenes at C3 scale
-// (tests/gpu_error_model.py): tau 0.02 -> 3.6e-5, 0.015 -> 4.5e-5, 0.01 -> 6.1e-5
-constexpr float kMomentRefineTau = 0.015f;
+// Threshold on S / sqrt(max(sum_chunks |chunk sum|^2, sum_blocks |block sum|^2))
+// below which a direct-correlator FP32 value is re-evaluated exactly
+// (dg_correlate.cu); see DESIGN.md "Parity" for the error model behind it.
+constexpr float kRefineTau = 0.02f;
+// block-moment correlator: S < tau * max(sqrt(A), Q). Worst
+// unrefined relative error on the stress scenes of tests/test_gpu_error_model.py
+// (+30/+40 dB tone and chirp, forced block lengths at the truncation edge) vs the
+// reference, by tau (tests/gpu_tau_sweep.py): 0.015 -> 3.2e-5, 0.02 -> 2.3e-5,
+// 0.025 -> 2.1e-5 at C3 cost 49.9 / 51.9 / 54.9 ms; 0.02 keeps >= 4x margin to the
+// 1e-4 contract on every scene.
+constexpr float kMomentRefineTau = 0.02f;
 
 // --------------------------------------------------------------------------
 // launchers (dg_kernels.cu). All asynchronous on `st`.
@@ -244,6 +248,8 @@ struct RefineCtx {
     int N;
     double fs, wl;
     double* raw;              // [S*pairs*P] (batch: [P])
+    const double* trig;       // re-rank only (nullable): [chain][4] host-libm phasors
+    const int* unit_step;     // refine rows (nullable): global step of each row
 };
 void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t st);
 // refine steps [row0, row1) of a bitmap with one P32-element row per step
@@ -254,6 +260,9 @@ void launch_refine_rows(const uint32_t* bits, int64_t row0, int64_t row1, int64_
 void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
                           cudaStream_t st);
 void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st);
+// steps[step[u]][i] += units[u][i], u in order (parts of split steps: exact)
+void launch_sum_units(const double* units, int U, int64_t n, const int* step, double* steps,
+                      cudaStream_t st);
 void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st);
 void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,
                 cudaStream_t st);
@@ -275,6 +284,9 @@ void launch_first_max(const double* v, int64_t P, const double* vmax, unsigned l
 // n_items_hint: host-side count of near-peak cells (sizes the launch)
 void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
                    RefineCtx ctx, double* ex, cudaStream_t st);
+// exact offsets of every re-rank chain (cells[ci], step sp) -> out[ci * SP + sp]
+void launch_chain_offsets(const int* cells, int n, int SP, RefineCtx ctx, dg_pair_offsets* out,
+                          cudaStream_t st);
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,
                             const double* medians, double* acc_ex, double* grid_ex /* [cap][S] */,
                             cudaStream_t st);

@@ -72,17 +72,32 @@ __device__ __forceinline__ bool offsets_exact(double cx, double cy, double cz, c
 // FP64 phasor recurrence, ascending k, double accumulators. Used only for the
 // few elements whose FP32 value cannot meet the relative tolerance and for the
 // near-peak re-rank; cos/sin are CUDA's (<= 1 ulp apart from glibc's).
+// tg (nullable): {cos(step), sin(step), cos(phase0), sin(phase0)} from the host's
+// libm (the reference's own std::cos / std::sin, exact_peak), so the chain is
+// bit-identical to the reference's; without it CUDA's sincos (<= 1 ulp off).
+__device__ __forceinline__ void chain_trig(long long kb, double fdoa, double fs,
+                                           const double* tg, double* rot_re, double* rot_im,
+                                           double* ph_re, double* ph_im) {
+    if (tg) {
+        *rot_re = tg[0];
+        *rot_im = tg[1];
+        *ph_re = tg[2];
+        *ph_im = tg[3];
+        return;
+    }
+    const double step = __ddiv_rn(__dmul_rn(kTwoPi, fdoa), fs);
+    sincos(step, rot_im, rot_re);
+    sincos(__dmul_rn(step, (double)kb), ph_im, ph_re);
+}
+
 __device__ double correlate_exact(const double2* __restrict__ y1, const double2* __restrict__ y2,
-                                  int N, long long d, double fdoa, double fs) {
+                                  int N, long long d, double fdoa, double fs,
+                                  const double* tg = nullptr) {
     const long long kb = d < 0 ? -d : 0;
     const long long ke = (N - d) < N ? (N - d) : N;
     if (kb >= ke) return 0.0;
-    const double step = __ddiv_rn(__dmul_rn(kTwoPi, fdoa), fs);
-    double rot_im, rot_re;
-    sincos(step, &rot_im, &rot_re);
-    const double phase0 = __dmul_rn(step, (double)kb);
-    double ph_im, ph_re;
-    sincos(phase0, &ph_im, &ph_re);
+    double rot_im, rot_re, ph_im, ph_re;
+    chain_trig(kb, fdoa, fs, tg, &rot_re, &rot_im, &ph_re, &ph_im);
     double acc_re = 0.0, acc_im = 0.0;
     const double2* b = y2 + d;
     // one reference iteration (correlate.hpp:59-69), operation order unchanged
@@ -488,9 +503,11 @@ k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
 
 // sfdoa (nullable): the candidates' FDOA in the same bucket order, so the
 // candidate evaluators read contiguous values instead of gathering fdoa[p]
-__global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __restrict__ cursor,
-                          int* __restrict__ sorted, const double* __restrict__ fdoa,
-                          double* __restrict__ sfdoa) {
+// Candidates whose bin lies outside the planned bins [bin0, bin0 + nbins) are
+// skipped (another part of a split step owns them; cursors outside are unset).
+__global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int bin0, int nbins,
+                          int* __restrict__ cursor, int* __restrict__ sorted,
+                          const double* __restrict__ fdoa, double* __restrict__ sfdoa) {
     // four independent cursor atomics in flight per thread (latency-bound)
     constexpr int U = 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -500,6 +517,8 @@ __global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int* __re
         for (int u = 0; u < U; ++u) {
             const int64_t p = p0 + u * stride;
             dd[u] = p < P ? d[p] : kNoOverlap;
+            if (dd[u] != kNoOverlap && (unsigned)(dd[u] + N - 1 - bin0) >= (unsigned)nbins)
+                dd[u] = kNoOverlap;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -574,10 +593,11 @@ __global__ void k_compact_flags(const uint32_t* __restrict__ bits, int64_t n_wor
     }
 }
 
-__device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, int64_t p) {
+__device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, int64_t p,
+                                                const double* tg) {
     if (c.offsets) {
         const dg_pair_offsets o = c.offsets[p];
-        return correlate_exact(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz, c.fs);
+        return correlate_exact(c.y64, c.y64 + c.stride, c.N, o.tdoa_samples, o.fdoa_hz, c.fs, tg);
     }
     const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
     long long tdoa;
@@ -586,7 +606,27 @@ __device__ __forceinline__ double exact_element(const RefineCtx& c, int64_t sp, 
     const int ri = c.pair_rx[2 * pr], rj = c.pair_rx[2 * pr + 1];
     const double2* y1 = c.y64 + (s * c.R + ri) * c.stride;
     const double2* y2 = c.y64 + (s * c.R + rj) * c.stride;
-    return correlate_exact(y1, y2, c.N, tdoa, fdoa, c.fs);
+    return correlate_exact(y1, y2, c.N, tdoa, fdoa, c.fs, tg);
+}
+
+// the exact offsets of every re-rank chain (cell ci, step sp) -> out[ci * SP + sp],
+// for the host's libm phasor values (chain_trig)
+__global__ void k_chain_offsets(const int* __restrict__ cells, int n, int SP, RefineCtx c,
+                                dg_pair_offsets* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n * SP;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ci = i / SP, sp = i - ci * SP;
+        const int64_t p = cells[ci];
+        dg_pair_offsets o;
+        if (c.offsets) {
+            o = c.offsets[p];
+        } else {
+            long long tdoa;
+            offsets_exact(c.x[p], c.y[p], c.z[p], c.pg[sp], c.fs, c.wl, &tdoa, &o.fdoa_hz);
+            o.tdoa_samples = tdoa;
+        }
+        out[i] = o;
+    }
 }
 
 // Eq. 11 in FP64 for one element, split across a group of T threads (a warp, or
@@ -692,7 +732,8 @@ k_refine_rows(const int64_t* __restrict__ list, const unsigned long long* __rest
     for (int64_t i = (int64_t)blockIdx.x * per + threadIdx.x / T; i < n;
          i += (int64_t)gridDim.x * per) {
         const int64_t e = base + list[i];
-        const int64_t sp = e / P32, p = e - sp * P32;
+        const int64_t row = e / P32, p = e - row * P32;
+        const int64_t sp = c.unit_step ? c.unit_step[row] : row;  // global step of the row
         const int64_t s = sp / c.pairs, pr = sp - s * c.pairs;
         long long tdoa;
         double fdoa;
@@ -701,7 +742,7 @@ k_refine_rows(const int64_t* __restrict__ list, const unsigned long long* __rest
         const double v = correlate_fp64_group<T>(c.y64 + (s * c.R + ri) * c.stride,
                                                  c.y64 + (s * c.R + rj) * c.stride, c.N, tdoa,
                                                  fdoa, c.fs);
-        if (threadIdx.x % T == 0) c.raw[sp * c.P + p] = v;
+        if (threadIdx.x % T == 0) c.raw[row * c.P + p] = v;
     }
 }
 
@@ -718,6 +759,18 @@ __global__ void k_combine_pairs(const double* __restrict__ raw, int S, int pairs
         for (int q = 1; q < pairs; ++q) g = __dadd_rn(g, r[q * P]);
         grids[i] = g;
     }
+}
+
+// steps[step[u]][i] += units[u][i] over the units in order (multi-GPU slabs:
+// the parts of a step hold disjoint candidates, so the sum is exact)
+__global__ void k_sum_units(const double* __restrict__ units, int U, int64_t n,
+                            const int* __restrict__ step, double* __restrict__ steps) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int u = 0; u < U; ++u) {
+            double* o = steps + (int64_t)step[u] * n + i;
+            *o = __dadd_rn(*o, units[(int64_t)u * n + i]);
+        }
 }
 
 __global__ void k_scale(double* __restrict__ v, int64_t P, const double* __restrict__ median) {
@@ -832,7 +885,7 @@ __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ 
     if (t % stride) return;
     for (int64_t i = t / stride; i < total; i += (int64_t)gridDim.x * blockDim.x / stride) {
         const int64_t ci = i / SP, sp = i - ci * SP;
-        ex[i] = exact_element(c, sp, cells[ci]);
+        ex[i] = exact_element(c, sp, cells[ci], c.trig ? c.trig + 4 * i : nullptr);
     }
 }
 
@@ -846,7 +899,8 @@ __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ 
 constexpr int kRrT = 256;
 
 __device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* __restrict__ y2,
-                                int N, long long d, double fdoa, double fs, double* out) {
+                                int N, long long d, double fdoa, double fs, const double* tg,
+                                double* out) {
     __shared__ double2 pbuf[2][kRrT], hbuf[2][kRrT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long kb = d < 0 ? -d : 0;
@@ -855,10 +909,8 @@ __device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* _
         if (tid == 0) *out = 0.0;
         return;
     }
-    const double step = __ddiv_rn(__dmul_rn(kTwoPi, fdoa), fs);
     double rot_im, rot_re, ph_im, ph_re;
-    sincos(step, &rot_im, &rot_re);
-    sincos(__dmul_rn(step, (double)kb), &ph_im, &ph_re);
+    chain_trig(kb, fdoa, fs, tg, &rot_re, &rot_im, &ph_re, &ph_im);
     double acc_re = 0.0, acc_im = 0.0;
     const double2* b = y2 + d;
     const long long n = ke - kb;
@@ -926,7 +978,7 @@ k_rerank_cta(const int* __restrict__ cells, const int* __restrict__ n_cells, int
             y1 = c.y64 + (s * c.R + c.pair_rx[2 * pr]) * c.stride;
             y2 = c.y64 + (s * c.R + c.pair_rx[2 * pr + 1]) * c.stride;
         }
-        exact_chain_cta(y1, y2, c.N, tdoa, fdoa, c.fs, ex + i);
+        exact_chain_cta(y1, y2, c.N, tdoa, fdoa, c.fs, c.trig ? c.trig + 4 * i : nullptr, ex + i);
         __syncthreads();
     }
 }
@@ -1288,7 +1340,7 @@ void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int*
     const int ts = correlate_task_size();
     k_scan<<<1, kScanThreads, 0, st>>>(hist + bin0, nb, ts, off + bin0, toff + bin0, boff + bin0,
                                        cursor + bin0, n_tasks, n_buckets);
-    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, cursor, sorted, fdoa, sfdoa);
+    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, bin0, nb, cursor, sorted, fdoa, sfdoa);
     k_build_tasks<<<blocks_for(nb, 256), 256, 0, st>>>(hist + bin0, nb, bin0, N, ts, off + bin0,
                                                       toff + bin0, boff + bin0, tasks, buckets, ubin, B);
 }
@@ -1328,6 +1380,11 @@ void launch_refine(const int64_t* list, int64_t n, RefineCtx ctx, cudaStream_t s
 void launch_combine_pairs(const double* raw, int S, int pairs, int64_t P, double* grids,
                           cudaStream_t st) {
     k_combine_pairs<<<blocks_for((int64_t)S * P, 256), 256, 0, st>>>(raw, S, pairs, P, grids);
+}
+
+void launch_sum_units(const double* units, int U, int64_t n, const int* step, double* steps,
+                      cudaStream_t st) {
+    if (U > 0 && n > 0) k_sum_units<<<blocks_for(n, 256), 256, 0, st>>>(units, U, n, step, steps);
 }
 
 void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st) {
@@ -1393,6 +1450,11 @@ void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hi
     }
     k_rerank<<<blocks_for((int64_t)cap * SP, 64, 148LL * 64), 64, 0, st>>>(cells, n_cells, cap,
                                                                            SP, ctx, ex, 1);
+}
+
+void launch_chain_offsets(const int* cells, int n, int SP, RefineCtx ctx, dg_pair_offsets* out,
+                          cudaStream_t st) {
+    k_chain_offsets<<<blocks_for((int64_t)n * SP, 128), 128, 0, st>>>(cells, n, SP, ctx, out);
 }
 
 void launch_recombine_cells(const int* n_cells, int cap, const double* ex, int S, int pairs,

@@ -8,14 +8,29 @@ from . import _capi
 from ._capi import check, lib
 
 
-class Engine:
-    """Owns a ``dg_engine`` bound to one CUDA device."""
+def device_count() -> int:
+    n = C.c_int()
+    check(lib.dg_device_count(C.byref(n)))
+    return n.value
 
-    def __init__(self, device: int = 0):
+
+class Engine:
+    """Owns a ``dg_engine`` bound to one CUDA device, or to several
+    (``devices``: one process drives every listed GPU; whole-run solves are
+    sharded across them, dg_engine_create_multi)."""
+
+    def __init__(self, device: int = 0, devices=None):
         h = C.c_void_p()
-        check(lib.dg_engine_create(int(device), C.byref(h)))
+        if devices is not None and len(devices) > 1:
+            arr = (C.c_int * len(devices))(*[int(d) for d in devices])
+            check(lib.dg_engine_create_multi(arr, len(devices), C.byref(h)))
+            self.devices = [int(d) for d in devices]
+        else:
+            dev = int(devices[0]) if devices else int(device)
+            check(lib.dg_engine_create(dev, C.byref(h)))
+            self.devices = [dev]
         self._h = h
-        self.device = int(device)
+        self.device = self.devices[0]
 
     @property
     def handle(self):

@@ -356,6 +356,26 @@ def correlate_steps(grid: CandidateGrid, staged: StagedSnapshots, s_begin: int, 
                 kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
 
 
+def correlate_units(grid: CandidateGrid, staged: StagedSnapshots, units, raw_device: int,
+                    options: GeolocateOptions | None = None, stream=None,
+                    profile: bool = False) -> dict:
+    """Raw surfaces [len(units)][P] (device pointer) of work units (step, part,
+    parts) — dg_correlate_units, the unit-sharded half of geolocate_snapshots."""
+    options = options or GeolocateOptions()
+    res = _capi.dg_result()
+    opt = _options(options, stream, profile)
+    arr = (_capi.dg_work_unit * max(len(units), 1))(
+        *[_capi.dg_work_unit(int(s), int(p), int(n), 0, 0) for s, p, n in units])
+    check(lib.dg_correlate_units(grid.engine.handle, grid.handle, staged.handle, arr, len(units),
+                                 C.byref(opt), C.c_void_p(int(raw_device)), C.byref(res)))
+    return dict(n_refined=res.n_refined, sum_overlap_samples=res.sum_overlap_samples,
+                correlate_ms=res.correlate_ms, moments_ms=res.moments_ms,
+                evaluate_ms=res.evaluate_ms, moment_ffma2=res.moment_ffma2,
+                evaluate_ffma2=res.evaluate_ffma2, direct_steps=res.direct_steps,
+                evaluate_tc_flop=res.evaluate_tc_flop,
+                kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
+
+
 def accumulate_peak(grid: CandidateGrid, staged: StagedSnapshots, grids_device: int,
                     medians_device: int | None = None, options: GeolocateOptions | None = None,
                     **kw) -> GeolocateResult:

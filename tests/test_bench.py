@@ -23,3 +23,17 @@ def test_reference_arm_line():
     assert line["value"] > 0 and line["unit"] == "correlations/s"
     assert line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_plugin_workload_matches_reference():
+    """bench.py regenerates the reference's BenchWorkload (bench.hpp:65-88) bit for bit."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from oracle.bindings import RefLib
+    y1r, y2r, offr, _ = RefLib().build_workload(30_000, 4096, 5e6, 1)
+    y1, y2, off = bench.build_workload(30_000, 4096, 5e6, 1)
+    assert np.array_equal(y1, y1r) and np.array_equal(y2, y2r) and np.array_equal(off, offr)
+    y1r, _, offr, _ = RefLib().build_workload(10_000, 1000, 2e6, 77)
+    y1, _, off = bench.build_workload(10_000, 1000, 2e6, 77)
+    assert np.array_equal(y1, y1r) and np.array_equal(off, offr)

@@ -56,9 +56,14 @@ CASES = {
     "chirp+40": (dict(kind="chirp", snr=40.0), {}),
     "four-20": (dict(kind="four", snr=-20.0), {}),
     "four+20": (dict(kind="four", snr=20.0), {}),
-    "tone+40_B768": (dict(kind="tone", snr=40.0), dict(correlator="moments", moment_block=768)),
+    # block lengths forced, moment count at the edge of its truncation bound
+    # (x = pi h B just below the planner's cap of 3.0: R = 14)
+    "tone+40_B768": (dict(kind="tone", snr=40.0, half_km=450.0),
+                     dict(correlator="moments", moment_block=768)),
     "tone+40_B640": (dict(kind="tone", snr=40.0), dict(correlator="moments", moment_block=640)),
-    "chirp+40_B768": (dict(kind="chirp", snr=40.0), dict(correlator="moments", moment_block=768)),
+    "chirp+40_B768": (dict(kind="chirp", snr=40.0, half_km=450.0),
+                      dict(correlator="moments", moment_block=768)),
+    "tone+40_B512": (dict(kind="tone", snr=40.0), dict(correlator="moments", moment_block=512)),
     "tone+40_1km": (dict(kind="tone", snr=40.0, half_km=200.0, spacing_km=1.0), {}),
     "tone+40_N250k": (dict(kind="tone", snr=40.0, dur=0.05, half_km=500.0), {}),
     "chirp+40_N250k": (dict(kind="chirp", snr=40.0, dur=0.05, half_km=500.0), {}),
@@ -82,6 +87,8 @@ def run_case(b2, ref, name):
     finally:
         eng.reset_tuning()
     e = rel_err(res.accumulated.values, want)
+    if tuning.get("correlator") == "moments":  # the forced block length was admissible
+        assert res.stats["direct_steps"] == 0, (name, res.stats)
     return dict(scene=name, cells=int(e.size), samples=int(sc.n_samples),
                 max_rel=float(e.max()), p99999=float(np.quantile(e, 0.99999)),
                 refined=int(res.stats["n_refined"]), direct_steps=int(res.stats["direct_steps"]),

@@ -8,8 +8,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2508_06672_b200.sharding import (exchange_argmax, exchange_steps, gather_surface,
-                                            merge_argmax, slab_rows, step_range)
+from paper_2508_06672_b200.sharding import (exchange_argmax, exchange_units, gather_surface,
+                                            merge_argmax, shard_plan, slab_rows, step_range)
 
 
 def test_slab_rows_partition():
@@ -30,6 +30,34 @@ def test_step_range_partition():
             rng = [step_range(S, r, world) for r in range(world)]
             assert rng[0][0] == 0 and rng[-1][1] == S
             assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+
+
+@pytest.mark.parametrize("S,R", [(50, 2), (100, 2), (10, 3), (3, 4), (1, 2)])
+def test_shard_plan_balance(S, R):
+    """dg_shard_plan: every step is covered once (a whole unit, or all `world`
+    parts), whole steps are contiguous per rank, and every rank holds the same
+    work to within one whole step when steps >= world."""
+    pairs = R * (R - 1) // 2
+    steps = S * pairs
+    for world in (1, 2, 3, 4, 8):
+        plan = shard_plan(S, R, world)
+        cover = {}
+        for step, part, parts, rank in plan:
+            cover.setdefault(step, []).append((part, parts, rank))
+        assert sorted(cover) == list(range(steps))
+        for step, c in cover.items():
+            if len(c) == 1:
+                assert c[0][:2] == (0, 1)
+            else:
+                assert sorted(p for p, _, _ in c) == list(range(world))
+                assert all(n == world and p == r for p, n, r in c)
+        work = [sum(1.0 / n for _, _, n, r in plan if r == k) for k in range(world)]
+        assert max(work) - min(work) < 1e-9
+        assert abs(sum(work) - steps) < 1e-9
+        whole = shard_plan(S, R, world, whole_snapshots=True)
+        assert [u[0] for u in whole] == list(range(S))
+        assert all(u[3] == k for k in range(world) for u in whole
+                   if step_range(S, k, world)[0] <= u[0] < step_range(S, k, world)[1])
 
 
 def test_merge_argmax_tie_break():
@@ -62,11 +90,18 @@ def _worker(rank, world, port, q):
         sizes = [(slab_rows(n_lat, r, world)[1] - slab_rows(n_lat, r, world)[0]) * n_lon
                  for r in range(world)]
         got = gather_surface(local, sizes)
-        # snapshot-sharded surfaces -> latitude slabs, snapshots in order
+        # unit-sharded surfaces -> latitude slabs: whole steps and the disjoint
+        # parts of the remainder steps sum back to every step exactly
         S = 5
-        allsteps = torch.arange(S * n_lat * n_lon, dtype=torch.float64).view(S, -1)
-        s0, s1 = step_range(S, rank, world)
-        slab = exchange_steps(allsteps[s0:s1].clone(), S, n_lat, n_lon)
+        allsteps = torch.arange(S * n_lat * n_lon, dtype=torch.float64).view(S, -1) + 0.5
+        plan = shard_plan(S, 2, world)
+        mine = [u for u in plan if u[3] == rank]
+        local = torch.zeros((len(mine), n_lat * n_lon), dtype=torch.float64)
+        cells = torch.arange(n_lat * n_lon)
+        for i, (step, part, parts, _) in enumerate(mine):
+            keep = (cells % parts) == part
+            local[i][keep] = allsteps[step][keep]
+        slab = exchange_units(local, plan, rank, world, n_lat, n_lon, S)
         ok_steps = bool(torch.equal(slab, allsteps[:, r0 * n_lon:r1 * n_lon]))
         q.put((rank, peak, bool(torch.equal(got, full)) and ok_steps))
     finally:
