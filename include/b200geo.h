@@ -109,7 +109,8 @@ typedef struct {
     int moment_count;        /* 0 = planner's choice, else 8/10/12/14/16 */
     int evaluate_tensor;     /* 1: block sums on tcgen05 where they fit; 0: FFMA2 block loop */
     double refine_tau;       /* FP64 re-evaluation threshold of the moment path (0 = default) */
-    int allow_weaker_refine; /* permit refine_tau below the default (error-model studies only) */
+    int allow_weaker_refine; /* permit thresholds below the defaults (error-model studies only) */
+    double direct_refine_tau; /* the same for the direct correlator (0 = default) */
 } dg_tuning;
 void dg_tuning_default(dg_tuning* t);
 int dg_engine_set_tuning(dg_engine* engine, const dg_tuning* t);

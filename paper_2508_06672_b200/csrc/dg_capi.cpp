@@ -58,6 +58,7 @@ struct dg_session {
     double fs = 0;
     std::unique_ptr<DevMem> y32;  // float2 [2][stride]
     std::unique_ptr<DevMem> y64;  // double2 [2][stride]
+    std::unique_ptr<DevMem> e64;  // double [2][N+1]: prefix sums of |y|^2
     cudaStream_t st = nullptr;
     ~dg_session() {
         if (st) cudaStreamDestroy(st);
@@ -99,13 +100,22 @@ double jacobi_anger_tail(double x, int R) {
     return q < 1.0 ? t / (1.0 - q) : INFINITY;
 }
 
-constexpr double kMomentTail = 1e-8;
+// Truncation budget. Per block the Jacobi-Anger remainder is bounded by
+// tail(x, R) times the block's L1 norm, and a product stream that repeats with
+// the block length (e.g. a chirp product tone aliasing onto B) adds those
+// remainders coherently, so a candidate's truncation error is only bounded by
+// tail * ||z||_1 <= tail * sqrt(N) ||z||_2, while unrefined values are at least
+// tau ||z||_2 (the refinement test's noise scale). tail <= kTailBudget tau /
+// sqrt(N) keeps that term below 2e-6 relative (1/10 of the parity budget):
+// 1.8e-10 at N = 50,000 (R = 16 at C3's x = 2.94; a +40 dB chirp at the 1e-8
+// tail used before reached 6.5e-5, tests/test_gpu_error_model.py).
+constexpr double kTailBudget = 2e-6;
 // Largest Jacobi-Anger argument x = pi h B the planner admits. Past it the
 // coefficients a_m(x) grow and the block sums cancel more, so the FP32
 // evaluation error of sidelobe candidates in coherent buckets rises faster
 // than the refinement test tracks (measured on +40 dB tone / chirp scenes:
 // B = 768 at x = 3.5 reached 1.4e-4, B = 640 at x = 2.9 stayed at 3e-5;
-// tests/test_gpu_error_model.py). Below it R <= 14 always meets kMomentTail.
+// tests/test_gpu_error_model.py).
 constexpr double kMomentXMax = 3.0;
 constexpr size_t kEvalSmemMax = 200 * 1024;  // k_evaluate stages two buckets of moments
 constexpr int kMomentR[] = {8, 10, 12, 14, 16};
@@ -136,6 +146,7 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
     pl.nu_c = 0.5 * (nu_lo + nu_hi);
     const double half = 0.5 * (nu_hi - nu_lo) * (1.0 + 1e-9) + 1e-15;
     const double avg = (double)P_plan / d_span;  // candidates per TDOA bucket (approx.)
+    const double tail_max = kTailBudget * kMomentRefineTau / std::sqrt((double)N);
     // costs in FP32x2-MAC units per bucket: direct ~2.3 per candidate-sample;
     // moments R per sample (x1.5 for smem traffic) + (R + 5) per candidate-block
     double best = 2.3 * avg * N;
@@ -150,7 +161,7 @@ StepPlan plan_step(const StepRange& r, const StepRange* a, double a_margin_hz, i
         for (int R : kMomentR) {
             if (forceR && R != forceR) continue;
             // a forced R is used only where it meets the truncation bound too
-            if (jacobi_anger_tail(x, R) > kMomentTail) continue;
+            if (jacobi_anger_tail(x, R) > tail_max) continue;
             if (evaluate_smem_bytes(((N + B - 1) / B + kEvalG - 1) / kEvalG * kEvalG, R) >
                 kEvalSmemMax)
                 break;
@@ -245,7 +256,7 @@ struct Pipeline {
     // candidate block sums run on the tensor cores (dg_evaluate_tc.cu) or the
     // FFMA2 block loop (k_evaluate)
     dg_tuning tn{};
-    float tau = kMomentRefineTau;
+    float tau = kMomentRefineTau, tau_direct = kRefineTau;
     bool use_tc = true;
 
     ~Pipeline() {
@@ -262,6 +273,7 @@ struct Pipeline {
             tn = eng->tuning;
         }
         tau = tn.refine_tau > 0.0 ? (float)tn.refine_tau : kMomentRefineTau;
+        tau_direct = tn.direct_refine_tau > 0.0 ? (float)tn.direct_refine_tau : kRefineTau;
         use_tc = tn.evaluate_tensor != 0;
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
@@ -478,9 +490,10 @@ struct Pipeline {
 
     // phase B for slot s on lane s % n_lanes. y1_64 is the exact capture
     // (centring source).
-    void correlate(int s, const double2* y1_64, const float2* y1, const float2* y2, double fs,
-                   double* s_out, uint32_t* bits, int64_t flag_base, cudaEvent_t ev0,
-                   cudaEvent_t ev1, cudaEvent_t ev2) {
+    // e1 / e2: the captures' |y|^2 prefix sums (launch_energy_prefix)
+    void correlate(int s, const double2* y1_64, const float2* y1, const float2* y2,
+                   const double* e1, const double* e2, double fs, double* s_out, uint32_t* bits,
+                   int64_t flag_base, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t ev2) {
         const StepPlan& pl = plans[s];
         Lane& L = lanes[s % n_lanes];
         cudaStream_t st = L.st;
@@ -496,7 +509,7 @@ struct Pipeline {
             if (ev0) CK(cudaEventRecord(ev0, st));
             if (ev1) CK(cudaEventRecord(ev1, st));
             launch_correlate(L.tasks, L.n_tasks, max_tasks, L.sorted, fdoa_slot(s), y1, y2, N, fs,
-                             s_out, bits, flag_base, st);
+                             s_out, bits, flag_base, tau_direct, st);
             launches += 4;
             ++direct_steps;
         } else {
@@ -514,12 +527,12 @@ struct Pipeline {
                 launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
                                    (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
                                    nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
-                                   sm_count, st);
+                                   e1, e2, N, sm_count, st);
             else
                 launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
                                 (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
-                                nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
-                                sm_count, st);
+                                nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau, e1,
+                                e2, N, sm_count, st);
             launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, tc ? 1 : 0, L.work, st);
             launches += 7;
         }
@@ -551,6 +564,7 @@ int64_t run_refine(Scratch& sc, const uint32_t* bits, int64_t n_elems, const Ref
 // runs on the FP64 pipes while the lanes correlate later steps.
 // K = 0: everything refined at the end on the main stream (profiled runs).
 struct SideRefine {
+    static constexpr int kSerialBatch = 10;  // steps per batch of the K = 0 mode
     Scratch& sc;
     int steps, K;
     int64_t P, P32;
@@ -563,10 +577,10 @@ struct SideRefine {
     bool own_rs = false;
     SideRefine(Scratch& s, int n_steps, int64_t P_, int64_t P32_, int K_, cudaStream_t side)
         : sc(s), steps(n_steps), K(K_), P(P_), P32(P32_) {
-        const int nb = K > 0 ? steps : 1;  // at most one batch per step
+        const int nb = steps;  // at most one batch per step
         counts = sc.alloc<unsigned long long>(nb);
         CK(cudaMemsetAsync(counts, 0, nb * sizeof(unsigned long long), sc.st));
-        list = sc.alloc<int64_t>((size_t)(K > 0 ? std::min(K, steps) : steps) * P32);
+        list = sc.alloc<int64_t>((size_t)std::min(K > 0 ? K : kSerialBatch, steps) * P32);
         if (K > 0) {
             rs = side;
             if (!rs) {
@@ -606,8 +620,9 @@ struct SideRefine {
         }
     }
     void finish(const uint32_t* bits, const RefineCtx& ctx) {
-        if (K <= 0) {
-            launch_batch(bits, ctx, 0, steps, sc.st);
+        if (K <= 0) {  // profiled runs: everything at the end, on the main stream
+            for (int r0 = 0; r0 < steps; r0 += kSerialBatch)
+                launch_batch(bits, ctx, r0, std::min(steps, r0 + kSerialBatch), sc.st);
             return;
         }
         if (next < steps) {
@@ -740,6 +755,13 @@ int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
             raise(DG_EINVAL, "dg_tuning: unsupported moment count " + std::to_string(t->moment_count));
         if (!(t->refine_tau >= 0.0) || !std::isfinite(t->refine_tau))
             raise(DG_EINVAL, "dg_tuning: refine_tau must be finite and >= 0");
+        if (!(t->direct_refine_tau >= 0.0) || !std::isfinite(t->direct_refine_tau))
+            raise(DG_EINVAL, "dg_tuning: direct_refine_tau must be finite and >= 0");
+        if (t->direct_refine_tau > 0.0 && t->direct_refine_tau < kRefineTau &&
+            !t->allow_weaker_refine)
+            raise(DG_EINVAL, "dg_tuning: direct_refine_tau below the default " +
+                                 std::to_string(kRefineTau) +
+                                 " weakens the 1e-4 contract (set allow_weaker_refine)");
         if (t->refine_tau > 0.0 && t->refine_tau < kMomentRefineTau && !t->allow_weaker_refine)
             raise(DG_EINVAL, "dg_tuning: refine_tau below the default " +
                                  std::to_string(kMomentRefineTau) +
@@ -851,6 +873,8 @@ int dg_stage(dg_engine* eng, const double* y1, int64_t n1, double fs1, const dou
         CK(cudaMemcpyAsync(y64 + s->stride, y2, n1 * sizeof(double2), cudaMemcpyHostToDevice, s->st));
         launch_f64_to_f32(y64, y32, n1, s->st);
         launch_f64_to_f32(y64 + s->stride, y32 + s->stride, n1, s->st);
+        s->e64 = std::make_unique<DevMem>(2 * (n1 + 1) * sizeof(double));
+        launch_energy_prefix(y64, s->stride, 2, n1, static_cast<double*>(s->e64->p), s->st);
         CK(cudaStreamSynchronize(s->st));
         *out = s.release();
     });
@@ -866,6 +890,8 @@ int dg_stage_f32(dg_engine* eng, const float* y1, int64_t n1, double fs1, const 
         CK(cudaMemcpyAsync(y32 + s->stride, y2, n1 * sizeof(float2), cudaMemcpyHostToDevice, s->st));
         launch_f32_to_f64(y32, y64, n1, s->st);
         launch_f32_to_f64(y32 + s->stride, y64 + s->stride, n1, s->st);
+        s->e64 = std::make_unique<DevMem>(2 * (n1 + 1) * sizeof(double));
+        launch_energy_prefix(y64, s->stride, 2, n1, static_cast<double*>(s->e64->p), s->st);
         CK(cudaStreamSynchronize(s->st));
         *out = s.release();
     });
@@ -897,7 +923,9 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         pl.plan_window(sc, 1, s->fs);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
-        pl.correlate(0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+        const double* e64 = static_cast<const double*>(s->e64->p);
+        pl.correlate(0, y64, y32, y32 + s->stride, e64, e64 + (s->N + 1), s->fs, vals, bits, 0,
+                     nullptr, nullptr,
                      nullptr);
         RefineCtx ctx{};
         ctx.P = n;
@@ -1147,7 +1175,9 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         pl.plan_window(sc, 1, s->fs, approx, fp32_fdoa_margin(&h, 1, wl), g->full_size);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
         const auto* y64 = static_cast<const double2*>(s->y64->p) + kCapturePad;
-        pl.correlate(0, y64, y32, y32 + s->stride, s->fs, vals, bits, 0, nullptr, nullptr,
+        const double* e64 = static_cast<const double*>(s->e64->p);
+        pl.correlate(0, y64, y32, y32 + s->stride, e64, e64 + (s->N + 1), s->fs, vals, bits, 0,
+                     nullptr, nullptr,
                      nullptr);
         check_err_flag(sc, pl.err);
         static const int pair_rx[2] = {0, 1};
@@ -1610,6 +1640,24 @@ dg_options options_or_default(const dg_options* o) {
     return opt;
 }
 
+// the run's per-capture |y|^2 prefix sums, made on first use: behind the
+// capture upload on the engine's upload stream when staging is still in flight
+// (the correlator lanes wait for it with the captures), else on st; st (and so
+// everything ordered after it) waits for them
+const double* energy_prefix(const dg_staged* sn, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(sn->e_mu);
+    if (!sn->e64) {
+        cudaStream_t es = sn->ready ? sn->eng->upload : st;
+        auto e = std::make_unique<DevMem>(sn->S * sn->R * (sn->N + 1) * sizeof(double));
+        launch_energy_prefix(static_cast<const double2*>(sn->y64->p) + kCapturePad, sn->stride,
+                             sn->S * sn->R, sn->N, static_cast<double*>(e->p), es);
+        CK(cudaEventCreateWithFlags(&sn->e_ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(sn->e_ready, es));
+        sn->e64 = std::move(e);
+    }
+    return static_cast<const double*>(sn->e64->p);
+}
+
 // Units over the whole grid g: geometry, correlation, exact refinement -> raw
 // surfaces [n_units][P] (device). The step-sharded half of geolocate_snapshots
 // and, with every step of a snapshot range, the
@@ -1655,6 +1703,7 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
 
     Pipeline pl;
     pl.init(sc, eng, P, sn->N, SPl, opt.profile ? 1 : 2, eng->lane);
+    const double* e64 = energy_prefix(sn, st);
     // refine flags: one bitmap row of whole words per unit (bit p of unit i at
     // i * P32 + p), so batches of units are refined on a side stream while the
     // lanes correlate later units (FP64 refinement next to FP32 correlation)
@@ -1692,13 +1741,18 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         std::vector<StepUnit> wunits(units.begin() + w0, units.begin() + w0 + nw);
         pl.plan_window(sc, nw, fs, approx, fp32_fdoa_margin(hw, nw, wl), g->full_size,
                        /*exact_ranges=*/false, &wunits);
-        if (w0 == 0 && sn->ready) pl.wait_event(sn->ready);  // captures still uploading
+        if (w0 == 0) {  // captures still uploading / their energy sums
+            if (sn->ready) pl.wait_event(sn->ready);
+            pl.wait_event(sn->e_ready);
+        }
         for (int i = 0; i < nw; ++i) {  // phase B: bucket + correlate each unit
             const int lsp = w0 + i, sp = units[lsp].sp;
             const int s = sp / pairs, q = sp - s * pairs;
             const int64_t c1 = ((int64_t)s * R + geo.prx[2 * q]) * sn->stride;
             const int64_t c2 = ((int64_t)s * R + geo.prx[2 * q + 1]) * sn->stride;
-            pl.correlate(i, y64 + c1, y32 + c1, y32 + c2, fs, raw + (int64_t)lsp * P, bits,
+            const int64_t r1 = (int64_t)s * R + geo.prx[2 * q], r2 = (int64_t)s * R + geo.prx[2 * q + 1];
+            pl.correlate(i, y64 + c1, y32 + c1, y32 + c2, e64 + r1 * (sn->N + 1),
+                         e64 + r2 * (sn->N + 1), fs, raw + (int64_t)lsp * P, bits,
                          (int64_t)lsp * P32, opt.profile ? evs[3 * lsp] : nullptr,
                          opt.profile ? evs[3 * lsp + 1] : nullptr,
                          opt.profile ? evs[3 * lsp + 2] : nullptr);
@@ -2091,7 +2145,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     check_run(eng, g, sn, opt, res);
     set_device(eng);
     StreamGuard sg(opt.stream, eng->stream);
-    Scratch sc(sg.st);
+    Scratch sc(sg.st, &eng->arena);
     reset_stats(res);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (opt.profile) {
@@ -2238,7 +2292,7 @@ void geolocate_multi(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         set_device(e);
         gk[k] = grid_on(g, e);
         sk[k] = staged_on(sn, e);
-        scr[k] = std::make_unique<Scratch>(e->stream);
+        scr[k] = std::make_unique<Scratch>(e->stream, &e->arena);
         Scratch& sc = *scr[k];
         geo[k] = make_geo(sc, sk[k]);
         std::memset(&part[k], 0, sizeof(dg_result));
@@ -2418,7 +2472,7 @@ int dg_correlate_steps(dg_engine* eng, const dg_grid* g, const dg_staged* sn, in
             raise(DG_EINVAL, "dg_correlate_steps: normalisation needs a medians buffer");
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
-        Scratch sc(sg.st);
+        Scratch sc(sg.st, &eng->arena);
         reset_stats(res);
         const RunGeo geo = make_geo(sc, sn);
         correlate_steps_impl(eng, g, sn, geo, (int)s_begin, (int)s_end, opt, grids_device,
@@ -2450,7 +2504,7 @@ int dg_correlate_units(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
             raise(DG_EINVAL, "dg_correlate_units: null units / surfaces");
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
-        Scratch sc(sg.st);
+        Scratch sc(sg.st, &eng->arena);
         reset_stats(res);
         const RunGeo geo = make_geo(sc, sn);
         std::vector<StepUnit> u(n_units);
@@ -2470,7 +2524,7 @@ int dg_accumulate_peak(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
             raise(DG_EINVAL, "dg_accumulate_peak: null grids");
         set_device(eng);
         StreamGuard sg(opt.stream, eng->stream);
-        Scratch sc(sg.st);
+        Scratch sc(sg.st, &eng->arena);
         reset_stats(res);
         const RunGeo geo = make_geo(sc, sn);
         peak_impl(eng, g, sn, geo, grids_device,

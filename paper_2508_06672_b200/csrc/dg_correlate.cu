@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(32 * WPC, MINB)
 k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
             const int* __restrict__ sorted, const double* __restrict__ fdoa,
             const float2* __restrict__ y1, const float2* __restrict__ y2, int N, double fs,
-            double* __restrict__ s_out, uint32_t* __restrict__ flag_bits, int64_t flag_base) {
+            double* __restrict__ s_out, uint32_t* __restrict__ flag_bits, int64_t flag_base,
+            float tau) {
     using WarpSmem = WarpSmemT<CH>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,12 +120,16 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
 
     // this candidate's FP32 error scale: the block sums round relative to the
     // blocks (eb = sum_b |C_b|^2), the Horner chunk sums relative to the chunks
-    // (e2 = sum_c |chunk sum|^2). For noise both are ||z||_2^2; a tone at the
-    // candidate's frequency makes the chunk term CH/LB x larger, a chirp off its
-    // TDOA (coherent within blocks, not within chunks) the block term.
+    // (e2 = sum_c |chunk sum|^2), the phasor tables' rounding relative to the
+    // samples (z2 = ||z||_2^2, shared by the warp). For noise all three are
+    // ||z||_2^2; a tone at the candidate's frequency makes the chunk term CH/LB x
+    // larger, a chirp off its TDOA (coherent within blocks, not within chunks)
+    // the block term, and a product tone that aliases onto the block length
+    // (block sums cancel, the tables' systematic errors add up) needs the floor.
     double acc_re[NC], acc_im[NC], e2[NC], eb[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc_re[c] = acc_im[c] = e2[c] = eb[c] = 0.0;
+    float z2 = 0.f;
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int buf = ch & 1;
         const int c0 = kb0 + ch * CH;
@@ -149,6 +154,7 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
             zz.y = v0 ? fmaf(a.y, b0.x, -(a.x * b0.y)) : 0.f;
             zz.z = v1 ? fmaf(a.z, b1.x, a.w * b1.y) : 0.f;
             zz.w = v1 ? fmaf(a.w, b1.x, -(a.z * b1.y)) : 0.f;
+            z2 = fmaf(zz.x, zz.x, fmaf(zz.y, zz.y, fmaf(zz.z, zz.z, fmaf(zz.w, zz.w, z2))));
             zq[q] = zz;
         }
         __syncwarp();
@@ -211,11 +217,13 @@ k_correlate(const Task* __restrict__ tasks, const int* __restrict__ n_tasks,
     }
 
 #pragma unroll
+    for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
+#pragma unroll
     for (int c = 0; c < NC; ++c) {
         if (p[c] < 0) continue;
         const double s = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
         s_out[p[c]] = s;
-        if (s < (double)kRefineTau * sqrt(fmax(e2[c], eb[c]))) {
+        if (s < (double)tau * sqrt(fmax(fmax(e2[c], eb[c]), (double)z2))) {
             const int64_t e = flag_base + p[c];
             atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
         }
@@ -227,14 +235,15 @@ namespace {
 template <int NC, int LB, int CH, int WPC, int MINB>
 void launch_variant(int n_tasks_max, cudaStream_t st, const Task* tasks, const int* n_tasks,
                     const int* sorted, const double* fdoa, const float2* y1, const float2* y2,
-                    int N, double fs, double* s_out, uint32_t* flag_bits, int64_t flag_base) {
+                    int N, double fs, double* s_out, uint32_t* flag_bits, int64_t flag_base,
+                    float tau) {
     auto kern = k_correlate<NC, LB, CH, WPC, MINB>;
     const size_t smem = sizeof(WarpSmemT<CH>) * WPC;
     static size_t attr[64] = {};
     ensure_smem(kern, smem, attr);
     const int blocks = (n_tasks_max + WPC - 1) / WPC;
     kern<<<blocks, 32 * WPC, smem, st>>>(tasks, n_tasks, sorted, fdoa, y1, y2, N, fs, s_out,
-                                         flag_bits, flag_base);
+                                         flag_bits, flag_base, tau);
 }
 
 }  // namespace
@@ -245,10 +254,11 @@ int correlate_task_size() { return 64; }
 
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
-                      double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st) {
+                      double* s_out, uint32_t* flag_bits, int64_t flag_base, float tau,
+                      cudaStream_t st) {
     if (max_tasks <= 0) return;
     launch_variant<2, 16, 256, 4, 3>(max_tasks, st, tasks, n_tasks, sorted, fdoa, y1, y2, N, fs,
-                                     s_out, flag_bits, flag_base);
+                                     s_out, flag_bits, flag_base, tau);
 }
 
 }  // namespace dg

@@ -119,6 +119,25 @@ __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
     }
 }
 
+// a bucket's ||z||_2^2 estimate from the captures' |y|^2 prefix sums: sum over its
+// blocks (absolute index, length B, clipped to the overlap [kb, ke)) of
+// E1_b E2_b / len_b — exact when either capture has a constant envelope within
+// a block; the moment path's refinement floor. Threads t < nt of a group each
+// take blocks t, t + nt, ...; the caller reduces the partial sums in order.
+__device__ __forceinline__ double bucket_z2_part(const double* __restrict__ e1,
+                                                 const double* __restrict__ e2, int N, int d,
+                                                 int B, int t, int nt) {
+    const int kb = d < 0 ? -d : 0, ke = d > 0 ? N - d : N;
+    double acc = 0.0;
+    for (int b = kb / B + t; b * B < ke; b += nt) {
+        const int lo = max(kb, b * B), hi = min(ke, (b + 1) * B);
+        if (lo >= hi) continue;
+        const double E1 = e1[hi] - e1[lo], E2 = e2[hi + d] - e2[lo + d];
+        acc = fma(E1, E2 / (double)(hi - lo), acc);
+    }
+    return acc;
+}
+
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
     float2 d;
     asm("{.reg .b64 ra, rb, rd;\n\t"

@@ -24,7 +24,7 @@
 // (two tcgen05.ld.32x32b.x16) and runs the group sums as
 // k_evaluate does: A, V, |C_b|^2 on FFMA2 with W_j = W_1^j (FP64 recurrence,
 // rounded once), FP64 anchors across groups, refinement flag
-// S < tau max(sqrt(sum |C_b|^2), Q).
+// S < tau max(sqrt(sum |C_b|^2), sqrt(sum_m a_m^2 Q_m^2), ||z||_2).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -157,7 +157,8 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
               int* __restrict__ queue, const int* __restrict__ sorted,
               const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p,
               int B, const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
-              uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
+              uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau,
+              const double* __restrict__ e1, const double* __restrict__ e2, int N) {
     constexpr int G = kTcG;
     static_assert(R <= kTcK && R % 2 == 0, "moments");
     const TcLayout L = tc_layout(nbmax, R);
@@ -169,7 +170,8 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
     __shared__ uint64_t full[kTcStages], empty[kTcStages], mma_bar;
     __shared__ int slot_u[kTcStages];
     __shared__ uint32_t tmem_base_s;
-    __shared__ float q2s;
+    __shared__ float qm2[kTcK];  // Q_m^2 = sum_b |M_m[b]|^2 of the bucket
+    __shared__ double z2w[kTcThreads / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nbk = *n_buckets;
@@ -238,15 +240,21 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         const float2* mb = ring + sl * L.ring_f2;
         const int ng = (nb + G - 1) / G;
         const int np = 2 * G * ng;  // B rows / TMEM columns used by this bucket
-        if (warp == 0) {  // Q = ||M_0||_2 (fixed order, as k_evaluate)
+        for (int m = warp; m < R; m += kTcThreads / 32) {  // Q_m^2, fixed order
             float q2 = 0.f;
             for (int b = lane; b < nb; b += 32) {
-                const float2 v = mb[b * R];
+                const float2 v = mb[b * R + m];
                 q2 = fmaf(v.x, v.x, fmaf(v.y, v.y, q2));
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-            if (lane == 0) q2s = q2;
+            if (lane == 0) qm2[m] = q2;
+        }
+        {  // ||z||_2^2 of the bucket (the floor of the error scale), fixed order
+            double z2 = bucket_z2_part(e1, e2, N, bk.d, B, tid, kTcThreads);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) z2 += __shfl_xor_sync(0xffffffffu, z2, o);
+            if (lane == 0) z2w[warp] = z2;
         }
         // B operand: per (block b, K chunk c) the rows 2b (Re) and 2b + 1 (Im),
         // columns 8c .. 8c + 7, three BF16 parts; zeros beyond nb / R
@@ -279,7 +287,9 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         }
         __syncthreads();
         if (tid == 0) mbar_arrive(&empty[sl]);  // the ring slot is free again
-        const double qscale = sqrt((double)q2s);
+        double zfloor = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTcThreads / 32; ++w) zfloor += z2w[w];
 
         for (int t0 = 0; t0 < bk.count; t0 += 128) {
             const double nu = p >= 0 ? fd / fs - nu_c : 0.0;
@@ -292,6 +302,9 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             // warps without a candidate in this tile skip the Bessel terms and the
             // epilogue (their A rows are zero); tcgen05.ld stays warp-uniform
             const bool warp_live = __any_sync(0xffffffffu, pc >= 0);
+            // the moments' own FP32 rounding as this candidate's block sums inherit
+            // it: sqrt(sum_m a_m^2 Q_m^2)
+            double qe2 = 0.0;
             // ---- A operand: this thread's candidate, c_m rounded to FP32 (as the
             // FFMA2 path) and split exactly into three BF16 parts ----
             {
@@ -302,8 +315,10 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                     double jv[R];
                     bessel_j<R>(3.141592653589793 * nu * (double)B, jv);
 #pragma unroll
-                    for (int m = 0; m < R; ++m)
+                    for (int m = 0; m < R; ++m) {
                         cf[m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
+                        qe2 = fma((double)cf[m] * cf[m], (double)qm2[m], qe2);
+                    }
                 }
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -412,7 +427,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             if (pc >= 0) {
                 const double sv = sqrt(acc_re * acc_re + acc_im * acc_im);
                 s_out[pc] = sv;
-                if (sv < (double)tau * fmax(sqrt(en), qscale)) {
+                if (sv < (double)tau * sqrt(fmax(fmax(en, qe2), zfloor))) {
                     const int64_t e = flag_base + pc;
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
@@ -431,7 +446,8 @@ template <int R>
 void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                          const int* sorted, const double* fdoa, double fs, const double* nu_c,
                          int B, const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
-                         int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
+                         int64_t flag_base, float tau, const double* e1, const double* e2, int N,
+                         int sm_count, cudaStream_t st) {
     auto kern = k_evaluate_tc<R>;
     const TcLayout L = tc_layout(nbmax, R);
     // CTAs per SM bounded by TMEM (512 columns per SM): request enough shared
@@ -450,7 +466,7 @@ void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue
     int grid = sm_count * resident;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
     kern<<<grid, kTcThreads, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c, B, mom,
-                                         nbmax, s_out, flag_bits, flag_base, tau);
+                                         nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N);
 }
 
 }  // namespace
@@ -463,11 +479,11 @@ bool evaluate_tc_supported(int nbmax, int R) {
 void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                        uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
-                        cudaStream_t st) {
+                        uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
+                        const double* e2, int N, int sm_count, cudaStream_t st) {
 #define DG_TC_CASE(RR)                                                                          \
     evaluate_tc_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
-                            mom, nbmax, s_out, flag_bits, flag_base, tau, sm_count, st)
+                            mom, nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N, sm_count, st)
     switch (R) {
         case 8: DG_TC_CASE(8); break;
         case 10: DG_TC_CASE(10); break;

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <exception>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -70,21 +71,71 @@ struct DevMem {
     DevMem& operator=(const DevMem&) = delete;
 };
 
-// stream-ordered scratch for one call
+// Engine-owned device workspace of the run drivers: one allocation reused by
+// every call, grown to the previous calls' high-water mark, so a solve never
+// waits in the host for the stream-ordered pool to grow by gigabytes
+// (intermittent 3-600 ms stalls at C5 in r01). One call at a time uses it
+// (try_lock); a concurrent call on the same engine takes pool memory instead.
+struct Arena {
+    std::mutex mu;
+    char* base = nullptr;
+    size_t cap = 0, want = 0;
+    ~Arena() {
+        if (base) cudaFree(base);
+    }
+};
+
+// scratch for one call: bump allocation in the engine's arena when it holds
+// it, else stream-ordered pool memory
 struct Scratch {
     cudaStream_t st;
     std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t s) : st(s) {}
+    Arena* arena = nullptr;
+    size_t used = 0, total = 0;
+    explicit Scratch(cudaStream_t s, Arena* a = nullptr) : st(s) {
+        if (a && a->mu.try_lock()) {
+            arena = a;
+            if (a->want > a->cap) {  // grow to the last call's need (calls are synchronous)
+                if (a->base) CK(cudaFree(a->base));
+                a->base = nullptr;
+                a->cap = 0;
+                // the pool memory those calls took goes back to the driver first
+                int dev = 0;
+                cudaMemPool_t pool;
+                CK(cudaGetDevice(&dev));
+                CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+                CK(cudaDeviceSynchronize());
+                CK(cudaMemPoolTrimTo(pool, 0));
+                void* p = nullptr;
+                CK(cudaMalloc(&p, a->want));
+                a->base = static_cast<char*>(p);
+                a->cap = a->want;
+            }
+        }
+    }
     template <class T>
     T* alloc(size_t n) {
-        void* p = nullptr;
         if (n == 0) n = 1;
+        const size_t bytes = (n * sizeof(T) + 255) & ~size_t(255);
+        total += bytes;
+        if (arena && used + bytes <= arena->cap) {
+            void* p = arena->base + used;
+            used += bytes;
+            return static_cast<T*>(p);
+        }
+        void* p = nullptr;
         CK(cudaMallocAsync(&p, n * sizeof(T), st));
         ptrs.push_back(p);
         return static_cast<T*>(p);
     }
     ~Scratch() {
         for (void* p : ptrs) cudaFreeAsync(p, st);
+        if (arena) {
+            // an error may leave work queued on the arena: finish it first
+            if (std::uncaught_exceptions() > 0) cudaDeviceSynchronize();
+            if (total > arena->want) arena->want = total;
+            arena->mu.unlock();
+        }
     }
 };
 
@@ -128,6 +179,7 @@ struct dg_engine {
     // 64 KB queued behind capture uploads on the copy engine)
     std::mutex tables_mu;
     std::unique_ptr<dg::DevMem> tables;
+    dg::Arena arena;  // workspace of the whole-run drivers
     // pinned double buffer of the file writers (dg_io.cpp), kept across calls
     std::mutex stage_mu;
     void* stage_host[2] = {nullptr, nullptr};
@@ -182,8 +234,14 @@ struct dg_staged {
     std::unique_ptr<dg::DevMem> y32, y64;
     std::vector<dg_state> states;
     cudaEvent_t ready = nullptr;  // async staging: the upload's completion
+    // per capture [S*R][N+1] exclusive prefix sums of |y|^2 (FP64), made on first
+    // use (the moment path's refinement floor, launch_energy_prefix)
+    mutable std::mutex e_mu;
+    mutable std::unique_ptr<dg::DevMem> e64;
+    mutable cudaEvent_t e_ready = nullptr;
     ~dg_staged() {
         if (ready) cudaEventDestroy(ready);
+        if (e_ready) cudaEventDestroy(e_ready);
     }
 };
 

@@ -83,10 +83,13 @@ inline int64_t capture_stride(int64_t n) {
 }
 constexpr int kL = 16;       // phasor table length (samples per inner block)
 
-// Threshold on S / sqrt(max(sum_chunks |chunk sum|^2, sum_blocks |block sum|^2))
-// below which a direct-correlator FP32 value is re-evaluated exactly
-// (dg_correlate.cu); see DESIGN.md "Parity" for the error model behind it.
-constexpr float kRefineTau = 0.02f;
+// Threshold on S / sqrt(max(sum_chunks |chunk sum|^2, sum_blocks |block sum|^2,
+// ||z||_2^2)) below which a direct-correlator FP32 value is re-evaluated exactly
+// (dg_correlate.cu); see DESIGN.md "Parity" for the error model behind it. The
+// +40 dB chirp scenes, whose product tones alias onto the 16-sample blocks,
+// showed ~1e-6 ||z||_2 errors (tests/gpu_error_diag.py): 0.04 -> 2.5e-5, 0.06
+// keeps them near 1.7e-5 (tests/test_gpu_error_model.py).
+constexpr float kRefineTau = 0.06f;
 // block-moment correlator: S < tau * max(sqrt(A), Q). Worst
 // unrefined relative error on the stress scenes of tests/test_gpu_error_model.py
 // (+30/+40 dB tone and chirp, forced block lengths at the truncation edge) vs the
@@ -113,6 +116,10 @@ void launch_geometry_steps(const double* x, const double* y, const double* z, in
                            const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
                            double* fdoa_out, int* hist, int nbins, double* s_out,
                            unsigned long long* overlap, int* err, cudaStream_t st);
+// per capture (n_caps rows of `stride` elements) the exclusive prefix sums of
+// |y|^2 in FP64: out[c][k], k <= N
+void launch_energy_prefix(const double2* y, int64_t stride, int64_t n_caps, int64_t N,
+                          double* out, cudaStream_t st);
 // exact TDOA range (first / last non-empty bin) of each of n_steps histograms
 void launch_hist_range(const int* hist, int nbins, int n_steps, int N, StepRange* out,
                        cudaStream_t st);
@@ -139,7 +146,8 @@ void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int*
 int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,
                       const double* fdoa, const float2* y1, const float2* y2, int N, double fs,
-                      double* s_out, uint32_t* flag_bits, int64_t flag_base, cudaStream_t st);
+                      double* s_out, uint32_t* flag_bits, int64_t flag_base, float tau,
+                      cudaStream_t st);
 
 // block-moment correlator (dg_moments.cu)
 void launch_center(const double2* y, const float2* y2, int N, const double* nu_c, float2* y1c,
@@ -154,11 +162,12 @@ void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bi
 // per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue);
 // sfdoa = the candidates' FDOA in bucket order (launch_bucket's sfdoa)
 size_t evaluate_smem_bytes(int nbmax, int R);
+// e1 / e2: the two captures' |y|^2 prefix sums (launch_energy_prefix), N samples
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                      int max_buckets, const int* sorted, const double* fdoa, double fs,
                      const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                     uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
-                     cudaStream_t st);
+                     uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
+                     const double* e2, int N, int sm_count, cudaStream_t st);
 
 // surface writers (dg_writers.cu): "%.17g" text in kFmtSlot-byte slots, CSV rows
 // at scanned offsets, P5 pixels
@@ -213,8 +222,8 @@ bool evaluate_tc_supported(int nbmax, int R);
 void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                        uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
-                        cudaStream_t st);
+                        uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
+                        const double* e2, int N, int sm_count, cudaStream_t st);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the current device, once
 // per (call site, device, larger size): function attributes are per device and one

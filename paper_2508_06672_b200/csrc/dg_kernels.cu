@@ -421,6 +421,38 @@ k_hist_range(const int* __restrict__ hist, int nbins, int N, StepRange* __restri
     }
 }
 
+// Exclusive prefix sums of |y|^2 per capture, FP64 (one CTA per capture):
+// E[c][k] = sum_{i<k} |y_c[i]|^2. A bucket's ||z||_2^2 estimate is then
+// sum_b E1_b E2_b / len_b over its blocks (exact for constant-envelope
+// signals), the moment path's refinement floor (k_evaluate*).
+constexpr int kEnergyThreads = 1024;
+
+__global__ void __launch_bounds__(kEnergyThreads)
+k_energy_prefix(const double2* __restrict__ y, int64_t stride, int64_t N, double* __restrict__ out) {
+    __shared__ double sh[kEnergyThreads];
+    const double2* yc = y + (int64_t)blockIdx.x * stride;
+    double* o = out + (int64_t)blockIdx.x * (N + 1);
+    const int t = threadIdx.x;
+    const int64_t per = (N + kEnergyThreads - 1) / kEnergyThreads;
+    const int64_t k0 = min(N, t * per), k1 = min(N, k0 + per);
+    double s = 0.0;
+    for (int64_t k = k0; k < k1; ++k) s = fma(yc[k].x, yc[k].x, fma(yc[k].y, yc[k].y, s));
+    sh[t] = s;
+    __syncthreads();
+    for (int off = 1; off < kEnergyThreads; off <<= 1) {  // inclusive Hillis-Steele scan
+        const double v = t >= off ? sh[t - off] : 0.0;
+        __syncthreads();
+        sh[t] += v;
+        __syncthreads();
+    }
+    double run = sh[t] - s;  // exclusive prefix of this thread's range
+    for (int64_t k = k0; k < k1; ++k) {
+        o[k] = run;
+        run = fma(yc[k].x, yc[k].x, fma(yc[k].y, yc[k].y, run));
+    }
+    if (t == kEnergyThreads - 1) o[N] = sh[t];
+}
+
 // ---------------------------------------------------------------------------
 // Bucketing over the step's TDOA range only (bins [bin0, bin0 + nbins)):
 // exclusive scans of per-d counts, per-d warp-task counts and non-empty bins,
@@ -1301,6 +1333,11 @@ void launch_geometry_steps(const double* x, const double* y, const double* z, in
             x, y, z, P, pg + s0, m, fs, wl, N, d_out + (int64_t)s0 * P, fdoa_out + (int64_t)s0 * P,
             hist + (int64_t)s0 * nbins, nbins, s_out + (int64_t)s0 * P, overlap, err);
     }
+}
+
+void launch_energy_prefix(const double2* y, int64_t stride, int64_t n_caps, int64_t N,
+                          double* out, cudaStream_t st) {
+    if (n_caps > 0) k_energy_prefix<<<(int)n_caps, kEnergyThreads, 0, st>>>(y, stride, N, out);
 }
 
 void launch_hist_range(const int* hist, int nbins, int n_steps, int N, StepRange* out,

@@ -275,7 +275,8 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
            int* __restrict__ queue, const int* __restrict__ sorted,
            const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p, int B,
            const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
-           uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau) {
+           uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau,
+           const double* __restrict__ e1, const double* __restrict__ e2, int N) {
     extern __shared__ float4 smem4[];
     __shared__ uint64_t full[kEvalStages], empty[kEvalStages];
     __shared__ int slot_u[kEvalStages];
@@ -334,17 +335,27 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
         const Bucket bk = buckets[u];
         const int nb = bk.nb;
         const float4* mb = smem4 + sl * buf_f4;
-        // Q = ||M_0||_2 of the bucket: the scale of the moments' own FP32
-        // rounding, which every candidate of a coherent bucket inherits
-        // (DESIGN.md section 6); per warp, fixed-order reduction
-        float q2 = 0.f;
-        for (int b = lane; b < nb; b += 32) {
-            const float4 v = mb[b * (R / 2)];
-            q2 = fmaf(v.x, v.x, fmaf(v.y, v.y, q2));
-        }
+        // Q_m^2 = sum_b |M_m[b]|^2 of the bucket: the scale of the moments' own
+        // FP32 rounding, which every candidate of a coherent bucket inherits
+        // through its coefficients a_m; per warp,
+        // fixed-order reductions
+        float qm2[R];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-        const double qscale = sqrt((double)q2);
+        for (int m = 0; m < R; ++m) {
+            const float2* mb2 = reinterpret_cast<const float2*>(mb);
+            float q2 = 0.f;
+            for (int b = lane; b < nb; b += 32) {
+                const float2 v = mb2[b * R + m];
+                q2 = fmaf(v.x, v.x, fmaf(v.y, v.y, q2));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+            qm2[m] = q2;
+        }
+        // ||z||_2^2 of the bucket (the floor of the error scale), per warp
+        double zfloor = bucket_z2_part(e1, e2, N, bk.d, B, lane, 32);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) zfloor += __shfl_xor_sync(0xffffffffu, zfloor, o);
 
         for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
             int p[kEvalNC];
@@ -352,6 +363,7 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
             float cf[kEvalNC][R];
             float wtr[kEvalNC][G], wti[kEvalNC][G];
             double sr[kEvalNC], si[kEvalNC];  // e^{i 2 pi nu B G}
+            double qe2[kEvalNC];               // sum_m a_m^2 Q_m^2
 #pragma unroll
             for (int c = 0; c < kEvalNC; ++c) {
                 const int slot = base + 32 * c + lane;
@@ -360,9 +372,12 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                 double jv[R];
                 bessel_j<R>(3.141592653589793 * nu[c] * (double)B, jv);
                 // a_m M_m = (2 - delta_m0) (-1)^(m/2) J_m M'_m  (M' = i^(m mod 2) M)
+                qe2[c] = 0.0;
 #pragma unroll
-                for (int m = 0; m < R; ++m)
+                for (int m = 0; m < R; ++m) {
                     cf[c][m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
+                    qe2[c] = fma((double)cf[c][m] * cf[c][m], (double)qm2[m], qe2[c]);
+                }
                 // W_j = W_1^j by an FP64 recurrence from one FP64 sincospi (error
                 // ~1e-15), each rounded once to FP32; e^{i 2 pi nu B G} = W_G
                 const double x1 = nu[c] * (double)B;
@@ -426,15 +441,15 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                     ar[c] = nr;
                 }
             }
-            // FP32 error scale of this candidate: max(sqrt(sum_b |C_b|^2), Q)
-            // (DESIGN.md section 6); below tau of it the value is re-evaluated
-            // in FP64
+            // FP32 error scale of this candidate: max(sqrt(sum_b |C_b|^2),
+            // sqrt(sum_m a_m^2 Q_m^2)); below tau of it the
+            // value is re-evaluated in FP64
 #pragma unroll
             for (int c = 0; c < kEvalNC; ++c) {
                 if (p[c] < 0) continue;
                 const double sv = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
                 s_out[p[c]] = sv;
-                if (sv < (double)tau * fmax(sqrt(en[c]), qscale)) {
+                if (sv < (double)tau * sqrt(fmax(fmax(en[c], qe2[c]), zfloor))) {
                     const int64_t e = flag_base + p[c];
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
@@ -523,7 +538,8 @@ template <int R>
 void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                       const int* sorted, const double* fdoa, double fs, const double* nu_c, int B,
                       const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
-                      int64_t flag_base, float tau, int sm_count, cudaStream_t st) {
+                      int64_t flag_base, float tau, const double* e1, const double* e2, int N,
+                      int sm_count, cudaStream_t st) {
     auto kern = k_evaluate<R, kEvalG>;
     const size_t smem = evaluate_smem(nbmax, R);
     static size_t attr[64] = {};
@@ -531,7 +547,8 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
     int grid = sm_count * 4;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
     kern<<<grid, 32 * kEvalWarps, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c,
-                                              B, mom, nbmax, s_out, flag_bits, flag_base, tau);
+                                              B, mom, nbmax, s_out, flag_bits, flag_base, tau, e1,
+                                              e2, N);
 }
 
 }  // namespace
@@ -579,11 +596,11 @@ size_t evaluate_smem_bytes(int nbmax, int R) { return evaluate_smem(nbmax, R); }
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                      int max_buckets, const int* sorted, const double* fdoa, double fs,
                      const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                     uint32_t* flag_bits, int64_t flag_base, float tau, int sm_count,
-                     cudaStream_t st) {
+                     uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
+                     const double* e2, int N, int sm_count, cudaStream_t st) {
 #define DG_EVAL_CASE(RR)                                                                    \
     evaluate_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
-                         mom, nbmax, s_out, flag_bits, flag_base, tau, sm_count, st)
+                         mom, nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N, sm_count, st)
     switch (R) {
         case 8: DG_EVAL_CASE(8); break;
         case 10: DG_EVAL_CASE(10); break;

@@ -18,7 +18,8 @@ import scenes  # noqa: E402
 import test_gpu_error_model as em  # noqa: E402
 from oracle.bindings import RefLib  # noqa: E402
 
-MOMENT_CASES = ["tone+40_B640", "tone+40_B512", "tone+40_B768", "tone+40_1km", "chirp+40_B768"]
+MOMENT_CASES = ["tone+40_B640", "tone+40_B512", "tone+40_B768", "tone+40_1km", "chirp+40_B768",
+                "chirp+40"]
 
 
 def c3_time(grid, staged, reps=5):
@@ -57,7 +58,8 @@ def main():
         row = {"tau": tau}
         for name in MOMENT_CASES:
             kw, tuning = em.CASES[name]
-            em.CASES[name] = (kw, {**tuning, "refine_tau": tau, "allow_weaker_refine": 1})
+            em.CASES[name] = (kw, {**tuning, "correlator": "moments", "refine_tau": tau,
+                                   "allow_weaker_refine": 1})
             r = em.run_case(b2, ref, name)
             em.CASES[name] = (kw, tuning)
             row[name] = r["max_rel"]
