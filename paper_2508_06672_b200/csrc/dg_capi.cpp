@@ -102,14 +102,14 @@ double jacobi_anger_tail(double x, int R) {
 
 // Truncation budget. Per block the Jacobi-Anger remainder is bounded by
 // tail(x, R) times the block's L1 norm, and a product stream that repeats with
-// the block length (e.g. a chirp product tone aliasing onto B) adds those
+// the block length (e.g. a chirp product tone aliasing onto B) can add those
 // remainders coherently, so a candidate's truncation error is only bounded by
 // tail * ||z||_1 <= tail * sqrt(N) ||z||_2, while unrefined values are at least
-// tau ||z||_2 (the refinement test's noise scale). tail <= kTailBudget tau /
-// sqrt(N) keeps that term below 2e-6 relative (1/10 of the parity budget):
-// 1.8e-10 at N = 50,000 (R = 16 at C3's x = 2.94; a +40 dB chirp at the 1e-8
-// tail used before reached 6.5e-5, tests/test_gpu_error_model.py).
-constexpr double kTailBudget = 2e-6;
+// tau ||z||_2 (the refinement test's floor). tail <= kTailBudget tau / sqrt(N)
+// keeps that term below 1e-5 relative, half the 2e-5 margin the error model
+// holds (tests/test_gpu_error_model.py): 9e-10 at N = 50,000 (C3: B = 512 with
+// R = 14, or B = 640 with R = 16; the planner's cost model picks).
+constexpr double kTailBudget = 1e-5;
 // Largest Jacobi-Anger argument x = pi h B the planner admits. Past it the
 // coefficients a_m(x) grow and the block sums cancel more, so the FP32
 // evaluation error of sidelobe candidates in coherent buckets rises faster

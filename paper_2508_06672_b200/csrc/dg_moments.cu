@@ -65,38 +65,38 @@ __global__ void k_center(const double2* __restrict__ y, const float2* __restrict
 // Moments of all d-buckets, blocks aligned to ABSOLUTE sample index (block b
 // covers y1 samples [bB, (b+1)B); a bucket uses the blocks meeting its
 // overlap, masked to it), so buckets with neighbouring d share the same y1
-// rows and overlapping y2 windows. Work item = (group of G consecutive TDOA
-// values starting at an even d0, chunk of CB absolute blocks); persistent
-// grid, one 16-warp CTA per SM:
+// rows and overlapping y2 windows. Work item = (group of G = 128 consecutive
+// TDOA values starting at an even d0, chunk of CB = 4 absolute blocks);
+// persistent grid, one 16-warp CTA per SM:
 //   stage   per block row: y1c[bB .. +B) and the y2 window [bB+d0 .. +B+G+2)
-//           (zero-padded array) by per-row TMA bulk copies, rows padded so the
-//           lane = block reads are conflict-free (y1: LDS.128 across 8-lane
-//           quarters; y2 at any shift: LDS.64 across 16-lane halves);
-//           double-buffered with full/empty mbarriers (item k+1 lands while
-//           item k is computed; no __syncthreads)
-//   compute warp w = TDOA values d0 + BPW w + (lane / CB), lane % CB = block;
-//           each lane runs its whole block: z = y1c conj(y2) in registers,
-//           folded by T_m(-t) = (-1)^m T_m(t) (R/2 FFMA2 per sample),
-//           Chebyshev rows broadcast; moments written directly
-// L2 -> SM traffic is (B + (B + G)) samples per block for G buckets instead of
-// 2B per bucket.
+//           (zero-padded array) by per-row TMA bulk copies; double-buffered
+//           with full/empty mbarriers (item k+1 lands while item k is
+//           computed; no __syncthreads)
+//   compute warp w = (block w / 4, TDOA values d0 + 32 (w % 4) + lane): one
+//           block per warp, so the y1 samples are warp-uniform broadcasts
+//           (one shared-memory wavefront per LDS.128) and the y2 samples of
+//           the 32 lanes are 32 consecutive words (conflict-free); each lane
+//           runs its whole block: z = y1c conj(y2) in registers, folded by
+//           T_m(-t) = (-1)^m T_m(t) (R/2 FFMA2 per sample), Chebyshev rows
+//           broadcast; moments written directly
+// Per two folded sample pairs a warp reads 2 (y1) + 8 (y2) + R/2 (table)
+// shared-memory wavefronts (8 + 8 + R/2 with the 8-blocks-per-warp mapping of
+// r01, where the y1 reads were 4-way redundant across quarter-warps); L2 -> SM
+// traffic is (B + (B + G)) samples per block row for G buckets.
 template <int B, int R>
 struct MomLayout {
-    static constexpr int CB = B >= 512 ? 8 : 16;       // blocks per item
-    static constexpr int BPW = 32 / CB;                // TDOA values per warp
-    static constexpr int G = BPW * kMomWarps;           // TDOA values per item
+    static constexpr int WG = 4;                        // 32-value TDOA groups per item
+    static constexpr int CB = kMomWarps / WG;           // blocks per item
+    static constexpr int G = 32 * WG;                   // TDOA values per item
     static constexpr int RP = (2 * R + 3) / 4 * 4;      // table row: T_m(t_j), T_m(t_j+1) pairs
-    static constexpr int RS1 = B + 2;                   // y1 row (float2): 4 banks mod 32
+    static constexpr int RS1 = B;                       // y1 row (float2): broadcast reads
     static constexpr int W2 = B + G + 2;                // y2 window samples copied
-    // y2 row: 2 float2 mod 16, so a 16-lane half-warp's (8 blocks x 2 TDOA values)
-    // LDS.64 at any shift covers 16 distinct bank pairs
-    static constexpr int RM2 = 2;
-    static constexpr int RS2 = (W2 + 15 - RM2) / 16 * 16 + RM2;
+    static constexpr int RS2 = W2;                      // consecutive lanes: consecutive words
     static constexpr size_t table_floats = (size_t)B / 4 * RP;  // one row per two folded pairs
     static constexpr size_t stage_f2 = (size_t)CB * (RS1 + RS2);  // one buffer
     static constexpr size_t smem = ((table_floats * sizeof(float) + 15) & ~(size_t)15) +
                                    2 * stage_f2 * sizeof(float2);
-    static_assert(RS2 % 16 == RM2 && RS2 >= W2 && W2 % 2 == 0, "y2 row padding");
+    static_assert(W2 % 2 == 0 && RS1 % 2 == 0, "16-byte rows");
     static_assert(smem <= 227 * 1024 - 64, "k_moments stage exceeds shared memory");
 };
 
@@ -116,7 +116,7 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
     static_assert(R % 2 == 0 && R <= kMaxMoments, "moment count");
     static_assert(kMomThreads % 32 == 0, "mapping");
     using L = MomLayout<B, R>;
-    constexpr int CB = L::CB, BPW = L::BPW, G = L::G;
+    constexpr int CB = L::CB, WG = L::WG, G = L::G;
     constexpr int RP = L::RP, RS1 = L::RS1, RS2 = L::RS2, W2 = L::W2;
     extern __shared__ float4 smem4[];
     float* ts = reinterpret_cast<float*>(smem4);  // [B/2][RP]
@@ -125,10 +125,8 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
     __shared__ uint64_t full[2], empty[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // a 16-lane half-warp = 8 blocks x 2 TDOA values, so the y2 LDS.64 at shifts
-    // t, t+1 fill each other's bank gaps (row stride 4 banks mod 32)
-    const int blk = CB == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : (lane & 7);
-    const int hb = CB == 16 ? ((lane >> 3) & 1) : (lane >> 3);
+    const int blk = warp / WG;              // block row of the item (warp-uniform)
+    const int t = 32 * (warp % WG) + lane;  // TDOA slot in the group
     const int nitems = ngroups * cpb;
     const int nblk_abs = (N + B - 1) / B;
 
@@ -173,7 +171,6 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
             issue(nitem, buf ^ 1);
         }
         const int g = item / cpb, c = item - g * cpb;
-        const int t = BPW * warp + hb;                 // TDOA slot in the group
         const int bin = bin_lo + g * G + t;
         const int u = (bin >= bin0 && bin < bin0 + nbins) ? ubin[bin - bin0] : -1;
         const int d = bin - (N - 1);
