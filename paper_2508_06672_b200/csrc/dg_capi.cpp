@@ -233,7 +233,7 @@ struct Lane {
 struct Pipeline {
     int64_t P = 0;
     int N = 0, nbins = 0, max_tasks = 0, slots = 0, sm_count = 148, n_lanes = 1;
-    int *d = nullptr, *hist = nullptr, *err = nullptr;
+    int *d = nullptr, *rank = nullptr, *hist = nullptr, *err = nullptr;
     double* fdoa = nullptr;
     StepRange* range = nullptr;
     double* nu_c = nullptr;  // [slots]
@@ -284,9 +284,10 @@ struct Pipeline {
         const int64_t mt = P / correlate_task_size() + std::min<int64_t>(P, nbins) + 1;
         max_tasks = (int)std::min<int64_t>(mt, INT32_MAX);
         // phase-A window: per-slot d + fdoa + histogram, within ~4 GB
-        const int64_t per_slot = 12 * P + 4 * (int64_t)nbins + 64;
+        const int64_t per_slot = 16 * P + 4 * (int64_t)nbins + 64;
         slots = (int)std::max<int64_t>(1, std::min<int64_t>(n_steps, (4ll << 30) / per_slot));
         d = sc.alloc<int>((size_t)P * slots);
+        rank = sc.alloc<int>((size_t)P * slots);
         fdoa = sc.alloc<double>((size_t)P * slots);
         hist = sc.alloc<int>((size_t)nbins * slots);
         range = sc.alloc<StepRange>(slots);
@@ -368,6 +369,7 @@ struct Pipeline {
     }
 
     int* d_slot(int s) const { return d + (size_t)s * P; }
+    int* rank_slot(int s) const { return rank + (size_t)s * P; }
     double* fdoa_slot(int s) const { return fdoa + (size_t)s * P; }
     int* hist_slot(int s) const { return hist + (size_t)s * nbins; }
 
@@ -504,7 +506,8 @@ struct Pipeline {
         }
         if (pl.direct) {
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
-                          L.n_tasks, L.n_buckets, d_slot(s), P, L.sorted, L.tasks, L.buckets,
+                          L.n_tasks, L.n_buckets, d_slot(s), rank_slot(s), P, L.sorted, L.tasks,
+                          L.buckets,
                           L.ubin, 0, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             if (ev1) CK(cudaEventRecord(ev1, st));
@@ -514,7 +517,8 @@ struct Pipeline {
             ++direct_steps;
         } else {
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
-                          L.n_tasks, L.n_buckets, d_slot(s), P, L.sorted, L.tasks, L.buckets,
+                          L.n_tasks, L.n_buckets, d_slot(s), rank_slot(s), P, L.sorted, L.tasks,
+                          L.buckets,
                           L.ubin, pl.B, st, fdoa_slot(s), L.sfdoa);
             launch_center(y1_64, y2, N, nu_c + s, L.y1c, L.y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
@@ -918,7 +922,8 @@ int dg_correlate_batch(dg_session* s, const dg_pair_offsets* batch, int64_t n, d
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
         CK(cudaMemcpyAsync(off, batch, n * sizeof(dg_pair_offsets), cudaMemcpyHostToDevice, s->st));
         pl.reset_ranges(sc, 1);
-        launch_offsets_hist(off, n, pl.N, pl.d_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), vals,
+        launch_offsets_hist(off, n, pl.N, pl.d_slot(0), pl.rank_slot(0), pl.fdoa_slot(0),
+                            pl.hist_slot(0), vals,
                             pl.overlap, pl.range, s->st);
         pl.plan_window(sc, 1, s->fs);
         const auto* y32 = static_cast<const float2*>(s->y32->p) + kCapturePad;
@@ -1169,7 +1174,7 @@ int dg_correlate_snapshot(dg_session* s, const dg_grid* g, const dg_state* rx_i,
         CK(cudaMemsetAsync(bits, 0, n_words * sizeof(uint32_t), s->st));
         pl.reset_ranges(sc, 1);
         launch_geometry_hist(g->x, g->y, g->z, P, pg, s->fs, wl, pl.N, pl.d_slot(0),
-                             pl.fdoa_slot(0), pl.hist_slot(0), vals, pl.overlap, pl.err, pl.range,
+                             pl.rank_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), vals, pl.overlap, pl.err, pl.range,
                              s->st);
         const StepRange* approx = pl.lattice_ranges(sc, g, &h, 1, s->fs, wl);
         pl.plan_window(sc, 1, s->fs, approx, fp32_fdoa_margin(&h, 1, wl), g->full_size);
@@ -1725,7 +1730,7 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         // histograms, B / R / centre frequency from the FP32 lattice ranges
         if (w0 > 0) CK(cudaMemsetAsync(pl.hist, 0, sizeof(int) * pl.nbins * nw, st));
         launch_geometry_steps(g->x, g->y, g->z, P, upg + w0, nw, fs, wl, pl.N, pl.d_slot(0),
-                              pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins, raw + (int64_t)w0 * P,
+                              pl.rank_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins, raw + (int64_t)w0 * P,
                               pl.overlap, pl.err, st);
         launch_hist_range(pl.hist_slot(0), pl.nbins, nw, pl.N, pl.range, st);
         launches += (nw + 63) / 64 + 1;

@@ -107,14 +107,14 @@ void launch_grid_ecef(const double* row_a, const double* row_z, const double* co
 // geometry + histogram over grid points (geometry.hpp:51-83, bit-exact)
 void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
                           const PairGeom* pg_dev, double fs, double wl, int N, int* d_out,
-                          double* fdoa_out, int* hist, double* s_out,
+                          int* rank_out, double* fdoa_out, int* hist, double* s_out,
                           unsigned long long* overlap, int* err, StepRange* range,
                           cudaStream_t st);
 // every step of a window in one pass: d/fdoa/surface slices of stride P,
 // histograms of stride nbins (no exact ranges; see k_geometry_steps)
 void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
                            const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
-                           double* fdoa_out, int* hist, int nbins, double* s_out,
+                           int* rank_out, double* fdoa_out, int* hist, int nbins, double* s_out,
                            unsigned long long* overlap, int* err, cudaStream_t st);
 // per capture (n_caps rows of `stride` elements) the exclusive prefix sums of
 // |y|^2 in FP64: out[c][k], k <= N
@@ -128,7 +128,7 @@ void launch_predict_offsets(const double* x, const double* y, const double* z, i
                             int* err, cudaStream_t st);
 // the same from caller offsets (correlate_batch path)
 void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
-                         double* fdoa_out, int* hist, double* s_out,
+                         int* rank_out, double* fdoa_out, int* hist, double* s_out,
                          unsigned long long* overlap, StepRange* range, cudaStream_t st);
 // planning ranges over a whole lattice (FP32, partition-independent)
 void launch_lattice_rel(const double* x, const double* y, const double* z, int64_t P, double cx,
@@ -138,10 +138,11 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 // bins [bin0, bin0 + nb) of the TDOA histogram (bin = d + N - 1) -> d-sorted
 // candidate ids, warp tasks of <= correlate_task_size() candidates and one
 // Bucket per non-empty bin (blocks of length B; B = 0 skips buckets)
+// rank: each candidate's rank in its bin (the geometry pass's histogram atomic)
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
-                   int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st,
-                   const double* fdoa = nullptr, double* sfdoa = nullptr);
+                   int* cursor, int* n_tasks, int* n_buckets, const int* d, const int* rank,
+                   int64_t P, int* sorted, Task* tasks, Bucket* buckets, int* ubin, int B,
+                   cudaStream_t st, const double* fdoa = nullptr, double* sfdoa = nullptr);
 // candidates per warp task of the active correlator variant (32 x candidates/lane)
 int correlate_task_size();
 void launch_correlate(const Task* tasks, const int* n_tasks, int max_tasks, const int* sorted,

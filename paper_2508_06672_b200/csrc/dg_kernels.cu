@@ -195,8 +195,10 @@ struct RangeAcc {
     }
 };
 
+// rank_out[p]: the histogram atomic's old value, this candidate's rank in its
+// TDOA bin, so k_scatter places it without atomics
 __device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdoa, int N,
-                                           int* d_out, double* fdoa_out, int* hist,
+                                           int* d_out, int* rank_out, double* fdoa_out, int* hist,
                                            double* s_out, unsigned long long& ovl, RangeAcc& ra) {
     if (tdoa >= N || tdoa <= -N) {  // empty overlap (also catches llround overflow)
         d_out[p] = kNoOverlap;
@@ -205,7 +207,7 @@ __device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdo
         const int d = (int)tdoa;
         d_out[p] = d;
         fdoa_out[p] = fdoa;
-        atomicAdd(&hist[d + N - 1], 1);
+        rank_out[p] = atomicAdd(&hist[d + N - 1], 1);
         ovl += (unsigned long long)(N - (d < 0 ? -d : d));
         const unsigned long long k = f64_key(fdoa);
         ra.fmin = min(ra.fmin, k);
@@ -218,7 +220,8 @@ __device__ __forceinline__ void emit_point(int64_t p, long long tdoa, double fdo
 __global__ void k_geometry_hist(const double* __restrict__ x, const double* __restrict__ y,
                                 const double* __restrict__ z, int64_t P,
                                 const PairGeom* __restrict__ pg, double fs, double wl, int N,
-                                int* __restrict__ d_out, double* __restrict__ fdoa_out,
+                                int* __restrict__ d_out, int* __restrict__ rank_out,
+                                double* __restrict__ fdoa_out,
                                 int* __restrict__ hist, double* __restrict__ s_out,
                                 unsigned long long* __restrict__ overlap, int* __restrict__ err,
                                 StepRange* __restrict__ range) {
@@ -230,7 +233,7 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
         long long tdoa;
         double fdoa;
         if (!offsets_exact(x[p], y[p], z[p], g, fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
-        emit_point(p, tdoa, fdoa, N, d_out, fdoa_out, hist, s_out, ovl, ra);
+        emit_point(p, tdoa, fdoa, N, d_out, rank_out, fdoa_out, hist, s_out, ovl, ra);
     }
     ovl = warp_sum_u64(ovl);
     if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
@@ -248,7 +251,7 @@ constexpr int kGeoStepsMax = 64;  // steps per launch (shared-memory receiver ta
 __global__ void __launch_bounds__(256)
 k_geometry_steps(const double* __restrict__ x, const double* __restrict__ y,
                  const double* __restrict__ z, int64_t P, const PairGeom* __restrict__ pg, int n,
-                 double fs, double wl, int N, int* __restrict__ d_out,
+                 double fs, double wl, int N, int* __restrict__ d_out, int* __restrict__ rank_out,
                  double* __restrict__ fdoa_out, int* __restrict__ hist, int nbins,
                  double* __restrict__ s_out, unsigned long long* __restrict__ overlap,
                  int* __restrict__ err) {
@@ -265,7 +268,8 @@ k_geometry_steps(const double* __restrict__ x, const double* __restrict__ y,
             long long tdoa;
             double fdoa;
             if (!offsets_exact(cx, cy, cz, sg[s], fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
-            emit_point(p, tdoa, fdoa, N, d_out + (int64_t)s * P, fdoa_out + (int64_t)s * P,
+            emit_point(p, tdoa, fdoa, N, d_out + (int64_t)s * P, rank_out + (int64_t)s * P,
+                       fdoa_out + (int64_t)s * P,
                        hist + (int64_t)s * nbins, s_out + (int64_t)s * P, ovl, ra);
         }
     }
@@ -291,7 +295,8 @@ __global__ void k_predict_offsets(const double* __restrict__ x, const double* __
 }
 
 __global__ void k_offsets_hist(const dg_pair_offsets* __restrict__ off, int64_t P, int N,
-                               int* __restrict__ d_out, double* __restrict__ fdoa_out,
+                               int* __restrict__ d_out, int* __restrict__ rank_out,
+                               double* __restrict__ fdoa_out,
                                int* __restrict__ hist, double* __restrict__ s_out,
                                unsigned long long* __restrict__ overlap,
                                StepRange* __restrict__ range) {
@@ -300,7 +305,8 @@ __global__ void k_offsets_hist(const dg_pair_offsets* __restrict__ off, int64_t 
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         const dg_pair_offsets o = off[p];
-        emit_point(p, o.tdoa_samples, o.fdoa_hz, N, d_out, fdoa_out, hist, s_out, ovl, ra);
+        emit_point(p, o.tdoa_samples, o.fdoa_hz, N, d_out, rank_out, fdoa_out, hist, s_out, ovl,
+                   ra);
     }
     ovl = warp_sum_u64(ovl);
     if ((threadIdx.x & 31) == 0 && ovl) atomicAdd(overlap, ovl);
@@ -534,33 +540,22 @@ k_scan(const int* __restrict__ hist, int nbins, int ts, int* __restrict__ off,
 }
 
 // sfdoa (nullable): the candidates' FDOA in the same bucket order, so the
-// candidate evaluators read contiguous values instead of gathering fdoa[p]
+// candidate evaluators read contiguous values instead of gathering fdoa[p].
+// Each candidate goes to its bin's start plus its rank in the bin (taken by
+// the geometry pass's histogram atomic): no atomics here, a streaming pass.
 // Candidates whose bin lies outside the planned bins [bin0, bin0 + nbins) are
-// skipped (another part of a split step owns them; cursors outside are unset).
-__global__ void k_scatter(const int* __restrict__ d, int64_t P, int N, int bin0, int nbins,
-                          int* __restrict__ cursor, int* __restrict__ sorted,
-                          const double* __restrict__ fdoa, double* __restrict__ sfdoa) {
-    // four independent cursor atomics in flight per thread (latency-bound)
-    constexpr int U = 4;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < P; p0 += U * stride) {
-        int dd[U], pos[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t p = p0 + u * stride;
-            dd[u] = p < P ? d[p] : kNoOverlap;
-            if (dd[u] != kNoOverlap && (unsigned)(dd[u] + N - 1 - bin0) >= (unsigned)nbins)
-                dd[u] = kNoOverlap;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            pos[u] = dd[u] != kNoOverlap ? atomicAdd(&cursor[dd[u] + N - 1], 1) : -1;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (pos[u] >= 0) {
-                sorted[pos[u]] = (int)(p0 + u * stride);
-                if (sfdoa) sfdoa[pos[u]] = fdoa[p0 + u * stride];
-            }
+// skipped (another part of a split step owns them; their offsets are unset).
+__global__ void k_scatter(const int* __restrict__ d, const int* __restrict__ rank, int64_t P, int N,
+                          int bin0, int nbins, const int* __restrict__ off,
+                          int* __restrict__ sorted, const double* __restrict__ fdoa,
+                          double* __restrict__ sfdoa) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int dd = d[p];
+        if (dd == kNoOverlap || (unsigned)(dd + N - 1 - bin0) >= (unsigned)nbins) continue;
+        const int pos = off[dd + N - 1] + rank[p];
+        sorted[pos] = (int)p;
+        if (sfdoa) sfdoa[pos] = fdoa[p];
     }
 }
 
@@ -1317,20 +1312,22 @@ void launch_grid_ecef(const double* ra, const double* rz, const double* cc, cons
 
 void launch_geometry_hist(const double* x, const double* y, const double* z, int64_t P,
                           const PairGeom* pg, double fs, double wl, int N, int* d_out,
-                          double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
-                          int* err, StepRange* range, cudaStream_t st) {
-    k_geometry_hist<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, N, d_out, fdoa_out,
-                                                        hist, s_out, overlap, err, range);
+                          int* rank_out, double* fdoa_out, int* hist, double* s_out,
+                          unsigned long long* overlap, int* err, StepRange* range,
+                          cudaStream_t st) {
+    k_geometry_hist<<<blocks_for(P, 256), 256, 0, st>>>(x, y, z, P, pg, fs, wl, N, d_out, rank_out,
+                                                        fdoa_out, hist, s_out, overlap, err, range);
 }
 
 void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
                            const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
-                           double* fdoa_out, int* hist, int nbins, double* s_out,
+                           int* rank_out, double* fdoa_out, int* hist, int nbins, double* s_out,
                            unsigned long long* overlap, int* err, cudaStream_t st) {
     for (int s0 = 0; s0 < n; s0 += kGeoStepsMax) {
         const int m = n - s0 < kGeoStepsMax ? n - s0 : kGeoStepsMax;
         k_geometry_steps<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
-            x, y, z, P, pg + s0, m, fs, wl, N, d_out + (int64_t)s0 * P, fdoa_out + (int64_t)s0 * P,
+            x, y, z, P, pg + s0, m, fs, wl, N, d_out + (int64_t)s0 * P, rank_out + (int64_t)s0 * P,
+            fdoa_out + (int64_t)s0 * P,
             hist + (int64_t)s0 * nbins, nbins, s_out + (int64_t)s0 * P, overlap, err);
     }
 }
@@ -1352,10 +1349,10 @@ void launch_predict_offsets(const double* x, const double* y, const double* z, i
 }
 
 void launch_offsets_hist(const dg_pair_offsets* off, int64_t P, int N, int* d_out,
-                         double* fdoa_out, int* hist, double* s_out, unsigned long long* overlap,
-                         StepRange* range, cudaStream_t st) {
-    k_offsets_hist<<<blocks_for(P, 256), 256, 0, st>>>(off, P, N, d_out, fdoa_out, hist, s_out,
-                                                       overlap, range);
+                         int* rank_out, double* fdoa_out, int* hist, double* s_out,
+                         unsigned long long* overlap, StepRange* range, cudaStream_t st) {
+    k_offsets_hist<<<blocks_for(P, 256), 256, 0, st>>>(off, P, N, d_out, rank_out, fdoa_out, hist,
+                                                       s_out, overlap, range);
 }
 
 void launch_lattice_rel(const double* x, const double* y, const double* z, int64_t P, double cx,
@@ -1371,13 +1368,13 @@ void launch_range_fp32(const float4* rel, int64_t P, const RxPairF32* rx, int n_
 }
 
 void launch_bucket(int* hist, int bin0, int nb, int N, int* off, int* toff, int* boff,
-                   int* cursor, int* n_tasks, int* n_buckets, const int* d, int64_t P, int* sorted,
-                   Task* tasks, Bucket* buckets, int* ubin, int B, cudaStream_t st,
-                   const double* fdoa, double* sfdoa) {
+                   int* cursor, int* n_tasks, int* n_buckets, const int* d, const int* rank,
+                   int64_t P, int* sorted, Task* tasks, Bucket* buckets, int* ubin, int B,
+                   cudaStream_t st, const double* fdoa, double* sfdoa) {
     const int ts = correlate_task_size();
     k_scan<<<1, kScanThreads, 0, st>>>(hist + bin0, nb, ts, off + bin0, toff + bin0, boff + bin0,
                                        cursor + bin0, n_tasks, n_buckets);
-    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, P, N, bin0, nb, cursor, sorted, fdoa, sfdoa);
+    k_scatter<<<blocks_for(P, 256), 256, 0, st>>>(d, rank, P, N, bin0, nb, off, sorted, fdoa, sfdoa);
     k_build_tasks<<<blocks_for(nb, 256), 256, 0, st>>>(hist + bin0, nb, bin0, N, ts, off + bin0,
                                                       toff + bin0, boff + bin0, tasks, buckets, ubin, B);
 }

@@ -165,8 +165,19 @@ def geolocate_sharded(grid, staged, options=None, gather=True, group=None, strea
     `staged`: every rank's StagedSnapshots of the whole run (captures are
     small next to the surfaces). Returns (argmax_value, argmax_index,
     full_surface_or_None, detections, correlation stats of this rank) on
-    every rank.
+    every rank. The engine calls, the torch ops and the collectives all run
+    in order on one CUDA stream (`stream`, a raw cudaStream_t, or the current
+    torch stream).
     """
+    import torch
+
+    ext = (torch.cuda.ExternalStream(stream) if stream is not None
+           else torch.cuda.current_stream())
+    with torch.cuda.stream(ext):
+        return _geolocate_sharded(grid, staged, options, gather, group, ext.cuda_stream, profile)
+
+
+def _geolocate_sharded(grid, staged, options, gather, group, stream, profile):
     import torch
     import torch.distributed as dist
 
@@ -194,8 +205,6 @@ def geolocate_sharded(grid, staged, options=None, gather=True, group=None, strea
     elif mine:
         stats = correlate_units(grid, staged, [u[:3] for u in mine], local.data_ptr(), options,
                                 stream=stream, profile=profile)
-    if stream is not None:
-        torch.cuda.ExternalStream(stream).synchronize()
     medians = None
     if norm:
         slab_all = exchange_units(local, plan, rank, world, n_lat, n_lon, S, group=group)
@@ -233,6 +242,7 @@ def geolocate_sharded(grid, staged, options=None, gather=True, group=None, strea
         sizes = [(b - a) * n_lon for a, b in (slab_rows(n_lat, r, world) for r in range(world))]
         full = gather_vector(acc[: slab.size()], sizes, group=group)
         if options.detect:
+            torch.cuda.current_stream().synchronize()  # dg_detect_emitters: engine stream
             box = [None]
             if rank == 0:
                 box[0] = detect_emitters(CorrelationGrid(grid, None), options.k_sigma,

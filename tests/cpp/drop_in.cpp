@@ -130,6 +130,33 @@ int main(int argc, char** argv) {
         w = std::max(w, worst_rel(b2.per_snapshot[s].values, ref.per_snapshot[s].values));
     check(w <= 1e-4, "per-snapshot grids within 1e-4 (worst " + std::to_string(w) + ")");
 
+    // the multi-GPU engine behind the same driver (dg_engine_create_multi): three
+    // device slots (the box's GPUs, repeated when fewer are visible) shard the
+    // run; every value must equal the one-GPU solve's bit for bit
+    {
+        const auto devs = b200::B200Backend::devices_for(3);
+        std::vector<int> slots(3);
+        for (int i = 0; i < 3; ++i) slots[i] = devs[static_cast<std::size_t>(i) % devs.size()];
+        const b200::B200Backend multi(slots);
+        check(multi.descriptor().workers == 3, "B200Backend over 3 device slots: workers == 3");
+        const GeolocateResult m3 = b200::geolocate_snapshots(snaps, grid, opt, &multi);
+        bool bits = m3.accumulated.values == b2.accumulated.values &&
+                    m3.detections.size() == b2.detections.size();
+        for (std::size_t s = 0; bits && s < b2.per_snapshot.size(); ++s)
+            bits = m3.per_snapshot[s].values == b2.per_snapshot[s].values;
+        check(bits, "multi-GPU engine: surfaces and detections bit-identical to one GPU");
+        const auto reg = b200::make_backend("b200", 0);
+        check(reg->descriptor().name == "b200" && reg->descriptor().workers >= 1,
+              "b200::make_backend(\"b200\", 0): every visible GPU");
+        bool threw = false;
+        try {
+            b200::make_backend("gpu");
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        check(threw, "make_backend(\"gpu\") rejected (test_backend.cpp:181)");
+    }
+
     // the reference's accumulated surface through both writer sets (io.hpp:171-280)
     const auto tmp = std::filesystem::temp_directory_path();
     const auto slurp = [](const std::filesystem::path& p) {
