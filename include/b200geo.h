@@ -111,6 +111,11 @@ typedef struct {
     double refine_tau;       /* FP64 re-evaluation threshold of the moment path (0 = default) */
     int allow_weaker_refine; /* permit thresholds below the defaults (error-model studies only) */
     double direct_refine_tau; /* the same for the direct correlator (0 = default) */
+    double noise_refine_tau;  /* moment path: threshold on the bucket's noise floor ||z||_2
+                                 (0 = default); refine_tau applies to the coherent excess */
+    int64_t surface_budget_bytes; /* per-snapshot surfaces held at once when the caller does not
+                                     want them back; past it a run is solved in snapshot chunks
+                                     (0 = default, 4 GiB) */
 } dg_tuning;
 void dg_tuning_default(dg_tuning* t);
 int dg_engine_set_tuning(dg_engine* engine, const dg_tuning* t);

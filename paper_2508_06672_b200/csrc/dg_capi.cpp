@@ -256,7 +256,7 @@ struct Pipeline {
     // candidate block sums run on the tensor cores (dg_evaluate_tc.cu) or the
     // FFMA2 block loop (k_evaluate)
     dg_tuning tn{};
-    float tau = kMomentRefineTau, tau_direct = kRefineTau;
+    float tau = kMomentRefineTau, tau_direct = kRefineTau, tau_noise = kNoiseRefineTau;
     bool use_tc = true;
 
     ~Pipeline() {
@@ -274,6 +274,7 @@ struct Pipeline {
         }
         tau = tn.refine_tau > 0.0 ? (float)tn.refine_tau : kMomentRefineTau;
         tau_direct = tn.direct_refine_tau > 0.0 ? (float)tn.direct_refine_tau : kRefineTau;
+        tau_noise = tn.noise_refine_tau > 0.0 ? (float)tn.noise_refine_tau : kNoiseRefineTau;
         use_tc = tn.evaluate_tensor != 0;
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
@@ -531,12 +532,12 @@ struct Pipeline {
                 launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
                                    (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
                                    nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
-                                   e1, e2, N, sm_count, st);
+                                   tau_noise, e1, e2, N, sm_count, st);
             else
                 launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
                                 (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
-                                nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau, e1,
-                                e2, N, sm_count, st);
+                                nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
+                                tau_noise, e1, e2, N, sm_count, st);
             launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, tc ? 1 : 0, L.work, st);
             launches += 7;
         }
@@ -759,6 +760,15 @@ int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
             raise(DG_EINVAL, "dg_tuning: unsupported moment count " + std::to_string(t->moment_count));
         if (!(t->refine_tau >= 0.0) || !std::isfinite(t->refine_tau))
             raise(DG_EINVAL, "dg_tuning: refine_tau must be finite and >= 0");
+        if (!(t->noise_refine_tau >= 0.0) || !std::isfinite(t->noise_refine_tau))
+            raise(DG_EINVAL, "dg_tuning: noise_refine_tau must be finite and >= 0");
+        if (t->noise_refine_tau > 0.0 && t->noise_refine_tau < kNoiseRefineTau &&
+            !t->allow_weaker_refine)
+            raise(DG_EINVAL, "dg_tuning: noise_refine_tau below the default " +
+                                 std::to_string(kNoiseRefineTau) +
+                                 " weakens the 1e-4 contract (set allow_weaker_refine)");
+        if (t->surface_budget_bytes < 0)
+            raise(DG_EINVAL, "dg_tuning: surface_budget_bytes < 0");
         if (!(t->direct_refine_tau >= 0.0) || !std::isfinite(t->direct_refine_tau))
             raise(DG_EINVAL, "dg_tuning: direct_refine_tau must be finite and >= 0");
         if (t->direct_refine_tau > 0.0 && t->direct_refine_tau < kRefineTau &&
@@ -1912,6 +1922,10 @@ struct SideJoin {
 // cells they are re-ranked in rounds in descending fast order, stopping once
 // the best exact value exceeds fast(next) / (1 - eps) >= exact(any later cell).
 constexpr double kPeakEps = 1e-4;
+// per-snapshot surfaces held at once when the caller does not want them: past
+// this the run is solved in chunks of snapshots (C5: 16M cells x 100 snapshots
+// would be 12.8 GB)
+constexpr int64_t kSurfaceBudget = 4ll << 30;
 constexpr int kRerankRound = 4096;
 
 struct PeakCells {
@@ -2020,9 +2034,12 @@ PeakCells exact_peak(const dg_grid* g, const dg_staged* sn, const RunGeo& geo, c
 
 // per_pitch: elements between snapshot rows of the host per_snapshot buffer
 // (0: P; a slab of a multi-GPU run writes its columns of the full rows)
+// acc_in (nullable): the surface already accumulated (chunked runs), else
+// accumulate `grids`
 void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunGeo& geo,
                const double* grids, const double* medians, const dg_options& opt,
-               bool acc_dev_allowed, dg_result* res, Scratch& sc, int64_t per_pitch = 0) {
+               bool acc_dev_allowed, dg_result* res, Scratch& sc, int64_t per_pitch = 0,
+               double* acc_in = nullptr) {
     const int64_t P = g->size();
     if (per_pitch == 0) per_pitch = P;
     const int S = geo.S;
@@ -2032,9 +2049,10 @@ void peak_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const RunG
     if (opt.peak_stage == 2 && !res->accumulated_device)
         raise(DG_EINVAL, "dg_options: peak_stage 2 needs the surface in accumulated_device");
     if (!(opt.peak_max >= 0.0)) raise(DG_EINVAL, "dg_options: peak_max < 0");
-    double* acc = acc_dev_allowed && res->accumulated_device ? res->accumulated_device
-                                                             : sc.alloc<double>(P);
-    if (opt.peak_stage != 2) {
+    double* acc = acc_in ? acc_in
+                  : acc_dev_allowed && res->accumulated_device ? res->accumulated_device
+                                                               : sc.alloc<double>(P);
+    if (opt.peak_stage != 2 && !acc_in) {
         launch_accumulate(grids, S, P, acc, st);
         launches += 1;
     }
@@ -2160,10 +2178,45 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
     }
     const RunGeo geo = make_geo(sc, sn);
     const int64_t P = g->size();
-    auto* grids = sc.alloc<double>((int64_t)geo.S * P);
     double* medians = opt.normalize_per_snapshot ? sc.alloc<double>(geo.S) : nullptr;
-    correlate_steps_impl(eng, g, sn, geo, 0, geo.S, opt, grids, medians, sc, res);
-    peak_impl(eng, g, sn, geo, grids, medians, opt, opt_in != nullptr, res, sc);
+    int64_t budget = kSurfaceBudget;
+    {
+        std::lock_guard<std::mutex> lk(eng->tables_mu);
+        if (eng->tuning.surface_budget_bytes > 0) budget = eng->tuning.surface_budget_bytes;
+    }
+    const int64_t chunk = std::max<int64_t>(1, budget / (P * (int64_t)sizeof(double)));
+    if (res->per_snapshot || chunk >= geo.S) {
+        auto* grids = sc.alloc<double>((int64_t)geo.S * P);
+        correlate_steps_impl(eng, g, sn, geo, 0, geo.S, opt, grids, medians, sc, res);
+        peak_impl(eng, g, sn, geo, grids, medians, opt, opt_in != nullptr, res, sc);
+    } else {
+        // per-snapshot surfaces not wanted and over budget: snapshots in chunks,
+        // each added to the running accumulated surface in snapshot order
+        // (bit-identical to accumulating them all at once)
+        double* acc = opt_in != nullptr && res->accumulated_device ? res->accumulated_device
+                                                                   : sc.alloc<double>(P);
+        auto* grids = sc.alloc<double>(chunk * P);
+        dg_result part{};
+        for (int s0 = 0; s0 < geo.S; s0 += (int)chunk) {
+            const int s1 = std::min<int>(geo.S, s0 + (int)chunk);
+            reset_stats(&part);
+            correlate_steps_impl(eng, g, sn, geo, s0, s1, opt, grids,
+                                 medians ? medians + s0 : nullptr, sc, &part);
+            launch_accumulate(grids, s1 - s0, P, acc, sc.st, s0 == 0);
+            res->n_refined += part.n_refined;
+            res->sum_overlap_samples += part.sum_overlap_samples;
+            res->kernel_launches += part.kernel_launches + 1;
+            res->correlate_launches += part.correlate_launches;
+            res->moment_ffma2 += part.moment_ffma2;
+            res->evaluate_ffma2 += part.evaluate_ffma2;
+            res->evaluate_tc_flop += part.evaluate_tc_flop;
+            res->direct_steps += part.direct_steps;
+            res->moments_ms += part.moments_ms;
+            res->evaluate_ms += part.evaluate_ms;
+            res->correlate_ms += part.correlate_ms;
+        }
+        peak_impl(eng, g, sn, geo, nullptr, medians, opt, opt_in != nullptr, res, sc, 0, acc);
+    }
     if (opt.profile) {
         CK(cudaEventRecord(e1, sc.st));
         CK(cudaEventSynchronize(e1));

@@ -138,6 +138,29 @@ __device__ __forceinline__ double bucket_z2_part(const double* __restrict__ e1,
     return acc;
 }
 
+// The block-moment refinement test. coh in [0, 1] is the
+// bucket's coherence: 0 when its moments carry only the energy an incoherent
+// (noise) product stream gives them, rho = sum_m Q_m^2 / <T_m^2> / (R ||z||_2^2)
+// ~ 1, and 1 from rho >= 1.5 on (a tone, or a chirp product aliasing onto the
+// block length, makes some moments coherent). The FP32 value S is re-evaluated
+// when it is small next to the noise floor ||z||_2 (tau_noise for incoherent
+// buckets, whose rounding has a ~3x smaller constant, rising to tau) or next
+// to the coherent part of its error scales, sqrt(max(en, qe2) - (1 - coh) zfloor)
+// (tau); a fully coherent bucket gets S < tau sqrt(max(en, qe2, zfloor)).
+__device__ __forceinline__ double bucket_coherence(const float* qm2, int R, double zfloor) {
+    double q = 0.0;
+    for (int m = 0; m < R; ++m) q += (m ? 2.0 : 1.0) * (double)qm2[m];  // <T_0^2> = 1, <T_m^2> ~ 1/2
+    const double rho = zfloor > 0.0 ? q / ((double)R * zfloor) : 1.0;
+    return fmin(fmax((rho - 1.0) * 2.0, 0.0), 1.0);
+}
+
+__device__ __forceinline__ bool refine_moment(double s, double en, double qe2, double zfloor,
+                                              double coh, float tau, float tau_noise) {
+    const double tf = (double)tau_noise + ((double)tau - (double)tau_noise) * coh;
+    const double ex = fmax(fmax(en, qe2) - (1.0 - coh) * zfloor, 0.0);
+    return s < tf * sqrt(zfloor) || s < (double)tau * sqrt(ex);
+}
+
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
     float2 d;
     asm("{.reg .b64 ra, rb, rd;\n\t"

@@ -24,7 +24,7 @@
 // (two tcgen05.ld.32x32b.x16) and runs the group sums as
 // k_evaluate does: A, V, |C_b|^2 on FFMA2 with W_j = W_1^j (FP64 recurrence,
 // rounded once), FP64 anchors across groups, refinement flag
-// S < tau max(sqrt(sum |C_b|^2), sqrt(sum_m a_m^2 Q_m^2), ||z||_2).
+// refine_moment (dg_device.cuh).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -157,7 +157,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
               int* __restrict__ queue, const int* __restrict__ sorted,
               const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p,
               int B, const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
-              uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau,
+              uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau, float tau_noise,
               const double* __restrict__ e1, const double* __restrict__ e2, int N) {
     constexpr int G = kTcG;
     static_assert(R <= kTcK && R % 2 == 0, "moments");
@@ -290,6 +290,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         double zfloor = 0.0;
 #pragma unroll
         for (int w = 0; w < kTcThreads / 32; ++w) zfloor += z2w[w];
+        const double coh = bucket_coherence(qm2, R, zfloor);
 
         for (int t0 = 0; t0 < bk.count; t0 += 128) {
             const double nu = p >= 0 ? fd / fs - nu_c : 0.0;
@@ -427,7 +428,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             if (pc >= 0) {
                 const double sv = sqrt(acc_re * acc_re + acc_im * acc_im);
                 s_out[pc] = sv;
-                if (sv < (double)tau * sqrt(fmax(fmax(en, qe2), zfloor))) {
+                if (refine_moment(sv, en, qe2, zfloor, coh, tau, tau_noise)) {
                     const int64_t e = flag_base + pc;
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
@@ -446,8 +447,8 @@ template <int R>
 void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                          const int* sorted, const double* fdoa, double fs, const double* nu_c,
                          int B, const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
-                         int64_t flag_base, float tau, const double* e1, const double* e2, int N,
-                         int sm_count, cudaStream_t st) {
+                         int64_t flag_base, float tau, float tau_noise, const double* e1,
+                         const double* e2, int N, int sm_count, cudaStream_t st) {
     auto kern = k_evaluate_tc<R>;
     const TcLayout L = tc_layout(nbmax, R);
     // CTAs per SM bounded by TMEM (512 columns per SM): request enough shared
@@ -466,7 +467,8 @@ void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue
     int grid = sm_count * resident;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
     kern<<<grid, kTcThreads, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c, B, mom,
-                                         nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N);
+                                         nbmax, s_out, flag_bits, flag_base, tau, tau_noise, e1,
+                                         e2, N);
 }
 
 }  // namespace
@@ -479,11 +481,13 @@ bool evaluate_tc_supported(int nbmax, int R) {
 void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                        uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
-                        const double* e2, int N, int sm_count, cudaStream_t st) {
+                        uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,
+                        const double* e1, const double* e2, int N, int sm_count,
+                        cudaStream_t st) {
 #define DG_TC_CASE(RR)                                                                          \
     evaluate_tc_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
-                            mom, nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N, sm_count, st)
+                            mom, nbmax, s_out, flag_bits, flag_base, tau, tau_noise, e1, e2, N, \
+                            sm_count, st)
     switch (R) {
         case 8: DG_TC_CASE(8); break;
         case 10: DG_TC_CASE(10); break;

@@ -90,13 +90,18 @@ constexpr int kL = 16;       // phasor table length (samples per inner block)
 // showed ~1e-6 ||z||_2 errors (tests/gpu_error_diag.py): 0.04 -> 2.5e-5, 0.06
 // keeps them near 1.7e-5 (tests/test_gpu_error_model.py).
 constexpr float kRefineTau = 0.06f;
-// block-moment correlator: S < tau * max(sqrt(A), Q). Worst
-// unrefined relative error on the stress scenes of tests/test_gpu_error_model.py
-// (+30/+40 dB tone and chirp, forced block lengths at the truncation edge) vs the
-// reference, by tau (tests/gpu_tau_sweep.py): 0.015 -> 3.2e-5, 0.02 -> 2.3e-5,
-// 0.025 -> 2.1e-5 at C3 cost 49.9 / 51.9 / 54.9 ms; 0.02 keeps >= 4x margin to the
-// 1e-4 contract on every scene.
+// block-moment correlator (refine_moment in dg_device.cuh): a
+// value is re-evaluated in FP64 when S is small next to the bucket's noise floor
+// ||z||_2 (tau_noise for incoherent buckets rising to tau for coherent ones) or
+// next to the coherent part of its error scales (tau). Worst unrefined relative
+// error on the stress scenes of tests/test_gpu_error_model.py vs the reference
+// (tests/gpu_tau_sweep.py): tau 0.015 -> 2.5e-5, 0.02 -> 1.8e-5 (coherent scenes);
+// tau_noise 0.005 / 0.01 / 0.02 -> 5.1e-5 / 3.7e-5 / 2.0e-5 on a +40 dB chirp with
+// the moments forced (its aliased product tones read as incoherent) and 2.3e-5 /
+// 1.5e-5 / 1.2e-5 on the C3 scene at 1 km, at 7k / 20k / 78k refined elements per C3
+// solve (52.0 / 52.0 / 55.7 ms). 0.014 keeps >= 5x margin on every scene.
 constexpr float kMomentRefineTau = 0.02f;
+constexpr float kNoiseRefineTau = 0.014f;
 
 // --------------------------------------------------------------------------
 // launchers (dg_kernels.cu). All asynchronous on `st`.
@@ -167,8 +172,8 @@ size_t evaluate_smem_bytes(int nbmax, int R);
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                      int max_buckets, const int* sorted, const double* fdoa, double fs,
                      const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                     uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
-                     const double* e2, int N, int sm_count, cudaStream_t st);
+                     uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,
+                     const double* e1, const double* e2, int N, int sm_count, cudaStream_t st);
 
 // surface writers (dg_writers.cu): "%.17g" text in kFmtSlot-byte slots, CSV rows
 // at scanned offsets, P5 pixels
@@ -223,8 +228,9 @@ bool evaluate_tc_supported(int nbmax, int R);
 void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                        uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
-                        const double* e2, int N, int sm_count, cudaStream_t st);
+                        uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,
+                        const double* e1, const double* e2, int N, int sm_count,
+                        cudaStream_t st);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for the current device, once
 // per (call site, device, larger size): function attributes are per device and one
@@ -273,7 +279,9 @@ void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st);
 // steps[step[u]][i] += units[u][i], u in order (parts of split steps: exact)
 void launch_sum_units(const double* units, int U, int64_t n, const int* step, double* steps,
                       cudaStream_t st);
-void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st);
+// acc = [acc +] sum_s grids[s] in snapshot order (first: no running sum)
+void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st,
+                       bool first = true);
 void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,
                 cudaStream_t st);
 // near-peak selection for the exact re-rank: count of cells >= thr; the cells

@@ -808,11 +808,14 @@ __global__ void k_scale(double* __restrict__ v, int64_t P, const double* __restr
         v[i] = __ddiv_rn(v[i], m);
 }
 
+// first: acc = g_0 + g_1 + ... (accumulate_grids, snapshot order); otherwise the
+// chunk continues a running sum: acc = acc + g_0 + ... (the same additions in
+// the same order, so a run accumulated chunk by chunk is bit-identical)
 __global__ void k_accumulate(const double* __restrict__ grids, int S, int64_t P,
-                             double* __restrict__ acc) {
+                             double* __restrict__ acc, int first) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
-        double a = grids[p];
+        double a = first ? grids[p] : __dadd_rn(acc[p], grids[p]);
         for (int s = 1; s < S; ++s) a = __dadd_rn(a, grids[(int64_t)s * P + p]);
         acc[p] = a;
     }
@@ -1425,8 +1428,9 @@ void launch_scale(double* v, int64_t P, const double* median, cudaStream_t st) {
     k_scale<<<blocks_for(P, 256), 256, 0, st>>>(v, P, median);
 }
 
-void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st) {
-    k_accumulate<<<blocks_for(P, 256), 256, 0, st>>>(grids, S, P, acc);
+void launch_accumulate(const double* grids, int S, int64_t P, double* acc, cudaStream_t st,
+                       bool first) {
+    k_accumulate<<<blocks_for(P, 256), 256, 0, st>>>(grids, S, P, acc, first ? 1 : 0);
 }
 
 void launch_max(const double* v, int64_t P, double* partial, int n_partial, double* out,

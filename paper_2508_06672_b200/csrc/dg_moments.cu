@@ -272,7 +272,7 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
            int* __restrict__ queue, const int* __restrict__ sorted,
            const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p, int B,
            const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
-           uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau,
+           uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau, float tau_noise,
            const double* __restrict__ e1, const double* __restrict__ e2, int N) {
     extern __shared__ float4 smem4[];
     __shared__ uint64_t full[kEvalStages], empty[kEvalStages];
@@ -353,6 +353,7 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
         double zfloor = bucket_z2_part(e1, e2, N, bk.d, B, lane, 32);
 #pragma unroll
         for (int o = 16; o; o >>= 1) zfloor += __shfl_xor_sync(0xffffffffu, zfloor, o);
+        const double coh = bucket_coherence(qm2, R, zfloor);
 
         for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
             int p[kEvalNC];
@@ -446,7 +447,7 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
                 if (p[c] < 0) continue;
                 const double sv = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
                 s_out[p[c]] = sv;
-                if (sv < (double)tau * sqrt(fmax(fmax(en[c], qe2[c]), zfloor))) {
+                if (refine_moment(sv, en[c], qe2[c], zfloor, coh, tau, tau_noise)) {
                     const int64_t e = flag_base + p[c];
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
@@ -535,8 +536,8 @@ template <int R>
 void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                       const int* sorted, const double* fdoa, double fs, const double* nu_c, int B,
                       const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
-                      int64_t flag_base, float tau, const double* e1, const double* e2, int N,
-                      int sm_count, cudaStream_t st) {
+                      int64_t flag_base, float tau, float tau_noise, const double* e1,
+                      const double* e2, int N, int sm_count, cudaStream_t st) {
     auto kern = k_evaluate<R, kEvalG>;
     const size_t smem = evaluate_smem(nbmax, R);
     static size_t attr[64] = {};
@@ -544,8 +545,8 @@ void evaluate_variant(const Bucket* buckets, const int* n_buckets, int* queue, i
     int grid = sm_count * 4;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
     kern<<<grid, 32 * kEvalWarps, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c,
-                                              B, mom, nbmax, s_out, flag_bits, flag_base, tau, e1,
-                                              e2, N);
+                                              B, mom, nbmax, s_out, flag_bits, flag_base, tau,
+                                              tau_noise, e1, e2, N);
 }
 
 }  // namespace
@@ -593,11 +594,12 @@ size_t evaluate_smem_bytes(int nbmax, int R) { return evaluate_smem(nbmax, R); }
 void launch_evaluate(int R, const Bucket* buckets, const int* n_buckets, int* queue,
                      int max_buckets, const int* sorted, const double* fdoa, double fs,
                      const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
-                     uint32_t* flag_bits, int64_t flag_base, float tau, const double* e1,
-                     const double* e2, int N, int sm_count, cudaStream_t st) {
+                     uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,
+                     const double* e1, const double* e2, int N, int sm_count, cudaStream_t st) {
 #define DG_EVAL_CASE(RR)                                                                    \
     evaluate_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
-                         mom, nbmax, s_out, flag_bits, flag_base, tau, e1, e2, N, sm_count, st)
+                         mom, nbmax, s_out, flag_bits, flag_base, tau, tau_noise, e1, e2, N,   \
+                         sm_count, st)
     switch (R) {
         case 8: DG_EVAL_CASE(8); break;
         case 10: DG_EVAL_CASE(10); break;

@@ -19,7 +19,7 @@ import test_gpu_error_model as em  # noqa: E402
 from oracle.bindings import RefLib  # noqa: E402
 
 MOMENT_CASES = ["tone+40_B640", "tone+40_B512", "tone+40_B768", "tone+40_1km", "chirp+40_B768",
-                "chirp+40"]
+                "chirp+40", "four-20_1km"]
 
 
 def c3_time(grid, staged, reps=5):
@@ -54,16 +54,17 @@ def main():
     out = []
     taus = [float(t) for t in (sys.argv[2].split(",") if len(sys.argv) > 2 else
                                ["0.015", "0.02", "0.025", "0.03"])]
+    key = sys.argv[3] if len(sys.argv) > 3 else "refine_tau"  # or noise_refine_tau
     for tau in taus:
-        row = {"tau": tau}
+        row = {key: tau}
         for name in MOMENT_CASES:
             kw, tuning = em.CASES[name]
-            em.CASES[name] = (kw, {**tuning, "correlator": "moments", "refine_tau": tau,
+            em.CASES[name] = (kw, {**tuning, "correlator": "moments", key: tau,
                                    "allow_weaker_refine": 1})
             r = em.run_case(b2, ref, name)
             em.CASES[name] = (kw, tuning)
             row[name] = r["max_rel"]
-        eng.set_tuning(refine_tau=tau, allow_weaker_refine=1)
+        eng.set_tuning(**{key: tau, "allow_weaker_refine": 1})
         row["c3_ms"], row["c3_refined"] = c3_time(grid, staged)
         eng.reset_tuning()
         print(json.dumps(row), flush=True)

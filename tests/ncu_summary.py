@@ -35,10 +35,15 @@ def raw(path):
 def main():
     print("# ncu --set full --clock-control none --import-source on, one mid-solve launch per kernel")
     print("# command: ncu --profile-from-start off --set full --import-source on --clock-control "
-          "none -k regex:<kernel> -s 20 -c 1 -o ... python tests/profile_solve.py  (C3)")
+          "none -k regex:<kernel> [-s 20] -c 1 -o ... python tests/profile_solve.py  (C3; "
+          "k_correlate: tests/profile_plugin.py, the BenchWorkload plugin pass)")
     for arg in sys.argv[1:]:
         name, path = arg.split("=", 1)
-        hdr, units, vals = raw(path)
+        try:
+            hdr, units, vals = raw(path)
+        except (subprocess.CalledProcessError, IndexError, FileNotFoundError):
+            print(f"== {name}\n  (no report at {path})")
+            continue
         col = {h: i for i, h in enumerate(hdr)}
         print(f"== {name}")
         for m in METRICS:

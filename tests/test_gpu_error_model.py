@@ -64,6 +64,8 @@ CASES = {
     "chirp+40_B768": (dict(kind="chirp", snr=40.0, half_km=450.0),
                       dict(correlator="moments", moment_block=768)),
     "tone+40_B512": (dict(kind="tone", snr=40.0), dict(correlator="moments", moment_block=512)),
+    # noise-dominated moment path at C3 density (four emitters at -20 dB, 1 km)
+    "four-20_1km": (dict(kind="four", snr=-20.0, half_km=200.0, spacing_km=1.0), {}),
     "tone+40_1km": (dict(kind="tone", snr=40.0, half_km=200.0, spacing_km=1.0), {}),
     "tone+40_N250k": (dict(kind="tone", snr=40.0, dur=0.05, half_km=500.0), {}),
     "chirp+40_N250k": (dict(kind="chirp", snr=40.0, dur=0.05, half_km=500.0), {}),

@@ -466,3 +466,21 @@ def test_geolocate_errors(b2):
         b2.geolocate_arrays(grid, states, caps, 1e6, 0.0)
     with pytest.raises(ValueError, match="no snapshots"):
         b2.geolocate_snapshots([], grid)
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_chunked_accumulation_bit_identical(b2, ref, tune, normalize):
+    """Runs over the per-snapshot surface budget are solved in snapshot chunks,
+    each added to the running accumulated surface in snapshot order: the same
+    additions in the same order, so the surface and the peak are bit-identical."""
+    sc = load_scene(ref, "DESK_FOURJAM")
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    staged = b2.StagedSnapshots(sc.states, sc.captures, sc.fs, sc.fc)
+    opts = b2.GeolocateOptions(k_sigma=sc.k_sigma, exclusion_radius_cells=sc.radius,
+                               normalize_per_snapshot=normalize)
+    whole = b2.geolocate_staged(grid, staged, opts, want_surface=True)
+    tune(surface_budget_bytes=3 * grid.size() * 8)  # chunks of 3 snapshots
+    chunked = b2.geolocate_staged(grid, staged, opts, want_surface=True)
+    assert np.array_equal(chunked.accumulated.values, whole.accumulated.values)
+    assert (chunked.argmax_index, chunked.argmax_value) == (whole.argmax_index, whole.argmax_value)
+    assert [d.grid_index for d in chunked.detections] == [d.grid_index for d in whole.detections]
