@@ -635,7 +635,7 @@ def measured_peaks():
         return {}
 
 
-NCU_SUMMARY = "profiles/r01_ncu_kernels.txt"
+NCU_SUMMARY = "profiles/r02_ncu_kernels.txt"
 
 
 def ncu_traffic(kernel):
