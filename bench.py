@@ -264,15 +264,25 @@ def ref_worker(args):
                             workers=workers, batch_size=4096)
         times.append(time.perf_counter() - t0)
     P = len(res["accumulated"])
-    print(json.dumps({"times": times[args.warmup:], "points": P,
-                      "snapshots": int(caps.shape[0]), "workers": workers,
-                      "argmax": int(np.argmax(res["accumulated"]))}))
+    out = {"times": times[args.warmup:], "points": P, "snapshots": int(caps.shape[0]),
+           "workers": workers, "argmax": int(np.argmax(res["accumulated"]))}
+    if args.extra_baselines:
+        # the reference's SerialBackend on one core, and its
+        # ParallelBatchedBackend at the paper's batch size of 8, on two snapshots
+        s2 = min(2, caps.shape[0])
+        for key, backend, w, bs in (("serial_1core", "serial", 1, 4096),
+                                    ("parallel_batch8", "parallel", workers, 8)):
+            t0 = time.perf_counter()
+            ref.geolocate(states[:s2], caps[:s2], cfg["fs"], FC, bounds, spacing, 0.0,
+                          backend=backend, workers=w, batch_size=bs)
+            out[key] = P * s2 / (time.perf_counter() - t0)
+    print(json.dumps(out))
 
 
-def run_ref_child(args, steps, warmup, sample_km, sample_snapshots, timeout):
+def run_ref_child(args, steps, warmup, sample_km, sample_snapshots, timeout, extra=False):
     cmd = [sys.executable, os.path.abspath(__file__), "--ref-worker", "--config", args.config,
            "--steps", str(steps), "--warmup", str(warmup), "--sample-km", str(sample_km),
-           "--sample-snapshots", str(sample_snapshots)]
+           "--sample-snapshots", str(sample_snapshots)] + (["--extra-baselines"] if extra else [])
     hangs = 0
     for _attempt in range(2):
         try:
@@ -478,14 +488,22 @@ def b200_arm(args, rank, world):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            d = run_ref_child(args, 1, 0, args.sample_km, args.cpu_sample_snapshots, timeout=900)
+            d = run_ref_child(args, 1, 0, args.sample_km, args.cpu_sample_snapshots, timeout=900,
+                              extra=True)
             cpu = {"value": d["points"] * d["snapshots"] / d["times"][0], "unit": UNIT,
                    "cores": d["workers"], "kind": "reference",
                    "sample": (f"{args.config} footprint at {args.sample_km:g} km stride "
                               f"({d['points']} points) x {d['snapshots']} snapshots, reference "
                               f"geolocate_snapshots, ParallelBatchedBackend({d['workers']}) batch "
                               f"4096, {d['times'][0]:.1f} s; {cpu_model()}"),
-                   "hangs": d["hangs"]}
+                   "hangs": d["hangs"],
+                   "serial_1core": {"value": d.get("serial_1core"), "unit": UNIT, "cores": 1,
+                                    "sample": "the same footprint, 2 snapshots, SerialBackend"},
+                   "parallel_batch8": {"value": d.get("parallel_batch8"), "unit": UNIT,
+                                       "cores": d["workers"],
+                                       "sample": "the same footprint, 2 snapshots, "
+                                                 "ParallelBatchedBackend batch 8 (the paper's "
+                                                 "default)"}}
         except Exception as e:  # the baseline is reported, never the product
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"[:300]}
@@ -687,6 +705,7 @@ def main():
                     help=argparse.SUPPRESS)
     ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--ref-plugin-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--extra-baselines", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.ref_worker:
         return ref_worker(args)
