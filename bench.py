@@ -604,6 +604,16 @@ def plugin_leg(args, b2, fp32_peak, with_cpu):
     best = rows[str(PLUGIN_POINTS)]
     # k_correlate FMA-pipe work: 2 FFMA2 per candidate-sample (A, B) = 8 FLOP
     fma_tf = 8.0 * ovl / best["s_per_run"] / 1e12
+    # the kernel's own launch time from the committed ncu launch list of the same
+    # pass (tests/profile_plugin.py); the live figure above includes the call's
+    # staging, planning and copies
+    kern_us = None
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r02_launches_plugin_summary.txt")):
+            if "k_correlate" in line:
+                kern_us = float(line.split()[-2])
+    except (OSError, ValueError, IndexError):
+        pass
     res = {"workload": f"BenchWorkload {PLUGIN_POINTS} points x {PLUGIN_SAMPLES} samples, seed 1 "
                        "(bench.hpp:65-88, regenerated bit for bit)",
            "overlap_samples": ovl, "batches": rows,
@@ -611,7 +621,13 @@ def plugin_leg(args, b2, fp32_peak, with_cpu):
                            "unit": "TFLOP/s", "frac": fma_tf / fp32_peak if fp32_peak else None,
                            "flop_definition": "8 per overlapping candidate-sample (2 FFMA2: the "
                                               "A / B phasor-table MACs), whole call incl. "
-                                              "staging and copies"},
+                                              "staging and copies",
+                           "kernel_us_ncu": kern_us,
+                           "achieved_kernel": 8.0 * ovl / (kern_us * 1e-6) / 1e12 if kern_us else None,
+                           "frac_kernel": (8.0 * ovl / (kern_us * 1e-6) / 1e12 / fp32_peak
+                                           if kern_us and fp32_peak else None),
+                           "kernel_source": "profiles/r02_launches_plugin_summary.txt (ncu "
+                                            "gpu__time_duration of the same pass)"},
            "reference_equivalent_tflops": 20.0 * ovl / best["s_per_run"] / 1e12}
     if with_cpu and not args.no_cpu_baseline:
         try:
