@@ -1711,14 +1711,19 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         hpg[u] = geo.hpg[units[u].sp];
         hstep[u] = units[u].sp;
     }
-    auto* upg = sc.alloc<PairGeom>(SPl);
     auto* ustep = sc.alloc<int>(SPl);
-    CK(cudaMemcpyAsync(upg, hpg.data(), SPl * sizeof(PairGeom), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(ustep, hstep.data(), SPl * sizeof(int), cudaMemcpyHostToDevice, st));
 
     Pipeline pl;
     pl.init(sc, eng, P, sn->N, SPl, opt.profile ? 1 : 2, eng->lane);
     const double* e64 = energy_prefix(sn, st);
+    // the geometry pass's receiver-group tables, one per 64 units of a window
+    std::vector<GeoScratch> geo_ws((pl.slots + 63) / 64);
+    for (auto& w : geo_ws) {
+        w.d_rx = sc.alloc<dg_state>(128);
+        w.d_groups = sc.alloc<GeoGroup>(64);
+        w.d_upair = sc.alloc<int2>(64);
+    }
     // refine flags: one bitmap row of whole words per unit (bit p of unit i at
     // i * P32 + p), so batches of units are refined on a side stream while the
     // lanes correlate later units (FP64 refinement next to FP32 correlation)
@@ -1739,9 +1744,10 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         // phase A: geometry of the whole window in one pass; bins from the
         // histograms, B / R / centre frequency from the FP32 lattice ranges
         if (w0 > 0) CK(cudaMemsetAsync(pl.hist, 0, sizeof(int) * pl.nbins * nw, st));
-        launch_geometry_steps(g->x, g->y, g->z, P, upg + w0, nw, fs, wl, pl.N, pl.d_slot(0),
-                              pl.rank_slot(0), pl.fdoa_slot(0), pl.hist_slot(0), pl.nbins, raw + (int64_t)w0 * P,
-                              pl.overlap, pl.err, st);
+        launch_geometry_units(g->x, g->y, g->z, P, hpg.data() + w0, nw, fs, wl, pl.N,
+                              pl.d_slot(0), pl.rank_slot(0), pl.fdoa_slot(0), pl.hist_slot(0),
+                              pl.nbins, raw + (int64_t)w0 * P, pl.overlap, pl.err, geo_ws.data(),
+                              st);
         launch_hist_range(pl.hist_slot(0), pl.nbins, nw, pl.N, pl.range, st);
         launches += (nw + 63) / 64 + 1;
         if (w0 == 0) {  // the rest of the run's state, while the first geometry pass runs

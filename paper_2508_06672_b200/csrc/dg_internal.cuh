@@ -115,12 +115,27 @@ void launch_geometry_hist(const double* x, const double* y, const double* z, int
                           int* rank_out, double* fdoa_out, int* hist, double* s_out,
                           unsigned long long* overlap, int* err, StepRange* range,
                           cudaStream_t st);
-// every step of a window in one pass: d/fdoa/surface slices of stride P,
-// histograms of stride nbins (no exact ranges; see k_geometry_steps)
-void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
-                           const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
+// every unit of a window in one pass, receivers shared within groups (the pairs
+// of a snapshot): d/rank/fdoa/surface slices of stride P, histograms of stride
+// nbins. `pg` is HOST memory; the grouping tables go through `ws` (one per 64
+// units of the window: pinned-free staging, device tables allocated by the caller).
+struct GeoGroup {
+    int rx0, nrx, u0, nu;  // receiver table slice, unit range
+};
+struct GeoScratch {
+    dg_state rx[128];
+    GeoGroup groups[64];
+    int2 upair[64];
+    int nrx = 0, ng = 0;
+    dg_state* d_rx = nullptr;
+    GeoGroup* d_groups = nullptr;
+    int2* d_upair = nullptr;
+};
+void launch_geometry_units(const double* x, const double* y, const double* z, int64_t P,
+                           const PairGeom* pg_host, int n, double fs, double wl, int N, int* d_out,
                            int* rank_out, double* fdoa_out, int* hist, int nbins, double* s_out,
-                           unsigned long long* overlap, int* err, cudaStream_t st);
+                           unsigned long long* overlap, int* err, GeoScratch* ws,
+                           cudaStream_t st);
 // per capture (n_caps rows of `stride` elements) the exclusive prefix sums of
 // |y|^2 in FP64: out[c][k], k <= N
 void launch_energy_prefix(const double2* y, int64_t stride, int64_t n_caps, int64_t N,

@@ -15,6 +15,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstring>
 #include <float.h>
 #include <limits.h>
 #include <math.h>
@@ -240,37 +241,74 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
     ra.flush(range);
 }
 
-// Phase A of a window of steps in one pass: each thread loads its candidate
-// once and predicts the offsets of every step of the window (receiver states
-// staged in shared memory), writing d[s][P], fdoa[s][P], the per-step TDOA
-// histograms and S = 0 for candidates without overlap. The ranges are not
+// Phase A of a window of units in one pass: each thread loads its candidate
+// once and predicts the offsets of every unit of the window, writing d[u][P],
+// rank[u][P], fdoa[u][P], the per-unit TDOA histograms and S = 0 for candidates
+// without overlap. The units come in groups that share receivers (the pairs of
+// one snapshot: correlate_snapshot_all_pairs, geolocate.hpp:79-94), and every
+// receiver's delay and Doppler (predict_geometry, geometry.hpp:51-64) is
+// computed once per candidate and group, then differenced for each pair — the
+// same operations as predict_pair_offsets on each pair, so bit-identical, with
+// R instead of R(R-1) receiver evaluations per snapshot. The ranges are not
 // reduced here: the bins come from the histograms (k_hist_range), B / R / the
 // centre frequency from the FP32 lattice ranges (k_range_fp32).
-constexpr int kGeoStepsMax = 64;  // steps per launch (shared-memory receiver table)
+constexpr int kGeoUnitsMax = 64;  // units per launch (shared-memory tables)
+constexpr int kGeoRxMax = 8;      // receivers per group
 
 __global__ void __launch_bounds__(256)
-k_geometry_steps(const double* __restrict__ x, const double* __restrict__ y,
-                 const double* __restrict__ z, int64_t P, const PairGeom* __restrict__ pg, int n,
-                 double fs, double wl, int N, int* __restrict__ d_out, int* __restrict__ rank_out,
+k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
+                 const double* __restrict__ z, int64_t P, const dg_state* __restrict__ rx,
+                 int nrx, const GeoGroup* __restrict__ groups, int ng,
+                 const int2* __restrict__ upair, int n, double fs, double wl, int N,
+                 int* __restrict__ d_out, int* __restrict__ rank_out,
                  double* __restrict__ fdoa_out, int* __restrict__ hist, int nbins,
                  double* __restrict__ s_out, unsigned long long* __restrict__ overlap,
                  int* __restrict__ err) {
-    __shared__ PairGeom sg[kGeoStepsMax];
-    for (int i = threadIdx.x; i < n * (int)(sizeof(PairGeom) / 8); i += blockDim.x)
-        reinterpret_cast<double*>(sg)[i] = reinterpret_cast<const double*>(pg)[i];
+    __shared__ dg_state srx[2 * kGeoUnitsMax];
+    __shared__ GeoGroup sgr[kGeoUnitsMax];
+    __shared__ int2 sup[kGeoUnitsMax];
+    for (int i = threadIdx.x; i < nrx * (int)(sizeof(dg_state) / 8); i += blockDim.x)
+        reinterpret_cast<double*>(srx)[i] = reinterpret_cast<const double*>(rx)[i];
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) sgr[i] = groups[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sup[i] = upair[i];
     __syncthreads();
     unsigned long long ovl = 0;
     RangeAcc ra;  // not flushed: ranges come from k_hist_range / k_range_fp32
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
         const double cx = x[p], cy = y[p], cz = z[p];
-        for (int s = 0; s < n; ++s) {
-            long long tdoa;
-            double fdoa;
-            if (!offsets_exact(cx, cy, cz, sg[s], fs, wl, &tdoa, &fdoa)) atomicExch(err, 1);
-            emit_point(p, tdoa, fdoa, N, d_out + (int64_t)s * P, rank_out + (int64_t)s * P,
-                       fdoa_out + (int64_t)s * P,
-                       hist + (int64_t)s * nbins, s_out + (int64_t)s * P, ovl, ra);
+        for (int g = 0; g < ng; ++g) {
+            const GeoGroup gr = sgr[g];
+            double del[kGeoRxMax], dop[kGeoRxMax];
+            bool ok[kGeoRxMax];
+#pragma unroll
+            for (int r = 0; r < kGeoRxMax; ++r)
+                if (r < gr.nrx) ok[r] = geometry_exact(cx, cy, cz, srx[gr.rx0 + r], wl, &del[r], &dop[r]);
+            for (int u = gr.u0; u < gr.u0 + gr.nu; ++u) {
+                const int2 ij = sup[u];
+                double di = 0.0, fi = 0.0, dj = 0.0, fj = 0.0;
+                bool oki = true, okj = true;
+#pragma unroll
+                for (int r = 0; r < kGeoRxMax; ++r) {
+                    if (r == ij.x) {
+                        di = del[r];
+                        fi = dop[r];
+                        oki = ok[r];
+                    }
+                    if (r == ij.y) {
+                        dj = del[r];
+                        fj = dop[r];
+                        okj = ok[r];
+                    }
+                }
+                // predict_pair_offsets (geometry.hpp:73-83): llround ties away from zero
+                const long long tdoa = llround(__dmul_rn(__dsub_rn(dj, di), fs));
+                const double fdoa = __dsub_rn(fj, fi);
+                if (!(oki && okj)) atomicExch(err, 1);
+                emit_point(p, tdoa, fdoa, N, d_out + (int64_t)u * P, rank_out + (int64_t)u * P,
+                           fdoa_out + (int64_t)u * P, hist + (int64_t)u * nbins,
+                           s_out + (int64_t)u * P, ovl, ra);
+            }
         }
     }
     ovl = warp_sum_u64(ovl);
@@ -1322,15 +1360,55 @@ void launch_geometry_hist(const double* x, const double* y, const double* z, int
                                                         fdoa_out, hist, s_out, overlap, err, range);
 }
 
-void launch_geometry_steps(const double* x, const double* y, const double* z, int64_t P,
+void launch_geometry_units(const double* x, const double* y, const double* z, int64_t P,
                            const PairGeom* pg, int n, double fs, double wl, int N, int* d_out,
                            int* rank_out, double* fdoa_out, int* hist, int nbins, double* s_out,
-                           unsigned long long* overlap, int* err, cudaStream_t st) {
-    for (int s0 = 0; s0 < n; s0 += kGeoStepsMax) {
-        const int m = n - s0 < kGeoStepsMax ? n - s0 : kGeoStepsMax;
-        k_geometry_steps<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
-            x, y, z, P, pg + s0, m, fs, wl, N, d_out + (int64_t)s0 * P, rank_out + (int64_t)s0 * P,
-            fdoa_out + (int64_t)s0 * P,
+                           unsigned long long* overlap, int* err, GeoScratch* ws,
+                           cudaStream_t st) {
+    const auto same = [](const dg_state& a, const dg_state& b) {
+        return std::memcmp(&a, &b, sizeof(dg_state)) == 0;
+    };
+    for (int s0 = 0; s0 < n; s0 += kGeoUnitsMax) {
+        const int m = n - s0 < kGeoUnitsMax ? n - s0 : kGeoUnitsMax;
+        // host: group consecutive units whose receivers fit one table (the pairs
+        // of one snapshot), receivers deduplicated bitwise
+        GeoScratch& h = ws[s0 / kGeoUnitsMax];
+        h.nrx = h.ng = 0;
+        for (int u = 0; u < m; ++u) {
+            const PairGeom& g = pg[s0 + u];
+            GeoGroup* cur = h.ng ? &h.groups[h.ng - 1] : nullptr;
+            auto find = [&](const dg_state& st) {
+                for (int r = 0; cur && r < cur->nrx; ++r)
+                    if (same(h.rx[cur->rx0 + r], st)) return r;
+                return -1;
+            };
+            int a = find(g.rx_i), b = find(g.rx_j);
+            const int need = (a < 0) + (b < 0 && !same(g.rx_i, g.rx_j));
+            if (!cur || cur->nrx + need > kGeoRxMax) {
+                h.groups[h.ng++] = GeoGroup{h.nrx, 0, u, 0};
+                cur = &h.groups[h.ng - 1];
+                a = b = -1;
+            }
+            if (a < 0) {
+                h.rx[h.nrx++] = g.rx_i;
+                a = cur->nrx++;
+            }
+            if (b < 0) {
+                b = same(g.rx_i, g.rx_j) ? a : -1;
+                if (b < 0) {
+                    h.rx[h.nrx++] = g.rx_j;
+                    b = cur->nrx++;
+                }
+            }
+            h.upair[u] = make_int2(a, b);
+            cur->nu++;
+        }
+        cudaMemcpyAsync(h.d_rx, h.rx, h.nrx * sizeof(dg_state), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(h.d_groups, h.groups, h.ng * sizeof(GeoGroup), cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(h.d_upair, h.upair, m * sizeof(int2), cudaMemcpyHostToDevice, st);
+        k_geometry_units<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
+            x, y, z, P, h.d_rx, h.nrx, h.d_groups, h.ng, h.d_upair, m, fs, wl, N,
+            d_out + (int64_t)s0 * P, rank_out + (int64_t)s0 * P, fdoa_out + (int64_t)s0 * P,
             hist + (int64_t)s0 * nbins, nbins, s_out + (int64_t)s0 * P, overlap, err);
     }
 }

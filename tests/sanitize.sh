@@ -11,7 +11,13 @@ mkdir -p $OUT
 SEL='test_block_moments_vs_reference[1-3000.0-12-640] or test_block_moments_vs_reference[1-3000.0-4000-768] or test_block_moments_vs_reference[1-0.0-200-640] or test_geolocate_scene_vs_reference[DESK_FOURJAM]'
 timeout 1200 compute-sanitizer --tool memcheck --leak-check no \
   python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "$SEL" > $OUT/memcheck.log 2>&1
+# r02: the multi-GPU engine (peer copies, work units with bucket-range parts), chunked
+# accumulation, the plateau re-rank rounds (CUB select / radix sort), unbounded detection
+SEL2='test_multi_engine_bit_identical[2-DESK_FOURJAM-False] or test_chunked_accumulation_bit_identical or test_plateau_argmax_is_first_max[9000] or test_detect_beyond_device_list_vs_reference'
+timeout 1800 compute-sanitizer --tool memcheck --leak-check no \
+  python -m pytest tests/test_gpu_multi.py tests/test_gpu_parity.py tests/test_gpu_peak.py -m gpu -q \
+  -p no:cacheprovider -k "$SEL2" > $OUT/memcheck_r02.log 2>&1
 timeout 1200 compute-sanitizer --tool racecheck \
   python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider \
   -k 'test_block_moments_vs_reference[1-3000.0-12-640]' > $OUT/racecheck.log 2>&1
-tail -n 3 $OUT/memcheck.log $OUT/racecheck.log
+tail -n 3 $OUT/memcheck.log $OUT/memcheck_r02.log $OUT/racecheck.log

@@ -91,6 +91,17 @@ TRIPLE_RX = {
     "emitters": [_chirp(0.1, -0.12, -3, 1e6, 50e-6)],
 }
 
+# four receivers: six pairs per snapshot (the all-pairs sum and the shared
+# per-receiver geometry pass, geolocate.hpp:79-94)
+QUAD_RX = {
+    **_base(3, 5.0, 4e-3, 2.048e6, 123),
+    **_grid(-0.4, 0.4, -0.4, 0.4, 0.02),
+    "backend": "serial", "batch_size": 8, "k_sigma": 5, "exclusion_radius_cells": 5,
+    "receivers": [_orbit(550e3, 53, -0.9, -0.7), _orbit(550e3, 53, 0.9, 0.5),
+                  _orbit(600e3, 80, 0.2, -1.5), _orbit(520e3, 97, -0.4, 0.9)],
+    "emitters": [_chirp(0.1, -0.12, -6, 1e6, 50e-6), _tone(-0.2, 0.2, -8, 1500)],
+}
+
 # BASELINE.json configs; receivers as paper_scenario.cfg
 _PAPER_RX = [_orbit(550e3, 53, -1.2, -1.1), _orbit(550e3, 53, 1.2, -0.7)]
 _FOUR = [_spoofer(0.5, -1.5, -20), _tone(0.5, 1.5, -20), _chirp(-0.5, -1.5, -20),

@@ -484,3 +484,30 @@ def test_chunked_accumulation_bit_identical(b2, ref, tune, normalize):
     assert np.array_equal(chunked.accumulated.values, whole.accumulated.values)
     assert (chunked.argmax_index, chunked.argmax_value) == (whole.argmax_index, whole.argmax_value)
     assert [d.grid_index for d in chunked.detections] == [d.grid_index for d in whole.detections]
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_four_receivers_vs_reference(b2, ref, normalize):
+    """Four receivers, six pairs per snapshot (correlate_snapshot_all_pairs,
+    geolocate.hpp:79-94): per-receiver geometry shared by the pairs of a
+    snapshot, pair sums in the reference's order; against the reference's own
+    geolocate_snapshots, and the multi-GPU engine bit-identical to one GPU."""
+    sc = load_scene(ref, "QUAD_RX")
+    assert sc.n_rx == 4
+    want = ref.geolocate(sc.states, sc.captures, sc.fs, sc.fc, sc.bounds, sc.spacing, sc.alt,
+                         backend="parallel", batch_size=4096, k_sigma=sc.k_sigma,
+                         radius=sc.radius, normalize=normalize, per_snapshot=True)
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt)
+    opts = b2.GeolocateOptions(k_sigma=sc.k_sigma, exclusion_radius_cells=sc.radius,
+                               normalize_per_snapshot=normalize)
+    res = b2.geolocate_arrays(grid, sc.states, sc.captures, sc.fs, sc.fc, opts)
+    per = np.stack([g.values for g in res.per_snapshot])
+    assert rel_err(per, want["per_snapshot"]).max() <= REL_TOL
+    assert res.argmax_index == int(np.argmax(want["accumulated"]))
+    if not normalize:
+        assert res.argmax_value == want["accumulated"][res.argmax_index]
+    assert [d.grid_index for d in res.detections] == [d["grid_index"] for d in want["detections"]]
+    eng = b2.Engine(devices=[0, 0, 0])
+    mgrid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt, engine=eng)
+    many = b2.geolocate_arrays(mgrid, sc.states, sc.captures, sc.fs, sc.fc, opts)
+    assert np.array_equal(many.accumulated.values, res.accumulated.values)
