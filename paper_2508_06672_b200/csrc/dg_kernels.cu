@@ -255,6 +255,9 @@ __global__ void k_geometry_hist(const double* __restrict__ x, const double* __re
 constexpr int kGeoUnitsMax = 64;  // units per launch (shared-memory tables)
 constexpr int kGeoRxMax = 8;      // receivers per group
 
+// KR: receivers per group the launch needs (2 for two-receiver runs: no
+// register tables beyond the pair)
+template <int KR>
 __global__ void __launch_bounds__(256)
 k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
                  const double* __restrict__ z, int64_t P, const dg_state* __restrict__ rx,
@@ -279,17 +282,17 @@ k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
         const double cx = x[p], cy = y[p], cz = z[p];
         for (int g = 0; g < ng; ++g) {
             const GeoGroup gr = sgr[g];
-            double del[kGeoRxMax], dop[kGeoRxMax];
-            bool ok[kGeoRxMax];
+            double del[KR], dop[KR];
+            bool ok[KR];
 #pragma unroll
-            for (int r = 0; r < kGeoRxMax; ++r)
+            for (int r = 0; r < KR; ++r)
                 if (r < gr.nrx) ok[r] = geometry_exact(cx, cy, cz, srx[gr.rx0 + r], wl, &del[r], &dop[r]);
             for (int u = gr.u0; u < gr.u0 + gr.nu; ++u) {
                 const int2 ij = sup[u];
                 double di = 0.0, fi = 0.0, dj = 0.0, fj = 0.0;
                 bool oki = true, okj = true;
 #pragma unroll
-                for (int r = 0; r < kGeoRxMax; ++r) {
+                for (int r = 0; r < KR; ++r) {
                     if (r == ij.x) {
                         di = del[r];
                         fi = dop[r];
@@ -1384,7 +1387,9 @@ void launch_geometry_units(const double* x, const double* y, const double* z, in
             };
             int a = find(g.rx_i), b = find(g.rx_j);
             const int need = (a < 0) + (b < 0 && !same(g.rx_i, g.rx_j));
-            if (!cur || cur->nrx + need > kGeoRxMax) {
+            // a new group unless this unit shares a receiver with the current one
+            // (pairs of one snapshot) and its receivers fit the table
+            if (!cur || (a < 0 && b < 0) || cur->nrx + need > kGeoRxMax) {
                 h.groups[h.ng++] = GeoGroup{h.nrx, 0, u, 0};
                 cur = &h.groups[h.ng - 1];
                 a = b = -1;
@@ -1406,7 +1411,11 @@ void launch_geometry_units(const double* x, const double* y, const double* z, in
         cudaMemcpyAsync(h.d_rx, h.rx, h.nrx * sizeof(dg_state), cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(h.d_groups, h.groups, h.ng * sizeof(GeoGroup), cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(h.d_upair, h.upair, m * sizeof(int2), cudaMemcpyHostToDevice, st);
-        k_geometry_units<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
+        int kr = 2;
+        for (int g = 0; g < h.ng; ++g) kr = std::max(kr, h.groups[g].nrx);
+        auto kern = kr <= 2 ? k_geometry_units<2> : kr <= 4 ? k_geometry_units<4>
+                                                             : k_geometry_units<kGeoRxMax>;
+        kern<<<blocks_for(P, 256, 148LL * 8), 256, 0, st>>>(
             x, y, z, P, h.d_rx, h.nrx, h.d_groups, h.ng, h.d_upair, m, fs, wl, N,
             d_out + (int64_t)s0 * P, rank_out + (int64_t)s0 * P, fdoa_out + (int64_t)s0 * P,
             hist + (int64_t)s0 * nbins, nbins, s_out + (int64_t)s0 * P, overlap, err);
