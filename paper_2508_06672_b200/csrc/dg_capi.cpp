@@ -221,7 +221,6 @@ struct Lane {
     float2 *y1c = nullptr, *y2p = nullptr;
     float2* mom = nullptr;
     size_t mom_cap = 0;
-    double* sfdoa = nullptr;  // candidates' FDOA in bucket order (moment path)
     unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
     cudaEvent_t done = nullptr;
     ~Lane() {
@@ -327,7 +326,6 @@ struct Pipeline {
             }
             CK(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
             L.sorted = sc.alloc<int>(P);
-            L.sfdoa = sc.alloc<double>(P);
             L.tasks = sc.alloc<Task>(max_tasks);
             L.buckets = sc.alloc<Bucket>(std::min<int64_t>(P, nbins));
             L.off = sc.alloc<int>(nbins);
@@ -520,7 +518,7 @@ struct Pipeline {
             launch_bucket(hist_slot(s), pl.bin0, pl.nbins, N, L.off, L.toff, L.boff, L.cursor,
                           L.n_tasks, L.n_buckets, d_slot(s), rank_slot(s), P, L.sorted, L.tasks,
                           L.buckets,
-                          L.ubin, pl.B, st, fdoa_slot(s), L.sfdoa);
+                          L.ubin, pl.B, st);
             launch_center(y1_64, y2, N, nu_c + s, L.y1c, L.y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
             launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
@@ -530,12 +528,12 @@ struct Pipeline {
             const bool tc = use_tc && evaluate_tc_supported(pl.nbmax, pl.R);
             if (tc)
                 launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
-                                   (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
+                                   (int)std::min<int64_t>(P, pl.nbins), L.sorted, fdoa_slot(s), fs,
                                    nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
                                    tau_noise, e1, e2, N, sm_count, st);
             else
                 launch_evaluate(pl.R, L.buckets, L.n_buckets, L.queue,
-                                (int)std::min<int64_t>(P, pl.nbins), L.sorted, L.sfdoa, fs,
+                                (int)std::min<int64_t>(P, pl.nbins), L.sorted, fdoa_slot(s), fs,
                                 nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
                                 tau_noise, e1, e2, N, sm_count, st);
             launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, tc ? 1 : 0, L.work, st);

@@ -155,7 +155,7 @@ template <int R>
 __global__ void __launch_bounds__(kTcThreads, 4)
 k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
               int* __restrict__ queue, const int* __restrict__ sorted,
-              const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p,
+              const double* __restrict__ fdoa, double fs, const double* __restrict__ nu_c_p,
               int B, const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
               uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau, float tau_noise,
               const double* __restrict__ e1, const double* __restrict__ e2, int N) {
@@ -236,7 +236,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         const int nb = bk.nb;
         // the first tile's candidate, loaded now so the latency hides under the B split
         int p = tid < bk.count ? sorted[bk.start + tid] : -1;
-        double fd = tid < bk.count ? sfdoa[bk.start + tid] : 0.0;
+        double fd = p >= 0 ? fdoa[p] : 0.0;
         const float2* mb = ring + sl * L.ring_f2;
         const int ng = (nb + G - 1) / G;
         const int np = 2 * G * ng;  // B rows / TMEM columns used by this bucket
@@ -298,7 +298,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             {
                 const int nx = t0 + 128 + tid;
                 p = nx < bk.count ? sorted[bk.start + nx] : -1;
-                fd = nx < bk.count ? sfdoa[bk.start + nx] : 0.0;
+                fd = p >= 0 ? fdoa[p] : 0.0;
             }
             // warps without a candidate in this tile skip the Bessel terms and the
             // epilogue (their A rows are zero); tcgen05.ld stays warp-uniform

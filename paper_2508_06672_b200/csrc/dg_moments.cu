@@ -270,7 +270,7 @@ template <int R, int G>
 __global__ void __launch_bounds__(32 * kEvalWarps, 4)
 k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
            int* __restrict__ queue, const int* __restrict__ sorted,
-           const double* __restrict__ sfdoa, double fs, const double* __restrict__ nu_c_p, int B,
+           const double* __restrict__ fdoa, double fs, const double* __restrict__ nu_c_p, int B,
            const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
            uint32_t* __restrict__ flag_bits, int64_t flag_base, float tau, float tau_noise,
            const double* __restrict__ e1, const double* __restrict__ e2, int N) {
@@ -366,7 +366,7 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
             for (int c = 0; c < kEvalNC; ++c) {
                 const int slot = base + 32 * c + lane;
                 p[c] = slot < bk.count ? sorted[bk.start + slot] : -1;
-                nu[c] = p[c] >= 0 ? sfdoa[bk.start + slot] / fs - nu_c : 0.0;
+                nu[c] = p[c] >= 0 ? fdoa[p[c]] / fs - nu_c : 0.0;
                 double jv[R];
                 bessel_j<R>(3.141592653589793 * nu[c] * (double)B, jv);
                 // a_m M_m = (2 - delta_m0) (-1)^(m/2) J_m M'_m  (M' = i^(m mod 2) M)
