@@ -176,6 +176,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nbk = *n_buckets;
     const double nu_c = *nu_c_p;
+    const double inv_fs = 1.0 / fs;  // (the fast path's nu; refinement and re-rank keep fdoa / fs)
 
     auto produce = [&](int k, bool block) -> bool {  // thread 0 (as k_evaluate)
         const int sl = k % kTcStages;
@@ -293,7 +294,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         const double coh = bucket_coherence(qm2, R, zfloor);
 
         for (int t0 = 0; t0 < bk.count; t0 += 128) {
-            const double nu = p >= 0 ? fd / fs - nu_c : 0.0;
+            const double nu = p >= 0 ? fma(fd, inv_fs, -nu_c) : 0.0;
             const int pc = p;  // this tile's candidate; p / fd now prefetch the next tile's
             {
                 const int nx = t0 + 128 + tid;
@@ -315,11 +316,16 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                 if (pc >= 0) {
                     double jv[R];
                     bessel_j<R>(3.141592653589793 * nu * (double)B, jv);
+                    float qa = 0.f, qb = 0.f;  // a scale: FP32, two independent chains
 #pragma unroll
                     for (int m = 0; m < R; ++m) {
                         cf[m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
-                        qe2 = fma((double)cf[m] * cf[m], (double)qm2[m], qe2);
+                        if (m & 1)
+                            qb = fmaf(cf[m] * cf[m], qm2[m], qb);
+                        else
+                            qa = fmaf(cf[m] * cf[m], qm2[m], qa);
                     }
+                    qe2 = (double)qa + (double)qb;
                 }
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {

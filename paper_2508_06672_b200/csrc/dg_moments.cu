@@ -366,16 +366,20 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
             for (int c = 0; c < kEvalNC; ++c) {
                 const int slot = base + 32 * c + lane;
                 p[c] = slot < bk.count ? sorted[bk.start + slot] : -1;
-                nu[c] = p[c] >= 0 ? fdoa[p[c]] / fs - nu_c : 0.0;
+                nu[c] = p[c] >= 0 ? fma(fdoa[p[c]], 1.0 / fs, -nu_c) : 0.0;
                 double jv[R];
                 bessel_j<R>(3.141592653589793 * nu[c] * (double)B, jv);
                 // a_m M_m = (2 - delta_m0) (-1)^(m/2) J_m M'_m  (M' = i^(m mod 2) M)
-                qe2[c] = 0.0;
+                float qa = 0.f, qb = 0.f;
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
                     cf[c][m] = (float)((m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -1.0 : 1.0) * jv[m]);
-                    qe2[c] = fma((double)cf[c][m] * cf[c][m], (double)qm2[m], qe2[c]);
+                    if (m & 1)
+                        qb = fmaf(cf[c][m] * cf[c][m], qm2[m], qb);
+                    else
+                        qa = fmaf(cf[c][m] * cf[c][m], qm2[m], qa);
                 }
+                qe2[c] = (double)qa + (double)qb;
                 // W_j = W_1^j by an FP64 recurrence from one FP64 sincospi (error
                 // ~1e-15), each rounded once to FP32; e^{i 2 pi nu B G} = W_G
                 const double x1 = nu[c] * (double)B;
