@@ -73,7 +73,46 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 }
 
 // J_0..J_{R-1}(x) (first kind), FP64: series for J_{R-1}, J_R (fast: m >> x),
-// then the stable backward recurrence J_{m-1} = (2m/x) J_m - J_{m+1}.
+// then the stable backward recurrence J_{m-1} = (2m/x) J_m - J_{m+1}. The series
+// J_n = (h^n / n!) sum_k a_k (h^2)^k, a_k = prod_{i<=k} -1 / (i (n + i)), h = x/2,
+// run as Horner polynomials in h^2 with compile-time coefficients (one DFMA per
+// term), h^n by repeated squaring.
+struct JSeries {
+    double a[13];  // a_0 .. a_12
+    double inv_fact;
+};
+__host__ __device__ constexpr JSeries jseries_coefs(int n) {
+    JSeries c{};
+    double a = 1.0;
+    c.a[0] = 1.0;
+    for (int k = 1; k <= 12; ++k) {
+        a *= -1.0 / ((double)k * (double)(n + k));
+        c.a[k] = a;
+    }
+    double f = 1.0;
+    for (int i = 2; i <= n; ++i) f /= (double)i;
+    c.inv_fact = f;
+    return c;
+}
+template <int E>
+__device__ __forceinline__ double ipow(double h) {  // h^E, E >= 0
+    if constexpr (E == 0) {
+        return 1.0;
+    } else if constexpr (E == 1) {
+        return h;
+    } else {
+        const double q = ipow<E / 2>(h);
+        return (E & 1) ? q * q * h : q * q;
+    }
+}
+template <int N>
+__device__ __forceinline__ double jseries(double h, double h2) {  // J_N(2h), |h| <~ 2
+    constexpr JSeries C = jseries_coefs(N);
+    double p = C.a[12];
+#pragma unroll
+    for (int k = 11; k >= 0; --k) p = fma(p, h2, C.a[k]);
+    return ipow<N>(h) * C.inv_fact * p;
+}
 template <int R>
 __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
     const double ax = fabs(x);
@@ -85,28 +124,8 @@ __device__ __forceinline__ void bessel_j(double x, double (&j)[R]) {
         return;
     }
     const double h = 0.5 * x, h2 = h * h;
-    // (x/2)^(R-1) / (R-1)!
-    double t = 1.0;
-#pragma unroll
-    for (int m = 1; m < R; ++m) t *= h * (1.0 / m);
-    double jr1 = 0.0, jr = 0.0;  // J_{R-1}, J_R
-    {
-        double term = t, s = t;
-#pragma unroll
-        for (int k = 1; k <= 12; ++k) {
-            term *= -h2 * (1.0 / (k * (R - 1 + k)));
-            s += term;
-        }
-        jr1 = s;
-        term = t * h * (1.0 / R);
-        s = term;
-#pragma unroll
-        for (int k = 1; k <= 12; ++k) {
-            term *= -h2 * (1.0 / (k * (R + k)));
-            s += term;
-        }
-        jr = s;
-    }
+    const double jr1 = jseries<R - 1>(h, h2);  // J_{R-1}
+    const double jr = jseries<R>(h, h2);       // J_R
     const double inv = 2.0 / x;
     j[R - 1] = jr1;
     double jp = jr, jc = jr1;
@@ -154,11 +173,22 @@ __device__ __forceinline__ double bucket_coherence(const float* qm2, int R, doub
     return fmin(fmax((rho - 1.0) * 2.0, 0.0), 1.0);
 }
 
-__device__ __forceinline__ bool refine_moment(double s, double en, double qe2, double zfloor,
-                                              double coh, float tau, float tau_noise) {
+// per-bucket constants of the test, compared on S^2 (no square roots per candidate)
+struct RefineBucket {
+    double thr0;  // (tau_f)^2 zfloor
+    double base;  // (1 - coh) zfloor
+    double tau2;  // tau^2
+};
+__device__ __forceinline__ RefineBucket refine_bucket(double zfloor, double coh, float tau,
+                                                      float tau_noise) {
     const double tf = (double)tau_noise + ((double)tau - (double)tau_noise) * coh;
-    const double ex = fmax(fmax(en, qe2) - (1.0 - coh) * zfloor, 0.0);
-    return s < tf * sqrt(zfloor) || s < (double)tau * sqrt(ex);
+    return RefineBucket{tf * tf * zfloor, (1.0 - coh) * zfloor, (double)tau * (double)tau};
+}
+// S < tau_f sqrt(zfloor)  or  S < tau sqrt(max(en, qe2) - (1 - coh) zfloor), on s2 = S^2
+__device__ __forceinline__ bool refine_moment(double s2, double en, double qe2,
+                                              const RefineBucket& r) {
+    const double ex = fmax(fmax(en, qe2) - r.base, 0.0);
+    return s2 < r.thr0 || s2 < r.tau2 * ex;
 }
 
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {

@@ -291,7 +291,8 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
         double zfloor = 0.0;
 #pragma unroll
         for (int w = 0; w < kTcThreads / 32; ++w) zfloor += z2w[w];
-        const double coh = bucket_coherence(qm2, R, zfloor);
+        const RefineBucket rfb =
+            refine_bucket(zfloor, bucket_coherence(qm2, R, zfloor), tau, tau_noise);
 
         for (int t0 = 0; t0 < bk.count; t0 += 128) {
             const double nu = p >= 0 ? fma(fd, inv_fs, -nu_c) : 0.0;
@@ -351,7 +352,8 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             // then every thread reads its lane of it (4 groups of 16 blocks)
             float wtr[G], wti[G];
             double sr = 1.0, si = 0.0;
-            double acc_re = 0.0, acc_im = 0.0, en = 0.0, ar = 1.0, ai = 0.0;
+            double acc_re = 0.0, acc_im = 0.0, ar = 1.0, ai = 0.0;
+            float en = 0.f;  // sum_b |C_b|^2: an error scale, FP32
             for (int c0 = 0; c0 < np; c0 += kChunkCols) {
                 const int nn = np - c0 < kChunkCols ? np - c0 : kChunkCols;
                 if (tid == 0) {
@@ -423,7 +425,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                     const double hr = (double)(A.x - V.y), hi = (double)(A.y + V.x);
                     acc_re = fma(ar, hr, fma(-ai, hi, acc_re));
                     acc_im = fma(ar, hi, fma(ai, hr, acc_im));
-                    en += (double)(E2.x + E2.y);
+                    en += E2.x + E2.y;
                     const double nr = fma(ar, sr, -ai * si);
                     ai = fma(ar, si, ai * sr);
                     ar = nr;
@@ -432,9 +434,9 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                 __syncthreads();
             }
             if (pc >= 0) {
-                const double sv = sqrt(acc_re * acc_re + acc_im * acc_im);
-                s_out[pc] = sv;
-                if (refine_moment(sv, en, qe2, zfloor, coh, tau, tau_noise)) {
+                const double s2 = acc_re * acc_re + acc_im * acc_im;
+                s_out[pc] = sqrt(s2);
+                if (refine_moment(s2, (double)en, qe2, rfb)) {
                     const int64_t e = flag_base + pc;
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }

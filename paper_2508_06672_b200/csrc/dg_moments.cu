@@ -353,7 +353,8 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
         double zfloor = bucket_z2_part(e1, e2, N, bk.d, B, lane, 32);
 #pragma unroll
         for (int o = 16; o; o >>= 1) zfloor += __shfl_xor_sync(0xffffffffu, zfloor, o);
-        const double coh = bucket_coherence(qm2, R, zfloor);
+        const RefineBucket rfb =
+            refine_bucket(zfloor, bucket_coherence(qm2, R, zfloor), tau, tau_noise);
 
         for (int base = warp * 32 * kEvalNC; base < bk.count; base += kEvalPass) {
             int p[kEvalNC];
@@ -449,9 +450,9 @@ k_evaluate(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets
 #pragma unroll
             for (int c = 0; c < kEvalNC; ++c) {
                 if (p[c] < 0) continue;
-                const double sv = sqrt(acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c]);
-                s_out[p[c]] = sv;
-                if (refine_moment(sv, en[c], qe2[c], zfloor, coh, tau, tau_noise)) {
+                const double s2 = acc_re[c] * acc_re[c] + acc_im[c] * acc_im[c];
+                s_out[p[c]] = sqrt(s2);
+                if (refine_moment(s2, en[c], qe2[c], rfb)) {
                     const int64_t e = flag_base + p[c];
                     atomicOr(&flag_bits[e >> 5], 1u << (e & 31));
                 }
