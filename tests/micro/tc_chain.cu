@@ -93,7 +93,7 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     unsigned long long* d;
     cudaMalloc(&d, sizeof(unsigned long long) * sms * 16);
-    cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     static unsigned long long h[148 * 16];
     const int Ns[] = {32, 64, 96, 128, 160, 192, 256};
     for (int mode = 0; mode < 2; ++mode)
@@ -109,7 +109,8 @@ int main() {
                     if (need > smem) continue;
                     const int reps = mode == 0 ? 200 : 2000;
                     k_chain<<<sms * per_sm, 128, smem>>>(n, chains, ncols, reps, mode, d);
-                    cudaError_t e = cudaDeviceSynchronize();
+                    cudaError_t e = cudaGetLastError();
+                    if (e == cudaSuccess) e = cudaDeviceSynchronize();
                     if (e != cudaSuccess) {
                         printf("error %s\n", cudaGetErrorString(e));
                         return 1;
