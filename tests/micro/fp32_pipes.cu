@@ -73,6 +73,16 @@ __global__ void k_fadd2(float* out, float s) {
     for (int i = 0; i < CH; ++i) a[i] = sum2(A[i]);
     FINISH
 }
+__global__ void k_fmul2(float* out, float s) {
+    SETUP
+    unsigned long long A[CH], B[CH];
+    for (int i = 0; i < CH; ++i) { A[i] = pk(a[i], a[i] + 1.f); B[i] = pk(b[i], b[i]); }
+    for (int it = 0; it < IT; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) asm volatile("mul.rn.f32x2 %0, %0, %1;" : "+l"(A[i]) : "l"(B[i]));
+    for (int i = 0; i < CH; ++i) a[i] = sum2(A[i]);
+    FINISH
+}
 // 1 FFMA2 + 1 scalar FFMA interleaved
 __global__ void k_mix(float* out, float s) {
     SETUP
@@ -133,7 +143,7 @@ int main() {
         void (*k)(float*, float);
         double instr_per_chain;  // warp instructions per (it, chain)
     } tests[] = {{"FFMA 3-reg", k_ffma, 1},   {"FMUL 2-reg", k_fmul, 1}, {"FADD 2-reg", k_fadd, 1},
-                 {"FFMA2", k_ffma2, 1},        {"FADD2", k_fadd2, 1},     {"FFMA2+FFMA", k_mix, 2},
+                 {"FFMA2", k_ffma2, 1},        {"FADD2", k_fadd2, 1},     {"FMUL2", k_fmul2, 1},     {"FFMA2+FFMA", k_mix, 2},
                  {"FFMA+ALU(3)", k_ffma_alu, 4}};
     for (auto& t : tests) {
         const float ms = run(t.k, out, blocks, threads);
