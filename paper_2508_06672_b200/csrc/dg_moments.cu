@@ -29,6 +29,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "dg_device.cuh"
 #include "dg_internal.cuh"
 
@@ -194,46 +196,55 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
             float2 acc[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) acc[m] = make_float2(0.f, 0.f);
-            for (int j0 = 0; j0 < B / 2; j0 += kMomRun) {
-                float2 part[R];
+            // the block loop, compiled twice: warps whose blocks lie inside their
+            // buckets' overlaps run it without the per-sample masks
+            auto run = [&](auto masked) {
+                constexpr bool kMasked = decltype(masked)::value;
+                for (int j0 = 0; j0 < B / 2; j0 += kMomRun) {
+                    float2 part[R];
 #pragma unroll
-                for (int m = 0; m < R; ++m) part[m] = make_float2(0.f, 0.f);
-#pragma unroll 4
-                for (int j = j0; j < j0 + kMomRun; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
-                    const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
-                    const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
-                    const float2 fa = r2[j], fb = r2[j + 1], ga = r2[B - 2 - j], gb = r2[B - 1 - j];
-                    const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
-                    const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
-                    const float2 zero = make_float2(0.f, 0.f);
-                    float2 z0 = cmulc(f1, f2, 0), z1 = cmulc(f1, f2, 1);
-                    float2 w1 = cmulc(g1, g2, 0), w0 = cmulc(g1, g2, 1);
-                    if (!interior) {
-                        if (!(j >= lo && j < hi)) z0 = zero;
-                        if (!(j + 1 >= lo && j + 1 < hi)) z1 = zero;
-                        if (!(B - 2 - j >= lo && B - 2 - j < hi)) w1 = zero;
-                        if (!(B - 1 - j >= lo && B - 1 - j < hi)) w0 = zero;
+                    for (int m = 0; m < R; ++m) part[m] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = j0; j < j0 + kMomRun; j += 2) {  // samples j, j+1 (front), B-2-j, B-1-j (back)
+                        const float4 f1 = *reinterpret_cast<const float4*>(r1 + j);
+                        const float4 g1 = *reinterpret_cast<const float4*>(r1 + B - 2 - j);
+                        const float2 fa = r2[j], fb = r2[j + 1], ga = r2[B - 2 - j], gb = r2[B - 1 - j];
+                        const float4 f2 = make_float4(fa.x, fa.y, fb.x, fb.y);
+                        const float4 g2 = make_float4(ga.x, ga.y, gb.x, gb.y);
+                        float2 z0 = cmulc(f1, f2, 0), z1 = cmulc(f1, f2, 1);
+                        float2 w1 = cmulc(g1, g2, 0), w0 = cmulc(g1, g2, 1);
+                        if constexpr (kMasked) {
+                            const float2 zero = make_float2(0.f, 0.f);
+                            if (!(j >= lo && j < hi)) z0 = zero;
+                            if (!(j + 1 >= lo && j + 1 < hi)) z1 = zero;
+                            if (!(B - 2 - j >= lo && B - 2 - j < hi)) w1 = zero;
+                            if (!(B - 1 - j >= lo && B - 1 - j < hi)) w0 = zero;
+                        }
+                        // pair j: (z0, w0); pair j+1: (z1, w1)
+                        const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
+                        const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
+                        const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
+                        const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
+                        // (T_m(t_j), T_m(t_j+1)) for m = 2qq, 2qq + 1 in one LDS.128
+                        const float4* tr = reinterpret_cast<const float4*>(ts + (j >> 1) * RP);
+#pragma unroll
+                        for (int qq = 0; qq < R / 2; ++qq) {
+                            const float4 t = tr[qq];
+                            part[2 * qq] = ffma2(u1, t.y, ffma2(u0, t.x, part[2 * qq]));
+                            part[2 * qq + 1] = ffma2(v1, t.w, ffma2(v0, t.z, part[2 * qq + 1]));
+                        }
                     }
-                    // pair j: (z0, w0); pair j+1: (z1, w1)
-                    const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
-                    const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
-                    const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
-                    const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
-                    // (T_m(t_j), T_m(t_j+1)) for m = 2qq, 2qq + 1 in one LDS.128
-                    const float4* tr = reinterpret_cast<const float4*>(ts + (j >> 1) * RP);
 #pragma unroll
-                    for (int qq = 0; qq < R / 2; ++qq) {
-                        const float4 t = tr[qq];
-                        part[2 * qq] = ffma2(u1, t.y, ffma2(u0, t.x, part[2 * qq]));
-                        part[2 * qq + 1] = ffma2(v1, t.w, ffma2(v0, t.z, part[2 * qq + 1]));
+                    for (int m = 0; m < R; ++m) {
+                        acc[m].x += part[m].x;
+                        acc[m].y += part[m].y;
                     }
                 }
-#pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    acc[m].x += part[m].x;
-                    acc[m].y += part[m].y;
-                }
-            }
+            };
+            if (interior)
+                run(std::false_type{});
+            else
+                run(std::true_type{});
             // odd moments are stored times i, so a candidate's block value is one
             // real-weighted sum  C_b = sum_m c_m M'_m  (k_evaluate)
             const int rb = babs - bf;
