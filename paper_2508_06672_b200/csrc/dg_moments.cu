@@ -221,10 +221,8 @@ k_moments(const Bucket* __restrict__ buckets, const int* __restrict__ ubin, int 
                             if (!(B - 1 - j >= lo && B - 1 - j < hi)) w0 = zero;
                         }
                         // pair j: (z0, w0); pair j+1: (z1, w1)
-                        const float2 u0 = make_float2(z0.x + w0.x, z0.y + w0.y);
-                        const float2 v0 = make_float2(z0.x - w0.x, z0.y - w0.y);
-                        const float2 u1 = make_float2(z1.x + w1.x, z1.y + w1.y);
-                        const float2 v1 = make_float2(z1.x - w1.x, z1.y - w1.y);
+                        const float2 u0 = add2(z0, w0), v0 = sub2(z0, w0);
+                        const float2 u1 = add2(z1, w1), v1 = sub2(z1, w1);
                         // (T_m(t_j), T_m(t_j+1)) for m = 2qq, 2qq + 1 in one LDS.128
                         const float4* tr = reinterpret_cast<const float4*>(ts + (j >> 1) * RP);
 #pragma unroll
