@@ -116,6 +116,10 @@ typedef struct {
     int64_t surface_budget_bytes; /* per-snapshot surfaces held at once when the caller does not
                                      want them back; past it a run is solved in snapshot chunks
                                      (0 = default, 4 GiB) */
+    int moment_fft;          /* 1: block moments as FFT cross-correlations (B >= 256);
+                                0: direct FP32x2 sums */
+    double fft_refine_kappa; /* FFT moments: weight of a lag window's excess energy in the
+                                refinement scale (0 = default) */
 } dg_tuning;
 void dg_tuning_default(dg_tuning* t);
 int dg_engine_set_tuning(dg_engine* engine, const dg_tuning* t);

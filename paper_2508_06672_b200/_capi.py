@@ -94,7 +94,8 @@ class dg_tuning(C.Structure):
     _fields_ = [("correlator", C.c_int), ("moment_block", C.c_int), ("moment_count", C.c_int),
                 ("evaluate_tensor", C.c_int), ("refine_tau", C.c_double),
                 ("allow_weaker_refine", C.c_int), ("direct_refine_tau", C.c_double),
-                ("noise_refine_tau", C.c_double), ("surface_budget_bytes", C.c_int64)]
+                ("noise_refine_tau", C.c_double), ("surface_budget_bytes", C.c_int64),
+                ("moment_fft", C.c_int), ("fft_refine_kappa", C.c_double)]
 
 
 DG_CORRELATOR_AUTO, DG_CORRELATOR_DIRECT, DG_CORRELATOR_MOMENTS = 0, 1, 2

@@ -219,6 +219,9 @@ struct Lane {
     Task* tasks = nullptr;
     Bucket* buckets = nullptr;
     float2 *y1c = nullptr, *y2p = nullptr;
+    float2* af = nullptr;  // FFT path: per (block, moment) spectra of the y1 blocks
+    float* fe = nullptr;   // FFT path: per (window, block, moment) correlation mean squares
+    float* qf = nullptr;   // FFT path: their sums over each bucket's blocks [bucket][16]
     float2* mom = nullptr;
     size_t mom_cap = 0;
     unsigned long long* work = nullptr;  // [2]: moment / evaluate FP32x2 MACs
@@ -257,6 +260,9 @@ struct Pipeline {
     dg_tuning tn{};
     float tau = kMomentRefineTau, tau_direct = kRefineTau, tau_noise = kNoiseRefineTau;
     bool use_tc = true;
+    bool use_fft = false;  // block moments as FFT cross-correlations (tuning moment_fft)
+    float fft_kappa = kFftRefineKappa;
+    int64_t fft_steps = 0;
 
     ~Pipeline() {
         if (window_ready) cudaEventDestroy(window_ready);
@@ -275,6 +281,8 @@ struct Pipeline {
         tau_direct = tn.direct_refine_tau > 0.0 ? (float)tn.direct_refine_tau : kRefineTau;
         tau_noise = tn.noise_refine_tau > 0.0 ? (float)tn.noise_refine_tau : kNoiseRefineTau;
         use_tc = tn.evaluate_tensor != 0;
+        use_fft = tn.moment_fft != 0;
+        fft_kappa = tn.fft_refine_kappa > 0.0 ? (float)tn.fft_refine_kappa : kFftRefineKappa;
         if (P_ > INT32_MAX) raise(DG_EINVAL, "b200: more than 2^31-1 candidates in one call");
         if (N_ > INT32_MAX / 2) raise(DG_EINVAL, "b200: capture longer than 2^30 samples");
         P = P_;
@@ -341,6 +349,12 @@ struct Pipeline {
             L.y2p = sc.alloc<float2>(ylen);
             CK(cudaMemsetAsync(L.y2p, 0, ylen * sizeof(float2), sc.st));
             CK(cudaMemsetAsync(L.work, 0, 3 * sizeof(unsigned long long), sc.st));
+            if (use_fft) {  // the largest block count the FFT path takes (B = 256)
+                L.af = sc.alloc<float2>(moments_fft_af_bytes(N, 256, kMaxMoments) /
+                                        sizeof(float2));
+                L.fe = sc.alloc<float>(moments_fft_fe_floats(N, 256, kMaxMoments));
+                L.qf = sc.alloc<float>((size_t)std::min<int64_t>(P, nbins) * kMaxMoments);
+            }
         }
         CK(cudaEventCreateWithFlags(&window_ready, cudaEventDisableTiming));
         static_assert(sizeof(kMomentB) / sizeof(kMomentB[0]) == kTables, "tables");
@@ -521,13 +535,27 @@ struct Pipeline {
                           L.ubin, pl.B, st);
             launch_center(y1_64, y2, N, nu_c + s, L.y1c, L.y2p, padf, st);
             if (ev0) CK(cudaEventRecord(ev0, st));
-            launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
-                           L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
+            const bool tc = use_tc && evaluate_tc_supported(pl.nbmax, pl.R);
+            // FFT moments only where the tensor-core evaluator carries their error term
+            FftErr fx{nullptr, 0.f};
+            if (use_fft && tc && moments_fft_supported(pl.B)) {
+                launch_moments_fft(pl.B, pl.R, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
+                                   L.y1c, L.y2p, padf, L.mom, pl.nbmax, L.af, L.fe, L.queue,
+                                   sm_count, st);
+                launch_fft_bucket_energy(L.buckets, L.n_buckets,
+                                         (int)std::min<int64_t>(P, pl.nbins), L.fe, pl.bin0,
+                                         kFftLen - pl.B, (N + pl.B - 1) / pl.B, N, pl.B, pl.R,
+                                         L.qf, st);
+                fx = FftErr{L.qf, fft_kappa};
+                ++fft_steps;
+            } else {
+                launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N,
+                               tcheb_for(pl.B), L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
+            }
             if (ev1) CK(cudaEventRecord(ev1, st));
             CK(cudaMemsetAsync(L.queue, 0, sizeof(int), st));
-            const bool tc = use_tc && evaluate_tc_supported(pl.nbmax, pl.R);
             if (tc)
-                launch_evaluate_tc(pl.R, L.buckets, L.n_buckets, L.queue,
+                launch_evaluate_tc(fx, pl.R, L.buckets, L.n_buckets, L.queue,
                                    (int)std::min<int64_t>(P, pl.nbins), L.sorted, fdoa_slot(s), fs,
                                    nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
                                    tau_noise, e1, e2, N, sm_count, st);
@@ -767,6 +795,14 @@ int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
                                  " weakens the 1e-4 contract (set allow_weaker_refine)");
         if (t->surface_budget_bytes < 0)
             raise(DG_EINVAL, "dg_tuning: surface_budget_bytes < 0");
+        if (t->moment_fft != 0 && t->moment_fft != 1)
+            raise(DG_EINVAL, "dg_tuning: moment_fft must be 0 or 1");
+        if (!(t->fft_refine_kappa >= 0.0) || !std::isfinite(t->fft_refine_kappa))
+            raise(DG_EINVAL, "dg_tuning: fft_refine_kappa must be finite and >= 0");
+        if (t->fft_refine_kappa > 0.0 && t->fft_refine_kappa < kFftRefineKappa &&
+            !t->allow_weaker_refine)
+            raise(DG_EINVAL, "dg_tuning: fft_refine_kappa below the default weakens the 1e-4 "
+                             "contract (set allow_weaker_refine)");
         if (!(t->direct_refine_tau >= 0.0) || !std::isfinite(t->direct_refine_tau))
             raise(DG_EINVAL, "dg_tuning: direct_refine_tau must be finite and >= 0");
         if (t->direct_refine_tau > 0.0 && t->direct_refine_tau < kRefineTau &&

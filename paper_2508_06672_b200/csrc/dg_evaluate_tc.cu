@@ -153,7 +153,7 @@ constexpr size_t kPartA = (size_t)128 * kTcK * 2;
 
 template <int R>
 __global__ void __launch_bounds__(kTcThreads, 4)
-k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
+k_evaluate_tc(const FftErr fx, const Bucket* __restrict__ buckets, const int* __restrict__ n_buckets,
               int* __restrict__ queue, const int* __restrict__ sorted,
               const double* __restrict__ fdoa, double fs, const double* __restrict__ nu_c_p,
               int B, const float2* __restrict__ mom, int nbmax, double* __restrict__ s_out,
@@ -171,6 +171,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
     __shared__ int slot_u[kTcStages];
     __shared__ uint32_t tmem_base_s;
     __shared__ float qm2[kTcK];  // Q_m^2 = sum_b |M_m[b]|^2 of the bucket
+    __shared__ float qf2m[kTcK];  // FFT moments: sum_b of the window's mean square
     __shared__ double z2w[kTcThreads / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -251,6 +252,9 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
             for (int o = 16; o; o >>= 1) q2 += __shfl_xor_sync(0xffffffffu, q2, o);
             if (lane == 0) qm2[m] = q2;
         }
+        // FFT moments: the rounding's scale, the lag window's energy over the bucket's
+        // blocks (k_fft_bucket_energy)
+        if (fx.qf && tid < R) qf2m[tid] = fx.qf[(size_t)u * kMaxMoments + tid];
         {  // ||z||_2^2 of the bucket (the floor of the error scale), fixed order
             double z2 = bucket_z2_part(e1, e2, N, bk.d, B, tid, kTcThreads);
 #pragma unroll
@@ -327,6 +331,18 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
                             qa = fmaf(cf[m] * cf[m], qm2[m], qa);
                     }
                     qe2 = (double)qa + (double)qb;
+                    if (fx.qf) {  // FFT moments: the window's excess energy, weighted
+                        float fa = 0.f, fb = 0.f;
+#pragma unroll
+                        for (int m = 0; m < R; ++m) {
+                            if (m & 1)
+                                fb = fmaf(cf[m] * cf[m], qf2m[m], fb);
+                            else
+                                fa = fmaf(cf[m] * cf[m], qf2m[m], fa);
+                        }
+                        const double qf2 = (double)fa + (double)fb;
+                        qe2 += (double)fx.kappa * fmax(qf2 - qe2, 0.0);
+                    }
                 }
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -452,7 +468,7 @@ k_evaluate_tc(const Bucket* __restrict__ buckets, const int* __restrict__ n_buck
 }
 
 template <int R>
-void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
+void evaluate_tc_variant(FftErr fx, const Bucket* buckets, const int* n_buckets, int* queue, int max_buckets,
                          const int* sorted, const double* fdoa, double fs, const double* nu_c,
                          int B, const float2* mom, int nbmax, double* s_out, uint32_t* flag_bits,
                          int64_t flag_base, float tau, float tau_noise, const double* e1,
@@ -474,7 +490,7 @@ void evaluate_tc_variant(const Bucket* buckets, const int* n_buckets, int* queue
     if (resident < 1) resident = 1;
     int grid = sm_count * resident;
     if (grid > max_buckets) grid = max_buckets > 0 ? max_buckets : 1;
-    kern<<<grid, kTcThreads, smem, st>>>(buckets, n_buckets, queue, sorted, fdoa, fs, nu_c, B, mom,
+    kern<<<grid, kTcThreads, smem, st>>>(fx, buckets, n_buckets, queue, sorted, fdoa, fs, nu_c, B, mom,
                                          nbmax, s_out, flag_bits, flag_base, tau, tau_noise, e1,
                                          e2, N);
 }
@@ -486,14 +502,14 @@ bool evaluate_tc_supported(int nbmax, int R) {
     return L.ncols <= 512 && L.bytes <= 200 * 1024 && R <= kTcK;
 }
 
-void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+void launch_evaluate_tc(FftErr fx, int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
                         uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,
                         const double* e1, const double* e2, int N, int sm_count,
                         cudaStream_t st) {
 #define DG_TC_CASE(RR)                                                                          \
-    evaluate_tc_variant<RR>(buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
+    evaluate_tc_variant<RR>(fx, buckets, n_buckets, queue, max_buckets, sorted, fdoa, fs, nu_c, B, \
                             mom, nbmax, s_out, flag_bits, flag_base, tau, tau_noise, e1, e2, N, \
                             sm_count, st)
     switch (R) {

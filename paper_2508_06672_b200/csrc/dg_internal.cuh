@@ -180,6 +180,32 @@ void launch_work_count(const Bucket* buckets, const int* n_buckets, int B, int R
 void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bin0, int nbins,
                     int N, const float* tcheb, const float2* y1c, const float2* y2p, int padf,
                     float2* mom, int nbmax, int sm_count, cudaStream_t st);
+// the same moments as FFT cross-correlations (dg_moments_fft.cu), for 256 <= B <= 768:
+// af = moments_fft_af_bytes of scratch, queue = one int of scratch; fe receives per
+// (window, block, moment) the mean square of the window's correlation, the scale of
+// the FFT's rounding (moments_fft_fe_floats of scratch)
+constexpr int kFftLen = 1024;
+// weight of the FFT rounding's window excess in the refinement scale (calibrated
+// on the error-model scenes)
+constexpr float kFftRefineKappa = 4.0f;
+bool moments_fft_supported(int B);
+size_t moments_fft_af_bytes(int N, int B, int R);
+size_t moments_fft_fe_floats(int N, int B, int R);
+void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int N,
+                        const float* tcheb, const float2* y1c, const float2* y2p, int padf,
+                        float2* mom, int nbmax, float2* af, float* fe, int* queue, int sm_count,
+                        cudaStream_t st);
+// what k_evaluate_tc needs of an FFT-moment step (qf = nullptr: direct moments):
+// qf[bucket * kMaxMoments + m] = sum over the bucket's blocks of fe of its lag window
+struct FftErr {
+    const float* qf;
+    float kappa;  // weight of the window's excess over the bucket's own moment energy
+};
+// qf of every bucket of a step (fe: launch_moments_fft's, window of a bin = (bin -
+// bin0) / G, fe[(window * R + m) * nblk + block])
+void launch_fft_bucket_energy(const Bucket* buckets, const int* n_buckets, int max_buckets,
+                              const float* fe, int bin0, int G, int nblk, int N, int B, int R,
+                              float* qf, cudaStream_t st);
 // per-bucket candidate evaluation; `queue` is a zeroed int (dynamic bucket queue);
 // sfdoa = the candidates' FDOA in bucket order (launch_bucket's sfdoa)
 size_t evaluate_smem_bytes(int nbmax, int R);
@@ -240,7 +266,7 @@ void launch_noise_combine(const uint64_t* seeds, int n_snap, int n_rx, int n_em,
 // the same evaluation with the block sums C_b on the tensor cores (dg_evaluate_tc.cu,
 // tcgen05 kind::tf32, split hi/lo operands); needs 2 nbmax <= 512 TMEM columns
 bool evaluate_tc_supported(int nbmax, int R);
-void launch_evaluate_tc(int R, const Bucket* buckets, const int* n_buckets, int* queue,
+void launch_evaluate_tc(FftErr fx, int R, const Bucket* buckets, const int* n_buckets, int* queue,
                         int max_buckets, const int* sorted, const double* fdoa, double fs,
                         const double* nu_c, int B, const float2* mom, int nbmax, double* s_out,
                         uint32_t* flag_bits, int64_t flag_base, float tau, float tau_noise,

@@ -19,6 +19,10 @@ import paper_2508_06672_b200 as b2  # noqa: E402
 def main():
     name = os.environ.get("DG_PROFILE_CONFIG", "C3")
     cfg = bench.WORKLOADS[name]
+    # tuning for the profiled solve, e.g. DG_PROFILE_TUNING=moment_fft=1 (test harness only)
+    tun = dict(kv.split("=") for kv in os.environ.get("DG_PROFILE_TUNING", "").split(",") if kv)
+    if tun:
+        b2.default_engine(0).set_tuning(**{k: int(v) for k, v in tun.items()})
     states, caps, bounds, spacing = bench.make_inputs(name)
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], bench.FC)
