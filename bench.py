@@ -13,12 +13,13 @@ accumulation, exact argmax and detect_emitters, all on the GPU.
 * e2e       — the same solve through the public API with host (pinned) captures:
               H2D of every capture and D2H of the accumulated surface inside the
               timed region.
-* roofline  — the dominant correlator kernel (k_moments at C3): its FMA-pipe
-              work counted on the device (k_work_count) over its event time,
-              against the FP32 CUDA-core peak measured in-process; the
-              tensor-core part of k_evaluate_tc against MEASURED_PEAKS.json's
-              BF16 figure; the reference-equivalent rate (20 FLOP per
-              overlapping sample) beside it.
+* roofline  — the dominant correlator kernel (k_evaluate_tc at C3): its
+              tensor-core FLOPs (split-BF16 MMAs issued) over its event time
+              against MEASURED_PEAKS.json's BF16 figure, beside its CUDA-core
+              FP32x2 work and the moment kernels' (FFT moments k_mfft: 5 L log2 L
+              per FFT; direct k_moments: FMA-pipe work counted by k_work_count)
+              against the FP32 peak measured in-process; the reference-equivalent
+              rate (20 FLOP per overlapping sample) beside them.
 * cpu_baseline / --impl reference — the reference's own CPU path (oracle/_ref,
               compiled from the unmodified reference headers) on this host's
               cores, on a bounded sample of the same workload.
@@ -438,16 +439,25 @@ def b200_arm(args, rank, world):
     mom_ms = last["moments_ms"]
     ev_ms = last["evaluate_ms"]
     corr_ms = mom_ms + ev_ms
-    # FMA-pipe work in FP32x2 operations x 4 FLOP-equivalents (k_work_count)
-    mom_tf = 4.0 * last["moment_ffma2"] / (mom_ms * 1e-3) / 1e12 if mom_ms else None
+    # moments: FFT FLOPs (5 L log2 L per FFT + 6 L per spectrum product), or the
+    # direct sums' FMA-pipe work in FP32x2 operations x 4 FLOP-equivalents (k_work_count)
+    fft_flop = last.get("moment_fft_flop") or 0.0
+    mom_name = "k_mfft" if fft_flop > 0 else "k_moments"
+    mom_work = fft_flop if fft_flop > 0 else 4.0 * last["moment_ffma2"]
+    mom_tf = mom_work / (mom_ms * 1e-3) / 1e12 if mom_ms else None
     ev_tf = 4.0 * last["evaluate_ffma2"] / (ev_ms * 1e-3) / 1e12 if ev_ms else None
     tc_flop = last.get("evaluate_tc_flop") or 0.0
     ev_name = "k_evaluate_tc" if tc_flop > 0 else "k_evaluate"
     tc_tf = tc_flop / (ev_ms * 1e-3) / 1e12 if ev_ms and tc_flop else None
     bf16_peak = measured_peaks().get("bf16_tflops")
     ovl = last["sum_overlap_samples"]
-    dominant = ev_name if ev_ms >= mom_ms else "k_moments"
-    achieved = ev_tf if dominant == ev_name else mom_tf
+    dominant = ev_name if ev_ms >= mom_ms else mom_name
+    if dominant == "k_evaluate_tc" and tc_tf and bf16_peak:  # the MMA kernel: tensor roofline
+        bound, achieved, peak_top = "tensor", tc_tf, bf16_peak
+        peak_src = "MEASURED_PEAKS.json bf16_tflops (dense BF16)"
+    else:
+        bound, achieved, peak_top = "fp32", (ev_tf if dominant == ev_name else mom_tf), peak
+        peak_src = "dg_fp32_peak_tflops FFMA probe in this process"
     launches = st.get("kernel_launches", last["kernel_launches"])
 
     # e2e: host (pinned) captures in, accumulated surface out, through the public API
@@ -526,20 +536,21 @@ def b200_arm(args, rank, world):
                        "precision": "FP32 correlator, FP64 geometry/accumulation/refine"},
             "e2e": e2e,
             "roofline": {
-                "bound": "fp32", "kernel": dominant, "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak if achieved and peak else None,
+                "bound": bound, "kernel": dominant, "achieved": achieved, "peak": peak_top,
+                "unit": "TFLOP/s", "frac": achieved / peak_top if achieved and peak_top else None,
                 "traffic": ncu_traffic(dominant),
                 "traffic_source": f"dram__bytes_read.sum + dram__bytes_write.sum per {dominant} "
                                   f"launch, {NCU_SUMMARY}",
-                "peak_source": "dg_fp32_peak_tflops FFMA probe in this process",
-                "flop_definition": "FMA-pipe work: 4 x the FP32x2 operations the kernel's "
-                                   "algorithm performs, counted on the device by k_work_count "
-                                   "(k_moments: B/2*(R+6) per bucket-block = R moment MACs per "
-                                   "folded sample pair + 2 complex products + 1 fold; "
-                                   "k_evaluate_tc: 3 per candidate-block on CUDA cores, the "
-                                   "block sums on tensor cores reported separately)",
-                "kernels": {"k_moments": {"ms": mom_ms, "tflops": mom_tf, "bound": "fp32 fma pipe",
-                                          "frac": mom_tf / peak if mom_tf and peak else None},
+                "peak_source": peak_src,
+                "flop_definition": "k_evaluate_tc (tensor): BF16 MMA FLOPs issued, 6 split "
+                                   "products x 2*128*np*16 per 128-candidate tile; CUDA-core "
+                                   "parts: 4 x FP32x2 operations counted on the device by "
+                                   "k_work_count (k_evaluate_tc: 3 per candidate-block; "
+                                   "k_moments: B/2*(R+6) per bucket-block); k_mfft: 5 L log2 L "
+                                   "per 1024-point FFT + 6 L per spectrum product",
+                "kernels": {mom_name: {"ms": mom_ms, "tflops": mom_tf, "bound": "fp32",
+                                       "frac": mom_tf / peak if mom_tf and peak else None,
+                                       "fp32_peak": peak},
                             ev_name: {"ms": ev_ms, "tflops": ev_tf,
                                       "frac": ev_tf / peak if ev_tf and peak else None,
                                       "tensor_tflops": tc_tf,

@@ -246,6 +246,9 @@ typedef struct {
                                    tensor-core path count*nb*3 (group sums on CUDA cores) */
     int64_t direct_steps;       /* (snapshot, pair) steps run on the direct correlator */
     double evaluate_tc_flop;    /* tensor-core FLOPs k_evaluate_tc issued (BF16 MMAs, 0 if none) */
+    double moment_fft_flop;     /* FFT moments (k_mfft_a + k_mfft): 5 L log2 L per 1024-point
+                                   FFT + 6 L per spectrum product; moment_ffma2 then counts the
+                                   direct sums the FFTs replaced */
 } dg_result;
 
 void dg_options_default(dg_options* opt);

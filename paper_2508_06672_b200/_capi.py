@@ -122,7 +122,8 @@ class dg_result(C.Structure):
                 ("moment_ffma2", C.c_double),
                 ("evaluate_ffma2", C.c_double),
                 ("direct_steps", C.c_int64),
-                ("evaluate_tc_flop", C.c_double)]
+                ("evaluate_tc_flop", C.c_double),
+                ("moment_fft_flop", C.c_double)]
 
 
 # every symbol include/b200geo.h declares (tests check the .so exports them)

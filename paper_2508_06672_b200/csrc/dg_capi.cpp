@@ -263,6 +263,7 @@ struct Pipeline {
     bool use_fft = false;  // block moments as FFT cross-correlations (tuning moment_fft)
     float fft_kappa = kFftRefineKappa;
     int64_t fft_steps = 0;
+    double fft_flop = 0.0;  // FFT moments: 5 L log2 L per FFT + 6 L per spectrum product
 
     ~Pipeline() {
         if (window_ready) cudaEventDestroy(window_ready);
@@ -548,6 +549,13 @@ struct Pipeline {
                                          L.qf, st);
                 fx = FftErr{L.qf, fft_kappa};
                 ++fft_steps;
+                {
+                    const double Lf = kFftLen, fftf = 5.0 * Lf * 10.0;  // log2 1024 = 10
+                    const int G = kFftLen - pl.B, nblk = (N + pl.B - 1) / pl.B;
+                    const int ngr = (pl.bin0 + pl.nbins - 1) / G - pl.bin0 / G + 1;
+                    fft_flop += (double)nblk * pl.R * fftf +
+                                (double)ngr * nblk * ((1.0 + pl.R) * fftf + pl.R * 6.0 * Lf);
+                }
             } else {
                 launch_moments(pl.B, pl.R, L.buckets, L.ubin, pl.bin0, pl.nbins, N,
                                tcheb_for(pl.B), L.y1c, L.y2p, padf, L.mom, pl.nbmax, sm_count, st);
@@ -771,6 +779,7 @@ void dg_tuning_default(dg_tuning* t) {
     std::memset(t, 0, sizeof *t);
     t->correlator = DG_CORRELATOR_AUTO;
     t->evaluate_tensor = 1;
+    t->moment_fft = 1;
 }
 
 int dg_engine_set_tuning(dg_engine* e, const dg_tuning* t) {
@@ -1677,6 +1686,7 @@ void reset_stats(dg_result* r) {
     r->evaluate_ffma2 = 0.0;
     r->direct_steps = 0;
     r->evaluate_tc_flop = 0.0;
+    r->moment_fft_flop = 0.0;
 }
 
 dg_options options_or_default(const dg_options* o) {
@@ -1850,6 +1860,7 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
     res->evaluate_ffma2 += (double)work[1];
     res->evaluate_tc_flop += (double)work[2];
     res->direct_steps += pl.direct_steps;
+    res->moment_fft_flop += pl.fft_flop;
     if (opt.profile) {
         double tm = 0.0, te = 0.0;
         for (int i = 0; i < SPl; ++i) {
@@ -2251,6 +2262,7 @@ void geolocate_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn, const
             res->evaluate_ffma2 += part.evaluate_ffma2;
             res->evaluate_tc_flop += part.evaluate_tc_flop;
             res->direct_steps += part.direct_steps;
+            res->moment_fft_flop += part.moment_fft_flop;
             res->moments_ms += part.moments_ms;
             res->evaluate_ms += part.evaluate_ms;
             res->correlate_ms += part.correlate_ms;
@@ -2540,6 +2552,7 @@ void geolocate_multi(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
         res->evaluate_ffma2 += a.evaluate_ffma2;
         res->evaluate_tc_flop += a.evaluate_tc_flop;
         res->direct_steps += a.direct_steps;
+        res->moment_fft_flop += a.moment_fft_flop;
         res->kernel_launches += a.kernel_launches + pr[k].kernel_launches;
         res->n_reranked += pr[k].n_reranked;
     }

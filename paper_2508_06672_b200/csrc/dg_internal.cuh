@@ -201,8 +201,8 @@ struct FftErr {
     const float* qf;
     float kappa;  // weight of the window's excess over the bucket's own moment energy
 };
-// qf of every bucket of a step (fe: launch_moments_fft's, window of a bin = (bin -
-// bin0) / G, fe[(window * R + m) * nblk + block])
+// qf of every bucket of a step (fe: launch_moments_fft's, window of a bin = bin / G -
+// bin0 / G, fe[(window * R + m) * nblk + block])
 void launch_fft_bucket_energy(const Bucket* buckets, const int* n_buckets, int max_buckets,
                               const float* fe, int bin0, int G, int nblk, int N, int B, int R,
                               float* qf, cudaStream_t st);

@@ -96,7 +96,9 @@ k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, in
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= total) break;
         const int g = it / nblk, b = it - g * nblk;
-        const int bin_a = bin0 + g * G;  // first bin of the window
+        // windows at absolute multiples of G, so any bin-range part of a step (the
+        // multi-GPU work units) computes every moment with the same FFTs
+        const int bin_a = (bin0 / G + g) * G;  // first bin of the window
         const int d0 = bin_a - (N - 1);
         const float2* afb = af + (size_t)b * R * kFftL;
         if (lane == 0) {  // moment 0's spectrum, in flight during the window's FFT
@@ -118,7 +120,7 @@ k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, in
             roff[k] = -1;
             const int t = lane + 32 * k;
             const int bin = bin_a + t;
-            if (t < G && bin < bin0 + nbins) {
+            if (t < G && bin >= bin0 && bin < bin0 + nbins) {
                 const int u = ubin[bin - bin0];
                 if (u >= 0) {
                     const int d = bin - (N - 1);
@@ -184,7 +186,7 @@ __global__ void k_fft_bucket_energy(const Bucket* __restrict__ buckets,
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int u = i / R, m = i - u * R;
         const Bucket bk = buckets[u];
-        const int win = (bk.d + N - 1 - bin0) / G;
+        const int win = (bk.d + N - 1) / G - bin0 / G;
         const int bf = (bk.d < 0 ? -bk.d : 0) / B;
         const float* f = fe + ((size_t)win * R + m) * nblk + bf;
         float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
@@ -219,7 +221,7 @@ size_t moments_fft_af_bytes(int N, int B, int R) {
 
 size_t moments_fft_fe_floats(int N, int B, int R) {
     const int nblk = (N + B - 1) / B, G = kFftL - B;
-    const int ngroups = (2 * N - 1 + G - 1) / G;
+    const int ngroups = (2 * N - 1 + G - 1) / G + 1;
     return (size_t)ngroups * nblk * R;
 }
 
@@ -229,7 +231,7 @@ void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int 
                         cudaStream_t st) {
     const int nblk = (N + B - 1) / B;
     const int G = kFftL - B;
-    const int ngroups = (nbins + G - 1) / G;
+    const int ngroups = (bin0 + nbins - 1) / G - bin0 / G + 1;  // absolute windows
     const size_t smem = sizeof(FftSmem);
     static size_t attr_a[64] = {}, attr_m[64] = {};
     ensure_smem(k_mfft_a, smem, attr_a);

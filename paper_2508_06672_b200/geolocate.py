@@ -278,7 +278,8 @@ def _run(grid: CandidateGrid, options: GeolocateOptions, n_snap: int, call, *, w
                  kernel_launches=res.kernel_launches, n_detections=res.n_detections,
                  moments_ms=res.moments_ms, evaluate_ms=res.evaluate_ms,
                  moment_ffma2=res.moment_ffma2, evaluate_ffma2=res.evaluate_ffma2,
-                 direct_steps=res.direct_steps, evaluate_tc_flop=res.evaluate_tc_flop)
+                 direct_steps=res.direct_steps, evaluate_tc_flop=res.evaluate_tc_flop,
+                 moment_fft_flop=res.moment_fft_flop)
     per_list = [CorrelationGrid(grid, per[s]) for s in range(n_snap)] if per is not None else []
     return GeolocateResult(grid, per_list, CorrelationGrid(grid, acc), detections,
                            int(res.argmax_index), float(res.argmax_value), stats)
@@ -352,7 +353,7 @@ def correlate_steps(grid: CandidateGrid, staged: StagedSnapshots, s_begin: int, 
                 correlate_ms=res.correlate_ms, moments_ms=res.moments_ms,
                 evaluate_ms=res.evaluate_ms, moment_ffma2=res.moment_ffma2,
                 evaluate_ffma2=res.evaluate_ffma2, direct_steps=res.direct_steps,
-                evaluate_tc_flop=res.evaluate_tc_flop,
+                evaluate_tc_flop=res.evaluate_tc_flop, moment_fft_flop=res.moment_fft_flop,
                 kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
 
 
@@ -372,7 +373,7 @@ def correlate_units(grid: CandidateGrid, staged: StagedSnapshots, units, raw_dev
                 correlate_ms=res.correlate_ms, moments_ms=res.moments_ms,
                 evaluate_ms=res.evaluate_ms, moment_ffma2=res.moment_ffma2,
                 evaluate_ffma2=res.evaluate_ffma2, direct_steps=res.direct_steps,
-                evaluate_tc_flop=res.evaluate_tc_flop,
+                evaluate_tc_flop=res.evaluate_tc_flop, moment_fft_flop=res.moment_fft_flop,
                 kernel_launches=res.kernel_launches, correlate_launches=res.correlate_launches)
 
 

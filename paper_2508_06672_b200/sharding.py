@@ -197,7 +197,8 @@ def _geolocate_sharded(grid, staged, options, gather, group, stream, profile):
     med = torch.empty(max(len(mine), 1), dtype=torch.float64, device=dev)
     stats = dict(n_refined=0, sum_overlap_samples=0.0, correlate_ms=0.0, moments_ms=0.0,
                  evaluate_ms=0.0, moment_ffma2=0.0, evaluate_ffma2=0.0, direct_steps=0,
-                 evaluate_tc_flop=0.0, kernel_launches=0, correlate_launches=0)
+                 evaluate_tc_flop=0.0, moment_fft_flop=0.0, kernel_launches=0,
+                 correlate_launches=0)
     if mine and norm:
         stats = correlate_steps(grid, staged, mine[0][0], mine[0][0] + len(mine),
                                 local.data_ptr(), med.data_ptr(), options, stream=stream,

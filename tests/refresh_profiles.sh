@@ -22,15 +22,19 @@ timeout 900 python tests/test_gpu_error_model.py $OUT/error_model.json > $OUT/er
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
   --csv --log-file $OUT/launches.csv python tests/profile_solve.py > $OUT/launches.log 2>&1
 python tests/launch_summary.py $OUT/launches.csv > $OUT/launches_summary.txt 2>&1
-for k in k_moments k_evaluate_tc; do
+for k in k_mfft k_evaluate_tc; do
   timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -k regex:$k -s 20 -c 1 -f -o $OUT/ncu_$k python tests/profile_solve.py > $OUT/ncu_$k.log 2>&1
+    -k regex:"$k\b" -s 20 -c 1 -f -o $OUT/ncu_$k python tests/profile_solve.py > $OUT/ncu_$k.log 2>&1
 done
+# the direct-sum moment kernel (tuning moment_fft = 0)
+DG_PROFILE_TUNING=moment_fft=0 timeout 900 ncu --profile-from-start off --set full --import-source on \
+  --clock-control none -k regex:k_moments -s 20 -c 1 -f -o $OUT/ncu_k_moments python tests/profile_solve.py \
+  > $OUT/ncu_k_moments.log 2>&1
 timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
   -k regex:k_refine_rows -c 1 -f -o $OUT/ncu_k_refine_rows python tests/profile_solve.py \
   > $OUT/ncu_k_refine_rows.log 2>&1
 bash tests/ncu_plugin.sh
-python tests/ncu_summary.py k_moments=$OUT/ncu_k_moments.ncu-rep \
+python tests/ncu_summary.py k_mfft=$OUT/ncu_k_mfft.ncu-rep k_moments=$OUT/ncu_k_moments.ncu-rep \
   k_evaluate_tc=$OUT/ncu_k_evaluate_tc.ncu-rep k_refine_rows=$OUT/ncu_k_refine_rows.ncu-rep \
   k_correlate=$OUT/ncu_r2_k_correlate.ncu-rep > $OUT/ncu_kernels.txt 2>&1
 ls -la $OUT

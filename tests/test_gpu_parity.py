@@ -160,14 +160,16 @@ def test_correlate_batch_vs_reference(b2, ref, n, count, fs, span, seed, mode, t
 @pytest.mark.parametrize("block", [64, 128, 256, 512, 640, 768])
 @pytest.mark.parametrize("span,tdoa_span", [(2e4, 50_000), (3e3, 4_000), (0.0, 200),
                                             (3e3, 12)])  # ~250 per bucket: 2 tiles
-@pytest.mark.parametrize("tc", [1, 0])  # block sums on tcgen05 / FFMA2 block loop
-def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, tc, tune):
+# block sums on tcgen05 with FFT / direct-sum moments, or the FFMA2 block loop
+@pytest.mark.parametrize("tc,fft", [(1, 1), (1, 0), (0, 0)])
+def test_block_moments_vs_reference(b2, ref, block, span, tdoa_span, tc, fft, tune):
     """The block-moment correlator at every block length against the reference,
     on buckets dense enough that it is the planner's choice (many candidates
-    per TDOA), including FDOA == 0 (x = 0) and the full TDOA range; candidate
-    evaluation on the tensor cores (k_evaluate_tc, B = 256 and 512 at 50k
-    samples: 2 nb <= 512 TMEM columns) and on the FFMA2 block loop."""
-    tune(correlator="moments", moment_block=block, evaluate_tensor=tc)
+    per TDOA), including FDOA == 0 (x = 0) and the full TDOA range; moments as
+    FFT cross-correlations (k_mfft, B >= 256) or direct sums (k_moments);
+    candidate evaluation on the tensor cores (k_evaluate_tc) and on the FFMA2
+    block loop."""
+    tune(correlator="moments", moment_block=block, evaluate_tensor=tc, moment_fft=fft)
     n, fs, count = 50_000, 5e6, 6_000
     rng = np.random.default_rng(block + int(span))
     y1, y2 = gauss(rng, n), gauss(rng, n)
