@@ -43,16 +43,22 @@ struct FftSmem {
     uint64_t bar[kFftWarps];
 };
 
-__global__ void __launch_bounds__(32 * kFftWarps, 1)
+constexpr int kAWarps = 12;  // k_mfft_a: only a transpose buffer per warp
+struct FftASmem {
+    float2 tw[kFftL];
+    float2 xbuf[kAWarps][kXbuf];
+};
+
+__global__ void __launch_bounds__(32 * kAWarps, 1)
 k_mfft_a(const float2* __restrict__ y1c, int N, int B, int R, int nblk,
          const float* __restrict__ tcheb, float2* __restrict__ af) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    FftSmem& sm = *reinterpret_cast<FftSmem*>(smem_raw);
+    FftASmem& sm = *reinterpret_cast<FftASmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     fft1024_twiddles(sm.tw, threadIdx.x, blockDim.x);
     __syncthreads();
     const int total = nblk * R;
-    for (int it = blockIdx.x * kFftWarps + warp; it < total; it += gridDim.x * kFftWarps) {
+    for (int it = blockIdx.x * kAWarps + warp; it < total; it += gridDim.x * kAWarps) {
         const int b = it / R, m = it - b * R;
         float2 v[32];
 #pragma unroll
@@ -67,7 +73,7 @@ k_mfft_a(const float2* __restrict__ y1c, int N, int B, int R, int nblk,
             }
             v[i] = a;
         }
-        fft1024_warp<false>(v, sm.tw, sm.w[warp].xbuf, lane);
+        fft1024_warp<false>(v, sm.tw, sm.xbuf[warp], lane);
         float2* dst = af + (size_t)it * kFftL;
         constexpr float inv = 1.0f / kFftL;
 #pragma unroll
@@ -176,29 +182,39 @@ k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, in
     }
 }
 
-// one thread per (bucket, m): qf[u][m] = sum_{b in the bucket's blocks} fe[window][m][b]
-// (contiguous in b)
+// one warp per bucket: qf[u][m] = sum_{b in the bucket's blocks} fe[window][m][b]
+// (contiguous in b: coalesced; every moment's loads in flight together)
+template <int R>
 __global__ void k_fft_bucket_energy(const Bucket* __restrict__ buckets,
                                     const int* __restrict__ n_buckets, const float* __restrict__ fe,
-                                    int bin0, int G, int nblk, int N, int B, int R,
+                                    int bin0, int G, int nblk, int N, int B,
                                     float* __restrict__ qf) {
-    const int total = *n_buckets * R;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const int u = i / R, m = i - u * R;
+    const int lane = threadIdx.x & 31;
+    const int nbk = *n_buckets;
+    for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nbk;
+         u += (gridDim.x * blockDim.x) >> 5) {
         const Bucket bk = buckets[u];
         const int win = (bk.d + N - 1) / G - bin0 / G;
         const int bf = (bk.d < 0 ? -bk.d : 0) / B;
-        const float* f = fe + ((size_t)win * R + m) * nblk + bf;
-        float e0 = 0.f, e1 = 0.f, e2 = 0.f, e3 = 0.f;
-        int b = 0;
-        for (; b + 4 <= bk.nb; b += 4) {
-            e0 += f[b];
-            e1 += f[b + 1];
-            e2 += f[b + 2];
-            e3 += f[b + 3];
+        const float* f = fe + (size_t)win * R * nblk + bf;
+        float e[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) e[m] = 0.f;
+        for (int b = lane; b < bk.nb; b += 32) {
+#pragma unroll
+            for (int m = 0; m < R; ++m) e[m] += f[(size_t)m * nblk + b];
         }
-        for (; b < bk.nb; ++b) e0 += f[b];
-        qf[(size_t)u * kMaxMoments + m] = (e0 + e1) + (e2 + e3);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) e[m] += __shfl_xor_sync(0xffffffffu, e[m], o);
+        }
+        if (lane < R) {
+            float v = 0.f;
+#pragma unroll
+            for (int m = 0; m < R; ++m) v = lane == m ? e[m] : v;
+            qf[(size_t)u * kMaxMoments + lane] = v;
+        }
     }
 }
 
@@ -207,9 +223,18 @@ __global__ void k_fft_bucket_energy(const Bucket* __restrict__ buckets,
 void launch_fft_bucket_energy(const Bucket* buckets, const int* n_buckets, int max_buckets,
                               const float* fe, int bin0, int G, int nblk, int N, int B, int R,
                               float* qf, cudaStream_t st) {
-    const int blocks = (max_buckets * R + 255) / 256;
-    k_fft_bucket_energy<<<blocks < 148 * 8 ? blocks : 148 * 8, 256, 0, st>>>(
-        buckets, n_buckets, fe, bin0, G, nblk, N, B, R, qf);
+    const int blocks = (max_buckets + 7) / 8;
+    const int grid = blocks < 148 * 16 ? blocks : 148 * 16;
+#define DG_FBE(RR)                                                                             \
+    k_fft_bucket_energy<RR><<<grid, 256, 0, st>>>(buckets, n_buckets, fe, bin0, G, nblk, N, B, qf)
+    switch (R) {
+        case 8: DG_FBE(8); break;
+        case 10: DG_FBE(10); break;
+        case 12: DG_FBE(12); break;
+        case 14: DG_FBE(14); break;
+        default: DG_FBE(16); break;
+    }
+#undef DG_FBE
 }
 
 bool moments_fft_supported(int B) { return B >= 256 && B <= 768; }
@@ -232,12 +257,12 @@ void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int 
     const int nblk = (N + B - 1) / B;
     const int G = kFftL - B;
     const int ngroups = (bin0 + nbins - 1) / G - bin0 / G + 1;  // absolute windows
-    const size_t smem = sizeof(FftSmem);
+    const size_t smem = sizeof(FftSmem), smem_a = sizeof(FftASmem);
     static size_t attr_a[64] = {}, attr_m[64] = {};
-    ensure_smem(k_mfft_a, smem, attr_a);
+    ensure_smem(k_mfft_a, smem_a, attr_a);
     ensure_smem(k_mfft, smem, attr_m);
-    const int ga = (nblk * R + kFftWarps - 1) / kFftWarps;
-    k_mfft_a<<<ga < sm_count ? ga : sm_count, 32 * kFftWarps, smem, st>>>(y1c, N, B, R, nblk,
+    const int ga = (nblk * R + kAWarps - 1) / kAWarps;
+    k_mfft_a<<<ga < sm_count ? ga : sm_count, 32 * kAWarps, smem_a, st>>>(y1c, N, B, R, nblk,
                                                                           tcheb, af);
     cudaMemsetAsync(queue, 0, sizeof(int), st);
     k_mfft<<<sm_count, 32 * kFftWarps, smem, st>>>(ubin, bin0, nbins, ngroups, G, N, B, R, nblk,
