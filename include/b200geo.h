@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 6
+#define DG_ABI_VERSION 7
 
 enum {
     DG_OK = 0,

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in syms if s not in exported]
     assert not missing, missing
     assert sorted(_capi.EXPORTS) == syms
-    assert _capi.lib.dg_abi_version() == 6
+    assert _capi.lib.dg_abi_version() == 7
 
 
 def test_library_is_sm100a():
