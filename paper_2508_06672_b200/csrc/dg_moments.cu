@@ -20,7 +20,9 @@
 //
 //   k_center    y1c[k] = fp32(y1[k] e^{i 2 pi nu_c k})           (FP64 math)
 //   k_moments   per (bucket, 32-block chunk): z into shared memory, then
-//               M_m[b] on FFMA2 with the Chebyshev table broadcast from smem
+//               M_m[b] on FFMA2 with the Chebyshev table broadcast from smem (the
+//               direct sums: B < 256, the FFMA2 evaluator, or tuning moment_fft = 0;
+//               otherwise dg_moments_fft.cu computes the same moments by FFTs)
 //   k_evaluate  one warp = up to 64 candidates of one bucket (2 per lane):
 //               J_m(x) by series + backward recurrence (FP64), block loop on
 //               FFMA2 with the bucket's moments as broadcast loads, Horner in
