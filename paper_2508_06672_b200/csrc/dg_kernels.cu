@@ -1250,7 +1250,6 @@ __global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restric
                          dg_emitter_estimate* __restrict__ out, int* __restrict__ n_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     DetCand* c = reinterpret_cast<DetCand*>(smem);
-    __shared__ int n_acc, excluded;
     const int n = min(*n_cands, cap);
     int m = 1;
     while (m < n) m <<= 1;
@@ -1262,7 +1261,6 @@ __global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restric
             c[i].key = LLONG_MAX;
         }
     }
-    if (threadIdx.x == 0) n_acc = 0;
     __syncthreads();
     for (int k = 2; k <= m; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
@@ -1280,31 +1278,36 @@ __global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restric
             }
             __syncthreads();
         }
-    // accepted entries are compacted to the front of c[] as they are found
-    for (int idx = 0; idx < n; ++idx) {
-        const DetCand cur = c[idx];
-        if (threadIdx.x == 0) excluded = 0;
-        __syncthreads();
-        for (int a = threadIdx.x; a < n_acc; a += blockDim.x) {
-            const int dl = abs(cur.ilat - c[a].ilat), dn = abs(cur.ilon - c[a].ilon);
-            if (max(dl, dn) <= radius) excluded = 1;
+    // the greedy pass (correlate.hpp:177-199) in one warp: accepted entries are
+    // compacted to the front of c[] as they are found, the exclusion test over
+    // them is one ballot per candidate (no block barriers)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int acc = 0;
+        for (int idx = 0; idx < n; ++idx) {
+            const DetCand cur = c[idx];
+            bool ex = false;
+            for (int a = lane; a < acc; a += 32) {
+                const int dl = abs(cur.ilat - c[a].ilat), dn = abs(cur.ilon - c[a].ilon);
+                ex |= max(dl, dn) <= radius;
+            }
+            if (__any_sync(0xffffffffu, ex)) continue;
+            if (lane == 0) {
+                c[acc] = cur;  // acc <= idx, so this never clobbers unvisited entries
+                dg_emitter_estimate e;
+                e.lat_deg = (double)cur.ilat;  // lattice coordinates filled in on the host
+                e.lon_deg = (double)cur.ilon;
+                e.alt_m = 0.0;
+                e.grid_index = (int64_t)cur.ilat * n_lon + cur.ilon;
+                e.score = cur.score;
+                e.score_zsigma = (cur.score - stats[0]) / stats[2];
+                out[acc] = e;
+            }
+            ++acc;
+            __syncwarp();
         }
-        __syncthreads();
-        if (threadIdx.x == 0 && !excluded) {
-            c[n_acc] = cur;  // n_acc <= idx, so this never clobbers unvisited entries
-            dg_emitter_estimate e;
-            e.lat_deg = (double)cur.ilat;  // lattice coordinates filled in on the host
-            e.lon_deg = (double)cur.ilon;
-            e.alt_m = 0.0;
-            e.grid_index = (int64_t)cur.ilat * n_lon + cur.ilon;
-            e.score = cur.score;
-            e.score_zsigma = (cur.score - stats[0]) / stats[2];
-            out[n_acc] = e;
-            ++n_acc;
-        }
-        __syncthreads();
+        if (lane == 0) *n_out = acc;
     }
-    if (threadIdx.x == 0) *n_out = n_acc;
 }
 
 __global__ void k_f64_to_f32(const double2* __restrict__ in, float2* __restrict__ out, int64_t n) {
