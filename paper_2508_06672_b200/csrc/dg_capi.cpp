@@ -539,7 +539,10 @@ struct Pipeline {
             const bool tc = use_tc && evaluate_tc_supported(pl.nbmax, pl.R);
             // FFT moments only where the tensor-core evaluator carries their error term
             FftErr fx{nullptr, 0.f};
-            if (use_fft && tc && moments_fft_supported(pl.B)) {
+            // (k_mfft addresses moment rows in 32-bit: a bound no realistic run reaches)
+            const bool fft_fits =
+                std::min<int64_t>(P, pl.nbins) * (int64_t)pl.nbmax * pl.R < (int64_t)INT32_MAX;
+            if (use_fft && tc && fft_fits && moments_fft_supported(pl.B)) {
                 launch_moments_fft(pl.B, pl.R, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
                                    L.y1c, L.y2p, padf, L.mom, pl.nbmax, L.af, L.fe, L.queue,
                                    sm_count, st);
