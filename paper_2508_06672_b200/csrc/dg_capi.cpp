@@ -221,6 +221,7 @@ struct Lane {
     float2 *y1c = nullptr, *y2p = nullptr;
     float2* af = nullptr;  // FFT path: per (block, moment) spectra of the y1 blocks
     float* fe = nullptr;   // FFT path: per (window, block, moment) correlation mean squares
+    int* fqueue = nullptr;  // FFT path: work queue + per-block spectrum counters
     float* qf = nullptr;   // FFT path: their sums over each bucket's blocks [bucket][16]
     float2* mom = nullptr;
     size_t mom_cap = 0;
@@ -354,6 +355,7 @@ struct Pipeline {
                 L.af = sc.alloc<float2>(moments_fft_af_bytes(N, 256, kMaxMoments) /
                                         sizeof(float2));
                 L.fe = sc.alloc<float>(moments_fft_fe_floats(N, 256, kMaxMoments));
+                L.fqueue = sc.alloc<int>((size_t)N / 256 + 2);
                 L.qf = sc.alloc<float>((size_t)std::min<int64_t>(P, nbins) * kMaxMoments);
             }
         }
@@ -544,7 +546,7 @@ struct Pipeline {
                 std::min<int64_t>(P, pl.nbins) * (int64_t)pl.nbmax * pl.R < (int64_t)INT32_MAX;
             if (use_fft && tc && fft_fits && moments_fft_supported(pl.B)) {
                 launch_moments_fft(pl.B, pl.R, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
-                                   L.y1c, L.y2p, padf, L.mom, pl.nbmax, L.af, L.fe, L.queue,
+                                   L.y1c, L.y2p, padf, L.mom, pl.nbmax, L.af, L.fe, L.fqueue,
                                    sm_count, st);
                 launch_fft_bucket_energy(L.buckets, L.n_buckets,
                                          (int)std::min<int64_t>(P, pl.nbins), L.fe, pl.bin0,

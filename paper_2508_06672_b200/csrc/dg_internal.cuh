@@ -181,7 +181,7 @@ void launch_moments(int B, int R, const Bucket* buckets, const int* ubin, int bi
                     int N, const float* tcheb, const float2* y1c, const float2* y2p, int padf,
                     float2* mom, int nbmax, int sm_count, cudaStream_t st);
 // the same moments as FFT cross-correlations (dg_moments_fft.cu), for 256 <= B <= 768:
-// af = moments_fft_af_bytes of scratch, queue = one int of scratch; fe receives per
+// af = moments_fft_af_bytes of scratch, queue = N / 256 + 2 ints of scratch; fe receives per
 // (window, block, moment) the mean square of the window's correlation, the scale of
 // the FFT's rounding (moments_fft_fe_floats of scratch)
 constexpr int kFftLen = 1024;

@@ -10,11 +10,12 @@
 //     M_m[b](d0 + t) = conj( IFFT_L( conj(FFT_L(a_m)) . FFT_L(s) )[t] ) / L.
 // Per (block, window) that is one forward FFT of s and R inverse FFTs, against
 // the direct sums' G * B / 2 * R FP32x2 MACs: ~9x fewer operations at B = 512.
-//   k_mfft_a   per (block, m): FFT of a_m, stored conj / L  (R * nblk warp FFTs)
-//   k_mfft     per (window, block), one warp each (persistent): FFT of s into the
-//              warp's shared buffer, then per m the pointwise product and the
-//              inverse FFT, outputs written straight to the buckets' moment rows
-//              (the layout k_evaluate_tc reads: [bucket][block][m], odd m times i)
+//   k_mfft     one persistent kernel, one warp per work unit from one queue:
+//              first the (block, m) spectra conj(FFT(a_m)) / L (R * nblk warp
+//              FFTs, published per block), then the (window, block) items: FFT of
+//              s into the warp's shared buffer, then per m the pointwise product
+//              and the inverse FFT, outputs written straight to the buckets' moment
+//              rows (the layout k_evaluate_tc reads: [bucket][block][m], odd m x i)
 // FFTs: dg_fft.cuh (warp-level, FP32, ~5e-7 of the vector's RMS).
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -43,48 +44,36 @@ struct FftSmem {
     uint64_t bar[kFftWarps];
 };
 
-constexpr int kAWarps = 12;  // k_mfft_a: only a transpose buffer per warp
-struct FftASmem {
-    float2 tw[kFftL];
-    float2 xbuf[kAWarps][kXbuf];
-};
-
-__global__ void __launch_bounds__(32 * kAWarps, 1)
-k_mfft_a(const float2* __restrict__ y1c, int N, int B, int R, int nblk,
-         const float* __restrict__ tcheb, float2* __restrict__ af) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    FftASmem& sm = *reinterpret_cast<FftASmem*>(smem_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    fft1024_twiddles(sm.tw, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int total = nblk * R;
-    for (int it = blockIdx.x * kAWarps + warp; it < total; it += gridDim.x * kAWarps) {
-        const int b = it / R, m = it - b * R;
-        float2 v[32];
+// one (block, moment) spectrum: conj(FFT(a_m)) / L, a_m[j] = y1c[bB + j] T_m(t_j)
+__device__ __forceinline__ void afft_unit(int b, int m, int lane, const float2* __restrict__ y1c,
+                                          int N, int B, int R, const float* __restrict__ tcheb,
+                                          const float2* tw, float2* xbuf, float2* __restrict__ af) {
+    float2 v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const int j = lane + 32 * i;
-            const int k = b * B + j;
-            float2 a = make_float2(0.f, 0.f);
-            if (j < B && k < N) {
-                const float2 y = y1c[k];
-                const float t = tcheb[j * kMaxMoments + m];
-                a = make_float2(y.x * t, y.y * t);
-            }
-            v[i] = a;
+    for (int i = 0; i < 32; ++i) {
+        const int j = lane + 32 * i;
+        const int k = b * B + j;
+        float2 a = make_float2(0.f, 0.f);
+        if (j < B && k < N) {
+            const float2 y = y1c[k];
+            const float t = tcheb[j * kMaxMoments + m];
+            a = make_float2(y.x * t, y.y * t);
         }
-        fft1024_warp<false>(v, sm.tw, sm.xbuf[warp], lane);
-        float2* dst = af + (size_t)it * kFftL;
-        constexpr float inv = 1.0f / kFftL;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) dst[lane + 32 * i] = make_float2(v[i].x * inv, -v[i].y * inv);
+        v[i] = a;
     }
+    fft1024_warp<false>(v, tw, xbuf, lane);
+    float2* dst = af + ((size_t)b * R + m) * kFftL;
+    constexpr float inv = 1.0f / kFftL;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) dst[lane + 32 * i] = make_float2(v[i].x * inv, -v[i].y * inv);
 }
 
 __global__ void __launch_bounds__(32 * kFftWarps, 1)
 k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, int N, int B,
-       int R, int nblk, const float2* __restrict__ af, const float2* __restrict__ y2p, int padf,
-       float2* __restrict__ mom, int nbmax, float* __restrict__ fe, int* __restrict__ queue) {
+       int R, int nblk, const float2* __restrict__ y1c, const float* __restrict__ tcheb,
+       float2* __restrict__ af, int* __restrict__ ready, const float2* __restrict__ y2p,
+       int padf, float2* __restrict__ mom, int nbmax, float* __restrict__ fe,
+       int* __restrict__ queue) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     FftSmem& sm = *reinterpret_cast<FftSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -95,13 +84,32 @@ k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, in
     FftWarpSmem& ws = sm.w[warp];
     uint64_t* bar = &sm.bar[warp];
     uint32_t phase = 0;  // completed TMA copies of this warp
-    const int total = ngroups * nblk;
+    // one queue: first the (block, moment) spectra (block-major), then the (window,
+    // block) items; an item waits until its block's R spectra are published. Every
+    // spectrum is claimed before any item, by a warp that never waits: no deadlock.
+    const int nA = nblk * R;
+    const int total = nA + ngroups * nblk;
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(queue, 1);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= total) break;
-        const int g = it / nblk, b = it - g * nblk;
+        if (it < nA) {
+            const int b = it / R, m = it - b * R;
+            afft_unit(b, m, lane, y1c, N, B, R, tcheb, sm.tw, ws.xbuf, af);
+            __threadfence();  // the spectrum, then its publication
+            __syncwarp();
+            if (lane == 0) atomicAdd(&ready[b], 1);
+            continue;
+        }
+        const int j = it - nA;
+        const int g = j / nblk, b = j - g * nblk;
+        if (lane == 0) {
+            while (*reinterpret_cast<volatile int*>(&ready[b]) < R) __nanosleep(64);
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // read by TMA below
+        }
+        __syncwarp();
         // windows at absolute multiples of G, so any bin-range part of a step (the
         // multi-GPU work units) computes every moment with the same FFTs
         const int bin_a = (bin0 / G + g) * G;  // first bin of the window
@@ -257,16 +265,14 @@ void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int 
     const int nblk = (N + B - 1) / B;
     const int G = kFftL - B;
     const int ngroups = (bin0 + nbins - 1) / G - bin0 / G + 1;  // absolute windows
-    const size_t smem = sizeof(FftSmem), smem_a = sizeof(FftASmem);
-    static size_t attr_a[64] = {}, attr_m[64] = {};
-    ensure_smem(k_mfft_a, smem_a, attr_a);
+    const size_t smem = sizeof(FftSmem);
+    static size_t attr_m[64] = {};
     ensure_smem(k_mfft, smem, attr_m);
-    const int ga = (nblk * R + kAWarps - 1) / kAWarps;
-    k_mfft_a<<<ga < sm_count ? ga : sm_count, 32 * kAWarps, smem_a, st>>>(y1c, N, B, R, nblk,
-                                                                          tcheb, af);
-    cudaMemsetAsync(queue, 0, sizeof(int), st);
+    // queue[0]: the work queue; queue[1 .. nblk]: published spectra per block
+    cudaMemsetAsync(queue, 0, (size_t)(nblk + 1) * sizeof(int), st);
     k_mfft<<<sm_count, 32 * kFftWarps, smem, st>>>(ubin, bin0, nbins, ngroups, G, N, B, R, nblk,
-                                                   af, y2p, padf, mom, nbmax, fe, queue);
+                                                   y1c, tcheb, af, queue + 1, y2p, padf, mom,
+                                                   nbmax, fe, queue);
 }
 
 }  // namespace dg
