@@ -578,7 +578,7 @@ struct Pipeline {
                                 nu_c + s, pl.B, L.mom, pl.nbmax, s_out, bits, flag_base, tau,
                                 tau_noise, e1, e2, N, sm_count, st);
             launch_work_count(L.buckets, L.n_buckets, pl.B, pl.R, tc ? 1 : 0, L.work, st);
-            launches += fx.fft ? 8 : 7;  // + k_fft_bucket_energy
+            launches += fx.qf ? 8 : 7;  // + k_fft_bucket_energy
         }
         if (ev2) CK(cudaEventRecord(ev2, st));
     }
