@@ -58,6 +58,34 @@ __device__ __forceinline__ bool geometry_exact(double cx, double cy, double cz, 
     return rho > 0.0;
 }
 
+// The same delay and Doppler with FMA contraction and a Newton-refined reciprocal
+// square root instead of IEEE division / square root (a few ulp from the exact
+// values): the candidate evaluation only needs FP32-class FDOA; the TDOA of a pair
+// is taken from these only away from a rounding boundary (pair_tdoa_fast), and the
+// FP64 refinement and the exact re-rank recompute both offsets with geometry_exact.
+__device__ __forceinline__ bool geometry_fast(double cx, double cy, double cz, const dg_state& rx,
+                                              double inv_wl, double* delay, double* dop) {
+    const double rx_ = rx.position.x - cx, ry = rx.position.y - cy, rz = rx.position.z - cz;
+    const double r2 = fma(rx_, rx_, fma(ry, ry, rz * rz));
+    double inv = rsqrt(r2);
+    inv = inv * fma(-0.5 * r2 * inv, inv, 1.5);  // one Newton step past rsqrt's ~1 ulp
+    const double rho = r2 * inv;
+    *delay = rho * (1.0 / kC);
+    const double dot = fma(rx_, rx.velocity.x, fma(ry, rx.velocity.y, rz * rx.velocity.z));
+    *dop = -(dot * inv) * inv_wl;
+    return r2 > 0.0;
+}
+// llround((dj - di) fs) from the fast delays when the product is farther than
+// 1e-6 + 1e-12 |t| samples from a half-integer (the fast-exact difference is below
+// 1e-9 samples at any sample rate these runs use); otherwise -1 (recompute exactly)
+__device__ __forceinline__ bool pair_tdoa_fast(double di, double dj, double fs, long long* tdoa) {
+    const double t = (dj - di) * fs;
+    const double a = fabs(t), f = a - floor(a);
+    if (fabs(f - 0.5) <= 1e-6 + 1e-12 * a) return false;
+    *tdoa = llround(t);
+    return true;
+}
+
 // predict_pair_offsets (geometry.hpp:73-83): llround ties away from zero.
 __device__ __forceinline__ bool offsets_exact(double cx, double cy, double cz, const PairGeom& g,
                                               double fs, double wl, long long* tdoa, double* fdoa) {
@@ -275,6 +303,7 @@ k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
     for (int i = threadIdx.x; i < ng; i += blockDim.x) sgr[i] = groups[i];
     for (int i = threadIdx.x; i < n; i += blockDim.x) sup[i] = upair[i];
     __syncthreads();
+    const double inv_wl = 1.0 / wl;
     unsigned long long ovl = 0;
     RangeAcc ra;  // not flushed: ranges come from k_hist_range / k_range_fp32
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
@@ -286,7 +315,8 @@ k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
             bool ok[KR];
 #pragma unroll
             for (int r = 0; r < KR; ++r)
-                if (r < gr.nrx) ok[r] = geometry_exact(cx, cy, cz, srx[gr.rx0 + r], wl, &del[r], &dop[r]);
+                if (r < gr.nrx)
+                    ok[r] = geometry_fast(cx, cy, cz, srx[gr.rx0 + r], inv_wl, &del[r], &dop[r]);
             for (int u = gr.u0; u < gr.u0 + gr.nu; ++u) {
                 const int2 ij = sup[u];
                 double di = 0.0, fi = 0.0, dj = 0.0, fj = 0.0;
@@ -304,9 +334,16 @@ k_geometry_units(const double* __restrict__ x, const double* __restrict__ y,
                         okj = ok[r];
                     }
                 }
-                // predict_pair_offsets (geometry.hpp:73-83): llround ties away from zero
-                const long long tdoa = llround(__dmul_rn(__dsub_rn(dj, di), fs));
-                const double fdoa = __dsub_rn(fj, fi);
+                // predict_pair_offsets (geometry.hpp:73-83): llround ties away from zero;
+                // exact delays where the fast ones sit near a rounding boundary
+                long long tdoa;
+                if (!pair_tdoa_fast(di, dj, fs, &tdoa)) {
+                    double ei, ej, xi, xj;
+                    geometry_exact(cx, cy, cz, srx[gr.rx0 + ij.x], wl, &ei, &xi);
+                    geometry_exact(cx, cy, cz, srx[gr.rx0 + ij.y], wl, &ej, &xj);
+                    tdoa = llround(__dmul_rn(__dsub_rn(ej, ei), fs));
+                }
+                const double fdoa = fj - fi;
                 if (!(oki && okj)) atomicExch(err, 1);
                 emit_point(p, tdoa, fdoa, N, d_out + (int64_t)u * P, rank_out + (int64_t)u * P,
                            fdoa_out + (int64_t)u * P, hist + (int64_t)u * nbins,
