@@ -513,3 +513,29 @@ def test_four_receivers_vs_reference(b2, ref, normalize):
     mgrid = b2.build_candidate_grid(b2.LatLonBounds(*sc.bounds), sc.spacing, sc.alt, engine=eng)
     many = b2.geolocate_arrays(mgrid, sc.states, sc.captures, sc.fs, sc.fc, opts)
     assert np.array_equal(many.accumulated.values, res.accumulated.values)
+
+
+def test_fft_moments_match_direct_sums(b2, tune):
+    """The two moment kernels on one C3-density scene (101 x 101 cells at 1 km, a
+    chirp of the reference simulator's scene, 2 snapshots of 50,000 samples): FFT
+    cross-correlations (k_mfft, default) and direct sums (k_moments, moment_fft = 0)
+    give surfaces within 2e-5 of each other (each is within the 1e-4 contract of
+    the reference; their FP32 roundings differ), the same exact argmax, and the
+    FFT path really ran (moment_fft_flop)."""
+    from paper_2508_06672_b200 import simulate as sim
+    from paper_2508_06672_b200.geodesy import GeodeticCoord
+    km = 0.0089932161
+    rx = [sim.CircularOrbit(550e3, 53.0, -1.2, -1.1), sim.CircularOrbit(550e3, 53.0, 1.2, -0.7)]
+    em = [sim.EmitterDef(GeodeticCoord(10 * km, -20 * km, 0.0), sim.ChirpSpec(2e6, 20e-6),
+                         -10.0, 650e3)]
+    sc = sim.Scenario(rx, em, 2, 1.0, 0.01, 5e6, 1575.42e6, 0.0, 11, 1.0)
+    states, caps, _, _ = sim.simulate_arrays(sc)
+    grid = b2.build_candidate_grid(b2.LatLonBounds(-50 * km, 50 * km, -50 * km, 50 * km), km)
+    fft = b2.geolocate_arrays(grid, states, caps, 5e6, 1575.42e6, b2.GeolocateOptions())
+    assert fft.stats["moment_fft_flop"] > 0 and fft.stats["direct_steps"] == 0
+    tune(moment_fft=0)
+    direct = b2.geolocate_arrays(grid, states, caps, 5e6, 1575.42e6, b2.GeolocateOptions())
+    assert direct.stats["moment_fft_flop"] == 0
+    assert rel_err(fft.accumulated.values, direct.accumulated.values).max() <= 2e-5
+    assert fft.argmax_index == direct.argmax_index
+    assert fft.argmax_value == direct.argmax_value
