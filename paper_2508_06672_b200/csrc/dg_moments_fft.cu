@@ -16,6 +16,11 @@
 //              s into the warp's shared buffer, then per m the pointwise product
 //              and the inverse FFT, outputs written straight to the buckets' moment
 //              rows (the layout k_evaluate_tc reads: [bucket][block][m], odd m x i)
+//              It also records each (window, block, m) correlation's mean square:
+//              FFT rounding spreads ~5e-7 of a window's RMS over all its lags, the
+//              scale the refinement test needs.
+//   k_fft_bucket_energy  one warp per bucket: those energies summed over the
+//              bucket's blocks for k_evaluate_tc.
 // FFTs: dg_fft.cuh (warp-level, FP32, ~5e-7 of the vector's RMS).
 #include <cuda_runtime.h>
 #include <stdint.h>
