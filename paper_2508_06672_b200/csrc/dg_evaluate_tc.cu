@@ -370,6 +370,8 @@ k_evaluate_tc(const FftErr fx, const Bucket* __restrict__ buckets, const int* __
             double sr = 1.0, si = 0.0;
             double acc_re = 0.0, acc_im = 0.0, ar = 1.0, ai = 0.0;
             float en = 0.f;  // sum_b |C_b|^2: an error scale, FP32
+            float w16r = 1.f, w16i = 0.f, pnd_r = 0.f, pnd_i = 0.f;
+            bool pend = false;
             for (int c0 = 0; c0 < np; c0 += kChunkCols) {
                 const int nn = np - c0 < kChunkCols ? np - c0 : kChunkCols;
                 if (tid == 0) {
@@ -404,8 +406,11 @@ k_evaluate_tc(const FftErr fx, const Bucket* __restrict__ buckets, const int* __
                     const double w8r = fma(br[4], br[4], -bi[4] * bi[4]), w8i = 2.0 * br[4] * bi[4];
                     const double w12r = fma(w8r, br[4], -w8i * bi[4]);
                     const double w12i = fma(w8r, bi[4], w8i * br[4]);
-                    sr = fma(w8r, w8r, -w8i * w8i);
-                    si = 2.0 * w8r * w8i;
+                    const double s16r = fma(w8r, w8r, -w8i * w8i), s16i = 2.0 * w8r * w8i;
+                    w16r = (float)s16r;
+                    w16i = (float)s16i;
+                    sr = fma(s16r, s16r, -s16i * s16i);  // W_32: the anchor step of a group pair
+                    si = 2.0 * s16r * s16i;
                     const float hr[4] = {1.f, (float)br[4], (float)w8r, (float)w12r};
                     const float hi4[4] = {0.f, (float)bi[4], (float)w8i, (float)w12i};
 #pragma unroll
@@ -438,16 +443,29 @@ k_evaluate_tc(const FftErr fx, const Bucket* __restrict__ buckets, const int* __
                         E1 = ffma2v(C1, C1, E1);
                     }
                     const float2 A = add2(A0, A1), V = add2(V0, V1), E2 = add2(E0, E1);
-                    const double hr = (double)(A.x - V.y), hi = (double)(A.y + V.x);
-                    acc_re = fma(ar, hr, fma(-ai, hi, acc_re));
-                    acc_im = fma(ar, hi, fma(ai, hr, acc_im));
+                    const float hr = A.x - V.y, hi = A.y + V.x;
                     en += E2.x + E2.y;
-                    const double nr = fma(ar, sr, -ai * si);
-                    ai = fma(ar, si, ai * sr);
-                    ar = nr;
+                    if (!pend) {  // groups in pairs: the first one waits in FP32
+                        pnd_r = hr;
+                        pnd_i = hi;
+                        pend = true;
+                    } else {  // pair sum h_g + W_16 h_{g+1} (FP32), then one FP64 anchor
+                        pnd_r = fmaf(w16r, hr, fmaf(-w16i, hi, pnd_r));
+                        pnd_i = fmaf(w16r, hi, fmaf(w16i, hr, pnd_i));
+                        acc_re = fma(ar, (double)pnd_r, fma(-ai, (double)pnd_i, acc_re));
+                        acc_im = fma(ar, (double)pnd_i, fma(ai, (double)pnd_r, acc_im));
+                        const double nr = fma(ar, sr, -ai * si);  // advance by W_32
+                        ai = fma(ar, si, ai * sr);
+                        ar = nr;
+                        pend = false;
+                    }
                 }
                 tc_fence_before();  // this chunk's TMEM reads done before the next MMAs
                 __syncthreads();
+            }
+            if (pend) {  // a last unpaired group
+                acc_re = fma(ar, (double)pnd_r, fma(-ai, (double)pnd_i, acc_re));
+                acc_im = fma(ar, (double)pnd_i, fma(ai, (double)pnd_r, acc_im));
             }
             if (pc >= 0) {
                 const double s2 = acc_re * acc_re + acc_im * acc_im;
