@@ -1798,7 +1798,7 @@ void correlate_units_impl(dg_engine* eng, const dg_grid* g, const dg_staged* sn,
                               pl.nbins, raw + (int64_t)w0 * P, pl.overlap, pl.err, geo_ws.data(),
                               st);
         launch_hist_range(pl.hist_slot(0), pl.nbins, nw, pl.N, pl.range, st);
-        launches += (nw + 63) / 64 + 1;
+        launches += (nw + 63) / 64 + 2;
         if (w0 == 0) {  // the rest of the run's state, while the first geometry pass runs
             pl.init_lanes(sc);
             bits = sc.alloc<uint32_t>(n_words);

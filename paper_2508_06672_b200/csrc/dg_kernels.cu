@@ -465,21 +465,39 @@ k_range_fp32(const float4* __restrict__ rel, int64_t P, const RxPairF32* __restr
 }
 
 // Exact TDOA range of each step of a window: the first and last non-empty
-// bin of its histogram (one CTA per step). The buckets are planned over these
-// bins, so every candidate lands in a planned bin whatever the error of the
-// FP32 planning pass (which now only sets B, R and the centre frequency).
+// bin of its histogram. The buckets are planned over these bins, so every
+// candidate lands in a planned bin whatever the error of the FP32 planning pass
+// (which now only sets B, R and the centre frequency). Grid (chunks, steps):
+// each CTA scans kHistRangeChunk bins and folds its extremes into the step's
+// range with atomics (k_range_init sets the empty range first).
 constexpr int kHistRangeThreads = 512;
+constexpr int kHistRangeChunk = 16 * kHistRangeThreads;
+
+__global__ void k_range_init(StepRange* __restrict__ out, int n_steps) {
+    for (int s = threadIdx.x; s < n_steps; s += blockDim.x) {
+        StepRange r;
+        r.fmin = ~0ull;
+        r.fmax = 0ull;
+        r.dmin = INT_MAX;
+        r.dmax = INT_MIN;
+        out[s] = r;
+    }
+}
 
 __global__ void __launch_bounds__(kHistRangeThreads)
 k_hist_range(const int* __restrict__ hist, int nbins, int N, StepRange* __restrict__ out) {
     __shared__ int red[2][kHistRangeThreads / 32];
-    const int* h = hist + (int64_t)blockIdx.x * nbins;
+    const int* h = hist + (int64_t)blockIdx.y * nbins;
+    const int b0 = blockIdx.x * kHistRangeChunk;
     int lo = INT_MAX, hi = INT_MIN;
-    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
-        if (h[b]) {
+#pragma unroll
+    for (int j = 0; j < kHistRangeChunk / kHistRangeThreads; ++j) {
+        const int b = b0 + j * kHistRangeThreads + threadIdx.x;
+        if (b < nbins && h[b]) {
             lo = min(lo, b);
             hi = max(hi, b);
         }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -496,12 +514,10 @@ k_hist_range(const int* __restrict__ hist, int nbins, int N, StepRange* __restri
             lo = min(lo, red[0][w]);
             hi = max(hi, red[1][w]);
         }
-        StepRange r;
-        r.fmin = ~0ull;
-        r.fmax = 0ull;
-        r.dmin = lo <= hi ? lo - (N - 1) : INT_MAX;
-        r.dmax = lo <= hi ? hi - (N - 1) : INT_MIN;
-        out[blockIdx.x] = r;
+        if (lo <= hi) {
+            atomicMin(&out[blockIdx.y].dmin, lo - (N - 1));
+            atomicMax(&out[blockIdx.y].dmax, hi - (N - 1));
+        }
     }
 }
 
@@ -997,19 +1013,22 @@ __global__ void k_rerank(const int* __restrict__ cells, const int* __restrict__ 
     }
 }
 
-// The same exact chains with the work of one chain spread over three warps of a
-// CTA (bit-identical: every FP64 operation and its order are the reference's,
-// only the thread that executes it changes). Per tile of kRrT samples, double
-// buffered: warp 1 forms the products p_k = y1[k] conj(y2[k+d]) (independent per
-// sample, all lanes), warp 2 lane 0 runs the phasor recurrence, warp 0 lane 0 the
-// accumulation acc += p_k ph_k; the single-lane chains issue 6-8 FP64 operations
-// per sample instead of 22, and the two chains overlap.
+// The same exact chains with the work of one chain spread over the four warps of
+// a CTA (bit-identical: every FP64 operation and its order are the reference's,
+// only the thread that executes it changes). Tiles of kRrT samples, three stages
+// in flight: in iteration t, warp 2 lane 0 runs the phasor recurrence for tile
+// t+1 (the critical chain: a dependent DMUL + DADD per sample), warp 1 forms the
+// products p_k = y1[k] conj(y2[k+d]) of tile t+1 (all of a lane's loads issued
+// before its arithmetic: one memory latency per tile), warp 3 the terms
+// q_k = p_k ph_k of tile t, and warp 0 lane 0 adds the terms of tile t-1 in
+// sample order (acc += q_k: two independent DADDs per sample).
 constexpr int kRrT = 256;
+constexpr int kRrThreads = 128;
 
 __device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* __restrict__ y2,
                                 int N, long long d, double fdoa, double fs, const double* tg,
                                 double* out) {
-    __shared__ double2 pbuf[2][kRrT], hbuf[2][kRrT];
+    __shared__ double2 pbuf[2][kRrT], hbuf[2][kRrT], qbuf[2][kRrT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const long long kb = d < 0 ? -d : 0;
     const long long ke = (N - d) < N ? (N - d) : N;
@@ -1023,39 +1042,66 @@ __device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* _
     const double2* b = y2 + d;
     const long long n = ke - kb;
     const int ntile = (int)((n + kRrT - 1) / kRrT);
-    auto produce = [&](int t) {  // warps 1 and 2: tile t into buffer t & 1
+    auto tile_len = [&](int t) { return (int)min((long long)kRrT, n - (long long)t * kRrT); };
+    auto products = [&](int t) {  // warp 1: p of tile t into pbuf[t & 1]
         const long long k0 = kb + (long long)t * kRrT;
-        const int len = (int)min((long long)kRrT, ke - k0);
-        const int bf = t & 1;
-        if (warp == 1) {
-            for (int i = lane; i < len; i += 32) {
-                const double2 a = __ldg(y1 + k0 + i), bb = __ldg(b + k0 + i);
-                const double b_re = bb.x, b_im = -bb.y;
-                pbuf[bf][i] = make_double2(__dsub_rn(__dmul_rn(a.x, b_re), __dmul_rn(a.y, b_im)),
-                                           __dadd_rn(__dmul_rn(a.x, b_im), __dmul_rn(a.y, b_re)));
+        const int len = tile_len(t), bf = t & 1;
+        constexpr int J = kRrT / 32;
+        double2 a[J], bb[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int i = lane + 32 * j;
+            if (i < len) {
+                a[j] = __ldg(y1 + k0 + i);
+                bb[j] = __ldg(b + k0 + i);
             }
-        } else if (warp == 2 && lane == 0) {
-#pragma unroll 4
-            for (int i = 0; i < len; ++i) {
-                hbuf[bf][i] = make_double2(ph_re, ph_im);
-                const double nr = __dsub_rn(__dmul_rn(ph_re, rot_re), __dmul_rn(ph_im, rot_im));
-                ph_im = __dadd_rn(__dmul_rn(ph_re, rot_im), __dmul_rn(ph_im, rot_re));
-                ph_re = nr;
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int i = lane + 32 * j;
+            if (i < len) {
+                const double b_re = bb[j].x, b_im = -bb[j].y;
+                pbuf[bf][i] =
+                    make_double2(__dsub_rn(__dmul_rn(a[j].x, b_re), __dmul_rn(a[j].y, b_im)),
+                                 __dadd_rn(__dmul_rn(a[j].x, b_im), __dmul_rn(a[j].y, b_re)));
             }
         }
     };
-    produce(0);
+    auto phasors = [&](int t) {  // warp 2 lane 0: ph of tile t into hbuf[t & 1]
+        const int len = tile_len(t), bf = t & 1;
+#pragma unroll 4
+        for (int i = 0; i < len; ++i) {
+            hbuf[bf][i] = make_double2(ph_re, ph_im);
+            const double nr = __dsub_rn(__dmul_rn(ph_re, rot_re), __dmul_rn(ph_im, rot_im));
+            ph_im = __dadd_rn(__dmul_rn(ph_re, rot_im), __dmul_rn(ph_im, rot_re));
+            ph_re = nr;
+        }
+    };
+    if (warp == 1) products(0);
+    else if (warp == 2 && lane == 0) phasors(0);
     __syncthreads();
-    for (int t = 0; t < ntile; ++t) {
-        if (t + 1 < ntile) produce(t + 1);
-        if (warp == 0 && lane == 0) {
-            const int bf = t & 1;
-            const int len = (int)min((long long)kRrT, n - (long long)t * kRrT);
+    for (int t = 0; t <= ntile; ++t) {
+        if (warp == 2) {
+            if (lane == 0 && t + 1 < ntile) phasors(t + 1);
+        } else if (warp == 1) {
+            if (t + 1 < ntile) products(t + 1);
+        } else if (warp == 3) {
+            if (t < ntile) {  // terms of tile t (its p and ph were written last iteration)
+                const int len = tile_len(t), bf = t & 1;
+                for (int i = lane; i < len; i += 32) {
+                    const double2 pk = pbuf[bf][i], hk = hbuf[bf][i];
+                    qbuf[bf][i] =
+                        make_double2(__dsub_rn(__dmul_rn(pk.x, hk.x), __dmul_rn(pk.y, hk.y)),
+                                     __dadd_rn(__dmul_rn(pk.x, hk.y), __dmul_rn(pk.y, hk.x)));
+                }
+            }
+        } else if (lane == 0 && t > 0) {  // warp 0: sum the terms of tile t-1
+            const int len = tile_len(t - 1), bf = (t - 1) & 1;
 #pragma unroll 8
             for (int i = 0; i < len; ++i) {
-                const double2 pk = pbuf[bf][i], hk = hbuf[bf][i];
-                acc_re = __dadd_rn(acc_re, __dsub_rn(__dmul_rn(pk.x, hk.x), __dmul_rn(pk.y, hk.y)));
-                acc_im = __dadd_rn(acc_im, __dadd_rn(__dmul_rn(pk.x, hk.y), __dmul_rn(pk.y, hk.x)));
+                const double2 q = qbuf[bf][i];
+                acc_re = __dadd_rn(acc_re, q.x);
+                acc_im = __dadd_rn(acc_im, q.y);
             }
         }
         __syncthreads();
@@ -1064,7 +1110,7 @@ __device__ void exact_chain_cta(const double2* __restrict__ y1, const double2* _
         *out = __dsqrt_rn(__dadd_rn(__dmul_rn(acc_re, acc_re), __dmul_rn(acc_im, acc_im)));
 }
 
-__global__ void __launch_bounds__(96)
+__global__ void __launch_bounds__(kRrThreads)
 k_rerank_cta(const int* __restrict__ cells, const int* __restrict__ n_cells, int cap, int SP,
              RefineCtx c, double* __restrict__ ex) {
     const int n = min(*n_cells, cap);
@@ -1469,7 +1515,9 @@ void launch_energy_prefix(const double2* y, int64_t stride, int64_t n_caps, int6
 
 void launch_hist_range(const int* hist, int nbins, int n_steps, int N, StepRange* out,
                        cudaStream_t st) {
-    k_hist_range<<<n_steps, kHistRangeThreads, 0, st>>>(hist, nbins, N, out);
+    k_range_init<<<1, 256, 0, st>>>(out, n_steps);
+    const int chunks = (nbins + kHistRangeChunk - 1) / kHistRangeChunk;
+    k_hist_range<<<dim3(chunks, n_steps), kHistRangeThreads, 0, st>>>(hist, nbins, N, out);
 }
 
 void launch_predict_offsets(const double* x, const double* y, const double* z, int64_t P,
@@ -1608,8 +1656,8 @@ void launch_first_max(const double* v, int64_t P, const double* vmax, unsigned l
 void launch_rerank(const int* cells, const int* n_cells, int cap, int n_items_hint, int SP,
                    RefineCtx ctx, double* ex, cudaStream_t st) {
     const int64_t items = (int64_t)std::min(n_items_hint, cap) * SP;
-    if (items <= 148 * 16) {  // one three-warp CTA per chain
-        k_rerank_cta<<<(int)std::max<int64_t>(items, 1), 96, 0, st>>>(cells, n_cells, cap, SP,
+    if (items <= 148 * 16) {  // one four-warp CTA per chain
+        k_rerank_cta<<<(int)std::max<int64_t>(items, 1), kRrThreads, 0, st>>>(cells, n_cells, cap, SP,
                                                                       ctx, ex);
         return;
     }
