@@ -1361,22 +1361,75 @@ __global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restric
             }
             __syncthreads();
         }
-    // the greedy pass (correlate.hpp:177-199) in one warp: accepted entries are
-    // compacted to the front of c[] as they are found, the exclusion test over
-    // them is one ballot per candidate (no block barriers)
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        int acc = 0;
-        for (int idx = 0; idx < n; ++idx) {
-            const DetCand cur = c[idx];
-            bool ex = false;
-            for (int a = lane; a < acc; a += 32) {
-                const int dl = abs(cur.ilat - c[a].ilat), dn = abs(cur.ilon - c[a].ilon);
-                ex |= max(dl, dn) <= radius;
+    // the greedy pass (correlate.hpp:177-199): candidate i (in sorted order) is
+    // kept iff no kept candidate before it lies within the Chebyshev radius.
+    // Blocks of 32 candidates in order: (A) all threads test the block against
+    // the kept list of the earlier blocks (one rejection bit per candidate);
+    // (B) warp 0 resolves the block itself: each lane's mask of conflicting
+    // earlier lanes, then the 32-step keep rule on bit masks, and appends the
+    // kept ones. A single warp walking the candidates one by one is
+    // latency-bound (~800 cycles per candidate at C3).
+    unsigned char* stat = reinterpret_cast<unsigned char*>(c + m);  // 1 kept, 2 rejected
+    unsigned short* klist = reinterpret_cast<unsigned short*>(stat + ((m + 15) & ~15));
+    __shared__ unsigned rejmask;
+    __shared__ int nkept;
+    if (threadIdx.x == 0) {
+        rejmask = 0;
+        nkept = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int base = 0; base < n; base += 32) {
+        const int nb = min(32, n - base);
+        const int nk = nkept;
+        unsigned my = 0;
+        for (int k = threadIdx.x; k < nk; k += blockDim.x) {  // (A)
+            const DetCand& kc = c[klist[k]];
+            const int kl = kc.ilat, kn = kc.ilon;
+            for (int q = 0; q < nb; ++q)
+                if (max(abs(kl - c[base + q].ilat), abs(kn - c[base + q].ilon)) <= radius)
+                    my |= 1u << q;
+        }
+        if (my) atomicOr(&rejmask, my);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // (B)
+            const int i = base + lane;
+            const bool valid = lane < nb;
+            const bool alive = valid && !((rejmask >> lane) & 1u);
+            unsigned pm = 0;  // earlier lanes of this block within the radius
+            if (alive) {
+                const int li = c[i].ilat, ni = c[i].ilon;
+                for (int q = 0; q < lane; ++q)
+                    if (max(abs(li - c[base + q].ilat), abs(ni - c[base + q].ilon)) <= radius)
+                        pm |= 1u << q;
             }
-            if (__any_sync(0xffffffffu, ex)) continue;
+            const unsigned am = __ballot_sync(0xffffffffu, alive);
+            unsigned kept = 0;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const unsigned pmq = __shfl_sync(0xffffffffu, pm, q);
+                if (((am >> q) & 1u) && !(pmq & kept)) kept |= 1u << q;
+            }
+            const bool keep = (kept >> lane) & 1u;
+            if (valid) stat[i] = keep ? 1 : 2;
+            if (keep) klist[nk + __popc(kept & ((1u << lane) - 1))] = (unsigned short)i;
+            __syncwarp();
             if (lane == 0) {
-                c[acc] = cur;  // acc <= idx, so this never clobbers unvisited entries
+                nkept = nk + __popc(kept);
+                rejmask = 0;
+            }
+        }
+        __syncthreads();
+    }
+    // kept candidates in sorted order (one warp, ballot compaction)
+    if (threadIdx.x < 32) {
+        int acc = 0;
+        for (int base = 0; base < n; base += 32) {
+            const int i = base + lane;
+            const bool keep = i < n && stat[i] == 1;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const DetCand cur = c[i];
                 dg_emitter_estimate e;
                 e.lat_deg = (double)cur.ilat;  // lattice coordinates filled in on the host
                 e.lon_deg = (double)cur.ilon;
@@ -1384,10 +1437,9 @@ __global__ void k_greedy(const DetCand* __restrict__ cands, const int* __restric
                 e.grid_index = (int64_t)cur.ilat * n_lon + cur.ilon;
                 e.score = cur.score;
                 e.score_zsigma = (cur.score - stats[0]) / stats[2];
-                out[acc] = e;
+                out[acc + __popc(bal & ((1u << lane) - 1))] = e;
             }
-            ++acc;
-            __syncwarp();
+            acc += __popc(bal);
         }
         if (lane == 0) *n_out = acc;
     }
@@ -1710,7 +1762,8 @@ void launch_greedy(const DetCand* cands, const int* n_cands, int cap, int radius
                    cudaStream_t st) {
     int m = 1;
     while (m < cap) m <<= 1;
-    const size_t smem = (size_t)m * sizeof(DetCand);
+    // candidates, statuses, kept list
+    const size_t smem = (size_t)m * sizeof(DetCand) + ((m + 15) & ~15) + (size_t)m * 2;
     cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_greedy<<<1, 1024, smem, st>>>(cands, n_cands, cap, radius, stats, n_lon, out, n_out);
 }

@@ -132,6 +132,23 @@ def test_detect_beyond_device_list_vs_reference(b2, ref):
                                    rtol=1e-12)
 
 
+def test_detect_dense_conflicts_vs_reference(b2, ref):
+    """Thousands of local maxima inside the device list with dense exclusion
+    conflicts (long kept/rejected chains for the parallel greedy rounds): equal to
+    the reference's sequential detect_emitters, including score ties."""
+    bounds, spacing = (0.0, 2.0, 0.0, 2.0), 0.01
+    grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
+    rng = np.random.default_rng(11)
+    v = rng.random(grid.size())
+    v[::7] = np.round(v[::7], 2)  # score ties broken by the lattice key
+    for k_sigma, radius in ((-1.0, 1), (-1.0, 3), (0.0, 2), (0.5, 8)):
+        want = ref.detect_emitters(bounds, spacing, 0.0, v, k_sigma, radius, cap=grid.size())
+        got = b2.detect_emitters(b2.CorrelationGrid(grid, v), k_sigma, radius)
+        assert len(want) > 10
+        assert [d.grid_index for d in got] == [w[0] for w in want]
+        assert [d.score for d in got] == [w[1] for w in want]
+
+
 def test_detect_capacity_recall(b2, ref):
     """n_detections reports the whole list; the Python driver fetches it all."""
     sc = load_scene(ref, "DESK_FOURJAM")
