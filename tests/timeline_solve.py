@@ -23,12 +23,19 @@ def main():
     states, caps, bounds, spacing = bench.make_inputs(name)
     grid = b2.build_candidate_grid(b2.LatLonBounds(*bounds), spacing)
     staged = b2.StagedSnapshots(states, caps, cfg["fs"], bench.FC)
-    opts = b2.GeolocateOptions()
+    # the bench's solve: detection on, surface kept on the device
+    opts = b2.GeolocateOptions(k_sigma=5.0, exclusion_radius_cells=5, detect=True)
+    acc = torch.empty(grid.size(), dtype=torch.float64, device="cuda")
+
+    def solve():
+        b2.geolocate_staged(grid, staged, opts, want_surface=False,
+                            accumulated_device=acc.data_ptr())
+
     for _ in range(2):
-        b2.geolocate_staged(grid, staged, opts)  # warm-up
+        solve()  # warm-up
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        b2.geolocate_staged(grid, staged, opts)
+        solve()
         torch.cuda.synchronize()
     ev = []
     for e in prof.events():
