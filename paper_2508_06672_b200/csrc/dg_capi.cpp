@@ -1508,7 +1508,7 @@ namespace {
 
 constexpr int kDetCap = 8192;
 // k_greedy holds the sorted list, statuses and 16-bit kept indices in shared memory
-// (25 + 2 bytes per entry: 216 KB at 8,192)
+// (24 + 1 + 2 bytes per entry: 216 KiB at 8,192)
 static_assert(kDetCap <= 8192, "k_greedy's shared-memory layout");
 
 // detect_emitters (correlate.hpp:127-201). Mean / sigma, the threshold and the
