@@ -245,10 +245,11 @@ struct Pipeline {
     cudaEvent_t window_ready = nullptr;
     unsigned long long* overlap = nullptr;
     static constexpr int kTables = 6;  // the block lengths of kMomentB
-    const float* tcheb[kTables] = {};
-    const float* tcheb_for(int B) const {
+    const float* tcheb[kTables] = {};   // [B][kMaxMoments] (k_moments)
+    const float* tchebT[kTables] = {};  // [kMaxMoments][B] (k_mfft: coalesced per moment)
+    const float* tcheb_for(int B, bool transposed = false) const {
         for (int i = 0; i < kTables; ++i)
-            if (kMomentB[i] == B) return tcheb[i];
+            if (kMomentB[i] == B) return transposed ? tchebT[i] : tcheb[i];
         raise(DG_ERUNTIME, "b200: no Chebyshev table for this block length");
     }
     std::vector<StepPlan> plans;
@@ -366,6 +367,7 @@ struct Pipeline {
             off[i] = total;
             total += (size_t)kMomentB[i] * kMaxMoments;
         }
+        const size_t offT = total;  // the transposed copies follow, same offsets
         {
             std::lock_guard<std::mutex> lk(eng->tables_mu);
             if (!eng->tables) {
@@ -374,14 +376,22 @@ struct Pipeline {
                     auto t = chebyshev_table(kMomentB[i]);
                     all.insert(all.end(), t.begin(), t.end());
                 }
+                for (int i = 0; i < kTables; ++i) {
+                    const int B = kMomentB[i];
+                    for (int m = 0; m < kMaxMoments; ++m)
+                        for (int j = 0; j < B; ++j)
+                            all.push_back(all[off[i] + (size_t)j * kMaxMoments + m]);
+                }
                 auto mem = std::make_unique<DevMem>(all.size() * sizeof(float));
                 CK(cudaMemcpy(mem->p, all.data(), all.size() * sizeof(float),
                               cudaMemcpyHostToDevice));
                 eng->tables = std::move(mem);
             }
         }
-        for (int i = 0; i < kTables; ++i)
+        for (int i = 0; i < kTables; ++i) {
             tcheb[i] = static_cast<const float*>(eng->tables->p) + off[i];
+            tchebT[i] = static_cast<const float*>(eng->tables->p) + offT + off[i];
+        }
     }
 
     int* d_slot(int s) const { return d + (size_t)s * P; }
@@ -545,7 +555,7 @@ struct Pipeline {
             const bool fft_fits =
                 std::min<int64_t>(P, pl.nbins) * (int64_t)pl.nbmax * pl.R < (int64_t)INT32_MAX;
             if (use_fft && tc && fft_fits && moments_fft_supported(pl.B)) {
-                launch_moments_fft(pl.B, pl.R, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B),
+                launch_moments_fft(pl.B, pl.R, L.ubin, pl.bin0, pl.nbins, N, tcheb_for(pl.B, true),
                                    L.y1c, L.y2p, padf, L.mom, pl.nbmax, L.af, L.fe, L.fqueue,
                                    sm_count, st);
                 launch_fft_bucket_energy(L.buckets, L.n_buckets,

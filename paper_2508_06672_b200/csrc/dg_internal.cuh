@@ -192,7 +192,7 @@ bool moments_fft_supported(int B);
 size_t moments_fft_af_bytes(int N, int B, int R);
 size_t moments_fft_fe_floats(int N, int B, int R);
 void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int N,
-                        const float* tcheb, const float2* y1c, const float2* y2p, int padf,
+                        const float* tchebT, const float2* y1c, const float2* y2p, int padf,
                         float2* mom, int nbmax, float2* af, float* fe, int* queue, int sm_count,
                         cudaStream_t st);
 // what k_evaluate_tc needs of an FFT-moment step (qf = nullptr: direct moments):

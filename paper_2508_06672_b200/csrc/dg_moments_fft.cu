@@ -50,8 +50,9 @@ struct FftSmem {
 };
 
 // one (block, moment) spectrum: conj(FFT(a_m)) / L, a_m[j] = y1c[bB + j] T_m(t_j)
+// (tchebT: the Chebyshev table moment-major, one coalesced row per moment)
 __device__ __forceinline__ void afft_unit(int b, int m, int lane, const float2* __restrict__ y1c,
-                                          int N, int B, int R, const float* __restrict__ tcheb,
+                                          int N, int B, int R, const float* __restrict__ tchebT,
                                           const float2* tw, float2* xbuf, float2* __restrict__ af) {
     float2 v[32];
 #pragma unroll
@@ -61,7 +62,7 @@ __device__ __forceinline__ void afft_unit(int b, int m, int lane, const float2* 
         float2 a = make_float2(0.f, 0.f);
         if (j < B && k < N) {
             const float2 y = y1c[k];
-            const float t = tcheb[j * kMaxMoments + m];
+            const float t = tchebT[m * B + j];
             a = make_float2(y.x * t, y.y * t);
         }
         v[i] = a;
@@ -75,7 +76,7 @@ __device__ __forceinline__ void afft_unit(int b, int m, int lane, const float2* 
 
 __global__ void __launch_bounds__(32 * kFftWarps, 1)
 k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, int N, int B,
-       int R, int nblk, const float2* __restrict__ y1c, const float* __restrict__ tcheb,
+       int R, int nblk, const float2* __restrict__ y1c, const float* __restrict__ tchebT,
        float2* __restrict__ af, int* __restrict__ ready, const float2* __restrict__ y2p,
        int padf, float2* __restrict__ mom, int nbmax, float* __restrict__ fe,
        int* __restrict__ queue) {
@@ -101,7 +102,7 @@ k_mfft(const int* __restrict__ ubin, int bin0, int nbins, int ngroups, int G, in
         if (it >= total) break;
         if (it < nA) {
             const int b = it / R, m = it - b * R;
-            afft_unit(b, m, lane, y1c, N, B, R, tcheb, sm.tw, ws.xbuf, af);
+            afft_unit(b, m, lane, y1c, N, B, R, tchebT, sm.tw, ws.xbuf, af);
             __threadfence();  // the spectrum, then its publication
             __syncwarp();
             if (lane == 0) atomicAdd(&ready[b], 1);
@@ -264,7 +265,7 @@ size_t moments_fft_fe_floats(int N, int B, int R) {
 }
 
 void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int N,
-                        const float* tcheb, const float2* y1c, const float2* y2p, int padf,
+                        const float* tchebT, const float2* y1c, const float2* y2p, int padf,
                         float2* mom, int nbmax, float2* af, float* fe, int* queue, int sm_count,
                         cudaStream_t st) {
     const int nblk = (N + B - 1) / B;
@@ -276,7 +277,7 @@ void launch_moments_fft(int B, int R, const int* ubin, int bin0, int nbins, int 
     // queue[0]: the work queue; queue[1 .. nblk]: published spectra per block
     cudaMemsetAsync(queue, 0, (size_t)(nblk + 1) * sizeof(int), st);
     k_mfft<<<sm_count, 32 * kFftWarps, smem, st>>>(ubin, bin0, nbins, ngroups, G, N, B, R, nblk,
-                                                   y1c, tcheb, af, queue + 1, y2p, padf, mom,
+                                                   y1c, tchebT, af, queue + 1, y2p, padf, mom,
                                                    nbmax, fe, queue);
 }
 
